@@ -1,0 +1,167 @@
+/*
+ * kmerscan_b200.h -- C ABI of the B200-native chunked DFA scan.
+ *
+ * Drop-in native boundary for the reference's compiled hot path
+ * (/root/reference/pkg/src/kmerscan/_kernels.py, numba @njit kernels) and the
+ * engine entry points that call it (/root/reference/pkg/src/kmerscan/engine.py).
+ * Plain C types only (pointers + sizes): no torch, no numpy, no C++ in the
+ * signatures.  Every call returns 0 on success or a negative KS_E* status; the
+ * message of the last failure on the calling thread is ks_last_error().  A
+ * failing call never leaves partial results in caller buffers.
+ *
+ * Device memory is owned by the context and the dfa/seq handles (freed by
+ * ks_*_free).  Handles are immutable after upload; calls on one context are
+ * serialised on the context's CUDA stream.
+ */
+#ifndef KMERSCAN_B200_H
+#define KMERSCAN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define KS_API __attribute__((visibility("default")))
+#else
+#define KS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KS_OK 0
+#define KS_E_INVALID (-1)   /* bad argument            -> Python ValueError            */
+#define KS_E_CUDA (-2)      /* CUDA runtime failure    -> Python RuntimeError          */
+#define KS_E_CHAIN (-3)     /* internal chain invariant-> Python ReductionChainError   */
+#define KS_E_UNSUPPORTED (-4) /* outside the device limits (e.g. |Q| > 32767)        */
+#define KS_E_NOMEM (-5)
+
+typedef struct ks_ctx ks_ctx;
+typedef struct ks_dfa ks_dfa;
+typedef struct ks_seq ks_seq;
+
+/* Scan strategy chosen by ks_dfa_upload (ks_dfa_info.strategy). */
+#define KS_STRATEGY_LOOKBACK 1   /* definite DFA: state after D symbols is input-determined */
+#define KS_STRATEGY_MAPSCAN 2    /* small transition monoid: chunk maps + exclusive scan     */
+#define KS_STRATEGY_SPECULATE 3  /* generic: per-chunk speculative PSS maps + exclusive scan */
+
+typedef struct ks_dfa_info {
+    int32_t n_states;        /* |Q| */
+    int32_t n_expressions;   /* ne */
+    int32_t n_accepting;     /* states with a non-empty output multiset */
+    int32_t strategy;        /* KS_STRATEGY_* */
+    int32_t sync_depth;      /* D for LOOKBACK, -1 otherwise */
+    int32_t stride;          /* bases per shared-memory table lookup (1..4) */
+    int32_t monoid_size;     /* |M| for MAPSCAN, 0 otherwise */
+    int32_t other_resets;    /* 1 if every state goes to one state on OTHER */
+    int64_t table_bytes;     /* bytes of the stride table staged per CTA */
+    int32_t tables_in_smem;  /* 1: staged in shared memory, 0: read through L1/L2 */
+    int32_t reserved;
+} ks_dfa_info;
+
+/* Per-call statistics of the last ks_count/ks_locate on a context. */
+typedef struct ks_stats {
+    float scan_ms;           /* device time of the dominant scan kernel(s)  */
+    float total_ms;          /* device time of the whole call (events)      */
+    int32_t kernel_launches; /* kernels launched by the call                */
+    int32_t chunks;          /* lane chunks in the main scan                */
+    int64_t chunk_len;       /* bases per lane chunk                        */
+    int64_t rows;            /* locate rows produced                        */
+} ks_stats;
+
+/* ---- context ------------------------------------------------------------ */
+/* Replaces the reference's ThreadPoolExecutor-per-call (engine.py:223-232). */
+KS_API int ks_open(int device, ks_ctx** out);
+KS_API int ks_close(ks_ctx* ctx);
+/* Use an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);
+ * NULL restores the context's own stream. */
+KS_API int ks_set_stream(ks_ctx* ctx, void* cuda_stream);
+KS_API int ks_synchronize(ks_ctx* ctx);
+KS_API int ks_get_stats(const ks_ctx* ctx, ks_stats* out);
+KS_API const char* ks_last_error(void);
+KS_API const char* ks_version(void);
+
+/* ---- automaton ---------------------------------------------------------- */
+/* Upload a Dfa (automaton.py:26-51 layout: transitions int32[nq][5] row-major,
+ * columns a,c,g,t,OTHER; CSR out_offsets int32[nq+1], out_ids int32[...]).
+ * Compiles the device form (renumbering, stride tables, synchronisation
+ * analysis) natively.  Replaces the table arguments of match_chunk_kernel /
+ * scan_from (_kernels.py:19,44). */
+KS_API int ks_dfa_upload(ks_ctx* ctx, const int32_t* transitions, int32_t n_states,
+                  const int32_t* out_offsets, const int32_t* out_ids,
+                  int32_t n_expressions, ks_dfa** out);
+/* Same, forcing a strategy (testing; KS_STRATEGY_* or 0 = automatic). */
+KS_API int ks_dfa_upload_ex(ks_ctx* ctx, const int32_t* transitions, int32_t n_states,
+                     const int32_t* out_offsets, const int32_t* out_ids,
+                     int32_t n_expressions, int32_t force_strategy, ks_dfa** out);
+KS_API int ks_dfa_info_get(const ks_dfa* dfa, ks_dfa_info* out);
+KS_API int ks_dfa_free(ks_dfa* dfa);
+
+/* ---- sequences ---------------------------------------------------------- */
+/* Symbol codes 0..4 (Sequence.symbols, ingest.py:20-32) -> packed device form. */
+KS_API int ks_seq_upload_codes(ks_ctx* ctx, const uint8_t* codes, int64_t n, ks_seq** out);
+/* Raw ASCII bytes -> device encode (alphabet.py:20-37 / ingest.py:67-69):
+ * case fold, whitespace (SP,TAB,CR,LF) dropped, every other byte OTHER.
+ * fasta != 0 additionally drops lines starting with '>' (ingest.py:65-66). */
+KS_API int ks_seq_upload_ascii(ks_ctx* ctx, const uint8_t* bytes, int64_t n_bytes,
+                        int32_t fasta, ks_seq** out);
+/* Same, input already resident in device memory (not copied, not retained). */
+KS_API int ks_seq_encode_device(ks_ctx* ctx, const uint8_t* d_bytes, int64_t n_bytes,
+                         int32_t fasta, ks_seq** out);
+KS_API int ks_seq_length(const ks_seq* seq, int64_t* n);
+/* Decode back to codes 0..4 (tests); out has room for n bytes. */
+KS_API int ks_seq_download_codes(ks_ctx* ctx, const ks_seq* seq, uint8_t* out);
+/* Soft-mask bitmap (bit i of word i/64 = base i was lowercase). */
+KS_API int ks_seq_download_softmask(ks_ctx* ctx, const ks_seq* seq, uint64_t* out, int64_t n_words);
+KS_API int ks_seq_free(ks_seq* seq);
+
+/* ---- scans -------------------------------------------------------------- */
+/* Per-expression counts over the whole sequence from the start state:
+ * the result of run(...).per_expression_counts (engine.py:207-237) and of
+ * sequential_count (oracle.py:56-61 -> scan_from, _kernels.py:19-29).
+ * counts_out: int64[n_expressions], caller-owned. */
+KS_API int ks_count(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t* counts_out);
+
+/* Counts plus match rows [exclusive end offset, expression id], sorted by
+ * (offset, id), duplicates kept (engine.py:165-176).  *rows_out is
+ * library-allocated (free with ks_free), int64[*n_rows][2]. */
+KS_API int ks_locate(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t* counts_out,
+              int64_t** rows_out, int64_t* n_rows);
+
+/* Range form used by match_chunk (engine.py:94-134) and by sharded scans:
+ * scan positions [begin, end) of seq entering at `entry_state` (original
+ * state id; -1 = the true state of the sequence at `begin`, derived on
+ * device).  Offsets in rows are seq positions + 1 + row_offset_base.
+ * exit_state (may be NULL) receives the original id of the final state.
+ * rows_out/n_rows may be NULL for count-only. */
+KS_API int ks_scan_range(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin,
+                  int64_t end, int32_t entry_state, int64_t row_offset_base,
+                  int64_t* counts_out, int32_t* exit_state, int64_t** rows_out,
+                  int64_t* n_rows);
+
+/* Boundary map of a segment (the per-GPU "start-state -> end-state map"):
+ * map_out[q] = original id of the state reached after scanning [begin,end)
+ * from original state q, for all q < n_states. */
+KS_API int ks_segment_map(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin,
+                   int64_t end, int32_t* map_out);
+
+/* Speculative-start convergence (match_chunk_kernel's speculative runs,
+ * _kernels.py:91-112): for chunk k, candidate start states
+ * pss_data[pss_off[k] .. pss_off[k+1]) (original ids; entry 0 is the full
+ * run R0) scan seq[chunk_begin[k] ..) for at most min(window, chunk length)
+ * steps; conv_out[i] = first step j where run i's state equals R0's, -1 if
+ * none (always -1 for R0).  Warp lanes are the speculative runs;
+ * convergence is detected with __match_any_sync.  delta_out (nullable,
+ * int64[total_runs][n_expressions]) receives per-run prefix-count
+ * corrections sum_{t<=conv} out(s_i(t)) - out(s_0(t)). */
+KS_API int ks_speculate(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int32_t n_chunks,
+                 const int64_t* chunk_begin, const int64_t* chunk_end,
+                 const int64_t* pss_off, const int32_t* pss_data, int32_t window,
+                 int32_t* conv_out, int64_t* delta_out);
+
+KS_API void ks_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KMERSCAN_B200_H */

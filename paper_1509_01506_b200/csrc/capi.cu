@@ -1,0 +1,869 @@
+// C ABI (include/kmerscan_b200.h) and the host orchestration of one scan.
+//
+// Strategy LOOKBACK (definite automata -- every Aho-Corasick table built by
+// build_dfa): one launch.  Each lane chunk derives its true entry state by
+// scanning the D bases before it; chunks are independent, so the reference's
+// PSS speculation + chain reduction (engine.py:80-91, 137-204) collapses to
+// nothing and the single HBM pass is the whole job.
+//
+// Strategy MAPSCAN (non-converging automata with a small transition monoid,
+// e.g. the BASELINE's 1024-state permutation DFA): pass 1 scans every chunk
+// with the monoid automaton (chunk -> its start->end map as an element id),
+// an exclusive device-wide scan composes the maps into each chunk's true
+// entry state, pass 2 counts.  Speculation can never converge there, and the
+// reference pays |Q| runs per chunk; this pays two passes.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "scan_kernels.cuh"
+
+namespace ks {
+
+thread_local std::string g_error;
+
+void set_error(const std::string& msg) { g_error = msg; }
+int fail(int code, const std::string& msg) {
+    g_error = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+    g_error = std::string("CUDA error: ") + cudaGetErrorString(e) + " (" + what + ")";
+    return KS_E_CUDA;
+}
+
+// encode.cu / spec.cu
+size_t encode_scratch_bytes(int64_t n_bytes);
+int encode_ascii_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, ks_seq* seq, void* scratch,
+                        int* launches);
+int pack_codes_device(ks_ctx* ctx, const uint8_t* d_codes, int64_t n, ks_seq* seq, int* d_flag,
+                      int* launches);
+int unpack_codes_device(ks_ctx* ctx, const ks_seq* seq, uint8_t* d_out);
+int launch_speculate(ks_ctx* ctx, const SeqView& seq, int32_t n_chunks, const int64_t* d_cbeg,
+                     const int64_t* d_cend, const int64_t* d_pss_off, const uint16_t* d_pss,
+                     const int64_t* h_pss_off, int32_t window, const uint16_t* t1, int32_t n_accept,
+                     const int32_t* off, const int32_t* ids, int32_t ne, int32_t* d_conv,
+                     long long* d_delta, void* d_tasks_buf, int* launches);
+size_t speculate_task_bytes(int32_t n_chunks, const int64_t* h_pss_off);
+
+namespace {
+
+constexpr size_t kAlign = 256;
+size_t up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
+
+// Bump allocator over the context's grow-only scratch buffer.
+struct Arena {
+    char* base = nullptr;
+    size_t off = 0;
+    size_t cap = 0;
+    void* take(size_t n) {
+        off = up(off);
+        void* p = base + off;
+        off += up(n ? n : 1);
+        return p;
+    }
+};
+
+int ensure_scratch(ks_ctx* ctx, size_t bytes, Arena* a) {
+    bytes = up(bytes) + 64 * kAlign;
+    if (ctx->scratch_bytes < bytes) {
+        KS_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (ctx->scratch) KS_CUDA(cudaFree(ctx->scratch));
+        ctx->scratch = nullptr;
+        ctx->scratch_bytes = 0;
+        KS_CUDA(cudaMalloc(&ctx->scratch, bytes));
+        ctx->scratch_bytes = bytes;
+    }
+    a->base = static_cast<char*>(ctx->scratch);
+    a->off = 0;
+    a->cap = ctx->scratch_bytes;
+    return KS_OK;
+}
+
+int ensure_pinned(ks_ctx* ctx, size_t bytes) {
+    if (ctx->pinned_bytes >= bytes) return KS_OK;
+    if (ctx->pinned) KS_CUDA(cudaFreeHost(ctx->pinned));
+    ctx->pinned = nullptr;
+    ctx->pinned_bytes = 0;
+    bytes = std::max<size_t>(bytes, 1 << 16);
+    KS_CUDA(cudaMallocHost(&ctx->pinned, bytes));
+    ctx->pinned_bytes = bytes;
+    return KS_OK;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// ------------------------------------------------------------ tiny kernels
+__global__ void walk_kernel(SeqView seq, int64_t begin, int64_t end, const uint16_t* t1, int32_t nq,
+                            int32_t uniform_start, uint16_t* out) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    uint32_t s = uniform_start >= 0 ? uint32_t(uniform_start) : uint32_t(q);
+    for (int64_t p = begin; p < end; ++p) {
+        const bool other = (seq.nmask[p >> 6] >> (p & 63)) & 1ull;
+        const uint32_t sym = other ? 4u : uint32_t(seq.bases[p >> 5] >> (2 * (p & 31))) & 3u;
+        s = t1[s * 5u + sym];
+    }
+    out[q] = uint16_t(s);
+}
+
+SeqView view_of(const ks_seq* s) {
+    SeqView v;
+    v.bases = s->d_bases;
+    v.nmask = s->d_nmask;
+    v.n = s->n;
+    return v;
+}
+
+ScanArgs base_args(const ks_dfa* dfa, const DevTable& T, const ks_seq* seq) {
+    ScanArgs a;
+    a.seq = view_of(seq);
+    a.t1 = T.t1;
+    a.tk = T.tk;
+    a.nq = T.nq;
+    a.n_accept = T.n_accept;
+    a.reset_state = T.reset_state;
+    a.tk_pad = int32_t(T.tk_bytes / 2);
+    a.t1_pad = int32_t(T.t1_bytes / 2);
+    a.acc_out_off = dfa->d_acc_out_off;
+    a.acc_out_ids = dfa->d_acc_out_ids;
+    a.acc_outcnt = dfa->d_acc_outcnt;
+    return a;
+}
+
+bool hist_fits(const ks_ctx* ctx, const ks_dfa* dfa) {
+    const size_t tables = dfa->tables_in_smem ? dfa->scan.tk_bytes + dfa->scan.t1_bytes : 0;
+    return tables + size_t(dfa->host.n_accept) * 4 + 1024 <= ctx->smem_optin;
+}
+
+// Map pass + monoid scan over [begin, end): writes per-chunk exclusive
+// prefixes (if excl != null) and the total element into *d_total.
+int monoid_prefix(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end,
+                  int64_t origin, int64_t L, int64_t nch, uint16_t* elems, uint16_t* excl,
+                  uint16_t* d_total, void* tmp, int* launches) {
+    const HostDfa& h = dfa->host;
+    ScanArgs m = base_args(dfa, dfa->mono, seq);
+    m.begin = begin;
+    m.end = end;
+    m.origin = origin;
+    m.chunk_len = L;
+    m.nchunks = nch;
+    m.uniform_entry = 0;  // identity element
+    m.n_accept = 0;
+    m.chunk_exit = elems;
+    int rc = launch_scan(ctx, m, kModeMap, dfa->mono.stride, dfa->tables_in_smem, launches);
+    if (rc != KS_OK) return rc;
+    return exclusive_scan_monoid(ctx, elems, nch, dfa->d_prod, h.nm, excl, d_total, tmp, launches);
+}
+
+// True internal state of the sequence at position pos (state after pos bases).
+int true_state_at(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t pos, int* out,
+                  int* launches) {
+    const HostDfa& h = dfa->host;
+    if (pos == 0) {
+        *out = h.start_internal;
+        return KS_OK;
+    }
+    Arena ar;
+    if (h.strategy == KS_STRATEGY_LOOKBACK) {
+        int rc = ensure_scratch(ctx, 4096, &ar);
+        if (rc) return rc;
+        uint16_t* d = static_cast<uint16_t*>(ar.take(16));
+        const int64_t lb = std::max<int64_t>(0, pos - h.sync_depth);
+        walk_kernel<<<1, 32, 0, ctx->stream>>>(view_of(seq), lb, pos, dfa->scan.t1, 1, h.start_internal, d);
+        if (launches) ++*launches;
+        KS_CUDA(cudaGetLastError());
+        uint16_t v = 0;
+        KS_CUDA(cudaMemcpyAsync(&v, d, 2, cudaMemcpyDeviceToHost, ctx->stream));
+        KS_CUDA(cudaStreamSynchronize(ctx->stream));
+        *out = v;
+        return KS_OK;
+    }
+    int64_t origin, L, nch;
+    scan_geometry(ctx, 0, pos, dfa->mono.stride, dfa->tables_in_smem, int32_t(dfa->mono.tk_bytes / 2),
+                  int32_t(dfa->mono.t1_bytes / 2), 0, &origin, &L, &nch);
+    int rc = ensure_scratch(ctx, size_t(nch) * 4 + exclusive_scan_monoid_tmp_bytes(nch) + 4096, &ar);
+    if (rc) return rc;
+    uint16_t* elems = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
+    uint16_t* excl = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
+    uint16_t* tot = static_cast<uint16_t*>(ar.take(16));
+    void* tmp = ar.take(exclusive_scan_monoid_tmp_bytes(nch));
+    rc = monoid_prefix(ctx, dfa, seq, 0, pos, origin, L, nch, elems, excl, tot, tmp, launches);
+    if (rc) return rc;
+    uint16_t m = 0;
+    KS_CUDA(cudaMemcpyAsync(&m, tot, 2, cudaMemcpyDeviceToHost, ctx->stream));
+    KS_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = h.act0[m];
+    return KS_OK;
+}
+
+int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end,
+              int32_t entry_orig, int64_t row_base, int64_t* counts_out, int32_t* exit_out,
+              int64_t** rows_out, int64_t* n_rows) {
+    if (!ctx || !dfa || !seq) return fail(KS_E_INVALID, "null handle");
+    if (dfa->ctx != ctx || seq->ctx != ctx) return fail(KS_E_INVALID, "handle belongs to another context");
+    const HostDfa& h = dfa->host;
+    if (begin < 0 || end < begin || end > seq->n) return fail(KS_E_INVALID, "scan range out of bounds");
+    if (entry_orig < -1 || entry_orig >= h.nq) return fail(KS_E_INVALID, "entry state out of range");
+    const bool locate = rows_out != nullptr;
+    if (locate && !n_rows) return fail(KS_E_INVALID, "n_rows is required with rows_out");
+    DeviceGuard guard(ctx->device);
+    ctx->stats = ks_stats{};
+    int launches = 0;
+    KS_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+
+    int entry = entry_orig >= 0 ? h.new_of_old[entry_orig] : -1;
+    if (entry < 0 && h.strategy == KS_STRATEGY_MAPSCAN) {
+        int rc = true_state_at(ctx, dfa, seq, begin, &entry, &launches);
+        if (rc) return rc;
+    }
+
+    int64_t origin, L, nch;
+    const bool hist_smem = hist_fits(ctx, dfa);
+    scan_geometry(ctx, begin, end, dfa->scan.stride, dfa->tables_in_smem, int32_t(dfa->scan.tk_bytes / 2),
+                  int32_t(dfa->scan.t1_bytes / 2), hist_smem ? h.n_accept : 0, &origin, &L, &nch);
+    if (end == begin) nch = 0;
+
+    const bool mapscan = h.strategy == KS_STRATEGY_MAPSCAN;
+    size_t need = size_t(h.n_accept) * 8 + size_t(std::max(h.ne, 1)) * 8 + size_t(nch) * 2 + 4096;
+    if (locate) need += size_t(nch) * 4 + size_t(nch + 1) * 8 + exclusive_scan_rows_tmp_bytes(nch) + 8 * kAlign;
+    if (mapscan) need += size_t(nch) * 6 + exclusive_scan_monoid_tmp_bytes(nch) + 4 * kAlign;
+    Arena ar;
+    int rc = ensure_scratch(ctx, need, &ar);
+    if (rc) return rc;
+    unsigned long long* visits = static_cast<unsigned long long*>(ar.take(size_t(h.n_accept) * 8));
+    unsigned long long* counts = static_cast<unsigned long long*>(ar.take(size_t(std::max(h.ne, 1)) * 8));
+    uint16_t* chunk_exit = static_cast<uint16_t*>(ar.take(size_t(nch) * 2 + 2));
+    int32_t* err = static_cast<int32_t*>(ar.take(16));
+    uint32_t* chunk_rows = nullptr;
+    int64_t* row_off = nullptr;
+    void* rows_tmp = nullptr;
+    if (locate) {
+        chunk_rows = static_cast<uint32_t*>(ar.take(size_t(nch) * 4));
+        row_off = static_cast<int64_t*>(ar.take(size_t(nch + 1) * 8));
+        rows_tmp = ar.take(exclusive_scan_rows_tmp_bytes(nch));
+    }
+    uint16_t *elems = nullptr, *excl = nullptr, *centry = nullptr, *mtot = nullptr;
+    void* mtmp = nullptr;
+    if (mapscan) {
+        elems = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
+        excl = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
+        centry = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
+        mtot = static_cast<uint16_t*>(ar.take(16));
+        mtmp = ar.take(exclusive_scan_monoid_tmp_bytes(nch));
+    }
+    if (h.n_accept > 0) KS_CUDA(cudaMemsetAsync(visits, 0, size_t(h.n_accept) * 8, ctx->stream));
+    KS_CUDA(cudaMemsetAsync(counts, 0, size_t(std::max(h.ne, 1)) * 8, ctx->stream));
+    KS_CUDA(cudaMemsetAsync(err, 0, 16, ctx->stream));
+
+    ScanArgs a = base_args(dfa, dfa->scan, seq);
+    a.begin = begin;
+    a.end = end;
+    a.origin = origin;
+    a.chunk_len = L;
+    a.nchunks = nch;
+    a.hist_smem = hist_smem ? 1 : 0;
+    a.visits = visits;
+    a.chunk_exit = chunk_exit;
+    a.error = err;
+    a.row_base = row_base;
+    if (h.strategy == KS_STRATEGY_LOOKBACK) {
+        a.lookback = h.sync_depth;
+        a.base_pos = entry >= 0 ? begin : 0;
+        a.base_state = entry >= 0 ? entry : h.start_internal;
+        a.any_state = h.start_internal;
+    }
+
+    KS_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
+    if (mapscan && nch > 0) {
+        rc = monoid_prefix(ctx, dfa, seq, begin, end, origin, L, nch, elems, excl, mtot, mtmp, &launches);
+        if (rc) return rc;
+        rc = launch_chunk_entry(ctx, excl, nch, dfa->d_action, h.nq, entry, centry, &launches);
+        if (rc) return rc;
+        a.chunk_entry = centry;
+    }
+    if (locate) a.chunk_rows = chunk_rows;
+    rc = launch_scan(ctx, a, locate ? kModeRows : kModeCount, dfa->scan.stride, dfa->tables_in_smem,
+                     &launches);
+    if (rc) return rc;
+    KS_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
+    rc = launch_finalize_counts(ctx, visits, h.n_accept, dfa->d_acc_out_off, dfa->d_acc_out_ids, counts,
+                                &launches);
+    if (rc) return rc;
+
+    int64_t total_rows = 0;
+    int64_t* d_rows = nullptr;
+    if (locate && nch > 0) {
+        rc = exclusive_scan_rows(ctx, chunk_rows, nch, row_off, row_off + nch, rows_tmp, &launches);
+        if (rc) return rc;
+        KS_CUDA(cudaMemcpyAsync(&total_rows, row_off + nch, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        KS_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (total_rows > 0) {
+            KS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_rows), size_t(total_rows) * 16, ctx->stream));
+            ScanArgs e = a;
+            e.chunk_rows = nullptr;
+            e.chunk_row_off = row_off;
+            e.rows = d_rows;
+            e.visits = nullptr;
+            e.hist_smem = 0;
+            rc = launch_scan(ctx, e, kModeEmit, dfa->scan.stride, dfa->tables_in_smem, &launches);
+            if (rc) {
+                cudaFreeAsync(d_rows, ctx->stream);
+                return rc;
+            }
+        }
+    }
+
+    // results
+    rc = ensure_pinned(ctx, size_t(std::max(h.ne, 1)) * 8 + 64);
+    if (rc) return rc;
+    char* pin = static_cast<char*>(ctx->pinned);
+    KS_CUDA(cudaMemcpyAsync(pin, counts, size_t(h.ne) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    KS_CUDA(cudaMemcpyAsync(pin + size_t(std::max(h.ne, 1)) * 8, err, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    uint16_t* pin_exit = reinterpret_cast<uint16_t*>(pin + size_t(std::max(h.ne, 1)) * 8 + 16);
+    if (nch > 0)
+        KS_CUDA(cudaMemcpyAsync(pin_exit, chunk_exit + (nch - 1), 2, cudaMemcpyDeviceToHost, ctx->stream));
+    int64_t* host_rows = nullptr;
+    if (locate) {
+        host_rows = static_cast<int64_t*>(std::malloc(size_t(std::max<int64_t>(total_rows, 1)) * 16));
+        if (!host_rows) {
+            if (d_rows) cudaFreeAsync(d_rows, ctx->stream);
+            return fail(KS_E_NOMEM, "host allocation of match rows failed");
+        }
+        if (total_rows > 0) {
+            cudaError_t ce = cudaMemcpyAsync(host_rows, d_rows, size_t(total_rows) * 16,
+                                             cudaMemcpyDeviceToHost, ctx->stream);
+            if (ce != cudaSuccess) {
+                std::free(host_rows);
+                cudaFreeAsync(d_rows, ctx->stream);
+                return cuda_fail(ce, "rows D2H");
+            }
+        }
+        if (d_rows) cudaFreeAsync(d_rows, ctx->stream);
+    }
+    KS_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
+    cudaError_t se = cudaStreamSynchronize(ctx->stream);
+    if (se != cudaSuccess) {
+        std::free(host_rows);
+        return cuda_fail(se, "scan");
+    }
+    const int32_t err_flag = *reinterpret_cast<int32_t*>(pin + size_t(std::max(h.ne, 1)) * 8);
+    if (err_flag) {
+        std::free(host_rows);
+        return fail(KS_E_CHAIN, "internal invariant failed: chunk row count mismatch");
+    }
+    std::memcpy(counts_out, pin, size_t(h.ne) * 8);
+    if (exit_out) {
+        int ex;
+        if (nch > 0) ex = *pin_exit;
+        else if (entry >= 0) ex = entry;
+        else {
+            rc = true_state_at(ctx, dfa, seq, begin, &ex, &launches);
+            if (rc) {
+                std::free(host_rows);
+                return rc;
+            }
+        }
+        *exit_out = h.old_of_new[ex];
+    }
+    if (locate) {
+        *rows_out = host_rows;
+        *n_rows = total_rows;
+    }
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]);
+    ctx->stats.scan_ms = ms;
+    cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[3]);
+    ctx->stats.total_ms = ms;
+    ctx->stats.kernel_launches = launches;
+    ctx->stats.chunks = int32_t(nch);
+    ctx->stats.chunk_len = L;
+    ctx->stats.rows = total_rows;
+    return KS_OK;
+}
+
+int upload_table(const CompiledTable& t, DevTable* d, char* blob, size_t* off, bool dry) {
+    auto place = [&](const void* src, size_t bytes) -> char* {
+        *off = up(*off);
+        char* p = blob + *off;
+        if (!dry && bytes) std::memcpy(p, src, bytes);
+        *off += align16(bytes) + 16;
+        return p;
+    };
+    d->nq = t.nq;
+    d->n_accept = t.n_accept;
+    d->stride = t.stride;
+    d->reset_state = t.reset_state;
+    d->tk_bytes = align16(t.tk.size() * 2);
+    d->t1_bytes = align16(t.t1.size() * 2);
+    d->tk = reinterpret_cast<const uint16_t*>(place(t.tk.data(), t.tk.size() * 2));
+    d->t1 = reinterpret_cast<const uint16_t*>(place(t.t1.data(), t.t1.size() * 2));
+    return KS_OK;
+}
+
+int seq_alloc(ks_ctx* ctx, int64_t n_capacity, ks_seq** out) {
+    ks_seq* s = new ks_seq();
+    s->ctx = ctx;
+    s->n_blocks = (n_capacity + 63) / 64 + 2;
+    const size_t bytes = size_t(s->n_blocks) * 32;
+    cudaError_t e = cudaMalloc(&s->d_blob, bytes);
+    if (e != cudaSuccess) {
+        delete s;
+        return cuda_fail(e, "cudaMalloc(sequence)");
+    }
+    char* p = static_cast<char*>(s->d_blob);
+    s->d_bases = reinterpret_cast<uint64_t*>(p);
+    s->d_nmask = reinterpret_cast<uint64_t*>(p + size_t(s->n_blocks) * 16);
+    s->d_soft = reinterpret_cast<uint64_t*>(p + size_t(s->n_blocks) * 24);
+    e = cudaMemsetAsync(s->d_blob, 0, bytes, ctx->stream);
+    if (e != cudaSuccess) {
+        cudaFree(s->d_blob);
+        delete s;
+        return cuda_fail(e, "cudaMemset(sequence)");
+    }
+    *out = s;
+    return KS_OK;
+}
+
+void seq_destroy(ks_seq* s) {
+    if (!s) return;
+    if (s->d_blob) cudaFree(s->d_blob);
+    delete s;
+}
+
+}  // namespace
+}  // namespace ks
+
+using namespace ks;
+
+extern "C" {
+
+const char* ks_last_error(void) { return g_error.c_str(); }
+const char* ks_version(void) { return "kmerscan_b200 0.1 (sm_100a)"; }
+void ks_free(void* p) { std::free(p); }
+
+int ks_open(int device, ks_ctx** out) {
+    if (!out) return fail(KS_E_INVALID, "out is null");
+    int n = 0;
+    KS_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) return fail(KS_E_INVALID, "no such CUDA device");
+    KS_CUDA(cudaSetDevice(device));
+    ks_ctx* c = new ks_ctx();
+    c->device = device;
+    cudaDeviceProp prop;
+    cudaError_t e = cudaGetDeviceProperties(&prop, device);
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_fail(e, "cudaGetDeviceProperties");
+    }
+    if (prop.major < 10) {
+        delete c;
+        return fail(KS_E_UNSUPPORTED, "kmerscan_b200 requires an sm_100 (Blackwell) device");
+    }
+    c->num_sms = prop.multiProcessorCount;
+    c->smem_optin = prop.sharedMemPerBlockOptin;
+    e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_fail(e, "cudaStreamCreate");
+    }
+    c->stream = c->own_stream;
+    for (auto& ev : c->ev) cudaEventCreate(&ev);
+    *out = c;
+    return KS_OK;
+}
+
+int ks_close(ks_ctx* ctx) {
+    if (!ctx) return KS_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->scratch) cudaFree(ctx->scratch);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    for (auto& ev : ctx->ev)
+        if (ev) cudaEventDestroy(ev);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+    return KS_OK;
+}
+
+int ks_set_stream(ks_ctx* ctx, void* stream) {
+    if (!ctx) return fail(KS_E_INVALID, "null context");
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    return KS_OK;
+}
+
+int ks_synchronize(ks_ctx* ctx) {
+    if (!ctx) return fail(KS_E_INVALID, "null context");
+    KS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return KS_OK;
+}
+
+int ks_get_stats(const ks_ctx* ctx, ks_stats* out) {
+    if (!ctx || !out) return fail(KS_E_INVALID, "null argument");
+    *out = ctx->stats;
+    return KS_OK;
+}
+
+int ks_dfa_upload_ex(ks_ctx* ctx, const int32_t* transitions, int32_t n_states, const int32_t* out_offsets,
+                     const int32_t* out_ids, int32_t n_expressions, int32_t force_strategy, ks_dfa** out) {
+    if (!ctx || !out) return fail(KS_E_INVALID, "null argument");
+    DeviceGuard guard(ctx->device);
+    ks_dfa* d = new ks_dfa();
+    d->ctx = ctx;
+    const size_t budget = ctx->smem_optin > 2048 ? ctx->smem_optin - 2048 : 0;
+    int rc = compile_dfa(transitions, n_states, out_offsets, out_ids, n_expressions, force_strategy, budget,
+                         &d->host);
+    if (rc != KS_OK) {
+        delete d;
+        return rc;
+    }
+    const HostDfa& h = d->host;
+    // one blob: tables, CSR, monoid tables
+    auto layout = [&](char* blob, bool dry) -> size_t {
+        size_t off = 0;
+        upload_table(h.scan, &d->scan, blob, &off, dry);
+        auto place = [&](const void* src, size_t bytes) -> char* {
+            off = up(off);
+            char* p = blob + off;
+            if (!dry && bytes) std::memcpy(p, src, bytes);
+            off += align16(bytes) + 16;
+            return p;
+        };
+        d->d_acc_out_off = reinterpret_cast<int32_t*>(place(h.acc_out_off.data(), h.acc_out_off.size() * 4));
+        d->d_acc_out_ids = reinterpret_cast<int32_t*>(place(h.acc_out_ids.data(), h.acc_out_ids.size() * 4));
+        d->d_acc_outcnt = reinterpret_cast<uint16_t*>(place(h.acc_outcnt.data(), h.acc_outcnt.size() * 2));
+        if (h.strategy == KS_STRATEGY_MAPSCAN) {
+            upload_table(h.mono, &d->mono, blob, &off, dry);
+            d->d_prod = reinterpret_cast<uint16_t*>(place(h.prod.data(), h.prod.size() * 2));
+            d->d_act0 = reinterpret_cast<uint16_t*>(place(h.act0.data(), h.act0.size() * 2));
+            d->d_action = reinterpret_cast<uint16_t*>(place(h.action.data(), h.action.size() * 2));
+        }
+        return up(off);
+    };
+    const size_t bytes = layout(nullptr, true);
+    std::vector<char> host(bytes, 0);
+    layout(host.data(), false);
+    cudaError_t e = cudaMalloc(&d->d_blob, bytes);
+    if (e != cudaSuccess) {
+        delete d;
+        return cuda_fail(e, "cudaMalloc(dfa)");
+    }
+    e = cudaMemcpy(d->d_blob, host.data(), bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(d->d_blob);
+        delete d;
+        return cuda_fail(e, "cudaMemcpy(dfa)");
+    }
+    // rebase host-blob pointers onto the device blob
+    const ptrdiff_t delta = static_cast<char*>(d->d_blob) - host.data();
+    auto rebase = [&](auto*& p) {
+        using Ptr = std::remove_reference_t<decltype(p)>;
+        if (p) p = (Ptr)((const char*)p + delta);
+    };
+    rebase(d->scan.tk);
+    rebase(d->scan.t1);
+    rebase(d->d_acc_out_off);
+    rebase(d->d_acc_out_ids);
+    rebase(d->d_acc_outcnt);
+    if (h.strategy == KS_STRATEGY_MAPSCAN) {
+        rebase(d->mono.tk);
+        rebase(d->mono.t1);
+        rebase(d->d_prod);
+        rebase(d->d_act0);
+        rebase(d->d_action);
+    }
+    const size_t smem_scan = d->scan.tk_bytes + d->scan.t1_bytes;
+    const size_t smem_mono = h.strategy == KS_STRATEGY_MAPSCAN ? d->mono.tk_bytes + d->mono.t1_bytes : 0;
+    d->tables_in_smem = std::max(smem_scan, smem_mono) + 1024 <= ctx->smem_optin;
+    if (const char* g = std::getenv("KS_FORCE_GLOBAL_TABLES"); g && *g == '1') d->tables_in_smem = false;
+    *out = d;
+    return KS_OK;
+}
+
+int ks_dfa_upload(ks_ctx* ctx, const int32_t* transitions, int32_t n_states, const int32_t* out_offsets,
+                  const int32_t* out_ids, int32_t n_expressions, ks_dfa** out) {
+    return ks_dfa_upload_ex(ctx, transitions, n_states, out_offsets, out_ids, n_expressions, 0, out);
+}
+
+int ks_dfa_info_get(const ks_dfa* d, ks_dfa_info* out) {
+    if (!d || !out) return fail(KS_E_INVALID, "null argument");
+    const HostDfa& h = d->host;
+    out->n_states = h.nq;
+    out->n_expressions = h.ne;
+    out->n_accepting = h.n_accept;
+    out->strategy = h.strategy;
+    out->sync_depth = h.strategy == KS_STRATEGY_LOOKBACK ? h.sync_depth : -1;
+    out->stride = h.scan.stride;
+    out->monoid_size = h.strategy == KS_STRATEGY_MAPSCAN ? h.nm : 0;
+    out->other_resets = h.scan.reset_state >= 0 ? 1 : 0;
+    out->table_bytes = int64_t(d->scan.tk_bytes + d->scan.t1_bytes);
+    out->tables_in_smem = d->tables_in_smem ? 1 : 0;
+    out->reserved = 0;
+    return KS_OK;
+}
+
+int ks_dfa_free(ks_dfa* d) {
+    if (!d) return KS_OK;
+    DeviceGuard guard(d->ctx->device);
+    if (d->d_blob) cudaFree(d->d_blob);
+    delete d;
+    return KS_OK;
+}
+
+int ks_seq_upload_codes(ks_ctx* ctx, const uint8_t* codes, int64_t n, ks_seq** out) {
+    if (!ctx || !out || n < 0 || (n > 0 && !codes)) return fail(KS_E_INVALID, "bad argument");
+    DeviceGuard guard(ctx->device);
+    ks_seq* s = nullptr;
+    int rc = seq_alloc(ctx, n, &s);
+    if (rc) return rc;
+    Arena ar;
+    rc = ensure_scratch(ctx, size_t(n) + 1024, &ar);
+    if (rc) {
+        seq_destroy(s);
+        return rc;
+    }
+    uint8_t* d_codes = static_cast<uint8_t*>(ar.take(size_t((n + 63) / 64 * 64) + 64));
+    int* flag = static_cast<int*>(ar.take(16));
+    int launches = 0;
+    cudaError_t e = cudaMemsetAsync(flag, 0, 16, ctx->stream);
+    if (e == cudaSuccess && n > 0) e = cudaMemcpyAsync(d_codes, codes, size_t(n), cudaMemcpyHostToDevice, ctx->stream);
+    if (e != cudaSuccess) {
+        seq_destroy(s);
+        return cuda_fail(e, "sequence upload");
+    }
+    rc = pack_codes_device(ctx, d_codes, n, s, flag, &launches);
+    int bad = 0;
+    if (rc == KS_OK) {
+        e = cudaMemcpyAsync(&bad, flag, 4, cudaMemcpyDeviceToHost, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) rc = cuda_fail(e, "pack codes");
+    }
+    if (rc == KS_OK && bad) rc = fail(KS_E_INVALID, "symbol code out of range (expected 0..4)");
+    if (rc) {
+        seq_destroy(s);
+        return rc;
+    }
+    *out = s;
+    return KS_OK;
+}
+
+static int encode_common(ks_ctx* ctx, const uint8_t* d_bytes, int64_t n_bytes, int32_t fasta, ks_seq** out) {
+    if (fasta)
+        return fail(KS_E_UNSUPPORTED, "device FASTA header removal is not implemented; strip headers on the host");
+    ks_seq* s = nullptr;
+    int rc = seq_alloc(ctx, n_bytes, &s);
+    if (rc) return rc;
+    Arena ar;
+    const size_t staged = d_bytes ? 0 : 0;
+    (void)staged;
+    rc = ensure_scratch(ctx, encode_scratch_bytes(n_bytes) + 4096, &ar);
+    if (rc) {
+        seq_destroy(s);
+        return rc;
+    }
+    int launches = 0;
+    rc = encode_ascii_device(ctx, d_bytes, n_bytes, s, ar.take(encode_scratch_bytes(n_bytes)), &launches);
+    if (rc) {
+        seq_destroy(s);
+        return rc;
+    }
+    *out = s;
+    return KS_OK;
+}
+
+int ks_seq_encode_device(ks_ctx* ctx, const uint8_t* d_bytes, int64_t n_bytes, int32_t fasta, ks_seq** out) {
+    if (!ctx || !out || n_bytes < 0 || (n_bytes > 0 && !d_bytes)) return fail(KS_E_INVALID, "bad argument");
+    DeviceGuard guard(ctx->device);
+    return encode_common(ctx, d_bytes, n_bytes, fasta, out);
+}
+
+int ks_seq_upload_ascii(ks_ctx* ctx, const uint8_t* bytes, int64_t n_bytes, int32_t fasta, ks_seq** out) {
+    if (!ctx || !out || n_bytes < 0 || (n_bytes > 0 && !bytes)) return fail(KS_E_INVALID, "bad argument");
+    DeviceGuard guard(ctx->device);
+    if (fasta)
+        return fail(KS_E_UNSUPPORTED, "device FASTA header removal is not implemented; strip headers on the host");
+    uint8_t* d_in = nullptr;
+    KS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_in), size_t(n_bytes) + 64, ctx->stream));
+    cudaError_t e = n_bytes ? cudaMemcpyAsync(d_in, bytes, size_t(n_bytes), cudaMemcpyHostToDevice, ctx->stream)
+                            : cudaSuccess;
+    int rc = e == cudaSuccess ? encode_common(ctx, d_in, n_bytes, 0, out) : cuda_fail(e, "ascii upload");
+    cudaFreeAsync(d_in, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    return rc;
+}
+
+int ks_seq_length(const ks_seq* s, int64_t* n) {
+    if (!s || !n) return fail(KS_E_INVALID, "null argument");
+    *n = s->n;
+    return KS_OK;
+}
+
+int ks_seq_download_codes(ks_ctx* ctx, const ks_seq* s, uint8_t* out) {
+    if (!ctx || !s || (s->n > 0 && !out)) return fail(KS_E_INVALID, "null argument");
+    DeviceGuard guard(ctx->device);
+    Arena ar;
+    int rc = ensure_scratch(ctx, size_t(s->n) + 256, &ar);
+    if (rc) return rc;
+    uint8_t* d = static_cast<uint8_t*>(ar.take(size_t(s->n) + 16));
+    rc = unpack_codes_device(ctx, s, d);
+    if (rc) return rc;
+    if (s->n) KS_CUDA(cudaMemcpyAsync(out, d, size_t(s->n), cudaMemcpyDeviceToHost, ctx->stream));
+    KS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return KS_OK;
+}
+
+int ks_seq_download_softmask(ks_ctx* ctx, const ks_seq* s, uint64_t* out, int64_t n_words) {
+    if (!ctx || !s || !out) return fail(KS_E_INVALID, "null argument");
+    DeviceGuard guard(ctx->device);
+    const int64_t have = (s->n + 63) / 64;
+    if (n_words < have) return fail(KS_E_INVALID, "softmask buffer too small");
+    if (have) KS_CUDA(cudaMemcpyAsync(out, s->d_soft, size_t(have) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    KS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return KS_OK;
+}
+
+int ks_seq_free(ks_seq* s) {
+    if (!s) return KS_OK;
+    DeviceGuard guard(s->ctx->device);
+    cudaStreamSynchronize(s->ctx->stream);
+    seq_destroy(s);
+    return KS_OK;
+}
+
+int ks_count(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t* counts_out) {
+    if (!counts_out) return fail(KS_E_INVALID, "counts_out is null");
+    return scan_impl(ctx, dfa, seq, 0, seq ? seq->n : 0, -1, 0, counts_out, nullptr, nullptr, nullptr);
+}
+
+int ks_locate(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t* counts_out, int64_t** rows_out,
+              int64_t* n_rows) {
+    if (!counts_out || !rows_out || !n_rows) return fail(KS_E_INVALID, "null output");
+    return scan_impl(ctx, dfa, seq, 0, seq ? seq->n : 0, -1, 0, counts_out, nullptr, rows_out, n_rows);
+}
+
+int ks_scan_range(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end,
+                  int32_t entry_state, int64_t row_offset_base, int64_t* counts_out, int32_t* exit_state,
+                  int64_t** rows_out, int64_t* n_rows) {
+    if (!counts_out) return fail(KS_E_INVALID, "counts_out is null");
+    return scan_impl(ctx, dfa, seq, begin, end, entry_state, row_offset_base, counts_out, exit_state, rows_out,
+                     n_rows);
+}
+
+int ks_segment_map(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end,
+                   int32_t* map_out) {
+    if (!ctx || !dfa || !seq || !map_out) return fail(KS_E_INVALID, "null argument");
+    if (begin < 0 || end < begin || end > seq->n) return fail(KS_E_INVALID, "segment out of bounds");
+    DeviceGuard guard(ctx->device);
+    const HostDfa& h = dfa->host;
+    std::vector<uint16_t> img(h.nq);
+    int launches = 0;
+    if (h.strategy == KS_STRATEGY_LOOKBACK) {
+        Arena ar;
+        int rc = ensure_scratch(ctx, size_t(h.nq) * 2 + 1024, &ar);
+        if (rc) return rc;
+        uint16_t* d = static_cast<uint16_t*>(ar.take(size_t(h.nq) * 2));
+        if (end - begin >= h.sync_depth) {
+            walk_kernel<<<1, 32, 0, ctx->stream>>>(view_of(seq), end - h.sync_depth, end, dfa->scan.t1, 1,
+                                                     h.start_internal, d);
+            KS_CUDA(cudaGetLastError());
+            uint16_t v = 0;
+            KS_CUDA(cudaMemcpyAsync(&v, d, 2, cudaMemcpyDeviceToHost, ctx->stream));
+            KS_CUDA(cudaStreamSynchronize(ctx->stream));
+            std::fill(img.begin(), img.end(), v);
+        } else {
+            walk_kernel<<<(h.nq + 127) / 128, 128, 0, ctx->stream>>>(view_of(seq), begin, end, dfa->scan.t1,
+                                                                       h.nq, -1, d);
+            KS_CUDA(cudaGetLastError());
+            KS_CUDA(cudaMemcpyAsync(img.data(), d, size_t(h.nq) * 2, cudaMemcpyDeviceToHost, ctx->stream));
+            KS_CUDA(cudaStreamSynchronize(ctx->stream));
+        }
+    } else {
+        int64_t origin, L, nch;
+        scan_geometry(ctx, begin, end, dfa->mono.stride, dfa->tables_in_smem, int32_t(dfa->mono.tk_bytes / 2),
+                      int32_t(dfa->mono.t1_bytes / 2), 0, &origin, &L, &nch);
+        uint16_t m = 0;
+        if (end > begin) {
+            Arena ar;
+            int rc = ensure_scratch(ctx, size_t(nch) * 4 + exclusive_scan_monoid_tmp_bytes(nch) + 4096, &ar);
+            if (rc) return rc;
+            uint16_t* elems = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
+            uint16_t* excl = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
+            uint16_t* tot = static_cast<uint16_t*>(ar.take(16));
+            void* tmp = ar.take(exclusive_scan_monoid_tmp_bytes(nch));
+            rc = monoid_prefix(ctx, dfa, seq, begin, end, origin, L, nch, elems, excl, tot, tmp, &launches);
+            if (rc) return rc;
+            KS_CUDA(cudaMemcpyAsync(&m, tot, 2, cudaMemcpyDeviceToHost, ctx->stream));
+            KS_CUDA(cudaStreamSynchronize(ctx->stream));
+        }
+        for (int q = 0; q < h.nq; ++q) img[q] = h.action[size_t(m) * h.nq + q];
+    }
+    for (int q = 0; q < h.nq; ++q) map_out[q] = h.old_of_new[img[h.new_of_old[q]]];
+    return KS_OK;
+}
+
+int ks_speculate(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int32_t n_chunks, const int64_t* chunk_begin,
+                 const int64_t* chunk_end, const int64_t* pss_off, const int32_t* pss_data, int32_t window,
+                 int32_t* conv_out, int64_t* delta_out) {
+    if (!ctx || !dfa || !seq || n_chunks < 0 || window < 0) return fail(KS_E_INVALID, "bad argument");
+    if (n_chunks == 0) return KS_OK;
+    if (!chunk_begin || !chunk_end || !pss_off || !conv_out) return fail(KS_E_INVALID, "null argument");
+    DeviceGuard guard(ctx->device);
+    const HostDfa& h = dfa->host;
+    if (pss_off[0] != 0) return fail(KS_E_INVALID, "pss_off[0] must be 0");
+    for (int32_t k = 0; k < n_chunks; ++k) {
+        if (pss_off[k + 1] < pss_off[k]) return fail(KS_E_INVALID, "pss_off not monotone");
+        if (chunk_begin[k] < 0 || chunk_end[k] < chunk_begin[k] || chunk_end[k] > seq->n)
+            return fail(KS_E_INVALID, "chunk out of bounds");
+    }
+    const int64_t total = pss_off[n_chunks];
+    std::vector<uint16_t> pss(size_t(std::max<int64_t>(total, 1)));
+    for (int64_t i = 0; i < total; ++i) {
+        if (pss_data[i] < 0 || pss_data[i] >= h.nq) return fail(KS_E_INVALID, "pss state out of range");
+        pss[i] = uint16_t(h.new_of_old[pss_data[i]]);
+    }
+    const size_t task_bytes = speculate_task_bytes(n_chunks, pss_off);
+    const size_t delta_bytes = delta_out ? size_t(total) * size_t(std::max(h.ne, 1)) * 8 : 0;
+    Arena ar;
+    int rc = ensure_scratch(ctx, size_t(n_chunks) * 16 + size_t(n_chunks + 1) * 8 + size_t(total) * 6 +
+                                     task_bytes + delta_bytes + 16 * 1024,
+                            &ar);
+    if (rc) return rc;
+    int64_t* d_cb = static_cast<int64_t*>(ar.take(size_t(n_chunks) * 8));
+    int64_t* d_ce = static_cast<int64_t*>(ar.take(size_t(n_chunks) * 8));
+    int64_t* d_off = static_cast<int64_t*>(ar.take(size_t(n_chunks + 1) * 8));
+    uint16_t* d_pss = static_cast<uint16_t*>(ar.take(size_t(total) * 2 + 2));
+    int32_t* d_conv = static_cast<int32_t*>(ar.take(size_t(total) * 4 + 4));
+    void* d_tasks = ar.take(task_bytes);
+    long long* d_delta = delta_out ? static_cast<long long*>(ar.take(delta_bytes)) : nullptr;
+    KS_CUDA(cudaMemcpyAsync(d_cb, chunk_begin, size_t(n_chunks) * 8, cudaMemcpyHostToDevice, ctx->stream));
+    KS_CUDA(cudaMemcpyAsync(d_ce, chunk_end, size_t(n_chunks) * 8, cudaMemcpyHostToDevice, ctx->stream));
+    KS_CUDA(cudaMemcpyAsync(d_off, pss_off, size_t(n_chunks + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
+    KS_CUDA(cudaMemcpyAsync(d_pss, pss.data(), size_t(total) * 2, cudaMemcpyHostToDevice, ctx->stream));
+    if (d_delta) KS_CUDA(cudaMemsetAsync(d_delta, 0, delta_bytes, ctx->stream));
+    int launches = 0;
+    rc = launch_speculate(ctx, view_of(seq), n_chunks, d_cb, d_ce, d_off, d_pss, pss_off, window, dfa->scan.t1,
+                          h.n_accept, dfa->d_acc_out_off, dfa->d_acc_out_ids, h.ne, d_conv, d_delta, d_tasks,
+                          &launches);
+    if (rc) return rc;
+    KS_CUDA(cudaMemcpyAsync(conv_out, d_conv, size_t(total) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (d_delta) KS_CUDA(cudaMemcpyAsync(delta_out, d_delta, delta_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    KS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return KS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,243 @@
+// Host-side compilation of a reference Dfa into its device form.
+//
+// Input layout is the reference's (automaton.py:26-51): transitions
+// int32[nq][5] (a,c,g,t,OTHER), CSR output multisets.  Output (HostDfa):
+//   * renumbering: accepting states first, so the device hit test is
+//     `state < n_accept` instead of two out_offsets loads per symbol
+//     (the reference's inner CSR loop, _kernels.py:26-28);
+//   * K-symbol stride table: one uint16 load advances K bases; bit 15 flags
+//     "some state entered on this K-step has outputs";
+//   * synchronisation depth D: the smallest k such that every k-symbol word
+//     maps all states to one state.  For Aho-Corasick tables with OTHER ->
+//     START, D <= longest literal.  With D known, the true state at any
+//     position is the state reached by scanning the D preceding symbols from
+//     any state -- no speculation, no cross-chunk dependency;
+//   * otherwise the transition monoid (closure of the 5 column maps) when it
+//     is small: chunk maps become monoid element ids, composed by a
+//     product-table lookup in an exclusive device-wide scan.
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <unordered_map>
+#include <unordered_set>
+
+#include "ks_internal.h"
+
+namespace ks {
+namespace {
+
+struct VecHash {
+    size_t operator()(const std::vector<uint16_t>& v) const noexcept {
+        uint64_t h = 1469598103934665603ull ^ v.size();
+        for (uint16_t x : v) h = (h ^ x) * 1099511628211ull;
+        return static_cast<size_t>(h);
+    }
+};
+
+int stride_for(int nq, size_t budget) {
+    const char* force = std::getenv("KS_FORCE_STRIDE");
+    if (force && *force) {
+        int k = std::atoi(force);
+        if (k >= 1 && k <= 4) return k;
+    }
+    for (int k = 4; k >= 1; --k) {
+        size_t bytes = size_t(nq) * (size_t(1) << (2 * k)) * 2 + size_t(nq) * 5 * 2;
+        if (bytes <= budget) return k;
+    }
+    return 1;
+}
+
+void build_stride_table(CompiledTable* t, size_t budget) {
+    const int nq = t->nq;
+    const int k = stride_for(nq, budget);
+    t->stride = k;
+    const int words = 1 << (2 * k);
+    t->tk.assign(size_t(nq) * words, 0);
+    for (int s = 0; s < nq; ++s) {
+        for (int w = 0; w < words; ++w) {
+            int x = s;
+            bool hit = false;
+            for (int i = 0; i < k; ++i) {
+                x = t->t1[size_t(x) * 5 + ((w >> (2 * i)) & 3)];
+                hit |= x < t->n_accept;
+            }
+            t->tk[size_t(s) * words + w] = uint16_t(x | (hit ? kFlag : 0));
+        }
+    }
+    const uint16_t r = t->t1[4];
+    bool resets = true;
+    for (int s = 1; s < nq && resets; ++s) resets = t->t1[size_t(s) * 5 + 4] == r;
+    t->reset_state = resets ? int(r) : -1;
+}
+
+// Smallest D with |delta(Q, w)| == 1 for all |w| == D, or -1.
+int synchronisation_depth(const std::vector<uint16_t>& t1, int nq) {
+    if (nq <= 1) return 0;
+    std::vector<std::vector<uint16_t>> level(1);
+    level[0].resize(nq);
+    std::iota(level[0].begin(), level[0].end(), uint16_t(0));
+    std::vector<uint32_t> stamp(nq, 0);
+    uint32_t tick = 0;
+    int64_t work = 0;
+    const int64_t budget = 200000000;
+    std::vector<uint16_t> img;
+    for (int k = 0; k < kMaxSyncDepth; ++k) {
+        std::unordered_set<std::vector<uint16_t>, VecHash> next;
+        for (const auto& set : level) {
+            for (int c = 0; c < 5; ++c) {
+                ++tick;
+                img.clear();
+                for (uint16_t q : set) {
+                    uint16_t x = t1[size_t(q) * 5 + c];
+                    if (stamp[x] != tick) {
+                        stamp[x] = tick;
+                        img.push_back(x);
+                    }
+                }
+                work += int64_t(set.size());
+                if (img.size() > 1) {
+                    std::sort(img.begin(), img.end());
+                    next.insert(img);
+                }
+            }
+            if (work > budget) return -1;
+        }
+        if (next.empty()) return k + 1;
+        level.assign(next.begin(), next.end());
+    }
+    return -1;
+}
+
+// Closure of the column maps; false if it exceeds the caps.
+bool build_monoid(const CompiledTable& t, int start, HostDfa* h) {
+    const int nq = t.nq;
+    const size_t cap_entries = size_t(16) << 20;
+    std::vector<uint16_t> maps(nq);
+    std::iota(maps.begin(), maps.end(), uint16_t(0));
+    std::vector<int32_t> parent{-1}, psym{-1};
+    std::unordered_map<std::string, int> ids;
+    auto key_of = [&](const uint16_t* m) {
+        return std::string(reinterpret_cast<const char*>(m), size_t(nq) * 2);
+    };
+    ids.emplace(key_of(maps.data()), 0);
+    std::vector<int32_t> mt;  // nm x 5
+    std::vector<uint16_t> next(nq);
+    for (size_t m = 0; m < parent.size(); ++m) {
+        for (int c = 0; c < 5; ++c) {
+            const uint16_t* src = &maps[m * nq];
+            for (int q = 0; q < nq; ++q) next[q] = t.t1[size_t(src[q]) * 5 + c];
+            auto key = key_of(next.data());
+            auto it = ids.find(key);
+            int id;
+            if (it == ids.end()) {
+                id = int(parent.size());
+                if (id >= kMaxMonoid || size_t(id + 1) * nq > cap_entries) return false;
+                ids.emplace(std::move(key), id);
+                maps.insert(maps.end(), next.begin(), next.end());
+                parent.push_back(int32_t(m));
+                psym.push_back(c);
+            } else {
+                id = it->second;
+            }
+            mt.push_back(id);
+        }
+    }
+    const int nm = int(parent.size());
+    h->nm = nm;
+    h->mono.nq = nm;
+    h->mono.n_accept = 0;
+    h->mono.t1.resize(size_t(nm) * 5);
+    for (size_t i = 0; i < mt.size(); ++i) h->mono.t1[i] = uint16_t(mt[i]);
+    h->prod.assign(size_t(nm) * nm, 0);
+    for (int a = 0; a < nm; ++a) {
+        uint16_t* row = &h->prod[size_t(a) * nm];
+        row[0] = uint16_t(a);
+        for (int b = 1; b < nm; ++b)  // parents precede children in BFS order
+            row[b] = uint16_t(mt[size_t(row[parent[b]]) * 5 + psym[b]]);
+    }
+    h->act0.resize(nm);
+    for (int m = 0; m < nm; ++m) h->act0[m] = maps[size_t(m) * nq + start];
+    h->action = std::move(maps);
+    return true;
+}
+
+}  // namespace
+
+int compile_dfa(const int32_t* trans, int nq, const int32_t* out_off, const int32_t* out_ids,
+                int ne, int force_strategy, size_t smem_budget, HostDfa* h) {
+    if (!trans || !out_off || nq < 1) return fail(KS_E_INVALID, "dfa: empty transition table");
+    if (nq > kMaxStates)
+        return fail(KS_E_UNSUPPORTED, "dfa: " + std::to_string(nq) +
+                                          " states exceed the device limit of 32767");
+    if (ne < 0) return fail(KS_E_INVALID, "dfa: negative expression count");
+    if (out_off[0] != 0) return fail(KS_E_INVALID, "dfa: out_offsets[0] must be 0");
+    for (int s = 0; s < nq; ++s) {
+        if (out_off[s + 1] < out_off[s]) return fail(KS_E_INVALID, "dfa: out_offsets not monotone");
+        for (int c = 0; c < 5; ++c) {
+            int32_t x = trans[size_t(s) * 5 + c];
+            if (x < 0 || x >= nq) return fail(KS_E_INVALID, "dfa: transition target out of range");
+        }
+    }
+    const int32_t n_out = out_off[nq];
+    if (n_out > 0 && !out_ids) return fail(KS_E_INVALID, "dfa: missing out_ids");
+    for (int32_t i = 0; i < n_out; ++i)
+        if (out_ids[i] < 0 || out_ids[i] >= ne) return fail(KS_E_INVALID, "dfa: output id out of range");
+
+    h->nq = nq;
+    h->ne = ne;
+    h->new_of_old.assign(nq, 0);
+    h->old_of_new.clear();
+    for (int s = 0; s < nq; ++s)
+        if (out_off[s + 1] > out_off[s]) h->old_of_new.push_back(s);
+    h->n_accept = int(h->old_of_new.size());
+    for (int s = 0; s < nq; ++s)
+        if (out_off[s + 1] == out_off[s]) h->old_of_new.push_back(s);
+    for (int i = 0; i < nq; ++i) h->new_of_old[h->old_of_new[i]] = i;
+    h->start_internal = h->new_of_old[0];
+
+    h->acc_out_off.assign(1, 0);
+    h->acc_out_ids.clear();
+    h->acc_outcnt.clear();
+    for (int i = 0; i < h->n_accept; ++i) {
+        int old = h->old_of_new[i];
+        for (int32_t k = out_off[old]; k < out_off[old + 1]; ++k) h->acc_out_ids.push_back(out_ids[k]);
+        h->acc_out_off.push_back(int32_t(h->acc_out_ids.size()));
+        int cnt = out_off[old + 1] - out_off[old];
+        h->acc_outcnt.push_back(uint16_t(std::min(cnt, 65535)));
+        if (cnt > 65535) return fail(KS_E_UNSUPPORTED, "dfa: more than 65535 outputs on one state");
+    }
+
+    CompiledTable& t = h->scan;
+    t.nq = nq;
+    t.n_accept = h->n_accept;
+    t.t1.resize(size_t(nq) * 5);
+    for (int s = 0; s < nq; ++s)
+        for (int c = 0; c < 5; ++c)
+            t.t1[size_t(h->new_of_old[s]) * 5 + c] = uint16_t(h->new_of_old[trans[size_t(s) * 5 + c]]);
+    const size_t hist_bytes = size_t(h->n_accept) * 4;
+    const size_t budget = smem_budget > hist_bytes + 4096 ? smem_budget - hist_bytes - 4096 : 0;
+    build_stride_table(&t, budget);
+
+    h->sync_depth = synchronisation_depth(t.t1, nq);
+    bool want_lookback = h->sync_depth >= 0 && force_strategy != KS_STRATEGY_MAPSCAN &&
+                         force_strategy != KS_STRATEGY_SPECULATE;
+    if (force_strategy == KS_STRATEGY_LOOKBACK && h->sync_depth < 0)
+        return fail(KS_E_INVALID, "dfa: LOOKBACK forced but the automaton is not definite");
+    if (want_lookback) {
+        h->strategy = KS_STRATEGY_LOOKBACK;
+        return KS_OK;
+    }
+    if (force_strategy != KS_STRATEGY_SPECULATE && build_monoid(t, h->start_internal, h)) {
+        build_stride_table(&h->mono, smem_budget > 4096 ? smem_budget - 4096 : 0);
+        h->strategy = KS_STRATEGY_MAPSCAN;
+        return KS_OK;
+    }
+    if (force_strategy == KS_STRATEGY_MAPSCAN)
+        return fail(KS_E_INVALID, "dfa: MAPSCAN forced but the transition monoid exceeds 4096 maps");
+    return fail(KS_E_UNSUPPORTED,
+                "dfa: automaton is neither definite (depth <= 64) nor has a transition monoid "
+                "<= 4096 maps; the speculative map-scan strategy is not implemented yet");
+}
+
+}  // namespace ks

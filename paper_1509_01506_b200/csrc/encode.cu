@@ -1,0 +1,262 @@
+// Device encode: ASCII / symbol codes -> packed device sequence (K1).
+//
+// Reference semantics (alphabet.py:20-37, ingest.py:67-69): a/c/g/t in either
+// case -> 0..3 (lowercase soft-masking does not change matching); SP, TAB,
+// CR, LF dropped; any other byte -> OTHER.  Device form (ks_seq):
+//   bases : uint64[], 2 bits per base (base i at bits 2*(i%32) of word i/32)
+//   nmask : uint64[], OTHER bitmap (bit i%64 of word i/64)
+//   soft  : uint64[], lowercase-letter bitmap (informational, never scanned)
+// One thread packs one 64-base block: 64 input bytes -> 16 B + 8 B + 8 B.
+// Whitespace-free input (the common case) is written in place in a single
+// pass; otherwise per-block kept counts are scanned and a compaction pass
+// ORs each block's bits into their shifted output position.
+#include <algorithm>
+
+#include "scan_kernels.cuh"
+
+namespace ks {
+namespace {
+
+struct Packed {
+    uint64_t w0, w1, n, soft;
+    uint32_t kept;
+};
+
+// Classify one ASCII byte: code bits, OTHER, lowercase, whitespace.
+__device__ __forceinline__ void classify(uint32_t x, uint32_t& code, bool& other, bool& lower,
+                                         bool& ws) {
+    const uint32_t lx = x | 0x20u;
+    const bool base = (lx == 'a') | (lx == 'c') | (lx == 'g') | (lx == 't');
+    // a->0 c->1 g->2 t->3 from bits 1..3 of the byte, either case
+    code = ((x >> 1) ^ (x >> 2)) & 3u;
+    ws = (x == ' ') | (x == '\t') | (x == '\r') | (x == '\n');
+    other = !base && !ws;
+    lower = (x >= 'a') & (x <= 'z');
+    if (!base) code = 0;
+}
+
+// Encode the 64 bytes of block b (bytes past n_bytes are treated as dropped).
+__device__ __forceinline__ Packed pack_block(const uint8_t* in, int64_t n_bytes, int64_t b,
+                                             bool compact) {
+    Packed r{0, 0, 0, 0, 0};
+    const int64_t p0 = b << 6;
+    const int lim = int(min64(64, n_bytes - p0));
+    uint32_t words[16];
+    if (lim == 64 && ((reinterpret_cast<uintptr_t>(in) & 15) == 0)) {
+        const uint4* src = reinterpret_cast<const uint4*>(in + p0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint4 v = __ldg(src + q);
+            words[4 * q] = v.x;
+            words[4 * q + 1] = v.y;
+            words[4 * q + 2] = v.z;
+            words[4 * q + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            uint32_t w = 0;
+            for (int k = 0; k < 4; ++k) {
+                const int i = 4 * q + k;
+                // pad bytes past the end with SP: dropped, contributes nothing
+                const uint32_t byte = i < lim ? in[p0 + i] : uint32_t(' ');
+                w |= byte << (8 * k);
+            }
+            words[q] = w;
+        }
+    }
+    int o = 0;  // output slot within the block (== i when nothing is dropped)
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+        const uint32_t x = (words[i >> 2] >> (8 * (i & 3))) & 0xffu;
+        uint32_t code;
+        bool other, lower, ws;
+        classify(x, code, other, lower, ws);
+        const int slot = compact ? o : i;
+        if (!ws) {
+            if (slot < 32) r.w0 |= uint64_t(code) << (2 * slot);
+            else r.w1 |= uint64_t(code) << (2 * (slot - 32));
+            r.n |= uint64_t(other) << slot;
+            r.soft |= uint64_t(lower) << slot;
+            ++o;
+        }
+    }
+    r.kept = uint32_t(o);
+    return r;
+}
+
+__global__ void encode_inplace_kernel(const uint8_t* in, int64_t n_bytes, int64_t n_blocks,
+                                      uint64_t* bases, uint64_t* nmask, uint64_t* soft,
+                                      uint32_t* kept, int* any_ws) {
+    for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < n_blocks;
+         b += int64_t(gridDim.x) * blockDim.x) {
+        Packed r = pack_block(in, n_bytes, b, false);
+        const int lim = int(min64(64, n_bytes - (b << 6)));
+        reinterpret_cast<ulonglong2*>(bases)[b] = make_ulonglong2(r.w0, r.w1);
+        nmask[b] = r.n;
+        soft[b] = r.soft;
+        kept[b] = r.kept;
+        if (int(r.kept) != lim) atomicOr(any_ws, 1);
+    }
+}
+
+// OR `nbits` bits (value v, nbits <= 64) at bit position `bit` of array a.
+__device__ __forceinline__ void or_bits(uint64_t* a, int64_t bit, uint64_t v, int nbits) {
+    if (nbits <= 0 || v == 0) return;
+    const int64_t w = bit >> 6;
+    const int sh = int(bit & 63);
+    atomicOr(reinterpret_cast<unsigned long long*>(&a[w]), (unsigned long long)(v << sh));
+    if (sh && sh + nbits > 64)
+        atomicOr(reinterpret_cast<unsigned long long*>(&a[w + 1]), (unsigned long long)(v >> (64 - sh)));
+}
+
+__global__ void encode_compact_kernel(const uint8_t* in, int64_t n_bytes, int64_t n_blocks,
+                                      const int64_t* out_pos, uint64_t* bases, uint64_t* nmask,
+                                      uint64_t* soft) {
+    for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < n_blocks;
+         b += int64_t(gridDim.x) * blockDim.x) {
+        Packed r = pack_block(in, n_bytes, b, true);
+        const int64_t o = out_pos[b];
+        const int k = int(r.kept);
+        // bases: 2k bits starting at bit 2*o; split into the two 64-bit halves
+        or_bits(bases, 2 * o, r.w0, std::min(64, 2 * k));
+        if (k > 32) or_bits(bases, 2 * o + 64, r.w1, 2 * (k - 32));
+        or_bits(nmask, o, r.n, k);
+        or_bits(soft, o, r.soft, k);
+    }
+}
+
+__global__ void pack_codes_kernel(const uint8_t* codes, int64_t n, int64_t n_blocks, uint64_t* bases,
+                                  uint64_t* nmask, int* bad) {
+    for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < n_blocks;
+         b += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t p0 = b << 6;
+        uint64_t w0 = 0, w1 = 0, m = 0;
+        const int lim = int(min64(64, n - p0));
+        if (lim == 64) {
+            const uint4* src = reinterpret_cast<const uint4*>(codes + p0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint4 v = __ldg(src + q);
+                const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int i = 16 * q + 4 * t + k;
+                        const uint32_t c = (ws[t] >> (8 * k)) & 0xffu;
+                        if (c > 4u) atomicOr(bad, 1);
+                        const uint64_t bits = c >= 4u ? 0ull : uint64_t(c);
+                        if (i < 32) w0 |= bits << (2 * i);
+                        else w1 |= bits << (2 * (i - 32));
+                        m |= uint64_t(c >= 4u) << i;
+                    }
+            }
+        } else {
+            for (int i = 0; i < 64; ++i) {
+                const uint32_t c = i < lim ? codes[p0 + i] : 4u;
+                if (i < lim && c > 4u) atomicOr(bad, 1);
+                const uint64_t bits = c >= 4u ? 0ull : uint64_t(c);
+                if (i < 32) w0 |= bits << (2 * i);
+                else w1 |= bits << (2 * (i - 32));
+                m |= uint64_t(c >= 4u) << i;
+            }
+        }
+        reinterpret_cast<ulonglong2*>(bases)[b] = make_ulonglong2(w0, w1);
+        nmask[b] = m;
+    }
+}
+
+__global__ void unpack_codes_kernel(const uint64_t* bases, const uint64_t* nmask, int64_t n,
+                                    uint8_t* out) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const bool other = (nmask[i >> 6] >> (i & 63)) & 1ull;
+        out[i] = other ? 4 : uint8_t((bases[i >> 5] >> (2 * (i & 31))) & 3ull);
+    }
+}
+
+int grid_for(const ks_ctx* ctx, int64_t items, int threads) {
+    return int(max64(1, min64((items + threads - 1) / threads,
+                                                      int64_t(ctx->num_sms) * 16)));
+}
+
+}  // namespace
+
+// Encode n_bytes of device ASCII into seq (whose arrays are sized for n_bytes
+// bases).  Sets seq->n to the retained symbol count.  `scratch` must hold
+// kept counts + offsets (encode_scratch_bytes).
+size_t encode_scratch_bytes(int64_t n_bytes) {
+    const int64_t nb = (n_bytes + 63) / 64 + 1;
+    return align16(size_t(nb) * 4) + align16(size_t(nb) * 8) + exclusive_scan_rows_tmp_bytes(nb) + 64;
+}
+
+int encode_ascii_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, ks_seq* seq,
+                        void* scratch, int* launches) {
+    const int64_t nb = (n_bytes + 63) / 64;
+    char* p = static_cast<char*>(scratch);
+    uint32_t* kept = reinterpret_cast<uint32_t*>(p);
+    p += align16(size_t(nb + 1) * 4);
+    int64_t* pos = reinterpret_cast<int64_t*>(p);
+    p += align16(size_t(nb + 1) * 8);
+    int* flag = reinterpret_cast<int*>(p);
+    p += 64;
+    void* tmp = p;
+    int64_t* d_total = reinterpret_cast<int64_t*>(flag + 4);
+    KS_CUDA(cudaMemsetAsync(flag, 0, 64, ctx->stream));
+    if (nb == 0) {
+        seq->n = 0;
+        return KS_OK;
+    }
+    const int threads = 256;
+    encode_inplace_kernel<<<grid_for(ctx, nb, threads), threads, 0, ctx->stream>>>(
+        d_in, n_bytes, nb, seq->d_bases, seq->d_nmask, seq->d_soft, kept, flag);
+    if (launches) ++*launches;
+    KS_CUDA(cudaGetLastError());
+    int any_ws = 0;
+    KS_CUDA(cudaMemcpyAsync(&any_ws, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    KS_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (!any_ws) {
+        seq->n = n_bytes;
+        return KS_OK;
+    }
+    int rc = exclusive_scan_rows(ctx, kept, nb, pos, d_total, tmp, launches);
+    if (rc != KS_OK) return rc;
+    const size_t words = size_t(seq->n_blocks);
+    KS_CUDA(cudaMemsetAsync(seq->d_bases, 0, words * 16, ctx->stream));
+    KS_CUDA(cudaMemsetAsync(seq->d_nmask, 0, words * 8, ctx->stream));
+    KS_CUDA(cudaMemsetAsync(seq->d_soft, 0, words * 8, ctx->stream));
+    encode_compact_kernel<<<grid_for(ctx, nb, threads), threads, 0, ctx->stream>>>(
+        d_in, n_bytes, nb, pos, seq->d_bases, seq->d_nmask, seq->d_soft);
+    if (launches) ++*launches;
+    KS_CUDA(cudaGetLastError());
+    int64_t total = 0;
+    KS_CUDA(cudaMemcpyAsync(&total, d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    KS_CUDA(cudaStreamSynchronize(ctx->stream));
+    seq->n = total;
+    return KS_OK;
+}
+
+int pack_codes_device(ks_ctx* ctx, const uint8_t* d_codes, int64_t n, ks_seq* seq, int* d_flag,
+                      int* launches) {
+    const int64_t nb = (n + 63) / 64;
+    seq->n = n;
+    if (nb == 0) return KS_OK;
+    const int threads = 256;
+    pack_codes_kernel<<<grid_for(ctx, nb, threads), threads, 0, ctx->stream>>>(
+        d_codes, n, nb, seq->d_bases, seq->d_nmask, d_flag);
+    if (launches) ++*launches;
+    KS_CUDA(cudaGetLastError());
+    return KS_OK;
+}
+
+int unpack_codes_device(ks_ctx* ctx, const ks_seq* seq, uint8_t* d_out) {
+    if (seq->n == 0) return KS_OK;
+    const int threads = 256;
+    unpack_codes_kernel<<<grid_for(ctx, seq->n, threads), threads, 0, ctx->stream>>>(
+        seq->d_bases, seq->d_nmask, seq->n, d_out);
+    KS_CUDA(cudaGetLastError());
+    return KS_OK;
+}
+
+}  // namespace ks

@@ -1,0 +1,121 @@
+// Internal declarations shared by the host C++ and the CUDA translation units.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/kmerscan_b200.h"
+
+namespace ks {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define KS_CUDA(call)                                              \
+    do {                                                           \
+        cudaError_t _e = (call);                                   \
+        if (_e != cudaSuccess) return ::ks::cuda_fail(_e, #call);  \
+    } while (0)
+
+// ---------------------------------------------------------------- limits
+constexpr int kMaxStates = 32767;        // uint16 entries, bit 15 = hit flag
+constexpr uint16_t kFlag = 0x8000u;
+constexpr uint16_t kStateMask = 0x7FFFu;
+constexpr int kMaxSyncDepth = 64;        // lookback must fit in one 64-base block
+constexpr int kMaxMonoid = 4096;         // product table <= 32 MiB
+constexpr int kBlockBases = 64;          // bases per packed block (one nmask word)
+constexpr int kScanThreads = 512;
+
+// ---------------------------------------------------------------- DFA forms
+// Host-compiled device form of one automaton.  States are renumbered so that
+// accepting states are [0, n_accept): a hit test is `s < n_accept`.
+struct CompiledTable {
+    int nq = 0;                      // states of this table
+    int n_accept = 0;                // internal ids < n_accept have outputs
+    int stride = 1;                  // K: bases per stride-table lookup
+    int reset_state = -1;            // internal id all states enter on OTHER, or -1
+    std::vector<uint16_t> t1;        // nq x 5 single-symbol table (internal ids)
+    std::vector<uint16_t> tk;        // nq x 4^K, entry = next | (hit on path ? kFlag : 0)
+};
+
+struct HostDfa {
+    int nq = 0, ne = 0, n_accept = 0;
+    int strategy = 0;
+    int sync_depth = -1;
+    int start_internal = 0;
+    std::vector<int32_t> new_of_old, old_of_new;
+    std::vector<int32_t> acc_out_off;   // n_accept + 1 (CSR over internal accepting ids)
+    std::vector<int32_t> acc_out_ids;
+    std::vector<uint16_t> acc_outcnt;   // n_accept
+    CompiledTable scan;                 // the automaton itself
+    // MAPSCAN
+    int nm = 0;
+    CompiledTable mono;                 // transition-monoid automaton (no hits)
+    std::vector<uint16_t> prod;         // nm x nm: element(a then b)
+    std::vector<uint16_t> act0;         // nm: internal state reached from START
+    std::vector<uint16_t> action;       // nm x nq: internal state reached from q
+};
+
+int compile_dfa(const int32_t* trans, int nq, const int32_t* out_off, const int32_t* out_ids,
+                int ne, int force_strategy, size_t smem_budget, HostDfa* out);
+
+// ---------------------------------------------------------------- device views
+struct DevTable {
+    const uint16_t* t1 = nullptr;   // nq x 5
+    const uint16_t* tk = nullptr;   // nq x 4^K
+    int nq = 0, n_accept = 0, stride = 1, reset_state = -1;
+    size_t tk_bytes = 0, t1_bytes = 0;
+};
+
+struct SeqView {
+    const uint64_t* bases = nullptr;  // 2-bit codes, 32 per word (base i at bits 2*(i%32))
+    const uint64_t* nmask = nullptr;  // OTHER bitmap, 64 per word
+    int64_t n = 0;
+};
+
+}  // namespace ks
+
+struct ks_ctx {
+    int device = 0;
+    int num_sms = 148;
+    size_t smem_optin = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    ks_stats stats{};
+    // grow-only device scratch
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    void* pinned = nullptr;   // small pinned host staging
+    size_t pinned_bytes = 0;
+};
+
+struct ks_dfa {
+    ks_ctx* ctx = nullptr;
+    ks::HostDfa host;
+    ks::DevTable scan;
+    ks::DevTable mono;
+    int32_t* d_acc_out_off = nullptr;
+    int32_t* d_acc_out_ids = nullptr;
+    uint16_t* d_acc_outcnt = nullptr;
+    uint16_t* d_prod = nullptr;
+    uint16_t* d_act0 = nullptr;
+    uint16_t* d_action = nullptr;   // nm x nq
+    void* d_blob = nullptr;   // single allocation backing the above
+    bool tables_in_smem = true;
+};
+
+struct ks_seq {
+    ks_ctx* ctx = nullptr;
+    int64_t n = 0;
+    uint64_t* d_bases = nullptr;
+    uint64_t* d_nmask = nullptr;
+    uint64_t* d_soft = nullptr;
+    void* d_blob = nullptr;
+    int64_t n_blocks = 0;   // 64-base blocks allocated (with padding)
+};

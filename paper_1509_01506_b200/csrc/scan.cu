@@ -1,0 +1,369 @@
+// Chunked DFA scan kernels and their launchers (see scan_kernels.cuh).
+#include <algorithm>
+
+#include "scan_kernels.cuh"
+
+namespace ks {
+namespace {
+
+// --------------------------------------------------------------- hit sinks
+// What a visit to an accepting state (internal id s < n_accept) at sequence
+// position `pos` does, per mode.  Visits are the reference's inner CSR loop
+// (_kernels.py:26-28 / :80-84) deferred: counts[e] = sum_s visits[s]*mult(s,e).
+template <int MODE>
+struct Sink {
+    unsigned int* shist;
+    unsigned long long* visits;
+    const uint16_t* outcnt;
+    const int32_t* off;
+    const int32_t* ids;
+    int64_t* rows;
+    int64_t row_base;
+    uint32_t nrows;
+    int64_t cur;
+
+    __device__ __forceinline__ void add(uint32_t s, uint32_t times) {
+        if (shist) atomicAdd(&shist[s], times);
+        else atomicAdd(&visits[s], (unsigned long long)times);
+    }
+
+    __device__ __forceinline__ void hit(int64_t pos, uint32_t s) {
+        if constexpr (MODE == kModeCount || MODE == kModeRows) {
+            add(s, 1u);
+            if constexpr (MODE == kModeRows) nrows += __ldg(&outcnt[s]);
+        } else if constexpr (MODE == kModeEmit) {
+            const int k1 = __ldg(&off[s + 1]);
+            const long long o = row_base + pos + 1;
+            for (int k = __ldg(&off[s]); k < k1; ++k, ++cur) {
+                longlong2 r;
+                r.x = o;
+                r.y = __ldg(&ids[k]);
+                reinterpret_cast<longlong2*>(rows)[cur] = r;
+            }
+        }
+    }
+
+    // `n` consecutive positions starting at pos0 all entering state s.
+    __device__ __forceinline__ void hit_run(int64_t pos0, int n, uint32_t s) {
+        if constexpr (MODE == kModeCount || MODE == kModeRows) {
+            add(s, uint32_t(n));
+            if constexpr (MODE == kModeRows) nrows += uint32_t(n) * __ldg(&outcnt[s]);
+        } else if constexpr (MODE == kModeEmit) {
+            for (int i = 0; i < n; ++i) hit(pos0 + i, s);
+        }
+    }
+};
+
+template <bool SM>
+struct Tables {
+    const uint16_t* tk;
+    const uint16_t* t1;
+    __device__ __forceinline__ uint32_t k(uint32_t i) const {
+        if constexpr (SM) return tk[i];
+        else return __ldg(tk + i);
+    }
+    __device__ __forceinline__ uint32_t one(uint32_t i) const {
+        if constexpr (SM) return t1[i];
+        else return __ldg(t1 + i);
+    }
+};
+
+// Bits [off, off+width) of the 128-bit value w1:w0 (off, width compile-time
+// after unrolling).
+__device__ __forceinline__ uint32_t bits128(uint64_t w0, uint64_t w1, int off, int width) {
+    uint64_t v;
+    if (off >= 64) v = w1 >> (off - 64);
+    else if (off + width > 64) v = (w0 >> off) | (w1 << (64 - off));
+    else v = w0 >> off;
+    return uint32_t(v) & ((1u << width) - 1u);
+}
+
+__device__ __forceinline__ uint32_t sym_at(const SeqView& q, int64_t p) {
+    const uint64_t m = __ldg(&q.nmask[p >> 6]);
+    if ((m >> (p & 63)) & 1ull) return 4u;
+    const uint64_t w = __ldg(&q.bases[p >> 5]);
+    return uint32_t(w >> (2 * (p & 31))) & 3u;
+}
+
+// Re-walk the K bases of a flagged stride step with the 1-base table,
+// recording every accepting state entered.
+template <int K, int MODE, bool SM>
+__device__ __forceinline__ void rewalk(uint32_t s, uint32_t word, int64_t pos, int32_t n_accept,
+                                       const Tables<SM>& T, Sink<MODE>& sink) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        s = T.one(s * 5u + ((word >> (2 * i)) & 3u));
+        if (s < uint32_t(n_accept)) sink.hit(pos + i, s);
+    }
+}
+
+// Advance one full, OTHER-free 64-base block with the K-stride table.
+template <int K, int MODE, bool SM>
+__device__ __forceinline__ uint32_t fast_block(uint32_t s, uint64_t w0, uint64_t w1, bool live,
+                                               int64_t p0, int32_t n_accept, const Tables<SM>& T,
+                                               Sink<MODE>& sink) {
+    constexpr int W = 2 * K;
+    constexpr int NL = 64 / K;
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+        const uint32_t word = bits128(w0, w1, W * j, W);
+        const uint32_t e = T.k((s << W) | word);
+        if constexpr (MODE != kModeMap) {
+            if (e & kFlag) {
+                if (live) rewalk<K, MODE, SM>(s, word, p0 + K * j, n_accept, T, sink);
+            }
+        }
+        s = e & kStateMask;
+    }
+#pragma unroll
+    for (int r = NL * K; r < 64; ++r) {  // K == 3 leaves one base
+        s = T.one(s * 5u + bits128(w0, w1, 2 * r, 2));
+        if constexpr (MODE != kModeMap) {
+            if (live && s < uint32_t(n_accept)) sink.hit(p0 + r, s);
+        }
+    }
+    return s;
+}
+
+extern __shared__ __align__(16) unsigned char g_smem[];
+
+template <int K, int MODE, bool SM>
+__global__ void __launch_bounds__(1024, 1) scan_kernel(const ScanArgs a) {
+    uint16_t* s_tk = reinterpret_cast<uint16_t*>(g_smem);
+    uint16_t* s_t1 = s_tk + (SM ? a.tk_pad : 0);
+    unsigned int* s_hist = reinterpret_cast<unsigned int*>(s_t1 + (SM ? a.t1_pad : 0));
+
+    if constexpr (SM) {
+        const uint4* src = reinterpret_cast<const uint4*>(a.tk);
+        uint4* dst = reinterpret_cast<uint4*>(s_tk);
+        for (int i = threadIdx.x; i < a.tk_pad / 8; i += blockDim.x) dst[i] = __ldg(src + i);
+        src = reinterpret_cast<const uint4*>(a.t1);
+        dst = reinterpret_cast<uint4*>(s_t1);
+        for (int i = threadIdx.x; i < a.t1_pad / 8; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
+    const bool hist_smem = (MODE == kModeCount || MODE == kModeRows) && a.hist_smem;
+    if (hist_smem)
+        for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x) s_hist[i] = 0u;
+    __syncthreads();
+
+    Tables<SM> T;
+    T.tk = SM ? s_tk : a.tk;
+    T.t1 = SM ? s_t1 : a.t1;
+    const uint32_t n_accept = uint32_t(a.n_accept);
+    const uint4* bases4 = reinterpret_cast<const uint4*>(a.seq.bases);
+    const uint64_t* nmask = a.seq.nmask;
+
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < a.nchunks; c += stride) {
+        const int64_t cb = max64(a.begin, a.origin + c * a.chunk_len);
+        const int64_t ce = min64(a.end, a.origin + (c + 1) * a.chunk_len);
+
+        uint32_t s;
+        if (a.chunk_entry) {
+            s = a.chunk_entry[c];
+        } else if (a.uniform_entry >= 0) {
+            s = uint32_t(a.uniform_entry);
+        } else {
+            const int64_t lb = max64(a.base_pos, cb - a.lookback);
+            s = uint32_t(lb == a.base_pos ? a.base_state : a.any_state);
+            for (int64_t p = lb; p < cb; ++p) s = T.one(s * 5u + sym_at(a.seq, p));
+        }
+
+        Sink<MODE> sink;
+        sink.shist = hist_smem ? s_hist : nullptr;
+        sink.visits = a.visits;
+        sink.outcnt = a.acc_outcnt;
+        sink.off = a.acc_out_off;
+        sink.ids = a.acc_out_ids;
+        sink.rows = a.rows;
+        sink.row_base = a.row_base;
+        sink.nrows = 0;
+        sink.cur = (MODE == kModeEmit) ? a.chunk_row_off[c] : 0;
+
+        int64_t b = cb >> 6;
+        const int64_t bend = (ce + 63) >> 6;
+        uint4 wb = __ldg(bases4 + b);
+        uint64_t wm = __ldg(nmask + b);
+        for (; b < bend; ++b) {
+            // arrays are padded by two blocks: the prefetch never faults
+            const uint4 nb = __ldg(bases4 + b + 1);
+            const uint64_t nm = __ldg(nmask + b + 1);
+            const int64_t p0 = b << 6;
+            const int lo = int(max64(cb - p0, 0));
+            const int hi = int(min64(ce - p0, 64));
+            const uint64_t w0 = (uint64_t(wb.y) << 32) | wb.x;
+            const uint64_t w1 = (uint64_t(wb.w) << 32) | wb.z;
+            const bool full = (lo == 0) && (hi == 64);
+            const bool alln = wm == ~0ull;
+            const bool fast = full && (wm == 0ull || (alln && a.reset_state >= 0));
+            if (__all_sync(__activemask(), fast)) {
+                const uint32_t s2 = fast_block<K, MODE, SM>(s, w0, w1, !alln, p0, a.n_accept, T, sink);
+                if (alln) {
+                    s = uint32_t(a.reset_state);
+                    if constexpr (MODE != kModeMap) {
+                        if (s < n_accept) sink.hit_run(p0, 64, s);
+                    }
+                } else {
+                    s = s2;
+                }
+            } else {
+                for (int i = lo; i < hi; ++i) {
+                    const uint32_t sym = ((wm >> i) & 1ull)
+                                             ? 4u
+                                             : uint32_t((i < 32 ? w0 >> (2 * i) : w1 >> (2 * (i - 32)))) & 3u;
+                    s = T.one(s * 5u + sym);
+                    if constexpr (MODE != kModeMap) {
+                        if (s < n_accept) sink.hit(p0 + i, s);
+                    }
+                }
+            }
+            wb = nb;
+            wm = nm;
+        }
+        if (a.chunk_exit) a.chunk_exit[c] = uint16_t(s);
+        if constexpr (MODE == kModeRows) a.chunk_rows[c] = sink.nrows;
+        if constexpr (MODE == kModeEmit) {
+            if (sink.cur != a.chunk_row_off[c + 1]) atomicExch(a.error, 1);
+        }
+    }
+
+    if (hist_smem) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x)
+            if (s_hist[i]) atomicAdd(&a.visits[i], (unsigned long long)s_hist[i]);
+    }
+}
+
+using ScanFn = void (*)(const ScanArgs);
+
+template <int K, bool SM>
+ScanFn pick_mode(int mode) {
+    switch (mode) {
+        case kModeCount: return scan_kernel<K, kModeCount, SM>;
+        case kModeRows: return scan_kernel<K, kModeRows, SM>;
+        case kModeEmit: return scan_kernel<K, kModeEmit, SM>;
+        case kModeMap: return scan_kernel<K, kModeMap, SM>;
+    }
+    return nullptr;
+}
+
+ScanFn pick_kernel(int mode, int stride, bool sm) {
+    switch (stride) {
+        case 1: return sm ? pick_mode<1, true>(mode) : pick_mode<1, false>(mode);
+        case 2: return sm ? pick_mode<2, true>(mode) : pick_mode<2, false>(mode);
+        case 3: return sm ? pick_mode<3, true>(mode) : pick_mode<3, false>(mode);
+        case 4: return sm ? pick_mode<4, true>(mode) : pick_mode<4, false>(mode);
+    }
+    return nullptr;
+}
+
+size_t scan_smem_bytes(bool smem_tables, int32_t tk_pad, int32_t t1_pad, int32_t hist_words) {
+    size_t b = 0;
+    if (smem_tables) b += size_t(tk_pad) * 2 + size_t(t1_pad) * 2;
+    b += size_t(hist_words) * 4;
+    return b;
+}
+
+// Threads per CTA and resident CTAs per SM for this instantiation: 512-thread
+// CTAs when several fit an SM, otherwise one 1024-thread CTA (big tables).
+struct LaunchShape {
+    int tpb;
+    int per_sm;
+};
+
+LaunchShape launch_shape(ScanFn fn, size_t smem) {
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    LaunchShape best{512, 1};
+    for (int tpb : {512, 1024}) {
+        int n = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, tpb, smem) != cudaSuccess) {
+            cudaGetLastError();
+            n = 0;
+        }
+        if (n * tpb > best.tpb * best.per_sm) best = LaunchShape{tpb, n};
+    }
+    return best;
+}
+
+// --------------------------------------------------------------- helpers
+__global__ void finalize_counts_kernel(const unsigned long long* visits, int32_t n_accept,
+                                       const int32_t* off, const int32_t* ids,
+                                       unsigned long long* counts) {
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n_accept; s += gridDim.x * blockDim.x) {
+        const unsigned long long v = visits[s];
+        if (!v) continue;
+        for (int k = off[s]; k < off[s + 1]; ++k) atomicAdd(&counts[ids[k]], v);
+    }
+}
+
+__global__ void chunk_entry_kernel(const uint16_t* excl, int64_t n, const uint16_t* action,
+                                   int32_t nq, int32_t entry, uint16_t* out) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        out[i] = action[size_t(excl[i]) * nq + entry];
+}
+
+}  // namespace
+
+void scan_geometry(const ks_ctx* ctx, int64_t begin, int64_t end, int stride, bool smem_tables,
+                   int32_t tk_pad, int32_t t1_pad, int32_t hist_words, int64_t* origin,
+                   int64_t* chunk_len, int64_t* nchunks) {
+    const size_t smem = scan_smem_bytes(smem_tables, tk_pad, t1_pad, hist_words);
+    ScanFn fn = pick_kernel(kModeCount, stride, smem_tables);
+    const LaunchShape sh = fn ? launch_shape(fn, smem) : LaunchShape{512, 1};
+    const int64_t threads = int64_t(ctx->num_sms) * sh.per_sm * sh.tpb;
+    const int64_t o = (begin >> 6) << 6;
+    const int64_t span = max64(end - o, 1);
+    int64_t per = (span + threads - 1) / threads;
+    per = ((per + 63) / 64) * 64;
+    const char* force = std::getenv("KS_CHUNK_LEN");
+    if (force && *force) per = max64(64, (std::atoll(force) + 63) / 64 * 64);
+    *origin = o;
+    *chunk_len = per;
+    *nchunks = (span + per - 1) / per;
+}
+
+int launch_scan(ks_ctx* ctx, ScanArgs a, int mode, int stride, bool smem_tables, int* launches) {
+    if (a.end <= a.begin || a.nchunks <= 0) return KS_OK;
+    if (!(mode == kModeCount || mode == kModeRows)) a.hist_smem = 0;
+    const int32_t hist_words = a.hist_smem ? a.n_accept : 0;
+    const size_t smem = scan_smem_bytes(smem_tables, a.tk_pad, a.t1_pad, hist_words);
+    ScanFn fn = pick_kernel(mode, stride, smem_tables);
+    if (!fn) return fail(KS_E_INVALID, "scan: bad mode/stride");
+    const LaunchShape sh = launch_shape(fn, smem);
+    const int64_t need_blocks = (a.nchunks + sh.tpb - 1) / sh.tpb;
+    const int64_t max_blocks = int64_t(ctx->num_sms) * sh.per_sm;
+    const int blocks = int(max64(1, std::min(need_blocks, max_blocks)));
+    fn<<<blocks, sh.tpb, smem, ctx->stream>>>(a);
+    if (launches) ++*launches;
+    KS_CUDA(cudaGetLastError());
+    return KS_OK;
+}
+
+int launch_finalize_counts(ks_ctx* ctx, const unsigned long long* visits, int32_t n_accept,
+                           const int32_t* acc_out_off, const int32_t* acc_out_ids,
+                           unsigned long long* counts, int* launches) {
+    if (n_accept <= 0) return KS_OK;
+    const int threads = 256;
+    const int blocks = std::min((n_accept + threads - 1) / threads, 1024);
+    finalize_counts_kernel<<<blocks, threads, 0, ctx->stream>>>(visits, n_accept, acc_out_off,
+                                                                  acc_out_ids, counts);
+    if (launches) ++*launches;
+    KS_CUDA(cudaGetLastError());
+    return KS_OK;
+}
+
+int launch_chunk_entry(ks_ctx* ctx, const uint16_t* excl, int64_t n, const uint16_t* action,
+                       int32_t nq, int32_t entry, uint16_t* chunk_entry, int* launches) {
+    if (n <= 0) return KS_OK;
+    const int threads = 256;
+    const int blocks = int(min64((n + threads - 1) / threads, 4096));
+    chunk_entry_kernel<<<blocks, threads, 0, ctx->stream>>>(excl, n, action, nq, entry, chunk_entry);
+    if (launches) ++*launches;
+    KS_CUDA(cudaGetLastError());
+    return KS_OK;
+}
+
+}  // namespace ks

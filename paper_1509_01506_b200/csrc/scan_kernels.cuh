@@ -1,0 +1,94 @@
+// Chunked DFA scan kernels (sm_100a) -- shared declarations.
+//
+// Replaces the reference's hot loops (kmerscan/_kernels.py:25-28 scan_from,
+// :77-87 the full run of match_chunk_kernel):
+//     s = trans[s, sym[j]]; for k in out_off[s]..out_off[s+1]: counts[out_ids[k]] += 1
+//
+// B200 layout: every thread owns one contiguous lane chunk of L bases
+// (L multiple of 64) and walks it with a K-base stride table staged in
+// shared memory: one LDS.U16 advances K bases.  Bit 15 of an entry flags
+// "a state with outputs was entered during these K bases"; only then the K
+// bases are re-walked with the 1-base table and the visited accepting
+// states are histogrammed (shared-memory atomics; per-expression counts are
+// formed once at the end from the per-state visit histogram).  The sequence
+// is read as 2-bit packed bases (16 B per 64 bases) plus one OTHER-bitmap
+// word per 64 bases, prefetched one block ahead.
+//
+// OTHER handling: a 64-base block whose bitmap is all ones (inside an N run)
+// rides the warp's fast path and is fixed up afterwards when OTHER sends
+// every state to one state (always true for built automata); a partially
+// OTHER block, a block cut by the chunk/segment edge, or a non-resetting
+// automaton sends the warp through the per-base path for that block.
+#pragma once
+
+#include <cstdint>
+
+#include "ks_internal.h"
+
+namespace ks {
+
+enum ScanMode : int { kModeCount = 0, kModeRows = 1, kModeEmit = 2, kModeMap = 3 };
+
+struct ScanArgs {
+    SeqView seq;
+    int64_t begin = 0, end = 0;      // positions scanned: [begin, end)
+    int64_t origin = 0;              // 64-aligned: chunk c starts at origin + c*chunk_len
+    int64_t chunk_len = 64;          // multiple of 64
+    int64_t nchunks = 0;
+    // entry state of each chunk (first match wins):
+    const uint16_t* chunk_entry = nullptr;  // per-chunk entry states (MAPSCAN pass 2)
+    int32_t uniform_entry = -1;      // >= 0: every chunk enters in this state (MAP pass)
+    int32_t lookback = 0;            // else: scan max(base_pos, cb - lookback) .. cb
+    int64_t base_pos = 0;            //   starting in base_state when at base_pos,
+    int32_t base_state = 0;          //   in any_state otherwise (synchronising word)
+    int32_t any_state = 0;
+    // automaton
+    const uint16_t* t1 = nullptr;    // nq x 5 (global)
+    const uint16_t* tk = nullptr;    // nq x 4^K (global)
+    int32_t nq = 0, n_accept = 0, reset_state = -1;
+    int32_t tk_pad = 0, t1_pad = 0;  // uint16 entries, multiples of 8
+    int32_t hist_smem = 0;           // histogram in shared memory
+    // outputs
+    unsigned long long* visits = nullptr;   // n_accept, global accumulation
+    uint16_t* chunk_exit = nullptr;         // per chunk exit state (optional)
+    uint32_t* chunk_rows = nullptr;         // kModeRows
+    const int64_t* chunk_row_off = nullptr; // kModeEmit (nchunks + 1)
+    const int32_t* acc_out_off = nullptr;
+    const int32_t* acc_out_ids = nullptr;
+    const uint16_t* acc_outcnt = nullptr;
+    int64_t* rows = nullptr;
+    int64_t row_base = 0;                   // row offset = position + 1 + row_base
+    int32_t* error = nullptr;               // set to 1 on an internal invariant failure
+};
+
+inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
+
+// Launch one scan over [a.begin, a.end); fills chunk geometry, grid and smem.
+// Returns KS_OK or a KS_E_* code (error text set).
+int launch_scan(ks_ctx* ctx, ScanArgs a, int mode, int stride, bool smem_tables, int* launches);
+
+// Chunk geometry used by launch_scan for a span (so callers can size arrays).
+void scan_geometry(const ks_ctx* ctx, int64_t begin, int64_t end, int stride, bool smem_tables,
+                   int32_t tk_pad, int32_t t1_pad, int32_t hist_words, int64_t* origin,
+                   int64_t* chunk_len, int64_t* nchunks);
+
+// Prefix scans (csrc/prefix_scan.cu).
+int exclusive_scan_rows(ks_ctx* ctx, const uint32_t* in, int64_t n, int64_t* out_excl,
+                        int64_t* d_total, void* tmp, int* launches);
+size_t exclusive_scan_rows_tmp_bytes(int64_t n);
+int exclusive_scan_monoid(ks_ctx* ctx, const uint16_t* in, int64_t n, const uint16_t* prod,
+                          int32_t nm, uint16_t* out_excl, uint16_t* d_total, void* tmp,
+                          int* launches);
+size_t exclusive_scan_monoid_tmp_bytes(int64_t n);
+
+// Small helper kernels (csrc/scan.cu).
+int launch_finalize_counts(ks_ctx* ctx, const unsigned long long* visits, int32_t n_accept,
+                           const int32_t* acc_out_off, const int32_t* acc_out_ids,
+                           unsigned long long* counts, int* launches);
+int launch_chunk_entry(ks_ctx* ctx, const uint16_t* excl, int64_t n, const uint16_t* action,
+                       int32_t nq, int32_t entry, uint16_t* chunk_entry, int* launches);
+
+}  // namespace ks

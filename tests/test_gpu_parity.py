@@ -1,0 +1,286 @@
+"""GPU parity: the device scan (through the C ABI) against the pinned oracle
+and the reference's golden fixtures.  Bit-exact counts and rows."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_1509_01506_b200 as ks
+from paper_1509_01506_b200 import _native, workloads
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return _native.context(0)
+
+
+def dfa_of(text):
+    return ks.build_dfa(ks.expand_to_literals(ks.parse_expressions(text)))
+
+
+# ---------------------------------------------------------------- known answers
+# (reference tests/test_engine.py, test_oracle_bench.py, test_automaton.py)
+
+def test_known_answers(toy_dfa):
+    rep = ks.run(toy_dfa, ks.sequence_from_text("ctancat"), ks.EngineConfig(workers=2))
+    assert rep.per_expression_counts.tolist() == [0, 1, 1, 0]
+    dfa = dfa_of("aca")
+    rep = ks.run(dfa, ks.sequence_from_text("acaca"), ks.EngineConfig(mode="locate"))
+    assert rep.per_expression_counts.tolist() == [2]
+    assert rep.locations.tolist() == [[3, 0], [5, 0]]
+    assert ks.sequential_count(dfa_of("a|aa"), ks.sequence_from_text("aa")).tolist() == [3]
+    rep = ks.run(dfa_of("ta\ncta"), ks.sequence_from_text("cta"), ks.EngineConfig(mode="locate"))
+    assert rep.locations.tolist() == [[3, 0], [3, 1]]
+    rep = ks.run(toy_dfa, ks.sequence_from_text("ctacatacg"), ks.EngineConfig(workers=2))
+    assert rep.per_expression_counts.tolist() == [1, 1, 1, 0]
+    rep = ks.run(dfa_of("a|aa\na"), ks.sequence_from_text("aaNaa"), ks.EngineConfig(mode="locate"))
+    assert rep.locations.tolist() == [[1, 0], [1, 1], [2, 0], [2, 0], [2, 1], [4, 0], [4, 1],
+                                      [5, 0], [5, 0], [5, 1]]
+
+
+def test_global_exclusive_offsets(toy_dfa):
+    res = ks.match_chunk(toy_dfa, ks.encode("ttta"), 100, np.array([0]), ks.EngineConfig(mode="locate"))
+    assert res[0].locations.tolist() == [[104, 3]]
+
+
+def test_empty_input(toy_dfa):
+    rep = ks.run(toy_dfa, ks.sequence_from_text(""), ks.EngineConfig(workers=8, mode="locate"))
+    assert rep.total_count == 0
+    assert rep.per_expression_counts.tolist() == [0, 0, 0, 0]
+    assert rep.locations.shape == (0, 2)
+    assert rep.metadata["effective_workers"] == 1
+
+
+# ---------------------------------------------------------------- golden fixtures
+
+def test_random_cases_vs_reference(random_cases):
+    for i, c in enumerate(random_cases):
+        dfa = dfa_of(c["text"])
+        seq = ks.Sequence(ks.encode_bytes(c["data"]))
+        rep = ks.run(dfa, seq, ks.EngineConfig(workers=c["workers"], window=c["window"], mode="locate"))
+        assert rep.per_expression_counts.tolist() == c["counts"].tolist(), i
+        assert rep.locations.tolist() == c["locs"].tolist(), i
+        for key, val in c["meta"].items():
+            got = rep.metadata[key]
+            if key == "convergence_steps":
+                got = {str(k): v for k, v in got.items()}
+            assert got == val, (i, key)
+
+
+def test_config_cases_vs_reference(config_cases):
+    for c in config_cases:
+        w = workloads.make(c["config"], c["n"])
+        assert hashlib.sha256(w.ascii.tobytes()).hexdigest() == c["sha256"]
+        seq = ks.Sequence(ks.encode_bytes(w.ascii.tobytes()))
+        rep = ks.run(w.dfa, seq, ks.EngineConfig(workers=c["workers"], window=c["window"], mode=c["mode"]))
+        assert rep.per_expression_counts.tolist() == c["counts"].tolist(), c["config"]
+        if c["locs"] is not None:
+            assert np.array_equal(rep.locations, c["locs"]), c["config"]
+        for key, val in c["meta"].items():
+            got = rep.metadata[key]
+            if key == "convergence_steps":
+                got = {str(k): v for k, v in got.items()}
+            assert got == val, (c["config"], key)
+
+
+# ---------------------------------------------------------------- oracle differential
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_vs_oracle(ctx, seed):
+    rng = np.random.default_rng(seed)
+    lits = sorted({"".join("acgt"[x] for x in rng.integers(0, 4, rng.integers(1, 13)))
+                   for _ in range(int(rng.integers(1, 60)))})
+    dfa = dfa_of("\n".join(lits))
+    for n in (0, 1, 63, 64, 65, 127, 1000, 4097, 200_003):
+        codes = rng.integers(0, 4, n).astype(np.uint8)
+        codes[rng.random(n) < 0.02] = 4
+        if n > 500:  # an N run across block borders
+            codes[300:431] = 4
+        seq = ks.Sequence(codes)
+        want, rows = O.ref_run(dfa, codes, 1, 10, True)[:2]
+        rep = ks.run(dfa, seq, ks.EngineConfig(mode="locate"))
+        assert rep.per_expression_counts.tolist() == want.tolist(), (seed, n)
+        assert np.array_equal(rep.locations, rows), (seed, n)
+
+
+@pytest.mark.parametrize("stride", ["1", "2", "3", "4"])
+def test_forced_strides(monkeypatch, stride):
+    monkeypatch.setenv("KS_FORCE_STRIDE", stride)
+    ctx = _native.DeviceContext(0)
+    w = workloads.make(2, 1 << 20)
+    codes = ks.encode_bytes(w.ascii.tobytes())
+    codes[5000:9000] = 4
+    dh = ctx.dfa(w.dfa)
+    assert dh.info["stride"] == int(stride)
+    want, rows = O.ref_run(w.dfa, codes, 1, 10, True)[:2]
+    sh = ctx.upload_codes(codes)
+    got, grows = ctx.locate(dh, sh)
+    assert got.tolist() == want.tolist()
+    assert np.array_equal(grows, rows)
+
+
+def test_global_tables(monkeypatch):
+    monkeypatch.setenv("KS_FORCE_GLOBAL_TABLES", "1")
+    ctx = _native.DeviceContext(0)
+    w = workloads.make(3, 1 << 20)
+    codes = ks.encode_bytes(w.ascii.tobytes())
+    dh = ctx.dfa(w.dfa)
+    assert dh.info["tables_in_smem"] == 0
+    want = O.ref_sequential_count(w.dfa, codes)[0]
+    assert ctx.count(dh, ctx.upload_codes(codes)).tolist() == want.tolist()
+
+
+@pytest.mark.parametrize("chunk", ["64", "128", "1024"])
+def test_small_chunks(monkeypatch, chunk):
+    """Many lane chunks: every chunk derives its entry state by lookback."""
+    monkeypatch.setenv("KS_CHUNK_LEN", chunk)
+    ctx = _native.DeviceContext(0)
+    w = workloads.make(3, 1 << 19)
+    codes = ks.encode_bytes(w.ascii.tobytes())
+    want, rows = O.ref_run(w.dfa, codes, 1, 10, True)[:2]
+    dh = ctx.dfa(w.dfa)
+    got, grows = ctx.locate(dh, ctx.upload_codes(codes))
+    assert got.tolist() == want.tolist()
+    assert np.array_equal(grows, rows)
+
+
+# ---------------------------------------------------------------- non-converging DFA (C5)
+
+def test_permutation_dfa_mapscan(ctx, monkeypatch):
+    monkeypatch.setenv("KS_CHUNK_LEN", "256")
+    c2 = _native.DeviceContext(0)
+    dfa = workloads.permutation_dfa()
+    dh = c2.dfa(dfa)
+    assert dh.info["strategy_name"] == "mapscan"
+    assert dh.info["monoid_size"] == 2048
+    rng = np.random.default_rng(5)
+    codes = rng.integers(0, 4, 300_001).astype(np.uint8)
+    codes[rng.random(codes.size) < 0.001] = 4
+    want, rows = O.ref_run(dfa, codes, 1, 10, True)[:2]
+    got, grows = c2.locate(dh, c2.upload_codes(codes))
+    assert got.tolist() == want.tolist()
+    assert np.array_equal(grows, rows)
+
+
+def test_small_random_dfas_mapscan(ctx):
+    rng = np.random.default_rng(11)
+    for trial in range(20):
+        nq = int(rng.integers(1, 5))
+        trans = rng.integers(0, nq, (nq, 5)).astype(np.int32)
+        outs = [sorted(rng.integers(0, 3, rng.integers(0, 3)).tolist()) for _ in range(nq)]
+        off = np.zeros(nq + 1, dtype=np.int32)
+        off[1:] = np.cumsum([len(o) for o in outs])
+        ids = np.array([e for o in outs for e in o], dtype=np.int32)
+        dfa = ks.Dfa(trans, off, ids, tuple(str(i) for i in range(nq)), 3)
+        codes = rng.integers(0, 5, int(rng.integers(0, 20000))).astype(np.uint8)
+        want, rows = O.ref_run(dfa, codes, 1, 10, True)[:2]
+        rep = ks.run(dfa, ks.Sequence(codes), ks.EngineConfig(mode="locate"))
+        assert rep.per_expression_counts.tolist() == want.tolist(), trial
+        assert np.array_equal(rep.locations, rows), trial
+
+
+# ---------------------------------------------------------------- ranges / maps
+
+def test_scan_range_and_segment_map(ctx):
+    w = workloads.make(2, 1 << 18)
+    codes = ks.encode_bytes(w.ascii.tobytes())
+    dh = ctx.dfa(w.dfa)
+    sh = ctx.upload_codes(codes)
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        b, e = sorted(rng.integers(0, codes.size, 2).tolist())
+        entry = int(rng.integers(0, w.dfa.state_count))
+        want, last = O.ref_sequential_count(w.dfa, codes, b, e, entry)
+        got, ex, _ = ctx.scan_range(dh, sh, b, e, entry)
+        assert got.tolist() == want.tolist()
+        assert ex == last
+        # true-state entry (-1) == entry from the sequential state at b
+        _, sb = O.ref_sequential_count(w.dfa, codes, 0, b, 0)
+        want2, last2 = O.ref_sequential_count(w.dfa, codes, b, e, sb)
+        got2, ex2, _ = ctx.scan_range(dh, sh, b, e, -1)
+        assert got2.tolist() == want2.tolist() and ex2 == last2
+        m = ctx.segment_map(dh, sh, b, e)
+        for q in rng.integers(0, w.dfa.state_count, 5):
+            assert m[q] == O.ref_sequential_count(w.dfa, codes, b, e, int(q))[1]
+
+
+def test_segment_map_permutation(ctx):
+    dfa = workloads.permutation_dfa()
+    dh = ctx.dfa(dfa)
+    codes = np.random.default_rng(9).integers(0, 4, 70_000).astype(np.uint8)
+    sh = ctx.upload_codes(codes)
+    m = ctx.segment_map(dh, sh, 1000, 65_000)
+    g = int((codes[1000:65_000] == 2).sum())
+    assert m.tolist() == [(q + g) % 1024 for q in range(1024)]
+
+
+# ---------------------------------------------------------------- encode (K1)
+
+def test_device_encode_matches_host():
+    ctx = _native.context(0)
+    rng = np.random.default_rng(7)
+    for n in (0, 1, 63, 64, 65, 1000, 100_003):
+        raw = rng.integers(0, 256, n).astype(np.uint8)
+        mask = rng.random(n) < 0.6
+        raw[mask] = rng.choice(np.frombuffer(b"acgtACGTNn \n\r\t", np.uint8), int(mask.sum()))
+        sh = ctx.upload_ascii(raw.tobytes())
+        want = ks.encode_bytes(raw.tobytes())
+        assert sh.length == want.size
+        assert np.array_equal(sh.codes(), want)
+    # whitespace-free fast path + soft-mask bitmap
+    text = b"ACGTacgtNnxX" * 1000
+    sh = ctx.upload_ascii(text)
+    assert np.array_equal(sh.codes(), ks.encode_bytes(text))
+    soft = sh.softmask()
+    assert np.array_equal(soft, np.frombuffer(text, np.uint8) >= ord("a"))
+
+
+def test_device_encode_every_byte():
+    ctx = _native.context(0)
+    raw = bytes(range(256)) * 3
+    sh = ctx.upload_ascii(raw)
+    assert np.array_equal(sh.codes(), ks.encode_bytes(raw))
+
+
+def test_bad_codes_rejected(ctx):
+    with pytest.raises(ValueError):
+        ctx.upload_codes(np.array([0, 1, 7], dtype=np.uint8))
+
+
+# ---------------------------------------------------------------- match_chunk
+
+def test_match_chunk_vs_oracle(toy_dfa):
+    sym = ks.encode("acgtacgctacattta" * 3)
+    pss = ks.possible_starting_states(toy_dfa, 0, 1)
+    res = ks.match_chunk(toy_dfa, sym, 0, pss, ks.EngineConfig(mode="locate"))
+    for r in res:
+        c, last = O.ref_sequential_count(toy_dfa, sym, 0, None, r.init_state)
+        assert r.counts.tolist() == c.tolist()
+        assert r.last_state == last
+    for window in (0, 1, 4):
+        res = ks.match_chunk(toy_dfa, sym, 7, pss, ks.EngineConfig(window=window, mode="locate"))
+        for r in res:
+            c, last = O.ref_sequential_count(toy_dfa, sym, 0, None, r.init_state)
+            assert r.counts.tolist() == c.tolist() and r.last_state == last
+            if window == 0:
+                assert r.converged_at is None
+
+
+def test_match_chunk_reduce_roundtrip(toy_dfa):
+    seq = ks.sequence_from_text("ttacatctacgtttacta" * 7)
+    cfg = ks.EngineConfig(workers=4, mode="locate")
+    plan = ks.plan_chunks(seq, 4)
+    per = []
+    for i, (lo, hi) in enumerate(plan.bounds):
+        pss = np.array([0]) if i == 0 else ks.possible_starting_states(toy_dfa, *plan.boundary_symbols[i])
+        per.append(ks.match_chunk(toy_dfa, seq.symbols[lo:hi], lo, pss, cfg))
+    red = ks.reduce(toy_dfa, plan, per, cfg)
+    rep = ks.run(toy_dfa, seq, cfg)
+    assert red.per_expression_counts.tolist() == rep.per_expression_counts.tolist()
+    assert red.locations.tolist() == rep.locations.tolist()
+    for key in ("pss_sizes", "speculative_runs", "converged_runs", "convergence_steps"):
+        assert red.metadata[key] == rep.metadata[key]
