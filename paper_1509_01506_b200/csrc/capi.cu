@@ -146,9 +146,47 @@ ScanArgs base_args(const ks_dfa* dfa, const DevTable& T, const ks_seq* seq) {
     return a;
 }
 
-bool hist_fits(const ks_ctx* ctx, const ks_dfa* dfa) {
-    const size_t tables = dfa->tables_in_smem ? dfa->scan.tk_bytes + dfa->scan.t1_bytes : 0;
-    return tables + size_t(dfa->host.n_accept) * 4 + 1024 <= ctx->smem_optin;
+// Kernel choice for one table: the fast column-major kernel when the table
+// has a fast form and fits, else the generic row-major kernel.
+struct ScanPlan {
+    bool fast = false;
+    bool hist_smem = false;
+};
+
+ScanPlan plan_for(const ks_ctx* ctx, const ks_dfa* dfa, const DevTable& T) {
+    ScanPlan p;
+    const int32_t A = T.n_accept;
+    if (T.fast_k > 0 && dfa->tables_in_smem &&
+        fast_smem_bytes(kModeCount, int32_t(T.t1z_bytes / 2), 0, fast_threads()) <= ctx->smem_optin) {
+        p.fast = true;
+        p.hist_smem = fast_smem_bytes(kModeCount, int32_t(T.t1z_bytes / 2), A, fast_threads()) <= ctx->smem_optin;
+        return p;
+    }
+    const size_t tables = dfa->tables_in_smem ? T.tk_bytes + T.t1_bytes : 0;
+    p.hist_smem = tables + size_t(A) * 4 + 1024 <= ctx->smem_optin;
+    return p;
+}
+
+void geometry(const ks_ctx* ctx, const ks_dfa* dfa, const DevTable& T, const ScanPlan& p, int64_t begin,
+              int64_t end, int64_t* origin, int64_t* L, int64_t* nch) {
+    if (p.fast) {
+        chunk_geometry(begin, end, int64_t(ctx->num_sms) * fast_threads(), origin, L, nch);
+        return;
+    }
+    scan_geometry(ctx, begin, end, T.stride, dfa->tables_in_smem, int32_t(T.tk_bytes / 2), int32_t(T.t1_bytes / 2),
+                  p.hist_smem ? T.n_accept : 0, origin, L, nch);
+}
+
+int dispatch(ks_ctx* ctx, const ks_dfa* dfa, const DevTable& T, const ScanPlan& p, ScanArgs a, int mode,
+             int* launches) {
+    a.hist_smem = p.hist_smem ? 1 : 0;
+    if (p.fast) {
+        a.tk = T.tkc;
+        a.t1 = T.t1z;
+        a.t1_pad = int32_t(T.t1z_bytes / 2);
+        return launch_scan_fast(ctx, a, mode, T.fast_k, launches);
+    }
+    return launch_scan(ctx, a, mode, T.stride, dfa->tables_in_smem, launches);
 }
 
 // Map pass + monoid scan over [begin, end): writes per-chunk exclusive
@@ -166,7 +204,7 @@ int monoid_prefix(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t beg
     m.uniform_entry = 0;  // identity element
     m.n_accept = 0;
     m.chunk_exit = elems;
-    int rc = launch_scan(ctx, m, kModeMap, dfa->mono.stride, dfa->tables_in_smem, launches);
+    int rc = dispatch(ctx, dfa, dfa->mono, plan_for(ctx, dfa, dfa->mono), m, kModeMap, launches);
     if (rc != KS_OK) return rc;
     return exclusive_scan_monoid(ctx, elems, nch, dfa->d_prod, h.nm, excl, d_total, tmp, launches);
 }
@@ -195,8 +233,7 @@ int true_state_at(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t pos
         return KS_OK;
     }
     int64_t origin, L, nch;
-    scan_geometry(ctx, 0, pos, dfa->mono.stride, dfa->tables_in_smem, int32_t(dfa->mono.tk_bytes / 2),
-                  int32_t(dfa->mono.t1_bytes / 2), 0, &origin, &L, &nch);
+    geometry(ctx, dfa, dfa->mono, plan_for(ctx, dfa, dfa->mono), 0, pos, &origin, &L, &nch);
     int rc = ensure_scratch(ctx, size_t(nch) * 4 + exclusive_scan_monoid_tmp_bytes(nch) + 4096, &ar);
     if (rc) return rc;
     uint16_t* elems = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
@@ -234,9 +271,8 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
     }
 
     int64_t origin, L, nch;
-    const bool hist_smem = hist_fits(ctx, dfa);
-    scan_geometry(ctx, begin, end, dfa->scan.stride, dfa->tables_in_smem, int32_t(dfa->scan.tk_bytes / 2),
-                  int32_t(dfa->scan.t1_bytes / 2), hist_smem ? h.n_accept : 0, &origin, &L, &nch);
+    const ScanPlan plan = plan_for(ctx, dfa, dfa->scan);
+    geometry(ctx, dfa, dfa->scan, plan, begin, end, &origin, &L, &nch);
     if (end == begin) nch = 0;
 
     const bool mapscan = h.strategy == KS_STRATEGY_MAPSCAN;
@@ -277,7 +313,6 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
     a.origin = origin;
     a.chunk_len = L;
     a.nchunks = nch;
-    a.hist_smem = hist_smem ? 1 : 0;
     a.visits = visits;
     a.chunk_exit = chunk_exit;
     a.error = err;
@@ -298,8 +333,7 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
         a.chunk_entry = centry;
     }
     if (locate) a.chunk_rows = chunk_rows;
-    rc = launch_scan(ctx, a, locate ? kModeRows : kModeCount, dfa->scan.stride, dfa->tables_in_smem,
-                     &launches);
+    rc = dispatch(ctx, dfa, dfa->scan, plan, a, locate ? kModeRows : kModeCount, &launches);
     if (rc) return rc;
     KS_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
     rc = launch_finalize_counts(ctx, visits, h.n_accept, dfa->d_acc_out_off, dfa->d_acc_out_ids, counts,
@@ -320,8 +354,9 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
             e.chunk_row_off = row_off;
             e.rows = d_rows;
             e.visits = nullptr;
-            e.hist_smem = 0;
-            rc = launch_scan(ctx, e, kModeEmit, dfa->scan.stride, dfa->tables_in_smem, &launches);
+            ScanPlan pe = plan;
+            pe.hist_smem = false;
+            rc = dispatch(ctx, dfa, dfa->scan, pe, e, kModeEmit, &launches);
             if (rc) {
                 cudaFreeAsync(d_rows, ctx->stream);
                 return rc;
@@ -413,6 +448,12 @@ int upload_table(const CompiledTable& t, DevTable* d, char* blob, size_t* off, b
     d->t1_bytes = align16(t.t1.size() * 2);
     d->tk = reinterpret_cast<const uint16_t*>(place(t.tk.data(), t.tk.size() * 2));
     d->t1 = reinterpret_cast<const uint16_t*>(place(t.t1.data(), t.t1.size() * 2));
+    d->fast_k = t.fast_k;
+    d->t1z_bytes = align16(t.t1z.size() * 2);
+    if (t.fast_k) {
+        d->tkc = reinterpret_cast<const uint16_t*>(place(t.tkc.data(), t.tkc.size() * 2));
+        d->t1z = reinterpret_cast<const uint16_t*>(place(t.t1z.data(), t.t1z.size() * 2));
+    }
     return KS_OK;
 }
 
@@ -577,12 +618,16 @@ int ks_dfa_upload_ex(ks_ctx* ctx, const int32_t* transitions, int32_t n_states, 
     };
     rebase(d->scan.tk);
     rebase(d->scan.t1);
+    rebase(d->scan.tkc);
+    rebase(d->scan.t1z);
     rebase(d->d_acc_out_off);
     rebase(d->d_acc_out_ids);
     rebase(d->d_acc_outcnt);
     if (h.strategy == KS_STRATEGY_MAPSCAN) {
         rebase(d->mono.tk);
         rebase(d->mono.t1);
+        rebase(d->mono.tkc);
+        rebase(d->mono.t1z);
         rebase(d->d_prod);
         rebase(d->d_act0);
         rebase(d->d_action);
@@ -794,8 +839,7 @@ int ks_segment_map(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t be
         }
     } else {
         int64_t origin, L, nch;
-        scan_geometry(ctx, begin, end, dfa->mono.stride, dfa->tables_in_smem, int32_t(dfa->mono.tk_bytes / 2),
-                      int32_t(dfa->mono.t1_bytes / 2), 0, &origin, &L, &nch);
+        geometry(ctx, dfa, dfa->mono, plan_for(ctx, dfa, dfa->mono), begin, end, &origin, &L, &nch);
         uint16_t m = 0;
         if (end > begin) {
             Arena ar;

@@ -65,6 +65,31 @@ void build_stride_table(CompiledTable* t, size_t budget) {
             t->tk[size_t(s) * words + w] = uint16_t(x | (hit ? kFlag : 0));
         }
     }
+    // fast form
+    t->fast_k = 0;
+    t->tkc.clear();
+    t->t1z.clear();
+    if (nq + 1 <= 4096 && !(std::getenv("KS_DISABLE_FAST") && *std::getenv("KS_DISABLE_FAST") == '1')) {
+        const int fk = nq + 1 <= 256 ? 4 : (nq + 1 <= 1024 ? 3 : 2);
+        const int sb = 16 - 2 * fk;  // state bits
+        const int fw = 1 << (2 * fk);
+        const int z = nq;
+        t->fast_k = fk;
+        t->t1z.assign(size_t(nq + 1) * 5, uint16_t(z));
+        std::copy(t->t1.begin(), t->t1.end(), t->t1z.begin());
+        t->tkc.assign(size_t(1) << 16, uint16_t(z << 1));
+        for (int w = 0; w < fw; ++w) {
+            for (int s = 0; s < nq; ++s) {
+                int x = s;
+                bool hit = false;
+                for (int i = 0; i < fk; ++i) {
+                    x = t->t1[size_t(x) * 5 + ((w >> (2 * i)) & 3)];
+                    hit |= x < t->n_accept;
+                }
+                t->tkc[(size_t(w) << sb) + s] = uint16_t((x << 1) | (hit ? 0x8000 : 0));
+            }
+        }
+    }
     const uint16_t r = t->t1[4];
     bool resets = true;
     for (int s = 1; s < nq && resets; ++s) resets = t->t1[size_t(s) * 5 + 4] == r;

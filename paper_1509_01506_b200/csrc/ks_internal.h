@@ -41,6 +41,11 @@ struct CompiledTable {
     int reset_state = -1;            // internal id all states enter on OTHER, or -1
     std::vector<uint16_t> t1;        // nq x 5 single-symbol table (internal ids)
     std::vector<uint16_t> tk;        // nq x 4^K, entry = next | (hit on path ? kFlag : 0)
+    // fast form (nq + 1 <= 4096): 128 KiB column-major K-stride table with a
+    // sink state Z = nq; entry at [(w << (16 - 2K)) + s] = (next << 1) | hit
+    int fast_k = 0;                  // 0 = not eligible
+    std::vector<uint16_t> tkc;       // 65536 entries
+    std::vector<uint16_t> t1z;       // (nq + 1) x 5, row Z -> Z
 };
 
 struct HostDfa {
@@ -70,6 +75,10 @@ struct DevTable {
     const uint16_t* tk = nullptr;   // nq x 4^K
     int nq = 0, n_accept = 0, stride = 1, reset_state = -1;
     size_t tk_bytes = 0, t1_bytes = 0;
+    const uint16_t* tkc = nullptr;  // fast form (see CompiledTable)
+    const uint16_t* t1z = nullptr;
+    int fast_k = 0;
+    size_t t1z_bytes = 0;
 };
 
 struct SeqView {

@@ -307,13 +307,8 @@ __global__ void chunk_entry_kernel(const uint16_t* excl, int64_t n, const uint16
 
 }  // namespace
 
-void scan_geometry(const ks_ctx* ctx, int64_t begin, int64_t end, int stride, bool smem_tables,
-                   int32_t tk_pad, int32_t t1_pad, int32_t hist_words, int64_t* origin,
-                   int64_t* chunk_len, int64_t* nchunks) {
-    const size_t smem = scan_smem_bytes(smem_tables, tk_pad, t1_pad, hist_words);
-    ScanFn fn = pick_kernel(kModeCount, stride, smem_tables);
-    const LaunchShape sh = fn ? launch_shape(fn, smem) : LaunchShape{512, 1};
-    const int64_t threads = int64_t(ctx->num_sms) * sh.per_sm * sh.tpb;
+void chunk_geometry(int64_t begin, int64_t end, int64_t threads, int64_t* origin, int64_t* chunk_len,
+                    int64_t* nchunks) {
     const int64_t o = (begin >> 6) << 6;
     const int64_t span = max64(end - o, 1);
     int64_t per = (span + threads - 1) / threads;
@@ -323,6 +318,15 @@ void scan_geometry(const ks_ctx* ctx, int64_t begin, int64_t end, int stride, bo
     *origin = o;
     *chunk_len = per;
     *nchunks = (span + per - 1) / per;
+}
+
+void scan_geometry(const ks_ctx* ctx, int64_t begin, int64_t end, int stride, bool smem_tables,
+                   int32_t tk_pad, int32_t t1_pad, int32_t hist_words, int64_t* origin,
+                   int64_t* chunk_len, int64_t* nchunks) {
+    const size_t smem = scan_smem_bytes(smem_tables, tk_pad, t1_pad, hist_words);
+    ScanFn fn = pick_kernel(kModeCount, stride, smem_tables);
+    const LaunchShape sh = fn ? launch_shape(fn, smem) : LaunchShape{512, 1};
+    chunk_geometry(begin, end, int64_t(ctx->num_sms) * sh.per_sm * sh.tpb, origin, chunk_len, nchunks);
 }
 
 int launch_scan(ks_ctx* ctx, ScanArgs a, int mode, int stride, bool smem_tables, int* launches) {

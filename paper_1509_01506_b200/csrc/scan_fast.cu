@@ -1,0 +1,366 @@
+// Fast chunked DFA scan for automata with |Q| < 4096 (every config C1-C5).
+//
+// Layout (all in shared memory, one 1024-thread CTA per SM):
+//   * 128 KiB column-major K-stride table: entry for (word w, state s) at
+//     byte address (w << LC) | (s << 1), LC = 17 - 2K, value
+//     (next << 1) | (hit << 15) where hit = "a state with outputs was entered
+//     during these K bases".  Bit 15 lies inside the field [LC, 17) that the
+//     next K bases overwrite, so the next lookup address is a single LOP3
+//     bit-select of the previous entry and the funnel-shifted input word:
+//     per K bases the critical path is SHF -> LOP3 -> LDS.
+//   * the 1-base table (|Q|+1) x 5 (row-major, OTHER column included) for
+//     re-walks, OTHER blocks and the lookback;
+//   * a per-lane ring of deferred hits: a flagged step only stores its table
+//     address (predicated STS, no divergence); every 8 steps each lane
+//     re-walks its own ring entries with the 1-base table and histograms the
+//     accepting states it enters (shared atomics).  This replaces the
+//     reference's per-symbol CSR output loop (_kernels.py:26-28, 80-84).
+//   * a "sink" state Z = |Q| whose row never flags: lanes of a warp that
+//     have no work for a block (N-run blocks, finished chunks) ride the fast
+//     path in Z instead of diverging.
+// The lane/chunk/entry-state logic is the one of scan.cu (lookback, uniform
+// or per-chunk entry states).
+#include <algorithm>
+
+#include "scan_kernels.cuh"
+
+namespace ks {
+namespace {
+
+constexpr int kRing = 8;  // steps between ring drains (ring depth)
+constexpr int kFastThreads = 1024;
+constexpr uint32_t kRingStride = 4u * kFastThreads;  // bytes between ring slots
+
+__device__ __forceinline__ uint32_t lds16(uint32_t addr) {
+    unsigned short v;
+    asm("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+// d = (f & m) | (e & ~m) in one LOP3 (the compiler splits it otherwise).
+template <uint32_t M>
+__device__ __forceinline__ uint32_t bitsel(uint32_t f, uint32_t e) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(d) : "r"(f), "r"(e), "n"(M));
+    return d;
+}
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return uint32_t(__cvta_generic_to_shared(p));
+}
+
+// K input bases of step j shifted so they start at bit LC; bits outside
+// [LC, LC + 2K) are garbage (removed by the bit-select).  x0..x3 are the
+// block's 128 bits; compile-time j makes this one SHF (funnel) or nothing.
+template <int K>
+__device__ __forceinline__ uint32_t field(const uint4& x, int j) {
+    constexpr int LC = 17 - 2 * K;
+    const int sh = 2 * K * j - LC;  // right shift of the 128-bit stream
+    if (sh < 0) return x.x << (-sh);
+    const int q = sh >> 5, r = sh & 31;
+    const uint32_t lo = q == 0 ? x.x : q == 1 ? x.y : q == 2 ? x.z : x.w;
+    const uint32_t hi = q == 0 ? x.y : q == 1 ? x.z : q == 2 ? x.w : 0u;
+    if (r == 0) return lo;
+    return __funnelshift_r(lo, hi, r);
+}
+
+struct Ctx {
+    uint32_t tk;        // shared address of the K-stride table
+    uint32_t t1;        // shared address of the 1-base table
+    unsigned int* hist; // shared histogram or null
+    unsigned long long* visits;
+    const uint16_t* outcnt;
+    const int32_t* off;
+    const int32_t* ids;
+    int64_t* rows;
+    int64_t row_base;
+    uint32_t n_accept;
+};
+
+template <int MODE>
+struct Lane {
+    uint32_t nrows = 0;
+    int64_t cur = 0;
+};
+
+template <int MODE>
+__device__ __forceinline__ void record(const Ctx& c, Lane<MODE>& L, int64_t pos, uint32_t s) {
+    if constexpr (MODE == kModeCount || MODE == kModeRows) {
+        if (c.hist) atomicAdd(&c.hist[s], 1u);
+        else atomicAdd(&c.visits[s], 1ull);
+        if constexpr (MODE == kModeRows) L.nrows += __ldg(&c.outcnt[s]);
+    } else if constexpr (MODE == kModeEmit) {
+        const int k1 = __ldg(&c.off[s + 1]);
+        for (int k = __ldg(&c.off[s]); k < k1; ++k, ++L.cur) {
+            longlong2 r;
+            r.x = c.row_base + pos + 1;
+            r.y = __ldg(&c.ids[k]);
+            reinterpret_cast<longlong2*>(c.rows)[L.cur] = r;
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t step1(const Ctx& c, uint32_t s, uint32_t sym) {
+    return lds16(c.t1 + (s * 5u + sym) * 2u);
+}
+
+// Re-walk one deferred K-step (ring value = its table byte address, or a
+// direct single-base hit tagged with bit 31).
+template <int K, int MODE>
+__device__ __forceinline__ void rewalk(const Ctx& c, Lane<MODE>& L, uint32_t v, int64_t pos) {
+    constexpr int LC = 17 - 2 * K;
+    if (v >> 31) {
+        record<MODE>(c, L, pos, v & 0x7fffu);
+        return;
+    }
+    uint32_t s = (v >> 1) & ((1u << (LC - 1)) - 1u);
+    const uint32_t w = v >> LC;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        s = step1(c, s, (w >> (2 * i)) & 3u);
+        if (s < c.n_accept) record<MODE>(c, L, pos + i, s);
+    }
+}
+
+template <int K, int MODE>
+__device__ __forceinline__ void drain(const Ctx& c, Lane<MODE>& L, unsigned am, uint32_t rp0,
+                                      uint32_t& rp, uint32_t ring_stride) {
+    const uint32_t cnt = (rp - rp0) / kRingStride;
+    for (uint32_t k = 0;; ++k) {
+        const bool mine = k < cnt;
+        if (!__any_sync(am, mine)) break;
+        if (mine) rewalk<K, MODE>(c, L, lds32(rp0 + k * ring_stride), 0);
+    }
+    rp = rp0;
+}
+
+// One full, OTHER-free 64-base block.  `live` lanes record hits; others ride
+// along in the sink state.
+template <int K, int MODE>
+__device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint32_t s, const uint4& xb,
+                                               int64_t p0, unsigned am, uint32_t rp0, uint32_t& rp,
+                                               uint32_t ring_stride) {
+    const uint64_t w0 = (uint64_t(xb.y) << 32) | xb.x;
+    const uint64_t w1 = (uint64_t(xb.w) << 32) | xb.z;
+    constexpr int NL = 64 / K;
+    constexpr int LC = 17 - 2 * K;
+    constexpr uint32_t FM = ((1u << (2 * K)) - 1u) << LC;  // field mask
+    constexpr bool RING = MODE == kModeCount || MODE == kModeRows;
+    uint32_t e = s << 1;  // entry form of the current state (no flag)
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+        const uint32_t a = bitsel<FM>(field<K>(xb, j), e);
+        e = lds16(c.tk + a);
+        if constexpr (RING) {
+            if (e & 0x8000u) {
+                sts32(rp, a);
+                rp += ring_stride;
+            }
+            if ((j % kRing) == kRing - 1 || j == NL - 1) drain<K, MODE>(c, L, am, rp0, rp, ring_stride);
+        } else if constexpr (MODE == kModeEmit) {
+            if (e & 0x8000u) rewalk<K, MODE>(c, L, a, p0 + K * j);
+        }
+    }
+    s = (e >> 1) & ((1u << (LC - 1)) - 1u);
+#pragma unroll
+    for (int r = NL * K; r < 64; ++r) {  // K == 3 leaves one base
+        const uint32_t sym = uint32_t(r < 32 ? w0 >> (2 * r) : w1 >> (2 * (r - 32))) & 3u;
+        s = step1(c, s, sym);
+        if constexpr (MODE != kModeMap) {
+            if (s < c.n_accept) record<MODE>(c, L, p0 + r, s);
+        }
+    }
+    return s;
+}
+
+__device__ __forceinline__ uint32_t sym_at(const SeqView& q, int64_t p) {
+    const uint64_t m = __ldg(&q.nmask[p >> 6]);
+    if ((m >> (p & 63)) & 1ull) return 4u;
+    const uint64_t w = __ldg(&q.bases[p >> 5]);
+    return uint32_t(w >> (2 * (p & 31))) & 3u;
+}
+
+extern __shared__ __align__(128) unsigned char f_smem[];
+
+template <int K, int MODE>
+__global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
+    constexpr bool RING = MODE == kModeCount || MODE == kModeRows;
+    constexpr int TK_BYTES = 1 << 17;
+    unsigned char* p_t1 = f_smem + TK_BYTES;
+    unsigned char* p_ring = p_t1 + size_t(a.t1_pad) * 2;
+    unsigned int* s_hist = reinterpret_cast<unsigned int*>(
+        p_ring + (RING ? size_t(kRing) * 4 * blockDim.x : 0));
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(a.tk);
+        uint4* dst = reinterpret_cast<uint4*>(f_smem);
+        for (int i = threadIdx.x; i < TK_BYTES / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+        src = reinterpret_cast<const uint4*>(a.t1);
+        dst = reinterpret_cast<uint4*>(p_t1);
+        for (int i = threadIdx.x; i < a.t1_pad / 8; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
+    const bool hist_smem = RING && a.hist_smem;
+    if (hist_smem)
+        for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x) s_hist[i] = 0u;
+    __syncthreads();
+
+    Ctx c;
+    c.tk = smem_addr(f_smem);
+    c.t1 = smem_addr(p_t1);
+    c.hist = hist_smem ? s_hist : nullptr;
+    c.visits = a.visits;
+    c.outcnt = a.acc_outcnt;
+    c.off = a.acc_out_off;
+    c.ids = a.acc_out_ids;
+    c.rows = a.rows;
+    c.row_base = a.row_base;
+    c.n_accept = uint32_t(a.n_accept);
+    const uint32_t sink = uint32_t(a.nq);  // the sink state Z
+    const uint32_t ring_stride = kRingStride;
+    const uint32_t rp0 = smem_addr(p_ring) + 4u * threadIdx.x;
+    uint32_t rp = rp0;
+
+    const uint4* bases4 = reinterpret_cast<const uint4*>(a.seq.bases);
+    const uint64_t* nmask = a.seq.nmask;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t ch = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; ch < a.nchunks; ch += stride) {
+        const unsigned am = __activemask();
+        const int64_t cb = max64(a.begin, a.origin + ch * a.chunk_len);
+        const int64_t ce = min64(a.end, a.origin + (ch + 1) * a.chunk_len);
+
+        uint32_t s;
+        if (a.chunk_entry) {
+            s = a.chunk_entry[ch];
+        } else if (a.uniform_entry >= 0) {
+            s = uint32_t(a.uniform_entry);
+        } else {
+            const int64_t lb = max64(a.base_pos, cb - a.lookback);
+            s = uint32_t(lb == a.base_pos ? a.base_state : a.any_state);
+            for (int64_t p = lb; p < cb; ++p) s = step1(c, s, sym_at(a.seq, p));
+        }
+        Lane<MODE> L;
+        if constexpr (MODE == kModeEmit) L.cur = a.chunk_row_off[ch];
+
+        const int64_t b0 = cb >> 6;
+        const int nblk = int(((ce + 63) >> 6) - b0);
+        const int nmax = __reduce_max_sync(am, nblk);  // warp-uniform trip count
+        uint4 wb = __ldg(bases4 + b0);
+        uint64_t wm = __ldg(nmask + b0);
+        for (int i = 0; i < nmax; ++i) {
+            const bool has = i < nblk;
+            const int64_t b = b0 + (has ? i : 0);
+            // arrays are padded by two blocks: the prefetch never faults
+            const uint4 nb = __ldg(bases4 + b + 1);
+            const uint64_t nm = __ldg(nmask + b + 1);
+            const int64_t p0 = b << 6;
+            const int lo = int(max64(cb - p0, 0));
+            const int hi = int(min64(ce - p0, 64));
+            const uint64_t w0 = (uint64_t(wb.y) << 32) | wb.x;
+            const uint64_t w1 = (uint64_t(wb.w) << 32) | wb.z;
+            const bool alln = wm == ~0ull;
+            const bool fast = !has || ((lo == 0) && (hi == 64) && (wm == 0ull || (alln && a.reset_state >= 0)));
+            if (__all_sync(am, fast)) {
+                const bool live = has && !alln;
+                const uint32_t s2 = fast_block<K, MODE>(c, L, live ? s : sink, wb, p0, am, rp0, rp,
+                                                        ring_stride);
+                if (live) {
+                    s = s2;
+                } else if (has) {
+                    s = uint32_t(a.reset_state);
+                    if constexpr (MODE != kModeMap) {
+                        if (s < c.n_accept) {
+                            if constexpr (MODE == kModeEmit) {
+                                for (int q = 0; q < 64; ++q) record<MODE>(c, L, p0 + q, s);
+                            } else {
+                                if (c.hist) atomicAdd(&c.hist[s], 64u);
+                                else atomicAdd(&c.visits[s], 64ull);
+                                if constexpr (MODE == kModeRows) L.nrows += 64u * __ldg(&c.outcnt[s]);
+                            }
+                        }
+                    }
+                }
+            } else if (has) {
+                for (int q = lo; q < hi; ++q) {
+                    const uint32_t sym = ((wm >> q) & 1ull)
+                                             ? 4u
+                                             : uint32_t((q < 32 ? w0 >> (2 * q) : w1 >> (2 * (q - 32)))) & 3u;
+                    s = step1(c, s, sym);
+                    if constexpr (MODE != kModeMap) {
+                        if (s < c.n_accept) record<MODE>(c, L, p0 + q, s);
+                    }
+                }
+            }
+            if (has) {
+                wb = nb;
+                wm = nm;
+            }
+        }
+        if (a.chunk_exit) a.chunk_exit[ch] = uint16_t(s);
+        if constexpr (MODE == kModeRows) a.chunk_rows[ch] = L.nrows;
+        if constexpr (MODE == kModeEmit) {
+            if (L.cur != a.chunk_row_off[ch + 1]) atomicExch(a.error, 1);
+        }
+    }
+
+    if (hist_smem) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x)
+            if (s_hist[i]) atomicAdd(&a.visits[i], (unsigned long long)s_hist[i]);
+    }
+}
+
+using FastFn = void (*)(const ScanArgs);
+
+template <int K>
+FastFn pick_mode(int mode) {
+    switch (mode) {
+        case kModeCount: return scan_fast_kernel<K, kModeCount>;
+        case kModeRows: return scan_fast_kernel<K, kModeRows>;
+        case kModeEmit: return scan_fast_kernel<K, kModeEmit>;
+        case kModeMap: return scan_fast_kernel<K, kModeMap>;
+    }
+    return nullptr;
+}
+
+FastFn pick(int mode, int k) {
+    switch (k) {
+        case 2: return pick_mode<2>(mode);
+        case 3: return pick_mode<3>(mode);
+        case 4: return pick_mode<4>(mode);
+    }
+    return nullptr;
+}
+
+}  // namespace
+
+size_t fast_smem_bytes(int mode, int32_t t1_pad, int32_t hist_words, int threads) {
+    const bool ring = mode == kModeCount || mode == kModeRows;
+    return size_t(1 << 17) + size_t(t1_pad) * 2 + (ring ? size_t(kRing) * 4 * threads : 0) +
+           size_t(hist_words) * 4;
+}
+
+int fast_threads() { return kFastThreads; }
+
+int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
+    if (a.end <= a.begin || a.nchunks <= 0) return KS_OK;
+    if (!(mode == kModeCount || mode == kModeRows)) a.hist_smem = 0;
+    FastFn fn = pick(mode, k);
+    if (!fn) return fail(KS_E_INVALID, "fast scan: bad mode/stride");
+    const size_t smem = fast_smem_bytes(mode, a.t1_pad, a.hist_smem ? a.n_accept : 0, kFastThreads);
+    if (smem > ctx->smem_optin) return fail(KS_E_UNSUPPORTED, "fast scan: shared memory budget exceeded");
+    KS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    const int64_t need = (a.nchunks + kFastThreads - 1) / kFastThreads;
+    const int blocks = int(max64(1, min64(need, int64_t(ctx->num_sms))));
+    fn<<<blocks, kFastThreads, smem, ctx->stream>>>(a);
+    if (launches) ++*launches;
+    KS_CUDA(cudaGetLastError());
+    return KS_OK;
+}
+
+}  // namespace ks

@@ -75,6 +75,14 @@ void scan_geometry(const ks_ctx* ctx, int64_t begin, int64_t end, int stride, bo
                    int32_t tk_pad, int32_t t1_pad, int32_t hist_words, int64_t* origin,
                    int64_t* chunk_len, int64_t* nchunks);
 
+void chunk_geometry(int64_t begin, int64_t end, int64_t threads, int64_t* origin, int64_t* chunk_len,
+                    int64_t* nchunks);
+
+// Fast shared-memory kernel for tables with a fast form (csrc/scan_fast.cu).
+int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches);
+size_t fast_smem_bytes(int mode, int32_t t1_pad, int32_t hist_words, int threads);
+int fast_threads();
+
 // Prefix scans (csrc/prefix_scan.cu).
 int exclusive_scan_rows(ks_ctx* ctx, const uint32_t* in, int64_t n, int64_t* out_excl,
                         int64_t* d_total, void* tmp, int* launches);

@@ -34,7 +34,7 @@ DEFAULT_WINDOW = 10
 
 __all__ = [
     "DEFAULT_WINDOW", "EngineConfig", "ChunkResult", "MatchReport", "ReductionChainError",
-    "possible_starting_states", "match_chunk", "reduce", "run", "sequential_count",
+    "possible_starting_states", "match_chunk", "reduce", "run", "scan_bytes", "sequential_count",
 ]
 
 
@@ -152,6 +152,23 @@ def run(dfa: Dfa, seq: Sequence, cfg: EngineConfig = EngineConfig()) -> MatchRep
     metadata["input_name"] = getattr(seq, "source_name", "")
     metadata["elapsed_seconds"] = time.perf_counter() - t0
     return MatchReport(counts, total, locations, metadata, dstats)
+
+
+def scan_bytes(dfa: Dfa, data, mode: str = "count", device: int = 0):
+    """Raw-mode ASCII bytes (host buffer) -> (counts, rows | None) with the
+    encode on the device (ks_seq_upload_ascii): the same result as
+    ``run(dfa, Sequence(encode_bytes(data)))`` without the host encode."""
+    if mode not in ("count", "locate"):
+        raise ValueError(f"unknown mode {mode!r}")
+    ctx = _native.context(device)
+    dh = ctx.dfa(dfa)
+    sh = ctx.upload_ascii(data)
+    try:
+        if mode == "locate":
+            return ctx.locate(dh, sh)
+        return ctx.count(dh, sh), None
+    finally:
+        sh.free()
 
 
 def sequential_count(dfa: Dfa, seq: Sequence, device: int = 0) -> np.ndarray:

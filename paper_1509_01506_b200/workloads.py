@@ -170,10 +170,16 @@ def _markov3(rng, n: int) -> np.ndarray:
     return out
 
 
-def make(k: int, n: int | None = None) -> Workload:
-    """Build workload C<k> (optionally with a shorter sequence of length n)."""
+def make(k: int, n: int | None = None, shard: int = 0) -> Workload:
+    """Build workload C<k> (optionally with a shorter sequence of length n).
+
+    ``shard`` > 0 draws another independent slice of the same distribution
+    (sequence stream ``[1509, k, 0, shard]``; the patterns are shared) -- the
+    per-rank slices of the weak-scaling multi-GPU runs.
+    """
     n = FULL_SIZES[k] if n is None else int(n)
-    srng, prng = _rng(k, 0), _rng(k, 1)
+    srng = _rng(k, 0) if shard == 0 else np.random.default_rng([1509, k, 0, shard])
+    prng = _rng(k, 1)
     text = None
     if k == 1:
         codes = _iid_codes(srng, n, None)
