@@ -43,6 +43,7 @@ int encode_ascii_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, ks_se
 int pack_codes_device(ks_ctx* ctx, const uint8_t* d_codes, int64_t n, ks_seq* seq, int* d_flag,
                       int* launches);
 int unpack_codes_device(ks_ctx* ctx, const ks_seq* seq, uint8_t* d_out);
+int linear_softmask_device(ks_ctx* ctx, const ks_seq* seq, uint64_t* d_out);
 int launch_speculate(ks_ctx* ctx, const SeqView& seq, int32_t n_chunks, const int64_t* d_cbeg,
                      const int64_t* d_cend, const int64_t* d_pss_off, const uint16_t* d_pss,
                      const int64_t* h_pss_off, int32_t window, const uint16_t* t1, int32_t n_accept,
@@ -114,11 +115,7 @@ __global__ void walk_kernel(SeqView seq, int64_t begin, int64_t end, const uint1
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nq) return;
     uint32_t s = uniform_start >= 0 ? uint32_t(uniform_start) : uint32_t(q);
-    for (int64_t p = begin; p < end; ++p) {
-        const bool other = (seq.nmask[p >> 6] >> (p & 63)) & 1ull;
-        const uint32_t sym = other ? 4u : uint32_t(seq.bases[p >> 5] >> (2 * (p & 31))) & 3u;
-        s = t1[s * 5u + sym];
-    }
+    for (int64_t p = begin; p < end; ++p) s = t1[s * 5u + seq_sym(seq, p)];
     out[q] = uint16_t(s);
 }
 
@@ -127,6 +124,7 @@ SeqView view_of(const ks_seq* s) {
     v.bases = s->d_bases;
     v.nmask = s->d_nmask;
     v.n = s->n;
+    v.lb = s->lb;
     return v;
 }
 
@@ -157,9 +155,9 @@ ScanPlan plan_for(const ks_ctx* ctx, const ks_dfa* dfa, const DevTable& T) {
     ScanPlan p;
     const int32_t A = T.n_accept;
     if (T.fast_k > 0 && dfa->tables_in_smem &&
-        fast_smem_bytes(kModeCount, int32_t(T.t1z_bytes / 2), 0, fast_threads()) <= ctx->smem_optin) {
-        p.fast = true;
-        p.hist_smem = fast_smem_bytes(kModeCount, int32_t(T.t1z_bytes / 2), A, fast_threads()) <= ctx->smem_optin;
+        fast_smem_bytes(kModeCount, int32_t(T.t1z_bytes / 2), A, fast_threads()) <= ctx->smem_optin) {
+        p.fast = true;  // the fast kernel keeps its visit histogram in shared memory
+        p.hist_smem = true;
         return p;
     }
     const size_t tables = dfa->tables_in_smem ? T.tk_bytes + T.t1_bytes : 0;
@@ -167,14 +165,14 @@ ScanPlan plan_for(const ks_ctx* ctx, const ks_dfa* dfa, const DevTable& T) {
     return p;
 }
 
-void geometry(const ks_ctx* ctx, const ks_dfa* dfa, const DevTable& T, const ScanPlan& p, int64_t begin,
-              int64_t end, int64_t* origin, int64_t* L, int64_t* nch) {
-    if (p.fast) {
-        chunk_geometry(begin, end, int64_t(ctx->num_sms) * fast_threads(), origin, L, nch);
-        return;
-    }
-    scan_geometry(ctx, begin, end, T.stride, dfa->tables_in_smem, int32_t(T.tk_bytes / 2), int32_t(T.t1_bytes / 2),
-                  p.hist_smem ? T.n_accept : 0, origin, L, nch);
+// Lane chunks are the sequence's units (64 << lb bases, see SeqView): chunk c
+// of a scan over [begin, end) is unit begin / S + c, clipped to the range.
+void geometry(const ks_seq* seq, int64_t begin, int64_t end, int64_t* origin, int64_t* L, int64_t* nch) {
+    const int64_t S = int64_t(64) << seq->lb;
+    const int64_t u0 = begin / S;
+    *origin = u0 * S;
+    *L = S;
+    *nch = end > begin ? (end - 1) / S - u0 + 1 : 0;
 }
 
 int dispatch(ks_ctx* ctx, const ks_dfa* dfa, const DevTable& T, const ScanPlan& p, ScanArgs a, int mode,
@@ -184,6 +182,13 @@ int dispatch(ks_ctx* ctx, const ks_dfa* dfa, const DevTable& T, const ScanPlan& 
         a.tk = T.tkc;
         a.t1 = T.t1z;
         a.t1_pad = int32_t(T.t1z_bytes / 2);
+        // high hit rates: count with direct histograms instead of the ring
+        if (mode == kModeCount && T.fast_k == 2) {
+            const char* env = std::getenv("KS_DIRECT");
+            const bool direct = env && *env ? *env == '1' : T.hit_rate > 0.01;
+            if (direct && fast_smem_bytes(kModeCountDirectId, 0, T.n_accept, fast_threads()) <= ctx->smem_optin)
+                mode = kModeCountDirectId;
+        }
         return launch_scan_fast(ctx, a, mode, T.fast_k, launches);
     }
     return launch_scan(ctx, a, mode, T.stride, dfa->tables_in_smem, launches);
@@ -233,7 +238,7 @@ int true_state_at(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t pos
         return KS_OK;
     }
     int64_t origin, L, nch;
-    geometry(ctx, dfa, dfa->mono, plan_for(ctx, dfa, dfa->mono), 0, pos, &origin, &L, &nch);
+    geometry(seq, 0, pos, &origin, &L, &nch);
     int rc = ensure_scratch(ctx, size_t(nch) * 4 + exclusive_scan_monoid_tmp_bytes(nch) + 4096, &ar);
     if (rc) return rc;
     uint16_t* elems = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
@@ -272,7 +277,7 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
 
     int64_t origin, L, nch;
     const ScanPlan plan = plan_for(ctx, dfa, dfa->scan);
-    geometry(ctx, dfa, dfa->scan, plan, begin, end, &origin, &L, &nch);
+    geometry(seq, begin, end, &origin, &L, &nch);
     if (end == begin) nch = 0;
 
     const bool mapscan = h.strategy == KS_STRATEGY_MAPSCAN;
@@ -449,6 +454,7 @@ int upload_table(const CompiledTable& t, DevTable* d, char* blob, size_t* off, b
     d->tk = reinterpret_cast<const uint16_t*>(place(t.tk.data(), t.tk.size() * 2));
     d->t1 = reinterpret_cast<const uint16_t*>(place(t.t1.data(), t.t1.size() * 2));
     d->fast_k = t.fast_k;
+    d->hit_rate = t.hit_rate;
     d->t1z_bytes = align16(t.t1z.size() * 2);
     if (t.fast_k) {
         d->tkc = reinterpret_cast<const uint16_t*>(place(t.tkc.data(), t.tkc.size() * 2));
@@ -457,10 +463,34 @@ int upload_table(const CompiledTable& t, DevTable* d, char* blob, size_t* off, b
     return KS_OK;
 }
 
+// Blocks per unit (2^lb): the fast scan gives each warp one tile (32 units)
+// at a time, so pick the unit size that minimises (tiles per warp, rounded
+// up) x (unit length + lookback), i.e. wave quantisation vs entry overhead.
+int choose_lb(const ks_ctx* ctx, int64_t n) {
+    if (const char* e = std::getenv("KS_TILE_LB"); e && *e) return std::min(6, std::max(0, std::atoi(e)));
+    const int64_t warps = int64_t(ctx->num_sms) * 32;
+    int best = 2;
+    double best_cost = 1e300;
+    for (int lb = 2; lb <= 5; ++lb) {
+        const int64_t tile = int64_t(2048) << lb;
+        const int64_t tiles = (n + tile - 1) / tile;
+        const int64_t per_warp = (tiles + warps - 1) / warps;
+        const double cost = double(per_warp) * double((64 << lb) + 32);
+        if (cost <= best_cost) {
+            best_cost = cost;
+            best = lb;
+        }
+    }
+    return best;
+}
+
 int seq_alloc(ks_ctx* ctx, int64_t n_capacity, ks_seq** out) {
     ks_seq* s = new ks_seq();
     s->ctx = ctx;
-    s->n_blocks = (n_capacity + 63) / 64 + 2;
+    s->lb = choose_lb(ctx, n_capacity);
+    const int64_t tile_blocks = int64_t(32) << s->lb;
+    const int64_t blocks = (n_capacity + 63) / 64;
+    s->n_blocks = ((blocks + tile_blocks - 1) / tile_blocks + 1) * tile_blocks;
     const size_t bytes = size_t(s->n_blocks) * 32;
     cudaError_t e = cudaMalloc(&s->d_blob, bytes);
     if (e != cudaSuccess) {
@@ -777,7 +807,15 @@ int ks_seq_download_softmask(ks_ctx* ctx, const ks_seq* s, uint64_t* out, int64_
     DeviceGuard guard(ctx->device);
     const int64_t have = (s->n + 63) / 64;
     if (n_words < have) return fail(KS_E_INVALID, "softmask buffer too small");
-    if (have) KS_CUDA(cudaMemcpyAsync(out, s->d_soft, size_t(have) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    if (have) {
+        Arena ar;
+        int rc = ensure_scratch(ctx, size_t(have) * 8 + 256, &ar);
+        if (rc) return rc;
+        uint64_t* d = static_cast<uint64_t*>(ar.take(size_t(have) * 8));
+        rc = linear_softmask_device(ctx, s, d);
+        if (rc) return rc;
+        KS_CUDA(cudaMemcpyAsync(out, d, size_t(have) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    }
     KS_CUDA(cudaStreamSynchronize(ctx->stream));
     return KS_OK;
 }
@@ -839,7 +877,7 @@ int ks_segment_map(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t be
         }
     } else {
         int64_t origin, L, nch;
-        geometry(ctx, dfa, dfa->mono, plan_for(ctx, dfa, dfa->mono), begin, end, &origin, &L, &nch);
+        geometry(seq, begin, end, &origin, &L, &nch);
         uint16_t m = 0;
         if (end > begin) {
             Arena ar;

@@ -82,13 +82,35 @@ void build_stride_table(CompiledTable* t, size_t budget) {
             for (int s = 0; s < nq; ++s) {
                 int x = s;
                 bool hit = false;
+                bool first_hit = false;
                 for (int i = 0; i < fk; ++i) {
                     x = t->t1[size_t(x) * 5 + ((w >> (2 * i)) & 3)];
                     hit |= x < t->n_accept;
+                    if (i == 0) first_hit = x < t->n_accept;
                 }
-                t->tkc[(size_t(w) << sb) + s] = uint16_t((x << 1) | (hit ? 0x8000 : 0));
+                // bit 15: any state on the K-step accepting (ring modes); for
+                // K = 2 also bit 13: the intermediate one, bit 14: the final one
+                // (direct counting).  Bits >= LC are overwritten by the next
+                // lookup's input field, so they never reach an address.
+                uint32_t v = uint32_t(x << 1) | (hit ? 0x8000u : 0u);
+                if (fk == 2) v |= (first_hit ? 0x2000u : 0u) | (x < t->n_accept ? 0x4000u : 0u);
+                t->tkc[(size_t(w) << sb) + s] = uint16_t(v);
             }
         }
+    }
+    {  // hit-rate estimate: 64 Ki uniform random bases from state 0 (xorshift)
+        uint64_t z = 0x9E3779B97F4A7C15ull;
+        int x = 0;
+        int64_t hits = 0;
+        const int steps = 1 << 16;
+        for (int i = 0; i < steps; ++i) {
+            z ^= z << 13;
+            z ^= z >> 7;
+            z ^= z << 17;
+            x = t->t1[size_t(x) * 5 + (z & 3)];
+            hits += x < t->n_accept;
+        }
+        t->hit_rate = double(hits) / steps;
     }
     const uint16_t r = t->t1[4];
     bool resets = true;

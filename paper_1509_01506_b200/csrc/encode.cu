@@ -85,32 +85,42 @@ __device__ __forceinline__ Packed pack_block(const uint8_t* in, int64_t n_bytes,
     return r;
 }
 
-__global__ void encode_inplace_kernel(const uint8_t* in, int64_t n_bytes, int64_t n_blocks,
+__global__ void encode_inplace_kernel(const uint8_t* in, int64_t n_bytes, int64_t n_blocks, int lb,
                                       uint64_t* bases, uint64_t* nmask, uint64_t* soft,
                                       uint32_t* kept, int* any_ws) {
     for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < n_blocks;
          b += int64_t(gridDim.x) * blockDim.x) {
         Packed r = pack_block(in, n_bytes, b, false);
         const int lim = int(min64(64, n_bytes - (b << 6)));
-        reinterpret_cast<ulonglong2*>(bases)[b] = make_ulonglong2(r.w0, r.w1);
-        nmask[b] = r.n;
-        soft[b] = r.soft;
+        const int64_t slot = blk_slot(b, lb);
+        reinterpret_cast<ulonglong2*>(bases)[slot] = make_ulonglong2(r.w0, r.w1);
+        nmask[slot] = r.n;
+        soft[slot] = r.soft;
         kept[b] = r.kept;
         if (int(r.kept) != lim) atomicOr(any_ws, 1);
     }
 }
 
-// OR `nbits` bits (value v, nbits <= 64) at bit position `bit` of array a.
-__device__ __forceinline__ void or_bits(uint64_t* a, int64_t bit, uint64_t v, int nbits) {
+// Storage word of linear 64-bit word w of a stream with `per_block` words
+// per 64-base block (2 for bases, 1 for the bitmaps).
+__device__ __forceinline__ int64_t word_slot(int64_t w, int per_block, int lb) {
+    return per_block == 2 ? 2 * blk_slot(w >> 1, lb) + (w & 1) : blk_slot(w, lb);
+}
+
+// OR `nbits` bits (value v, nbits <= 64) at linear bit position `bit`.
+__device__ __forceinline__ void or_bits(uint64_t* a, int64_t bit, uint64_t v, int nbits, int per_block,
+                                        int lb) {
     if (nbits <= 0 || v == 0) return;
     const int64_t w = bit >> 6;
     const int sh = int(bit & 63);
-    atomicOr(reinterpret_cast<unsigned long long*>(&a[w]), (unsigned long long)(v << sh));
+    atomicOr(reinterpret_cast<unsigned long long*>(&a[word_slot(w, per_block, lb)]),
+             (unsigned long long)(v << sh));
     if (sh && sh + nbits > 64)
-        atomicOr(reinterpret_cast<unsigned long long*>(&a[w + 1]), (unsigned long long)(v >> (64 - sh)));
+        atomicOr(reinterpret_cast<unsigned long long*>(&a[word_slot(w + 1, per_block, lb)]),
+                 (unsigned long long)(v >> (64 - sh)));
 }
 
-__global__ void encode_compact_kernel(const uint8_t* in, int64_t n_bytes, int64_t n_blocks,
+__global__ void encode_compact_kernel(const uint8_t* in, int64_t n_bytes, int64_t n_blocks, int lb,
                                       const int64_t* out_pos, uint64_t* bases, uint64_t* nmask,
                                       uint64_t* soft) {
     for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < n_blocks;
@@ -119,15 +129,15 @@ __global__ void encode_compact_kernel(const uint8_t* in, int64_t n_bytes, int64_
         const int64_t o = out_pos[b];
         const int k = int(r.kept);
         // bases: 2k bits starting at bit 2*o; split into the two 64-bit halves
-        or_bits(bases, 2 * o, r.w0, std::min(64, 2 * k));
-        if (k > 32) or_bits(bases, 2 * o + 64, r.w1, 2 * (k - 32));
-        or_bits(nmask, o, r.n, k);
-        or_bits(soft, o, r.soft, k);
+        or_bits(bases, 2 * o, r.w0, std::min(64, 2 * k), 2, lb);
+        if (k > 32) or_bits(bases, 2 * o + 64, r.w1, 2 * (k - 32), 2, lb);
+        or_bits(nmask, o, r.n, k, 1, lb);
+        or_bits(soft, o, r.soft, k, 1, lb);
     }
 }
 
-__global__ void pack_codes_kernel(const uint8_t* codes, int64_t n, int64_t n_blocks, uint64_t* bases,
-                                  uint64_t* nmask, int* bad) {
+__global__ void pack_codes_kernel(const uint8_t* codes, int64_t n, int64_t n_blocks, int lb,
+                                  uint64_t* bases, uint64_t* nmask, int* bad) {
     for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < n_blocks;
          b += int64_t(gridDim.x) * blockDim.x) {
         const int64_t p0 = b << 6;
@@ -162,18 +172,22 @@ __global__ void pack_codes_kernel(const uint8_t* codes, int64_t n, int64_t n_blo
                 m |= uint64_t(c >= 4u) << i;
             }
         }
-        reinterpret_cast<ulonglong2*>(bases)[b] = make_ulonglong2(w0, w1);
-        nmask[b] = m;
+        const int64_t slot = blk_slot(b, lb);
+        reinterpret_cast<ulonglong2*>(bases)[slot] = make_ulonglong2(w0, w1);
+        nmask[slot] = m;
     }
 }
 
-__global__ void unpack_codes_kernel(const uint64_t* bases, const uint64_t* nmask, int64_t n,
-                                    uint8_t* out) {
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += int64_t(gridDim.x) * blockDim.x) {
-        const bool other = (nmask[i >> 6] >> (i & 63)) & 1ull;
-        out[i] = other ? 4 : uint8_t((bases[i >> 5] >> (2 * (i & 31))) & 3ull);
-    }
+__global__ void unpack_codes_kernel(SeqView q, uint8_t* out) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < q.n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        out[i] = uint8_t(seq_sym(q, i));
+}
+
+__global__ void linear_mask_kernel(const uint64_t* mask, int64_t n_words, int lb, uint64_t* out) {
+    for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < n_words;
+         g += int64_t(gridDim.x) * blockDim.x)
+        out[g] = mask[blk_slot(g, lb)];
 }
 
 int grid_for(const ks_ctx* ctx, int64_t items, int threads) {
@@ -210,7 +224,7 @@ int encode_ascii_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, ks_se
     }
     const int threads = 256;
     encode_inplace_kernel<<<grid_for(ctx, nb, threads), threads, 0, ctx->stream>>>(
-        d_in, n_bytes, nb, seq->d_bases, seq->d_nmask, seq->d_soft, kept, flag);
+        d_in, n_bytes, nb, seq->lb, seq->d_bases, seq->d_nmask, seq->d_soft, kept, flag);
     if (launches) ++*launches;
     KS_CUDA(cudaGetLastError());
     int any_ws = 0;
@@ -227,7 +241,7 @@ int encode_ascii_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, ks_se
     KS_CUDA(cudaMemsetAsync(seq->d_nmask, 0, words * 8, ctx->stream));
     KS_CUDA(cudaMemsetAsync(seq->d_soft, 0, words * 8, ctx->stream));
     encode_compact_kernel<<<grid_for(ctx, nb, threads), threads, 0, ctx->stream>>>(
-        d_in, n_bytes, nb, pos, seq->d_bases, seq->d_nmask, seq->d_soft);
+        d_in, n_bytes, nb, seq->lb, pos, seq->d_bases, seq->d_nmask, seq->d_soft);
     if (launches) ++*launches;
     KS_CUDA(cudaGetLastError());
     int64_t total = 0;
@@ -244,7 +258,7 @@ int pack_codes_device(ks_ctx* ctx, const uint8_t* d_codes, int64_t n, ks_seq* se
     if (nb == 0) return KS_OK;
     const int threads = 256;
     pack_codes_kernel<<<grid_for(ctx, nb, threads), threads, 0, ctx->stream>>>(
-        d_codes, n, nb, seq->d_bases, seq->d_nmask, d_flag);
+        d_codes, n, nb, seq->lb, seq->d_bases, seq->d_nmask, d_flag);
     if (launches) ++*launches;
     KS_CUDA(cudaGetLastError());
     return KS_OK;
@@ -253,8 +267,22 @@ int pack_codes_device(ks_ctx* ctx, const uint8_t* d_codes, int64_t n, ks_seq* se
 int unpack_codes_device(ks_ctx* ctx, const ks_seq* seq, uint8_t* d_out) {
     if (seq->n == 0) return KS_OK;
     const int threads = 256;
-    unpack_codes_kernel<<<grid_for(ctx, seq->n, threads), threads, 0, ctx->stream>>>(
-        seq->d_bases, seq->d_nmask, seq->n, d_out);
+    SeqView q;
+    q.bases = seq->d_bases;
+    q.nmask = seq->d_nmask;
+    q.n = seq->n;
+    q.lb = seq->lb;
+    unpack_codes_kernel<<<grid_for(ctx, seq->n, threads), threads, 0, ctx->stream>>>(q, d_out);
+    KS_CUDA(cudaGetLastError());
+    return KS_OK;
+}
+
+int linear_softmask_device(ks_ctx* ctx, const ks_seq* seq, uint64_t* d_out) {
+    const int64_t words = (seq->n + 63) / 64;
+    if (words == 0) return KS_OK;
+    const int threads = 256;
+    linear_mask_kernel<<<grid_for(ctx, words, threads), threads, 0, ctx->stream>>>(seq->d_soft, words, seq->lb,
+                                                                                     d_out);
     KS_CUDA(cudaGetLastError());
     return KS_OK;
 }

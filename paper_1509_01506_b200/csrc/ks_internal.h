@@ -44,6 +44,7 @@ struct CompiledTable {
     // fast form (nq + 1 <= 4096): 128 KiB column-major K-stride table with a
     // sink state Z = nq; entry at [(w << (16 - 2K)) + s] = (next << 1) | hit
     int fast_k = 0;                  // 0 = not eligible
+    double hit_rate = 0;             // accepting-state visits per base on uniform random input
     std::vector<uint16_t> tkc;       // 65536 entries
     std::vector<uint16_t> t1z;       // (nq + 1) x 5, row Z -> Z
 };
@@ -79,13 +80,37 @@ struct DevTable {
     const uint16_t* t1z = nullptr;
     int fast_k = 0;
     size_t t1z_bytes = 0;
+    double hit_rate = 0;
 };
 
+// Packed sequence layout ("lane-tiled").  The sequence is cut into units of
+// B = 2^lb blocks (64 bases each); 32 consecutive units form a tile.  Within a
+// tile, block k of unit l is stored at block slot (k << 5) | l, so the 32
+// lanes of a warp that scan the 32 units of a tile read block k with one
+// fully coalesced 512-byte load.  bases: 16 B per block slot (2-bit codes,
+// base i of the block at bit 2i); nmask/soft: 8 B per block slot.
 struct SeqView {
-    const uint64_t* bases = nullptr;  // 2-bit codes, 32 per word (base i at bits 2*(i%32))
-    const uint64_t* nmask = nullptr;  // OTHER bitmap, 64 per word
+    const uint64_t* bases = nullptr;
+    const uint64_t* nmask = nullptr;
     int64_t n = 0;
+    int32_t lb = 4;   // log2(blocks per unit)
 };
+
+// Block slot of global block g (= position >> 6).
+__host__ __device__ inline int64_t blk_slot(int64_t g, int lb) {
+    const int64_t u = g >> lb;
+    return ((u >> 5) << (5 + lb)) | ((g & ((int64_t(1) << lb) - 1)) << 5) | (u & 31);
+}
+
+#ifdef __CUDACC__
+// Symbol code (0..4) at position p.
+__device__ __forceinline__ uint32_t seq_sym(const SeqView& q, int64_t p) {
+    const int64_t slot = blk_slot(p >> 6, q.lb);
+    const int i = int(p & 63);
+    if ((__ldg(&q.nmask[slot]) >> i) & 1ull) return 4u;
+    return uint32_t(__ldg(&q.bases[2 * slot + (i >> 5)]) >> (2 * (i & 31))) & 3u;
+}
+#endif
 
 }  // namespace ks
 
@@ -126,5 +151,6 @@ struct ks_seq {
     uint64_t* d_nmask = nullptr;
     uint64_t* d_soft = nullptr;
     void* d_blob = nullptr;
-    int64_t n_blocks = 0;   // 64-base blocks allocated (with padding)
+    int64_t n_blocks = 0;   // block slots allocated (whole tiles + one padding tile)
+    int32_t lb = 4;         // log2(blocks per unit), see SeqView
 };

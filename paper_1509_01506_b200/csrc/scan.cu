@@ -78,12 +78,6 @@ __device__ __forceinline__ uint32_t bits128(uint64_t w0, uint64_t w1, int off, i
     return uint32_t(v) & ((1u << width) - 1u);
 }
 
-__device__ __forceinline__ uint32_t sym_at(const SeqView& q, int64_t p) {
-    const uint64_t m = __ldg(&q.nmask[p >> 6]);
-    if ((m >> (p & 63)) & 1ull) return 4u;
-    const uint64_t w = __ldg(&q.bases[p >> 5]);
-    return uint32_t(w >> (2 * (p & 31))) & 3u;
-}
 
 // Re-walk the K bases of a flagged stride step with the 1-base table,
 // recording every accepting state entered.
@@ -166,7 +160,7 @@ __global__ void __launch_bounds__(1024, 1) scan_kernel(const ScanArgs a) {
         } else {
             const int64_t lb = max64(a.base_pos, cb - a.lookback);
             s = uint32_t(lb == a.base_pos ? a.base_state : a.any_state);
-            for (int64_t p = lb; p < cb; ++p) s = T.one(s * 5u + sym_at(a.seq, p));
+            for (int64_t p = lb; p < cb; ++p) s = T.one(s * 5u + seq_sym(a.seq, p));
         }
 
         Sink<MODE> sink;
@@ -182,12 +176,14 @@ __global__ void __launch_bounds__(1024, 1) scan_kernel(const ScanArgs a) {
 
         int64_t b = cb >> 6;
         const int64_t bend = (ce + 63) >> 6;
-        uint4 wb = __ldg(bases4 + b);
-        uint64_t wm = __ldg(nmask + b);
+        const int lb = a.seq.lb;
+        uint4 wb = __ldg(bases4 + blk_slot(b, lb));
+        uint64_t wm = __ldg(nmask + blk_slot(b, lb));
         for (; b < bend; ++b) {
-            // arrays are padded by two blocks: the prefetch never faults
-            const uint4 nb = __ldg(bases4 + b + 1);
-            const uint64_t nm = __ldg(nmask + b + 1);
+            // arrays are padded by a whole tile: the prefetch never faults
+            const int64_t ns = blk_slot(b + 1, lb);
+            const uint4 nb = __ldg(bases4 + ns);
+            const uint64_t nm = __ldg(nmask + ns);
             const int64_t p0 = b << 6;
             const int lo = int(max64(cb - p0, 0));
             const int hi = int(min64(ce - p0, 64));

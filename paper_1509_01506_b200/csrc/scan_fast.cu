@@ -28,6 +28,11 @@ namespace ks {
 namespace {
 
 constexpr int kRing = 8;  // steps between ring drains (ring depth)
+// Count mode with direct shared-memory histograms instead of the ring (K = 2,
+// high hit rates): bit 13 of an entry = the intermediate state is accepting
+// (counted per (first base, previous state) and resolved at the end), bit 14
+// = the final state is accepting (counted per state).  No re-walks at all.
+constexpr int kModeCountDirect = 4;
 constexpr int kFastThreads = 1024;
 constexpr uint32_t kRingStride = 4u * kFastThreads;  // bytes between ring slots
 
@@ -51,6 +56,15 @@ __device__ __forceinline__ uint32_t bitsel(uint32_t f, uint32_t e) {
     asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(d) : "r"(f), "r"(e), "n"(M));
     return d;
 }
+__device__ __forceinline__ void red_shared_add(uint32_t addr, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+// Predicated shared-memory increment (no branch around it).
+__device__ __forceinline__ void red_shared_inc_if(uint32_t addr, uint32_t cond) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %1, 0;\n\t@p red.shared.add.u32 [%0], 1;\n\t}"
+        ::"r"(addr), "r"(cond) : "memory");
+}
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return uint32_t(__cvta_generic_to_shared(p));
 }
@@ -73,8 +87,9 @@ __device__ __forceinline__ uint32_t field(const uint4& x, int j) {
 struct Ctx {
     uint32_t tk;        // shared address of the K-stride table
     uint32_t t1;        // shared address of the 1-base table
-    unsigned int* hist; // shared histogram or null
-    unsigned long long* visits;
+    const uint16_t* t1g;  // the same table in global memory (direct mode)
+    uint32_t hist2;     // direct mode: (first base, previous state) counters
+    uint32_t hist;      // shared address of the visit histogram (count/rows)
     const uint16_t* outcnt;
     const int32_t* off;
     const int32_t* ids;
@@ -91,9 +106,8 @@ struct Lane {
 
 template <int MODE>
 __device__ __forceinline__ void record(const Ctx& c, Lane<MODE>& L, int64_t pos, uint32_t s) {
-    if constexpr (MODE == kModeCount || MODE == kModeRows) {
-        if (c.hist) atomicAdd(&c.hist[s], 1u);
-        else atomicAdd(&c.visits[s], 1ull);
+    if constexpr (MODE == kModeCount || MODE == kModeRows || MODE == kModeCountDirect) {
+        red_shared_add(c.hist + 4u * s, 1u);
         if constexpr (MODE == kModeRows) L.nrows += __ldg(&c.outcnt[s]);
     } else if constexpr (MODE == kModeEmit) {
         const int k1 = __ldg(&c.off[s + 1]);
@@ -106,24 +120,21 @@ __device__ __forceinline__ void record(const Ctx& c, Lane<MODE>& L, int64_t pos,
     }
 }
 
+template <int MODE>
 __device__ __forceinline__ uint32_t step1(const Ctx& c, uint32_t s, uint32_t sym) {
+    if constexpr (MODE == kModeCountDirect) return __ldg(c.t1g + s * 5u + sym);
     return lds16(c.t1 + (s * 5u + sym) * 2u);
 }
 
-// Re-walk one deferred K-step (ring value = its table byte address, or a
-// direct single-base hit tagged with bit 31).
+// Re-walk one deferred K-step (ring value = its table byte address).
 template <int K, int MODE>
 __device__ __forceinline__ void rewalk(const Ctx& c, Lane<MODE>& L, uint32_t v, int64_t pos) {
     constexpr int LC = 17 - 2 * K;
-    if (v >> 31) {
-        record<MODE>(c, L, pos, v & 0x7fffu);
-        return;
-    }
     uint32_t s = (v >> 1) & ((1u << (LC - 1)) - 1u);
     const uint32_t w = v >> LC;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-        s = step1(c, s, (w >> (2 * i)) & 3u);
+        s = step1<MODE>(c, s, (w >> (2 * i)) & 3u);
         if (s < c.n_accept) record<MODE>(c, L, pos + i, s);
     }
 }
@@ -132,11 +143,9 @@ template <int K, int MODE>
 __device__ __forceinline__ void drain(const Ctx& c, Lane<MODE>& L, unsigned am, uint32_t rp0,
                                       uint32_t& rp, uint32_t ring_stride) {
     const uint32_t cnt = (rp - rp0) / kRingStride;
-    for (uint32_t k = 0;; ++k) {
-        const bool mine = k < cnt;
-        if (!__any_sync(am, mine)) break;
-        if (mine) rewalk<K, MODE>(c, L, lds32(rp0 + k * ring_stride), 0);
-    }
+    const uint32_t kmax = __reduce_max_sync(am, cnt);  // warp-uniform trip count
+    for (uint32_t k = 0; k < kmax; ++k)
+        if (k < cnt) rewalk<K, MODE>(c, L, lds32(rp0 + k * ring_stride), 0);
     rp = rp0;
 }
 
@@ -165,13 +174,17 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
             if ((j % kRing) == kRing - 1 || j == NL - 1) drain<K, MODE>(c, L, am, rp0, rp, ring_stride);
         } else if constexpr (MODE == kModeEmit) {
             if (e & 0x8000u) rewalk<K, MODE>(c, L, a, p0 + K * j);
+        } else if constexpr (MODE == kModeCountDirect) {
+            static_assert(K == 2, "direct counting is K = 2 only");
+            red_shared_inc_if(c.hist2 + ((a & 0x7FFEu) << 1), e & 0x2000u);
+            red_shared_inc_if(c.hist + ((e & 0x1FFEu) << 1), e & 0x4000u);
         }
     }
     s = (e >> 1) & ((1u << (LC - 1)) - 1u);
 #pragma unroll
     for (int r = NL * K; r < 64; ++r) {  // K == 3 leaves one base
         const uint32_t sym = uint32_t(r < 32 ? w0 >> (2 * r) : w1 >> (2 * (r - 32))) & 3u;
-        s = step1(c, s, sym);
+        s = step1<MODE>(c, s, sym);
         if constexpr (MODE != kModeMap) {
             if (s < c.n_accept) record<MODE>(c, L, p0 + r, s);
         }
@@ -179,41 +192,44 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
     return s;
 }
 
-__device__ __forceinline__ uint32_t sym_at(const SeqView& q, int64_t p) {
-    const uint64_t m = __ldg(&q.nmask[p >> 6]);
-    if ((m >> (p & 63)) & 1ull) return 4u;
-    const uint64_t w = __ldg(&q.bases[p >> 5]);
-    return uint32_t(w >> (2 * (p & 31))) & 3u;
-}
 
 extern __shared__ __align__(128) unsigned char f_smem[];
 
 template <int K, int MODE>
 __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     constexpr bool RING = MODE == kModeCount || MODE == kModeRows;
+    constexpr bool DIRECT = MODE == kModeCountDirect;
+    constexpr bool HIST = RING || DIRECT;
     constexpr int TK_BYTES = 1 << 17;
+    constexpr int H2_WORDS = 4 << 12;  // (first base, state) for K = 2
+    // layout: table | t1 (not in direct mode) | ring (ring modes) | hist | hist2 (direct)
     unsigned char* p_t1 = f_smem + TK_BYTES;
-    unsigned char* p_ring = p_t1 + size_t(a.t1_pad) * 2;
+    unsigned char* p_ring = p_t1 + (DIRECT ? 0 : size_t(a.t1_pad) * 2);
     unsigned int* s_hist = reinterpret_cast<unsigned int*>(
         p_ring + (RING ? size_t(kRing) * 4 * blockDim.x : 0));
+    unsigned int* s_hist2 = s_hist + ((a.n_accept + 3) & ~3);
     {
         const uint4* src = reinterpret_cast<const uint4*>(a.tk);
         uint4* dst = reinterpret_cast<uint4*>(f_smem);
         for (int i = threadIdx.x; i < TK_BYTES / 16; i += blockDim.x) dst[i] = __ldg(src + i);
-        src = reinterpret_cast<const uint4*>(a.t1);
-        dst = reinterpret_cast<uint4*>(p_t1);
-        for (int i = threadIdx.x; i < a.t1_pad / 8; i += blockDim.x) dst[i] = __ldg(src + i);
+        if constexpr (!DIRECT) {
+            src = reinterpret_cast<const uint4*>(a.t1);
+            dst = reinterpret_cast<uint4*>(p_t1);
+            for (int i = threadIdx.x; i < a.t1_pad / 8; i += blockDim.x) dst[i] = __ldg(src + i);
+        }
     }
-    const bool hist_smem = RING && a.hist_smem;
-    if (hist_smem)
+    if constexpr (HIST)
         for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x) s_hist[i] = 0u;
+    if constexpr (DIRECT)
+        for (int i = threadIdx.x; i < H2_WORDS; i += blockDim.x) s_hist2[i] = 0u;
     __syncthreads();
 
     Ctx c;
     c.tk = smem_addr(f_smem);
     c.t1 = smem_addr(p_t1);
-    c.hist = hist_smem ? s_hist : nullptr;
-    c.visits = a.visits;
+    c.hist = smem_addr(s_hist);
+    c.hist2 = smem_addr(s_hist2);
+    c.t1g = a.t1;
     c.outcnt = a.acc_outcnt;
     c.off = a.acc_out_off;
     c.ids = a.acc_out_ids;
@@ -227,37 +243,66 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
 
     const uint4* bases4 = reinterpret_cast<const uint4*>(a.seq.bases);
     const uint64_t* nmask = a.seq.nmask;
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t ch = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; ch < a.nchunks; ch += stride) {
-        const unsigned am = __activemask();
-        const int64_t cb = max64(a.begin, a.origin + ch * a.chunk_len);
-        const int64_t ce = min64(a.end, a.origin + (ch + 1) * a.chunk_len);
+    const int lb = a.seq.lb;
+    const int lane = threadIdx.x & 31;
+    // Warp w scans tiles t0 + w, t0 + w + nwarps, ...: lane l takes unit
+    // 32 t + l, so each block load of the warp is one contiguous 512 B run.
+    const int64_t u0 = a.origin / a.chunk_len;
+    const int64_t t0 = u0 >> 5;
+    const int64_t t1 = (u0 + a.nchunks - 1) >> 5;
+    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    constexpr unsigned am = 0xffffffffu;
+    for (int64_t t = t0 + ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); t <= t1; t += nwarps) {
+        const int64_t u = (t << 5) + lane;
+        const int64_t ch = u - u0;
+        const bool active = ch >= 0 && ch < a.nchunks;
+        const int64_t cb = active ? max64(a.begin, u * a.chunk_len) : 0;
+        const int64_t ce = active ? min64(a.end, (u + 1) * a.chunk_len) : 0;
 
-        uint32_t s;
-        if (a.chunk_entry) {
+        uint32_t s = sink;
+        if (!active) {
+        } else if (a.chunk_entry) {
             s = a.chunk_entry[ch];
         } else if (a.uniform_entry >= 0) {
             s = uint32_t(a.uniform_entry);
         } else {
-            const int64_t lb = max64(a.base_pos, cb - a.lookback);
-            s = uint32_t(lb == a.base_pos ? a.base_state : a.any_state);
-            for (int64_t p = lb; p < cb; ++p) s = step1(c, s, sym_at(a.seq, p));
+            const int64_t lbp = max64(a.base_pos, cb - a.lookback);
+            s = uint32_t(lbp == a.base_pos ? a.base_state : a.any_state);
+            int64_t lbk = -1;
+            uint4 xb = make_uint4(0, 0, 0, 0);
+            uint64_t xm = 0;
+            for (int64_t p = lbp; p < cb; ++p) {  // <= 64 positions, <= 2 blocks
+                if ((p >> 6) != lbk) {
+                    lbk = p >> 6;
+                    const int64_t slot = blk_slot(lbk, lb);
+                    xb = __ldg(bases4 + slot);
+                    xm = __ldg(nmask + slot);
+                }
+                const int q = int(p & 63);
+                const uint32_t word = q < 16 ? xb.x : q < 32 ? xb.y : q < 48 ? xb.z : xb.w;
+                const uint32_t sym = ((xm >> q) & 1ull) ? 4u : (word >> (2 * (q & 15))) & 3u;
+                s = step1<MODE>(c, s, sym);
+            }
         }
         Lane<MODE> L;
-        if constexpr (MODE == kModeEmit) L.cur = a.chunk_row_off[ch];
+        if constexpr (MODE == kModeEmit) L.cur = active ? a.chunk_row_off[ch] : 0;
 
-        const int64_t b0 = cb >> 6;
-        const int nblk = int(((ce + 63) >> 6) - b0);
+        // block k of this unit sits at slot ubase + 32 k
+        const int64_t ubase = (t << (5 + lb)) | lane;
+        const int64_t gfirst = u << lb;  // global block index of the unit's first block
+        const int k0 = active ? int((cb >> 6) - gfirst) : 0;
+        const int nblk = active ? int(((ce + 63) >> 6) - (cb >> 6)) : 0;
         const int nmax = __reduce_max_sync(am, nblk);  // warp-uniform trip count
-        uint4 wb = __ldg(bases4 + b0);
-        uint64_t wm = __ldg(nmask + b0);
+        uint4 wb = __ldg(bases4 + ubase + (int64_t(k0) << 5));
+        uint64_t wm = __ldg(nmask + ubase + (int64_t(k0) << 5));
         for (int i = 0; i < nmax; ++i) {
             const bool has = i < nblk;
-            const int64_t b = b0 + (has ? i : 0);
-            // arrays are padded by two blocks: the prefetch never faults
-            const uint4 nb = __ldg(bases4 + b + 1);
-            const uint64_t nm = __ldg(nmask + b + 1);
-            const int64_t p0 = b << 6;
+            const int k = k0 + (has ? i : 0);
+            // the next slot exists: arrays are padded by a whole tile
+            const int64_t ns = ubase + (int64_t(k + 1) << 5);
+            const uint4 nb = __ldg(bases4 + ns);
+            const uint64_t nm = __ldg(nmask + ns);
+            const int64_t p0 = (gfirst + k) << 6;
             const int lo = int(max64(cb - p0, 0));
             const int hi = int(min64(ce - p0, 64));
             const uint64_t w0 = (uint64_t(wb.y) << 32) | wb.x;
@@ -276,9 +321,8 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                         if (s < c.n_accept) {
                             if constexpr (MODE == kModeEmit) {
                                 for (int q = 0; q < 64; ++q) record<MODE>(c, L, p0 + q, s);
-                            } else {
-                                if (c.hist) atomicAdd(&c.hist[s], 64u);
-                                else atomicAdd(&c.visits[s], 64ull);
+                            } else {  // count / rows / direct
+                                red_shared_add(c.hist + 4u * s, 64u);
                                 if constexpr (MODE == kModeRows) L.nrows += 64u * __ldg(&c.outcnt[s]);
                             }
                         }
@@ -289,7 +333,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                     const uint32_t sym = ((wm >> q) & 1ull)
                                              ? 4u
                                              : uint32_t((q < 32 ? w0 >> (2 * q) : w1 >> (2 * (q - 32)))) & 3u;
-                    s = step1(c, s, sym);
+                    s = step1<MODE>(c, s, sym);
                     if constexpr (MODE != kModeMap) {
                         if (s < c.n_accept) record<MODE>(c, L, p0 + q, s);
                     }
@@ -300,17 +344,27 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                 wm = nm;
             }
         }
-        if (a.chunk_exit) a.chunk_exit[ch] = uint16_t(s);
-        if constexpr (MODE == kModeRows) a.chunk_rows[ch] = L.nrows;
-        if constexpr (MODE == kModeEmit) {
-            if (L.cur != a.chunk_row_off[ch + 1]) atomicExch(a.error, 1);
+        if (active) {
+            if (a.chunk_exit) a.chunk_exit[ch] = uint16_t(s);
+            if constexpr (MODE == kModeRows) a.chunk_rows[ch] = L.nrows;
+            if constexpr (MODE == kModeEmit) {
+                if (L.cur != a.chunk_row_off[ch + 1]) atomicExch(a.error, 1);
+            }
         }
     }
 
-    if (hist_smem) {
+    if constexpr (HIST) {
         __syncthreads();
         for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x)
             if (s_hist[i]) atomicAdd(&a.visits[i], (unsigned long long)s_hist[i]);
+    }
+    if constexpr (DIRECT) {  // resolve (first base, previous state) -> intermediate state
+        for (int i = threadIdx.x; i < H2_WORDS; i += blockDim.x) {
+            const unsigned int n = s_hist2[i];
+            if (!n) continue;
+            const uint32_t s1 = __ldg(a.t1 + (i & 0xFFF) * 5 + (i >> 12));
+            atomicAdd(&a.visits[s1], (unsigned long long)n);
+        }
     }
 }
 
@@ -319,6 +373,9 @@ using FastFn = void (*)(const ScanArgs);
 template <int K>
 FastFn pick_mode(int mode) {
     switch (mode) {
+        case kModeCountDirect:
+            if constexpr (K == 2) return scan_fast_kernel<2, kModeCountDirect>;
+            return nullptr;
         case kModeCount: return scan_fast_kernel<K, kModeCount>;
         case kModeRows: return scan_fast_kernel<K, kModeRows>;
         case kModeEmit: return scan_fast_kernel<K, kModeEmit>;
@@ -339,6 +396,8 @@ FastFn pick(int mode, int k) {
 }  // namespace
 
 size_t fast_smem_bytes(int mode, int32_t t1_pad, int32_t hist_words, int threads) {
+    if (mode == kModeCountDirect)
+        return size_t(1 << 17) + size_t((hist_words + 3) & ~3) * 4 + size_t(4 << 12) * 4;
     const bool ring = mode == kModeCount || mode == kModeRows;
     return size_t(1 << 17) + size_t(t1_pad) * 2 + (ring ? size_t(kRing) * 4 * threads : 0) +
            size_t(hist_words) * 4;
@@ -348,14 +407,17 @@ int fast_threads() { return kFastThreads; }
 
 int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
     if (a.end <= a.begin || a.nchunks <= 0) return KS_OK;
-    if (!(mode == kModeCount || mode == kModeRows)) a.hist_smem = 0;
+    const bool ring = mode == kModeCount || mode == kModeRows || mode == kModeCountDirect;
+    a.hist_smem = ring ? 1 : 0;
     FastFn fn = pick(mode, k);
     if (!fn) return fail(KS_E_INVALID, "fast scan: bad mode/stride");
-    const size_t smem = fast_smem_bytes(mode, a.t1_pad, a.hist_smem ? a.n_accept : 0, kFastThreads);
+    const size_t smem = fast_smem_bytes(mode, a.t1_pad, ring ? a.n_accept : 0, kFastThreads);
     if (smem > ctx->smem_optin) return fail(KS_E_UNSUPPORTED, "fast scan: shared memory budget exceeded");
     KS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    const int64_t need = (a.nchunks + kFastThreads - 1) / kFastThreads;
+    const int64_t u0 = a.origin / a.chunk_len;
+    const int64_t tiles = ((u0 + a.nchunks - 1) >> 5) - (u0 >> 5) + 1;
+    const int64_t need = (tiles * 32 + kFastThreads - 1) / kFastThreads;
     const int blocks = int(max64(1, min64(need, int64_t(ctx->num_sms))));
     fn<<<blocks, kFastThreads, smem, ctx->stream>>>(a);
     if (launches) ++*launches;

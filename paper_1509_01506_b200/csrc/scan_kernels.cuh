@@ -27,7 +27,7 @@
 
 namespace ks {
 
-enum ScanMode : int { kModeCount = 0, kModeRows = 1, kModeEmit = 2, kModeMap = 3 };
+enum ScanMode : int { kModeCount = 0, kModeRows = 1, kModeEmit = 2, kModeMap = 3, kModeCountDirectId = 4 };
 
 struct ScanArgs {
     SeqView seq;

@@ -27,11 +27,6 @@ struct SpecTask {
     int32_t first;  // pss index (>= 1) carried by lane 1
 };
 
-__device__ __forceinline__ uint32_t spec_sym(const SeqView& q, int64_t p) {
-    const uint64_t m = __ldg(&q.nmask[p >> 6]);
-    if ((m >> (p & 63)) & 1ull) return 4u;
-    return uint32_t(__ldg(&q.bases[p >> 5]) >> (2 * (p & 31))) & 3u;
-}
 
 __device__ __forceinline__ void add_outputs(long long* row, uint32_t s, int32_t n_accept,
                                             const int32_t* off, const int32_t* ids, long long v) {
@@ -58,7 +53,7 @@ __global__ void speculate_kernel(SeqView seq, const int64_t* cbeg, const int64_t
     uint32_t s = pss[o + (live ? run : 0)];
     int32_t conv = -1;
     for (int64_t j = 0; j < weff; ++j) {
-        const uint32_t sym = spec_sym(seq, cb + j);
+        const uint32_t sym = seq_sym(seq, cb + j);
         s = t1[s * 5u + sym];
         const uint32_t s0 = __shfl_sync(0xffffffffu, s, 0);
         const unsigned same = __match_any_sync(0xffffffffu, s) & 1u;

@@ -1,0 +1,7 @@
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+python tools/exp_scan.py --config 3 --n 268435456 --variants default,generic > gpurun_out/exp2_c3.txt 2>&1
+python tools/exp_scan.py --config 4 --n 268435456 --variants default,generic > gpurun_out/exp2_c4.txt 2>&1
+python tools/exp_scan.py --config 2 --n 268435456 --variants default,generic > gpurun_out/exp2_c2.txt 2>&1
+CMD="python tools/exp_scan.py --config 3 --n 268435456 --reps 1"
+$CMD > gpurun_out/exp2_plain.txt 2>&1 && ncu --set full --clock-control none --import-source on -k regex:scan_fast -s 1 -c 1 -o gpurun_out/prof_fast2_c3 $CMD > gpurun_out/ncu_exp2.log 2>&1
+echo done
