@@ -270,6 +270,24 @@ int ref_run(const int32_t* trans, int32_t nq, const int32_t* out_off, const int3
     return rc;
 }
 
+/* scan_from with location rows (_kernels.py:18-40): rows [g_off + j + 1, e]. */
+int64_t ref_scan_rows(const int32_t* trans, const int32_t* out_off, const int32_t* out_ids, const uint8_t* sym,
+                      int64_t start, int64_t end, int64_t state, int64_t g_off, int64_t* counts, int64_t** rows_out,
+                      int64_t* n_rows) {
+    Rows r = {NULL, 0, 0};
+    int64_t s = state;
+    for (int64_t j = start; j < end; ++j) {
+        s = trans[s * OTHER_SYMS + sym[j]];
+        for (int32_t k = out_off[s]; k < out_off[s + 1]; ++k) {
+            counts[out_ids[k]] += 1;
+            if (rows_push(&r, g_off + j + 1, out_ids[k])) return -1;
+        }
+    }
+    *rows_out = r.rows;
+    *n_rows = r.n;
+    return s;
+}
+
 int64_t ref_effective_workers(int64_t n, int64_t workers) {
     int64_t cap = n > 1 ? n : 1;
     return workers < cap ? workers : cap;
