@@ -1,6 +1,13 @@
-# usage: bash tools/gpu_round.sh [tag]   (run on the GPU box via gpurun)
+# usage: bash tools/gpu_round.sh TAG   (on the GPU box via gpurun)
 TAG=${1:-r}
+mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo "smoke rc=$?"
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu_$TAG.log
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu_$TAG.log
 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.log; echo "bench rc=$?"
 for c in 1 2 4 5; do python bench.py --config $c --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_${TAG}_c$c.json 2>> gpurun_out/bench_$TAG.log; done
+python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_${TAG}_ref.json 2>> gpurun_out/bench_$TAG.log
+CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1"
+$CMD > gpurun_out/plain_$TAG.json 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu1_$TAG.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:scan_fast -s 3 -c 1 -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu2_$TAG.log 2>&1
+echo "ncu rc=$?"
