@@ -65,6 +65,13 @@ __device__ __forceinline__ void red_shared_inc_if(uint32_t addr, uint32_t cond) 
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %1, 0;\n\t@p red.shared.add.u32 [%0], 1;\n\t}"
         ::"r"(addr), "r"(cond) : "memory");
 }
+// Keep a value in a register (stops the compiler from re-deriving shared
+// window bases / reloading constants inside the drain loops).
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+    uint32_t r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(x));
+    return r;
+}
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return uint32_t(__cvta_generic_to_shared(p));
 }
@@ -139,13 +146,28 @@ __device__ __forceinline__ void rewalk(const Ctx& c, Lane<MODE>& L, uint32_t v, 
     }
 }
 
+// Count/rows resolution of one deferred step.  For K = 2 the entry's bits
+// 13/14 say which of the two states accepts: re-reading the entry gives the
+// final state directly and the intermediate one is only re-derived when it
+// accepts.
+template <int K, int MODE>
+__device__ __forceinline__ void resolve(const Ctx& c, Lane<MODE>& L, uint32_t a) {
+    if constexpr (K == 2) {
+        const uint32_t e = lds16(c.tk + a);
+        if (e & 0x2000u) record<MODE>(c, L, 0, step1<MODE>(c, (a >> 1) & 0xFFFu, (a >> 13) & 3u));
+        if (e & 0x4000u) record<MODE>(c, L, 0, (e >> 1) & 0xFFFu);
+    } else {
+        rewalk<K, MODE>(c, L, a, 0);
+    }
+}
+
 template <int K, int MODE>
 __device__ __forceinline__ void drain(const Ctx& c, Lane<MODE>& L, unsigned am, uint32_t rp0,
                                       uint32_t& rp, uint32_t ring_stride) {
     const uint32_t cnt = (rp - rp0) / kRingStride;
     const uint32_t kmax = __reduce_max_sync(am, cnt);  // warp-uniform trip count
     for (uint32_t k = 0; k < kmax; ++k)
-        if (k < cnt) rewalk<K, MODE>(c, L, lds32(rp0 + k * ring_stride), 0);
+        if (k < cnt) resolve<K, MODE>(c, L, lds32(rp0 + k * ring_stride));
     rp = rp0;
 }
 
@@ -226,8 +248,8 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
 
     Ctx c;
     c.tk = smem_addr(f_smem);
-    c.t1 = smem_addr(p_t1);
-    c.hist = smem_addr(s_hist);
+    c.t1 = opaque(smem_addr(p_t1));
+    c.hist = opaque(smem_addr(s_hist));
     c.hist2 = smem_addr(s_hist2);
     c.t1g = a.t1;
     c.outcnt = a.acc_outcnt;
@@ -235,7 +257,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     c.ids = a.acc_out_ids;
     c.rows = a.rows;
     c.row_base = a.row_base;
-    c.n_accept = uint32_t(a.n_accept);
+    c.n_accept = opaque(uint32_t(a.n_accept));
     const uint32_t sink = uint32_t(a.nq);  // the sink state Z
     const uint32_t ring_stride = kRingStride;
     const uint32_t rp0 = smem_addr(p_ring) + 4u * threadIdx.x;
@@ -293,22 +315,31 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
         const int k0 = active ? int((cb >> 6) - gfirst) : 0;
         const int nblk = active ? int(((ce + 63) >> 6) - (cb >> 6)) : 0;
         const int nmax = __reduce_max_sync(am, nblk);  // warp-uniform trip count
-        uint4 wb = __ldg(bases4 + ubase + (int64_t(k0) << 5));
-        uint64_t wm = __ldg(nmask + ubase + (int64_t(k0) << 5));
+        // full (uncut) blocks of this unit are [kfl, kfh)
+        const int kfl = k0 + ((cb & 63) != 0);
+        const int kfh = active ? int((ce >> 6) - gfirst) : 0;
+        const bool resets = a.reset_state >= 0;
+        const uint4* pb = bases4 + ubase + (int64_t(k0) << 5);
+        const uint64_t* pm = nmask + ubase + (int64_t(k0) << 5);
+        uint4 wb = __ldg(pb);
+        uint64_t wm = __ldg(pm);
         for (int i = 0; i < nmax; ++i) {
             const bool has = i < nblk;
             const int k = k0 + (has ? i : 0);
             // the next slot exists: arrays are padded by a whole tile
-            const int64_t ns = ubase + (int64_t(k + 1) << 5);
-            const uint4 nb = __ldg(bases4 + ns);
-            const uint64_t nm = __ldg(nmask + ns);
+            if (has) {
+                pb += 32;
+                pm += 32;
+            }
+            const uint4 nb = __ldg(pb);
+            const uint64_t nm = __ldg(pm);
             const int64_t p0 = (gfirst + k) << 6;
-            const int lo = int(max64(cb - p0, 0));
-            const int hi = int(min64(ce - p0, 64));
             const uint64_t w0 = (uint64_t(wb.y) << 32) | wb.x;
             const uint64_t w1 = (uint64_t(wb.w) << 32) | wb.z;
-            const bool alln = wm == ~0ull;
-            const bool fast = !has || ((lo == 0) && (hi == 64) && (wm == 0ull || (alln && a.reset_state >= 0)));
+            const uint32_t mlo = uint32_t(wm), mhi = uint32_t(wm >> 32);
+            const bool alln = (mlo & mhi) == ~0u;
+            const bool clean = (mlo | mhi) == 0u;
+            const bool fast = !has || (k >= kfl && k < kfh && (clean || (alln && resets)));
             if (__all_sync(am, fast)) {
                 const bool live = has && !alln;
                 const uint32_t s2 = fast_block<K, MODE>(c, L, live ? s : sink, wb, p0, am, rp0, rp,
@@ -329,6 +360,8 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                     }
                 }
             } else if (has) {
+                const int lo = int(max64(cb - p0, 0));
+                const int hi = int(min64(ce - p0, 64));
                 for (int q = lo; q < hi; ++q) {
                     const uint32_t sym = ((wm >> q) & 1ull)
                                              ? 4u
