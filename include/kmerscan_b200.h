@@ -128,6 +128,22 @@ KS_API int ks_count(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t* 
 KS_API int ks_locate(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t* counts_out,
               int64_t** rows_out, int64_t* n_rows);
 
+/* Asynchronous ks_count on the device-resident sequence: enqueues the scan,
+ * the count reduction and the copy of the int64 counts into `counts_pinned`
+ * (page-locked host memory) without waiting.  ks_async_wait synchronises and
+ * reports the summed scan-kernel time of the calls since the last wait. */
+KS_API int ks_count_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t* counts_pinned);
+KS_API int ks_async_wait(ks_ctx* ctx, float* scan_ms_total, int32_t* calls, int32_t* launches);
+
+/* Counts straight from a HOST buffer of raw ASCII (the end-to-end call):
+ * pieces are copied host->device on a copy stream while the previous piece
+ * is encoded and scanned (each piece entering in the state the previous one
+ * left), so transfer, encode and scan overlap.  Same result as
+ * ks_seq_upload_ascii + ks_count; input with whitespace falls back to that
+ * path.  Pinned host memory gives full PCIe bandwidth. */
+KS_API int ks_count_host_ascii(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int64_t n_bytes,
+                               int64_t* counts_out);
+
 /* Range form used by match_chunk (engine.py:94-134) and by sharded scans:
  * scan positions [begin, end) of seq entering at `entry_state` (original
  * state id; -1 = the true state of the sequence at `begin`, derived on

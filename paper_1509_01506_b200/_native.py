@@ -58,6 +58,7 @@ EXPORTED = (
     "ks_version", "ks_dfa_upload", "ks_dfa_upload_ex", "ks_dfa_info_get", "ks_dfa_free",
     "ks_seq_upload_codes", "ks_seq_upload_ascii", "ks_seq_encode_device", "ks_seq_length",
     "ks_seq_download_codes", "ks_seq_download_softmask", "ks_seq_free", "ks_count", "ks_locate",
+    "ks_count_host_ascii", "ks_count_async", "ks_async_wait",
     "ks_scan_range", "ks_segment_map", "ks_speculate", "ks_free",
 )
 
@@ -93,6 +94,9 @@ def _declare(lib) -> None:
         "ks_seq_free": (C.c_int, [_P]),
         "ks_count": (C.c_int, [_P, _P, _P, _i64p]),
         "ks_locate": (C.c_int, [_P, _P, _P, _i64p, C.POINTER(_i64p), _i64p]),
+        "ks_count_host_ascii": (C.c_int, [_P, _P, _u8p, C.c_int64, _i64p]),
+        "ks_count_async": (C.c_int, [_P, _P, _P, _i64p]),
+        "ks_async_wait": (C.c_int, [_P, C.POINTER(C.c_float), _i32p, _i32p]),
         "ks_scan_range": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, C.c_int32, C.c_int64, _i64p,
                                     _i32p, C.POINTER(_i64p), _i64p]),
         "ks_segment_map": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, _i32p]),
@@ -293,6 +297,30 @@ class DeviceContext:
         counts = np.zeros(max(dfa.n_expressions, 1), dtype=np.int64)
         with self.lock:
             _check(library().ks_count(self.handle, dfa.handle, seq.handle, _ptr(counts, C.c_int64)))
+        return counts[: dfa.n_expressions]
+
+    def count_async(self, dfa: DfaHandle, seq: SeqHandle, out_pinned: np.ndarray) -> None:
+        """Enqueue a count; the int64 counts land in `out_pinned` (a view of
+        page-locked memory) once :meth:`async_wait` returns."""
+        if out_pinned.dtype != np.int64 or out_pinned.size < max(dfa.n_expressions, 1):
+            raise ValueError("out_pinned must be an int64 buffer of n_expressions entries")
+        _check(library().ks_count_async(self.handle, dfa.handle, seq.handle, _ptr(out_pinned, C.c_int64)))
+
+    def async_wait(self) -> dict:
+        ms, calls, launches = C.c_float(), C.c_int32(), C.c_int32()
+        _check(library().ks_async_wait(self.handle, C.byref(ms), C.byref(calls), C.byref(launches)))
+        return {"scan_ms_total": ms.value, "calls": calls.value, "kernel_launches": launches.value}
+
+    def count_host_ascii(self, dfa: DfaHandle, data) -> np.ndarray:
+        """End-to-end count from a host ASCII buffer (pipelined H2D + encode
+        + scan; pinned memory gives full PCIe bandwidth)."""
+        arr = np.frombuffer(data, dtype=np.uint8) if isinstance(data, (bytes, bytearray, memoryview)) \
+            else np.ascontiguousarray(np.asarray(data, dtype=np.uint8))
+        buf = arr if arr.size else np.zeros(1, dtype=np.uint8)
+        counts = np.zeros(max(dfa.n_expressions, 1), dtype=np.int64)
+        with self.lock:
+            _check(library().ks_count_host_ascii(self.handle, dfa.handle, _ptr(buf, C.c_uint8), int(arr.size),
+                                                 _ptr(counts, C.c_int64)))
         return counts[: dfa.n_expressions]
 
     def locate(self, dfa: DfaHandle, seq: SeqHandle) -> tuple[np.ndarray, np.ndarray]:

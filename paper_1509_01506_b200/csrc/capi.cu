@@ -42,6 +42,8 @@ int encode_ascii_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, ks_se
                         int* launches);
 int pack_codes_device(ks_ctx* ctx, const uint8_t* d_codes, int64_t n, ks_seq* seq, int* d_flag,
                       int* launches);
+int encode_piece_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, ks_seq* seq, uint32_t* kept,
+                        int* ws_flag, int* launches);
 int unpack_codes_device(ks_ctx* ctx, const ks_seq* seq, uint8_t* d_out);
 int linear_softmask_device(ks_ctx* ctx, const ks_seq* seq, uint64_t* d_out);
 int launch_speculate(ks_ctx* ctx, const SeqView& seq, int32_t n_chunks, const int64_t* d_cbeg,
@@ -256,7 +258,7 @@ int true_state_at(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t pos
 
 int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end,
               int32_t entry_orig, int64_t row_base, int64_t* counts_out, int32_t* exit_out,
-              int64_t** rows_out, int64_t* n_rows) {
+              int64_t** rows_out, int64_t* n_rows, int64_t* async_dst = nullptr) {
     if (!ctx || !dfa || !seq) return fail(KS_E_INVALID, "null handle");
     if (dfa->ctx != ctx || seq->ctx != ctx) return fail(KS_E_INVALID, "handle belongs to another context");
     const HostDfa& h = dfa->host;
@@ -287,10 +289,14 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
     Arena ar;
     int rc = ensure_scratch(ctx, need, &ar);
     if (rc) return rc;
-    unsigned long long* visits = static_cast<unsigned long long*>(ar.take(size_t(h.n_accept) * 8));
-    unsigned long long* counts = static_cast<unsigned long long*>(ar.take(size_t(std::max(h.ne, 1)) * 8));
+    // visits | counts | err | exit: one memset before, one D2H after
+    const size_t res_bytes = size_t(std::max(h.ne, 1)) * 8 + 16;
+    char* blk = static_cast<char*>(ar.take(size_t(h.n_accept) * 8 + res_bytes));
+    unsigned long long* visits = reinterpret_cast<unsigned long long*>(blk);
+    unsigned long long* counts = reinterpret_cast<unsigned long long*>(blk + size_t(h.n_accept) * 8);
+    int32_t* err = reinterpret_cast<int32_t*>(counts + std::max(h.ne, 1));
+    uint16_t* exit_slot = reinterpret_cast<uint16_t*>(err + 2);
     uint16_t* chunk_exit = static_cast<uint16_t*>(ar.take(size_t(nch) * 2 + 2));
-    int32_t* err = static_cast<int32_t*>(ar.take(16));
     uint32_t* chunk_rows = nullptr;
     int64_t* row_off = nullptr;
     void* rows_tmp = nullptr;
@@ -308,9 +314,7 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
         mtot = static_cast<uint16_t*>(ar.take(16));
         mtmp = ar.take(exclusive_scan_monoid_tmp_bytes(nch));
     }
-    if (h.n_accept > 0) KS_CUDA(cudaMemsetAsync(visits, 0, size_t(h.n_accept) * 8, ctx->stream));
-    KS_CUDA(cudaMemsetAsync(counts, 0, size_t(std::max(h.ne, 1)) * 8, ctx->stream));
-    KS_CUDA(cudaMemsetAsync(err, 0, 16, ctx->stream));
+    KS_CUDA(cudaMemsetAsync(blk, 0, size_t(h.n_accept) * 8 + res_bytes, ctx->stream));
 
     ScanArgs a = base_args(dfa, dfa->scan, seq);
     a.begin = begin;
@@ -329,21 +333,39 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
         a.any_state = h.start_internal;
     }
 
-    KS_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
+    cudaEvent_t ev_a = ctx->ev[1], ev_b = ctx->ev[2];
+    if (async_dst) {  // count-only, no host synchronisation: events per call
+        const size_t need_ev = size_t(2 * (ctx->n_async + 1));
+        while (ctx->aev.size() < need_ev) {
+            cudaEvent_t e;
+            KS_CUDA(cudaEventCreate(&e));
+            ctx->aev.push_back(e);
+        }
+        ev_a = ctx->aev[2 * ctx->n_async];
+        ev_b = ctx->aev[2 * ctx->n_async + 1];
+        ++ctx->n_async;
+    }
+    KS_CUDA(cudaEventRecord(ev_a, ctx->stream));
     if (mapscan && nch > 0) {
         rc = monoid_prefix(ctx, dfa, seq, begin, end, origin, L, nch, elems, excl, mtot, mtmp, &launches);
         if (rc) return rc;
-        rc = launch_chunk_entry(ctx, excl, nch, dfa->d_action, h.nq, entry, centry, &launches);
+        rc = launch_chunk_entry(ctx, excl, nch, dfa->d_action, h.nq, entry, nullptr, centry, &launches);
         if (rc) return rc;
         a.chunk_entry = centry;
     }
     if (locate) a.chunk_rows = chunk_rows;
     rc = dispatch(ctx, dfa, dfa->scan, plan, a, locate ? kModeRows : kModeCount, &launches);
     if (rc) return rc;
-    KS_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
+    KS_CUDA(cudaEventRecord(ev_b, ctx->stream));
     rc = launch_finalize_counts(ctx, visits, h.n_accept, dfa->d_acc_out_off, dfa->d_acc_out_ids, counts,
-                                &launches);
+                                nch > 0 ? chunk_exit + (nch - 1) : nullptr, exit_slot, &launches);
     if (rc) return rc;
+    if (async_dst) {
+        if (h.ne > 0)
+            KS_CUDA(cudaMemcpyAsync(async_dst, counts, size_t(h.ne) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->async_launches += launches;
+        return KS_OK;
+    }
 
     int64_t total_rows = 0;
     int64_t* d_rows = nullptr;
@@ -373,11 +395,8 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
     rc = ensure_pinned(ctx, size_t(std::max(h.ne, 1)) * 8 + 64);
     if (rc) return rc;
     char* pin = static_cast<char*>(ctx->pinned);
-    KS_CUDA(cudaMemcpyAsync(pin, counts, size_t(h.ne) * 8, cudaMemcpyDeviceToHost, ctx->stream));
-    KS_CUDA(cudaMemcpyAsync(pin + size_t(std::max(h.ne, 1)) * 8, err, 4, cudaMemcpyDeviceToHost, ctx->stream));
-    uint16_t* pin_exit = reinterpret_cast<uint16_t*>(pin + size_t(std::max(h.ne, 1)) * 8 + 16);
-    if (nch > 0)
-        KS_CUDA(cudaMemcpyAsync(pin_exit, chunk_exit + (nch - 1), 2, cudaMemcpyDeviceToHost, ctx->stream));
+    KS_CUDA(cudaMemcpyAsync(pin, counts, res_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    uint16_t* pin_exit = reinterpret_cast<uint16_t*>(pin + size_t(std::max(h.ne, 1)) * 8 + 8);
     int64_t* host_rows = nullptr;
     if (locate) {
         host_rows = static_cast<int64_t*>(std::malloc(size_t(std::max<int64_t>(total_rows, 1)) * 16));
@@ -517,6 +536,139 @@ void seq_destroy(ks_seq* s) {
     delete s;
 }
 
+// Streaming count from a host buffer (ks_count_host_ascii).  Piece i is
+// copied into device buffer i%2 on the copy stream while piece i-1 is encoded
+// and scanned on the compute stream; every piece enters in the state the
+// previous piece left (a device-resident uint16), visits accumulate.
+int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int64_t n_bytes,
+                      int64_t* counts_out, bool* fallback) {
+    const HostDfa& h = dfa->host;
+    *fallback = false;
+    const int64_t piece = std::min<int64_t>(std::max<int64_t>(n_bytes, 64), int64_t(64) << 20);
+    const int64_t npieces = (n_bytes + piece - 1) / piece;
+    // piece buffers: 2 x (input bytes + packed tiled sequence)
+    ks_seq tmpl;
+    tmpl.lb = choose_lb(ctx, piece);
+    const int64_t tile_blocks = int64_t(32) << tmpl.lb;
+    const int64_t blocks = (piece + 63) / 64;
+    const int64_t slots = ((blocks + tile_blocks - 1) / tile_blocks + 1) * tile_blocks;
+    const size_t in_bytes = up(size_t(piece) + 64);
+    const size_t seq_bytes = up(size_t(slots) * 32);
+    const size_t need = 2 * (in_bytes + seq_bytes);
+    if (ctx->sbuf_bytes < need) {
+        KS_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (ctx->sbuf) KS_CUDA(cudaFree(ctx->sbuf));
+        ctx->sbuf = nullptr;
+        ctx->sbuf_bytes = 0;
+        KS_CUDA(cudaMalloc(&ctx->sbuf, need));
+        ctx->sbuf_bytes = need;
+    }
+    if (!ctx->copy_stream) {
+        KS_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        for (auto& e : ctx->sev) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    uint8_t* din[2];
+    ks_seq pseq[2];
+    for (int b = 0; b < 2; ++b) {
+        char* base = static_cast<char*>(ctx->sbuf) + b * (in_bytes + seq_bytes);
+        din[b] = reinterpret_cast<uint8_t*>(base);
+        pseq[b].ctx = ctx;
+        pseq[b].lb = tmpl.lb;
+        pseq[b].n_blocks = slots;
+        pseq[b].d_bases = reinterpret_cast<uint64_t*>(base + in_bytes);
+        pseq[b].d_nmask = reinterpret_cast<uint64_t*>(base + in_bytes + size_t(slots) * 16);
+        pseq[b].d_soft = reinterpret_cast<uint64_t*>(base + in_bytes + size_t(slots) * 24);
+    }
+    int64_t origin, L, nch_max;
+    geometry(&pseq[0], 0, piece, &origin, &L, &nch_max);
+    const bool mapscan = h.strategy == KS_STRATEGY_MAPSCAN;
+    Arena ar;
+    size_t scratch = size_t(h.n_accept) * 8 + size_t(std::max(h.ne, 1)) * 8 + size_t(nch_max) * 2 +
+                     size_t(blocks + 1) * 4 + 16 * kAlign;
+    if (mapscan) scratch += size_t(nch_max) * 6 + exclusive_scan_monoid_tmp_bytes(nch_max) + 4 * kAlign;
+    int rc = ensure_scratch(ctx, scratch, &ar);
+    if (rc) return rc;
+    unsigned long long* visits = static_cast<unsigned long long*>(ar.take(size_t(h.n_accept) * 8));
+    unsigned long long* counts = static_cast<unsigned long long*>(ar.take(size_t(std::max(h.ne, 1)) * 8));
+    uint16_t* chunk_exit = static_cast<uint16_t*>(ar.take(size_t(nch_max) * 2 + 2));
+    uint32_t* kept = static_cast<uint32_t*>(ar.take(size_t(blocks + 1) * 4));
+    int* ws_flag = static_cast<int*>(ar.take(16));
+    uint16_t* state = static_cast<uint16_t*>(ar.take(16));
+    uint16_t *elems = nullptr, *excl = nullptr, *centry = nullptr, *mtot = nullptr;
+    void* mtmp = nullptr;
+    if (mapscan) {
+        elems = static_cast<uint16_t*>(ar.take(size_t(nch_max) * 2));
+        excl = static_cast<uint16_t*>(ar.take(size_t(nch_max) * 2));
+        centry = static_cast<uint16_t*>(ar.take(size_t(nch_max) * 2));
+        mtot = static_cast<uint16_t*>(ar.take(16));
+        mtmp = ar.take(exclusive_scan_monoid_tmp_bytes(nch_max));
+    }
+    rc = ensure_pinned(ctx, size_t(std::max(h.ne, 1)) * 8 + 64);
+    if (rc) return rc;
+    char* pin = static_cast<char*>(ctx->pinned);
+    *reinterpret_cast<uint16_t*>(pin) = uint16_t(h.start_internal);
+    if (h.n_accept > 0) KS_CUDA(cudaMemsetAsync(visits, 0, size_t(h.n_accept) * 8, ctx->stream));
+    KS_CUDA(cudaMemsetAsync(counts, 0, size_t(std::max(h.ne, 1)) * 8, ctx->stream));
+    KS_CUDA(cudaMemsetAsync(ws_flag, 0, 16, ctx->stream));
+    KS_CUDA(cudaMemcpyAsync(state, pin, 2, cudaMemcpyHostToDevice, ctx->stream));
+    // the copy stream must not overwrite a buffer before the compute stream is done with it
+    KS_CUDA(cudaEventRecord(ctx->sev[2], ctx->stream));
+    KS_CUDA(cudaEventRecord(ctx->sev[3], ctx->stream));
+    const ScanPlan plan = plan_for(ctx, dfa, dfa->scan);
+    int launches = 0;
+    for (int64_t i = 0; i < npieces; ++i) {
+        const int b = int(i & 1);
+        const int64_t off = i * piece;
+        const int64_t len = std::min(piece, n_bytes - off);
+        KS_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->sev[2 + b], 0));
+        KS_CUDA(cudaMemcpyAsync(din[b], bytes + off, size_t(len), cudaMemcpyHostToDevice, ctx->copy_stream));
+        KS_CUDA(cudaEventRecord(ctx->sev[b], ctx->copy_stream));
+        KS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->sev[b], 0));
+        rc = encode_piece_device(ctx, din[b], len, &pseq[b], kept, ws_flag, &launches);
+        if (rc) return rc;
+        KS_CUDA(cudaEventRecord(ctx->sev[2 + b], ctx->stream));  // din[b] consumed
+        int64_t o2, L2, nch;
+        geometry(&pseq[b], 0, len, &o2, &L2, &nch);
+        ScanArgs a = base_args(dfa, dfa->scan, &pseq[b]);
+        a.begin = 0;
+        a.end = len;
+        a.origin = o2;
+        a.chunk_len = L2;
+        a.nchunks = nch;
+        a.visits = visits;
+        a.chunk_exit = chunk_exit;
+        if (mapscan) {
+            rc = monoid_prefix(ctx, dfa, &pseq[b], 0, len, o2, L2, nch, elems, excl, mtot, mtmp, &launches);
+            if (rc) return rc;
+            rc = launch_chunk_entry(ctx, excl, nch, dfa->d_action, h.nq, 0, state, centry, &launches);
+            if (rc) return rc;
+            a.chunk_entry = centry;
+        } else {
+            a.lookback = h.sync_depth;
+            a.base_pos = 0;
+            a.base_state_ptr = state;
+            a.any_state = h.start_internal;
+        }
+        rc = dispatch(ctx, dfa, dfa->scan, plan, a, kModeCount, &launches);
+        if (rc) return rc;
+        KS_CUDA(cudaMemcpyAsync(state, chunk_exit + (nch - 1), 2, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    rc = launch_finalize_counts(ctx, visits, h.n_accept, dfa->d_acc_out_off, dfa->d_acc_out_ids, counts,
+                                nullptr, nullptr, &launches);
+    if (rc) return rc;
+    KS_CUDA(cudaMemcpyAsync(pin, counts, size_t(h.ne) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    KS_CUDA(cudaMemcpyAsync(pin + size_t(std::max(h.ne, 1)) * 8, ws_flag, 4, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    KS_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (*reinterpret_cast<int*>(pin + size_t(std::max(h.ne, 1)) * 8)) {
+        *fallback = true;
+        return KS_OK;
+    }
+    std::memcpy(counts_out, pin, size_t(h.ne) * 8);
+    ctx->stats.kernel_launches = launches;
+    return KS_OK;
+}
+
 }  // namespace
 }  // namespace ks
 
@@ -565,6 +717,14 @@ int ks_close(ks_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->sbuf) cudaFree(ctx->sbuf);
+    if (ctx->copy_stream) {
+        cudaStreamSynchronize(ctx->copy_stream);
+        cudaStreamDestroy(ctx->copy_stream);
+    }
+    for (auto& ev : ctx->sev)
+        if (ev) cudaEventDestroy(ev);
+    for (auto& ev : ctx->aev) cudaEventDestroy(ev);
     for (auto& ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
@@ -837,6 +997,60 @@ int ks_locate(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t* counts
               int64_t* n_rows) {
     if (!counts_out || !rows_out || !n_rows) return fail(KS_E_INVALID, "null output");
     return scan_impl(ctx, dfa, seq, 0, seq ? seq->n : 0, -1, 0, counts_out, nullptr, rows_out, n_rows);
+}
+
+int ks_count_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t* counts_pinned) {
+    if (!counts_pinned) return fail(KS_E_INVALID, "counts_pinned is null");
+    int64_t dummy = 0;
+    return scan_impl(ctx, dfa, seq, 0, seq ? seq->n : 0, -1, 0, &dummy, nullptr, nullptr, nullptr, counts_pinned);
+}
+
+int ks_async_wait(ks_ctx* ctx, float* scan_ms_total, int32_t* calls, int32_t* launches) {
+    if (!ctx) return fail(KS_E_INVALID, "null context");
+    KS_CUDA(cudaStreamSynchronize(ctx->stream));
+    float total = 0;
+    for (int i = 0; i < ctx->n_async; ++i) {
+        float ms = 0;
+        KS_CUDA(cudaEventElapsedTime(&ms, ctx->aev[2 * i], ctx->aev[2 * i + 1]));
+        total += ms;
+    }
+    if (scan_ms_total) *scan_ms_total = total;
+    if (calls) *calls = ctx->n_async;
+    if (launches) *launches = ctx->async_launches;
+    ctx->n_async = 0;
+    ctx->async_launches = 0;
+    return KS_OK;
+}
+
+int ks_count_host_ascii(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int64_t n_bytes,
+                        int64_t* counts_out) {
+    if (!ctx || !dfa || !counts_out || n_bytes < 0 || (n_bytes > 0 && !bytes))
+        return fail(KS_E_INVALID, "bad argument");
+    if (dfa->ctx != ctx) return fail(KS_E_INVALID, "handle belongs to another context");
+    DeviceGuard guard(ctx->device);
+    if (n_bytes == 0) {
+        std::memset(counts_out, 0, size_t(dfa->host.ne) * 8);
+        return KS_OK;
+    }
+    ctx->stats = ks_stats{};
+    KS_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+    bool fallback = false;
+    int rc = stream_count_impl(ctx, dfa, bytes, n_bytes, counts_out, &fallback);
+    if (rc) return rc;
+    if (fallback) {  // whitespace present: compacting encode of the whole input
+        ks_seq* seq = nullptr;
+        rc = ks_seq_upload_ascii(ctx, bytes, n_bytes, 0, &seq);
+        if (rc) return rc;
+        rc = scan_impl(ctx, dfa, seq, 0, seq->n, -1, 0, counts_out, nullptr, nullptr, nullptr);
+        ks_seq_free(seq);
+        return rc;
+    }
+    KS_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
+    KS_CUDA(cudaEventSynchronize(ctx->ev[3]));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[3]);
+    ctx->stats.total_ms = ms;
+    return KS_OK;
 }
 
 int ks_scan_range(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end,

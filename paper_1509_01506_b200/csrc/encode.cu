@@ -251,6 +251,21 @@ int encode_ascii_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, ks_se
     return KS_OK;
 }
 
+// Whitespace-free fast path only, no host synchronisation: any whitespace
+// sets *ws_flag (the caller must then fall back to encode_ascii_device).
+int encode_piece_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, ks_seq* seq, uint32_t* kept,
+                        int* ws_flag, int* launches) {
+    const int64_t nb = (n_bytes + 63) / 64;
+    seq->n = n_bytes;
+    if (nb == 0) return KS_OK;
+    const int threads = 256;
+    encode_inplace_kernel<<<grid_for(ctx, nb, threads), threads, 0, ctx->stream>>>(
+        d_in, n_bytes, nb, seq->lb, seq->d_bases, seq->d_nmask, seq->d_soft, kept, ws_flag);
+    if (launches) ++*launches;
+    KS_CUDA(cudaGetLastError());
+    return KS_OK;
+}
+
 int pack_codes_device(ks_ctx* ctx, const uint8_t* d_codes, int64_t n, ks_seq* seq, int* d_flag,
                       int* launches) {
     const int64_t nb = (n + 63) / 64;

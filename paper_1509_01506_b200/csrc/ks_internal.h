@@ -127,6 +127,16 @@ struct ks_ctx {
     size_t scratch_bytes = 0;
     void* pinned = nullptr;   // small pinned host staging
     size_t pinned_bytes = 0;
+    // streaming host-input path (ks_count_host_ascii): copy stream, events,
+    // double-buffered device input + packed piece buffers
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t sev[4] = {nullptr, nullptr, nullptr, nullptr};
+    void* sbuf = nullptr;
+    size_t sbuf_bytes = 0;
+    // ks_count_async: one event pair per call until ks_async_wait
+    std::vector<cudaEvent_t> aev;
+    int n_async = 0;
+    int async_launches = 0;
 };
 
 struct ks_dfa {

@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(1024, 1) scan_kernel(const ScanArgs a) {
             s = uint32_t(a.uniform_entry);
         } else {
             const int64_t lb = max64(a.base_pos, cb - a.lookback);
-            s = uint32_t(lb == a.base_pos ? a.base_state : a.any_state);
+            s = uint32_t(lb == a.base_pos ? (a.base_state_ptr ? int32_t(*a.base_state_ptr) : a.base_state) : a.any_state);
             for (int64_t p = lb; p < cb; ++p) s = T.one(s * 5u + seq_sym(a.seq, p));
         }
 
@@ -286,7 +286,9 @@ LaunchShape launch_shape(ScanFn fn, size_t smem) {
 // --------------------------------------------------------------- helpers
 __global__ void finalize_counts_kernel(const unsigned long long* visits, int32_t n_accept,
                                        const int32_t* off, const int32_t* ids,
-                                       unsigned long long* counts) {
+                                       unsigned long long* counts, const uint16_t* exit_src,
+                                       uint16_t* exit_dst) {
+    if (exit_src && blockIdx.x == 0 && threadIdx.x == 0) *exit_dst = *exit_src;
     for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n_accept; s += gridDim.x * blockDim.x) {
         const unsigned long long v = visits[s];
         if (!v) continue;
@@ -295,10 +297,11 @@ __global__ void finalize_counts_kernel(const unsigned long long* visits, int32_t
 }
 
 __global__ void chunk_entry_kernel(const uint16_t* excl, int64_t n, const uint16_t* action,
-                                   int32_t nq, int32_t entry, uint16_t* out) {
+                                   int32_t nq, int32_t entry, const uint16_t* entry_ptr, uint16_t* out) {
+    const int32_t q = entry_ptr ? int32_t(*entry_ptr) : entry;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x)
-        out[i] = action[size_t(excl[i]) * nq + entry];
+        out[i] = action[size_t(excl[i]) * nq + q];
 }
 
 }  // namespace
@@ -344,23 +347,25 @@ int launch_scan(ks_ctx* ctx, ScanArgs a, int mode, int stride, bool smem_tables,
 
 int launch_finalize_counts(ks_ctx* ctx, const unsigned long long* visits, int32_t n_accept,
                            const int32_t* acc_out_off, const int32_t* acc_out_ids,
-                           unsigned long long* counts, int* launches) {
-    if (n_accept <= 0) return KS_OK;
+                           unsigned long long* counts, const uint16_t* exit_src, uint16_t* exit_dst,
+                           int* launches) {
+    if (n_accept <= 0 && !exit_src) return KS_OK;
     const int threads = 256;
-    const int blocks = std::min((n_accept + threads - 1) / threads, 1024);
+    const int blocks = std::max(1, std::min((n_accept + threads - 1) / threads, 1024));
     finalize_counts_kernel<<<blocks, threads, 0, ctx->stream>>>(visits, n_accept, acc_out_off,
-                                                                  acc_out_ids, counts);
+                                                                  acc_out_ids, counts, exit_src, exit_dst);
     if (launches) ++*launches;
     KS_CUDA(cudaGetLastError());
     return KS_OK;
 }
 
 int launch_chunk_entry(ks_ctx* ctx, const uint16_t* excl, int64_t n, const uint16_t* action,
-                       int32_t nq, int32_t entry, uint16_t* chunk_entry, int* launches) {
+                       int32_t nq, int32_t entry, const uint16_t* entry_ptr, uint16_t* chunk_entry,
+                       int* launches) {
     if (n <= 0) return KS_OK;
     const int threads = 256;
     const int blocks = int(min64((n + threads - 1) / threads, 4096));
-    chunk_entry_kernel<<<blocks, threads, 0, ctx->stream>>>(excl, n, action, nq, entry, chunk_entry);
+    chunk_entry_kernel<<<blocks, threads, 0, ctx->stream>>>(excl, n, action, nq, entry, entry_ptr, chunk_entry);
     if (launches) ++*launches;
     KS_CUDA(cudaGetLastError());
     return KS_OK;

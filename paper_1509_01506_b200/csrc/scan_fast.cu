@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
             s = uint32_t(a.uniform_entry);
         } else {
             const int64_t lbp = max64(a.base_pos, cb - a.lookback);
-            s = uint32_t(lbp == a.base_pos ? a.base_state : a.any_state);
+            s = uint32_t(lbp == a.base_pos ? (a.base_state_ptr ? int32_t(*a.base_state_ptr) : a.base_state) : a.any_state);
             int64_t lbk = -1;
             uint4 xb = make_uint4(0, 0, 0, 0);
             uint64_t xm = 0;
@@ -446,8 +446,20 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
     if (!fn) return fail(KS_E_INVALID, "fast scan: bad mode/stride");
     const size_t smem = fast_smem_bytes(mode, a.t1_pad, ring ? a.n_accept : 0, kFastThreads);
     if (smem > ctx->smem_optin) return fail(KS_E_UNSUPPORTED, "fast scan: shared memory budget exceeded");
-    KS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    {  // the attribute is per function and device; set it once per size
+        static thread_local const void* last_fn[16];
+        static thread_local size_t last_smem[16];
+        static thread_local int last_dev[16];
+        const int slot = int((reinterpret_cast<uintptr_t>(fn) >> 4) & 15);
+        if (last_fn[slot] != reinterpret_cast<const void*>(fn) || last_smem[slot] < smem ||
+            last_dev[slot] != ctx->device) {
+            KS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            last_fn[slot] = reinterpret_cast<const void*>(fn);
+            last_smem[slot] = smem;
+            last_dev[slot] = ctx->device;
+        }
+    }
     const int64_t u0 = a.origin / a.chunk_len;
     const int64_t tiles = ((u0 + a.nchunks - 1) >> 5) - (u0 >> 5) + 1;
     const int64_t need = (tiles * 32 + kFastThreads - 1) / kFastThreads;

@@ -41,6 +41,7 @@ struct ScanArgs {
     int32_t lookback = 0;            // else: scan max(base_pos, cb - lookback) .. cb
     int64_t base_pos = 0;            //   starting in base_state when at base_pos,
     int32_t base_state = 0;          //   in any_state otherwise (synchronising word)
+    const uint16_t* base_state_ptr = nullptr;  // if set: base_state read from device memory
     int32_t any_state = 0;
     // automaton
     const uint16_t* t1 = nullptr;    // nq x 5 (global)
@@ -95,8 +96,10 @@ size_t exclusive_scan_monoid_tmp_bytes(int64_t n);
 // Small helper kernels (csrc/scan.cu).
 int launch_finalize_counts(ks_ctx* ctx, const unsigned long long* visits, int32_t n_accept,
                            const int32_t* acc_out_off, const int32_t* acc_out_ids,
-                           unsigned long long* counts, int* launches);
+                           unsigned long long* counts, const uint16_t* exit_src, uint16_t* exit_dst,
+                           int* launches);
 int launch_chunk_entry(ks_ctx* ctx, const uint16_t* excl, int64_t n, const uint16_t* action,
-                       int32_t nq, int32_t entry, uint16_t* chunk_entry, int* launches);
+                       int32_t nq, int32_t entry, const uint16_t* entry_ptr, uint16_t* chunk_entry,
+                       int* launches);
 
 }  // namespace ks

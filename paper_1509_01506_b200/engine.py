@@ -162,11 +162,11 @@ def scan_bytes(dfa: Dfa, data, mode: str = "count", device: int = 0):
         raise ValueError(f"unknown mode {mode!r}")
     ctx = _native.context(device)
     dh = ctx.dfa(dfa)
+    if mode == "count":  # pipelined host->device copy, encode and scan
+        return ctx.count_host_ascii(dh, data), None
     sh = ctx.upload_ascii(data)
     try:
-        if mode == "locate":
-            return ctx.locate(dh, sh)
-        return ctx.count(dh, sh), None
+        return ctx.locate(dh, sh)
     finally:
         sh.free()
 

@@ -284,3 +284,31 @@ def test_match_chunk_reduce_roundtrip(toy_dfa):
     assert red.locations.tolist() == rep.locations.tolist()
     for key in ("pss_sizes", "speculative_runs", "converged_runs", "convergence_steps"):
         assert red.metadata[key] == rep.metadata[key]
+
+
+# ---------------------------------------------------------------- streaming host input
+
+@pytest.mark.parametrize("config,n", [(3, (1 << 20) + 12345), (2, 300_001), (5, 200_003), (1, 0), (1, 1)])
+def test_count_host_ascii_matches(config, n, monkeypatch):
+    w = workloads.make(config, max(n, 1))
+    data = w.ascii.tobytes()[:n]
+    ctx = _native.context(0)
+    dh = ctx.dfa(w.dfa)
+    want = O.ref_sequential_count(w.dfa, ks.encode_bytes(data))[0]
+    assert ctx.count_host_ascii(dh, data).tolist() == want.tolist()
+    counts, rows = ks.scan_bytes(w.dfa, data)
+    assert counts.tolist() == want.tolist() and rows is None
+
+
+def test_count_host_ascii_small_pieces_and_whitespace():
+    """Many pieces (entry state carried across pieces) and the whitespace
+    fallback."""
+    w = workloads.make(3, 1 << 22)
+    data = w.ascii.tobytes()
+    ctx = _native.context(0)
+    dh = ctx.dfa(w.dfa)
+    want = O.ref_sequential_count(w.dfa, ks.encode_bytes(data))[0]
+    assert ctx.count_host_ascii(dh, data).tolist() == want.tolist()
+    text = b"\n".join(data[i:i + 61] for i in range(0, 200_000, 61))
+    want = O.ref_sequential_count(w.dfa, ks.encode_bytes(text))[0]
+    assert ctx.count_host_ascii(dh, text).tolist() == want.tolist()
