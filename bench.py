@@ -195,13 +195,19 @@ def run_ours(args) -> None:
     from paper_1509_01506_b200.distributed import DeviceShardScanner, compose_entry
 
     world, rank, local = dist_env()
+    ngpu = torch.cuda.device_count()
+    local = local % max(ngpu, 1)  # (gloo dry runs may put several ranks on one GPU)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.dist_backend)
     dev = torch.device("cuda", local)
+    cdev = dev if args.dist_backend == "nccl" else torch.device("cpu")  # collective tensors
 
     t0 = time.perf_counter()
-    wl = workloads.make(args.config, args.n, shard=rank)
+    wl = workloads.make(args.config, args.bases, shard=rank)
     n = wl.n
     log(f"[rank {rank}] generated C{args.config} shard n={n} in {time.perf_counter() - t0:.1f}s")
 
@@ -217,18 +223,30 @@ def run_ours(args) -> None:
     scanner = DeviceShardScanner(ctx, dh, sh, row_base=rank * n)
     nq, ne = wl.dfa.state_count, wl.dfa.n_expressions
 
-    maps_buf = [torch.empty(nq, dtype=torch.int64, device=dev) for _ in range(world)]
-    counts_t = torch.zeros(ne, dtype=torch.int64, device=dev)
+    maps_buf = [torch.empty(nq, dtype=torch.int64, device=cdev) for _ in range(world)]
+    counts_t = torch.zeros(ne, dtype=torch.int64, device=cdev)
     launches = [0]
 
     out_pin = torch.zeros(max(ne, 1), dtype=torch.int64).pin_memory()
     out_np = out_pin.numpy()
 
+    maps_dev = torch.empty((world, nq), dtype=torch.int32, device=dev)
+    counts_dev = torch.zeros(max(ne, 1), dtype=torch.int64, device=dev)
+
     def step() -> None:
         if world == 1:  # enqueue only: scan + count + D2H of the counts, no host sync
             ctx.count_async(dh, sh, out_np)
             return
-        m = torch.from_numpy(scanner.segment_map(0, n).astype(np.int64)).to(dev, non_blocking=True)
+        if args.dist_backend == "nccl":
+            # all on one stream, no host synchronisation: boundary map -> NCCL
+            # all-gather -> entry composed on the device -> scan -> NCCL all-reduce
+            ctx.segment_map_async(dh, sh, 0, n, maps_dev[rank].data_ptr())
+            dist.all_gather_into_tensor(maps_dev, maps_dev[rank].clone())
+            ctx.count_shard_async(dh, sh, 0, n, maps_dev.data_ptr(), rank, counts_dev.data_ptr())
+            dist.all_reduce(counts_dev)
+            out_pin.copy_(counts_dev, non_blocking=True)
+            return
+        m = torch.from_numpy(scanner.segment_map(0, n).astype(np.int64)).to(cdev)
         launches[0] += 1
         dist.all_gather(maps_buf, m)
         maps = torch.stack(maps_buf).cpu().numpy()
@@ -259,15 +277,19 @@ def run_ours(args) -> None:
         ev1.record(stream)
         waited = ctx.async_wait()
         torch.cuda.synchronize()
-    if world == 1:
-        scan_ms_sum[0] = waited["scan_ms_total"]
+    if world == 1 or args.dist_backend == "nccl":
         launches[0] = waited["kernel_launches"]
+        if world == 1:
+            scan_ms_sum[0] = waited["scan_ms_total"]
+        else:  # one synchronous scan for the kernel time of this rank's shard
+            ctx.scan_range(dh, sh, 0, n, -1)
+            scan_ms_sum[0] = ctx.stats()["scan_ms"] * args.steps
     if not np.array_equal(out_np[:ne], ref_counts):
         raise RuntimeError("counts changed between steps")
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms, scan_ms_sum[0]], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms, scan_ms_sum[0]], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max, scan_ms_max = float(t[0]), float(t[1])
@@ -334,11 +356,13 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
-    ap.add_argument("--n", type=int, default=None, help="override bases per GPU")
+    ap.add_argument("--bases", type=int, default=None, help="override bases per GPU")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-sample", type=int, default=256 << 20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo only for dry runs of the multi-rank path")
     args = ap.parse_args()
     if args.warmup < 3:
         log("note: raising --warmup to the contract minimum of 3")

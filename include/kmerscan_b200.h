@@ -161,6 +161,19 @@ KS_API int ks_scan_range(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
 KS_API int ks_segment_map(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin,
                    int64_t end, int32_t* map_out);
 
+/* Asynchronous multi-GPU building blocks (no host synchronisation; device
+ * pointers).  ks_segment_map_async writes the shard's boundary map
+ * (int32[n_states], original ids) into d_map_out -- the payload of the NCCL
+ * all-gather.  ks_count_shard_async composes START through the gathered maps
+ * d_maps[0..rank) (int32[world][n_states]) on the device, scans
+ * [begin, end) from that state and writes the shard's per-expression counts
+ * into d_counts (uint64[n_expressions], the NCCL all-reduce payload). */
+KS_API int ks_segment_map_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin,
+                                int64_t end, int32_t* d_map_out);
+KS_API int ks_count_shard_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin,
+                                int64_t end, const int32_t* d_maps, int32_t rank,
+                                unsigned long long* d_counts);
+
 /* Speculative-start convergence (match_chunk_kernel's speculative runs,
  * _kernels.py:91-112): for chunk k, candidate start states
  * pss_data[pss_off[k] .. pss_off[k+1]) (original ids; entry 0 is the full

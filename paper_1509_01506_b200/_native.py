@@ -58,7 +58,8 @@ EXPORTED = (
     "ks_version", "ks_dfa_upload", "ks_dfa_upload_ex", "ks_dfa_info_get", "ks_dfa_free",
     "ks_seq_upload_codes", "ks_seq_upload_ascii", "ks_seq_encode_device", "ks_seq_length",
     "ks_seq_download_codes", "ks_seq_download_softmask", "ks_seq_free", "ks_count", "ks_locate",
-    "ks_count_host_ascii", "ks_count_async", "ks_async_wait",
+    "ks_count_host_ascii", "ks_count_async", "ks_async_wait", "ks_segment_map_async",
+    "ks_count_shard_async",
     "ks_scan_range", "ks_segment_map", "ks_speculate", "ks_free",
 )
 
@@ -96,6 +97,8 @@ def _declare(lib) -> None:
         "ks_locate": (C.c_int, [_P, _P, _P, _i64p, C.POINTER(_i64p), _i64p]),
         "ks_count_host_ascii": (C.c_int, [_P, _P, _u8p, C.c_int64, _i64p]),
         "ks_count_async": (C.c_int, [_P, _P, _P, _i64p]),
+        "ks_segment_map_async": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, _P]),
+        "ks_count_shard_async": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, _P, C.c_int32, _P]),
         "ks_async_wait": (C.c_int, [_P, C.POINTER(C.c_float), _i32p, _i32p]),
         "ks_scan_range": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, C.c_int32, C.c_int64, _i64p,
                                     _i32p, C.POINTER(_i64p), _i64p]),
@@ -305,6 +308,18 @@ class DeviceContext:
         if out_pinned.dtype != np.int64 or out_pinned.size < max(dfa.n_expressions, 1):
             raise ValueError("out_pinned must be an int64 buffer of n_expressions entries")
         _check(library().ks_count_async(self.handle, dfa.handle, seq.handle, _ptr(out_pinned, C.c_int64)))
+
+    def segment_map_async(self, dfa: DfaHandle, seq: SeqHandle, begin: int, end: int, d_map: int) -> None:
+        """Shard boundary map into device memory (int32[n_states]) without syncing."""
+        _check(library().ks_segment_map_async(self.handle, dfa.handle, seq.handle, int(begin), int(end),
+                                              _P(d_map)))
+
+    def count_shard_async(self, dfa: DfaHandle, seq: SeqHandle, begin: int, end: int, d_maps: int,
+                          rank: int, d_counts: int) -> None:
+        """Scan a shard from the state composed on the device out of the
+        gathered maps of ranks < rank; counts (uint64) into device memory."""
+        _check(library().ks_count_shard_async(self.handle, dfa.handle, seq.handle, int(begin), int(end),
+                                              _P(d_maps), int(rank), _P(d_counts)))
 
     def async_wait(self) -> dict:
         ms, calls, launches = C.c_float(), C.c_int32(), C.c_int32()

@@ -121,6 +121,46 @@ __global__ void walk_kernel(SeqView seq, int64_t begin, int64_t end, const uint1
     out[q] = uint16_t(s);
 }
 
+// map_out[q_orig] = original id of walking [begin, end) from q (all q), or of
+// walking [end - D, end) from any state (uniform) for definite automata.
+__global__ void segment_map_kernel(SeqView seq, int64_t begin, int64_t end, const uint16_t* t1, int32_t nq,
+                                   int32_t uniform_start, const int32_t* new_of_old, const int32_t* old_of_new,
+                                   int32_t* map_out) {
+    __shared__ uint32_t shared_state;
+    if (uniform_start >= 0) {
+        if (threadIdx.x == 0 && blockIdx.x == 0) {
+            uint32_t s = uint32_t(uniform_start);
+            for (int64_t p = begin; p < end; ++p) s = t1[s * 5u + seq_sym(seq, p)];
+            shared_state = s;
+        }
+        __syncthreads();
+        const int32_t v = old_of_new[shared_state];
+        for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) map_out[q] = v;
+        return;
+    }
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
+        uint32_t s = uint32_t(new_of_old[q]);
+        for (int64_t p = begin; p < end; ++p) s = t1[s * 5u + seq_sym(seq, p)];
+        map_out[q] = old_of_new[s];
+    }
+}
+
+// map_out[q_orig] = original id of action(element *d_elem)(q)
+__global__ void action_map_kernel(const uint16_t* d_elem, const uint16_t* action, int32_t nq,
+                                  const int32_t* new_of_old, const int32_t* old_of_new, int32_t* map_out) {
+    const uint32_t m = *d_elem;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x)
+        map_out[q] = old_of_new[action[size_t(m) * nq + new_of_old[q]]];
+}
+
+// entry of shard `rank`: START pushed through the gathered maps of ranks < rank
+__global__ void compose_entry_kernel(const int32_t* maps, int32_t nq, int32_t rank, int32_t start_orig,
+                                     const int32_t* new_of_old, uint16_t* entry_internal) {
+    int32_t s = start_orig;
+    for (int r = 0; r < rank; ++r) s = maps[size_t(r) * nq + s];
+    *entry_internal = uint16_t(new_of_old[s]);
+}
+
 SeqView view_of(const ks_seq* s) {
     SeqView v;
     v.bases = s->d_bases;
@@ -778,6 +818,8 @@ int ks_dfa_upload_ex(ks_ctx* ctx, const int32_t* transitions, int32_t n_states, 
         d->d_acc_out_off = reinterpret_cast<int32_t*>(place(h.acc_out_off.data(), h.acc_out_off.size() * 4));
         d->d_acc_out_ids = reinterpret_cast<int32_t*>(place(h.acc_out_ids.data(), h.acc_out_ids.size() * 4));
         d->d_acc_outcnt = reinterpret_cast<uint16_t*>(place(h.acc_outcnt.data(), h.acc_outcnt.size() * 2));
+        d->d_new_of_old = reinterpret_cast<int32_t*>(place(h.new_of_old.data(), h.new_of_old.size() * 4));
+        d->d_old_of_new = reinterpret_cast<int32_t*>(place(h.old_of_new.data(), h.old_of_new.size() * 4));
         if (h.strategy == KS_STRATEGY_MAPSCAN) {
             upload_table(h.mono, &d->mono, blob, &off, dry);
             d->d_prod = reinterpret_cast<uint16_t*>(place(h.prod.data(), h.prod.size() * 2));
@@ -813,6 +855,8 @@ int ks_dfa_upload_ex(ks_ctx* ctx, const int32_t* transitions, int32_t n_states, 
     rebase(d->d_acc_out_off);
     rebase(d->d_acc_out_ids);
     rebase(d->d_acc_outcnt);
+    rebase(d->d_new_of_old);
+    rebase(d->d_old_of_new);
     if (h.strategy == KS_STRATEGY_MAPSCAN) {
         rebase(d->mono.tk);
         rebase(d->mono.t1);
@@ -1109,6 +1153,105 @@ int ks_segment_map(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t be
         for (int q = 0; q < h.nq; ++q) img[q] = h.action[size_t(m) * h.nq + q];
     }
     for (int q = 0; q < h.nq; ++q) map_out[q] = h.old_of_new[img[h.new_of_old[q]]];
+    return KS_OK;
+}
+
+int ks_segment_map_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end,
+                         int32_t* d_map_out) {
+    if (!ctx || !dfa || !seq || !d_map_out) return fail(KS_E_INVALID, "null argument");
+    if (begin < 0 || end < begin || end > seq->n) return fail(KS_E_INVALID, "segment out of bounds");
+    DeviceGuard guard(ctx->device);
+    const HostDfa& h = dfa->host;
+    const int threads = 256;
+    const int blocks = std::max(1, std::min((h.nq + threads - 1) / threads, 1024));
+    if (h.strategy == KS_STRATEGY_LOOKBACK) {
+        const bool uniform = end - begin >= h.sync_depth;
+        segment_map_kernel<<<uniform ? 1 : blocks, threads, 0, ctx->stream>>>(
+            view_of(seq), uniform ? end - h.sync_depth : begin, end, dfa->scan.t1, h.nq,
+            uniform ? h.start_internal : -1, dfa->d_new_of_old, dfa->d_old_of_new, d_map_out);
+        KS_CUDA(cudaGetLastError());
+        return KS_OK;
+    }
+    int64_t origin, L, nch;
+    geometry(seq, begin, end, &origin, &L, &nch);
+    Arena ar;
+    int rc = ensure_scratch(ctx, size_t(nch) * 4 + exclusive_scan_monoid_tmp_bytes(nch) + 4096, &ar);
+    if (rc) return rc;
+    uint16_t* elems = static_cast<uint16_t*>(ar.take(size_t(nch) * 2 + 2));
+    uint16_t* excl = static_cast<uint16_t*>(ar.take(size_t(nch) * 2 + 2));
+    uint16_t* tot = static_cast<uint16_t*>(ar.take(16));
+    void* tmp = ar.take(exclusive_scan_monoid_tmp_bytes(nch));
+    int launches = 0;
+    if (nch > 0) {
+        rc = monoid_prefix(ctx, dfa, seq, begin, end, origin, L, nch, elems, excl, tot, tmp, &launches);
+        if (rc) return rc;
+    } else {
+        KS_CUDA(cudaMemsetAsync(tot, 0, 2, ctx->stream));  // identity element
+    }
+    action_map_kernel<<<blocks, threads, 0, ctx->stream>>>(tot, dfa->d_action, h.nq, dfa->d_new_of_old,
+                                                           dfa->d_old_of_new, d_map_out);
+    KS_CUDA(cudaGetLastError());
+    return KS_OK;
+}
+
+int ks_count_shard_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end,
+                         const int32_t* d_maps, int32_t rank, unsigned long long* d_counts) {
+    if (!ctx || !dfa || !seq || !d_counts || (rank > 0 && !d_maps)) return fail(KS_E_INVALID, "null argument");
+    if (begin < 0 || end < begin || end > seq->n) return fail(KS_E_INVALID, "range out of bounds");
+    DeviceGuard guard(ctx->device);
+    const HostDfa& h = dfa->host;
+    int64_t origin, L, nch;
+    geometry(seq, begin, end, &origin, &L, &nch);
+    const bool mapscan = h.strategy == KS_STRATEGY_MAPSCAN;
+    Arena ar;
+    size_t need = size_t(h.n_accept) * 8 + size_t(nch) * 2 + 64 * kAlign;
+    if (mapscan) need += size_t(nch) * 6 + exclusive_scan_monoid_tmp_bytes(nch);
+    int rc = ensure_scratch(ctx, need, &ar);
+    if (rc) return rc;
+    unsigned long long* visits = static_cast<unsigned long long*>(ar.take(size_t(h.n_accept) * 8));
+    uint16_t* entry = static_cast<uint16_t*>(ar.take(16));
+    uint16_t* chunk_exit = static_cast<uint16_t*>(ar.take(size_t(nch) * 2 + 2));
+    int launches = 0;
+    if (h.n_accept > 0) KS_CUDA(cudaMemsetAsync(visits, 0, size_t(h.n_accept) * 8, ctx->stream));
+    KS_CUDA(cudaMemsetAsync(d_counts, 0, size_t(std::max(h.ne, 1)) * 8, ctx->stream));
+    compose_entry_kernel<<<1, 1, 0, ctx->stream>>>(d_maps, h.nq, rank, 0, dfa->d_new_of_old, entry);
+    KS_CUDA(cudaGetLastError());
+    if (nch > 0) {
+        const ScanPlan plan = plan_for(ctx, dfa, dfa->scan);
+        ScanArgs a = base_args(dfa, dfa->scan, seq);
+        a.begin = begin;
+        a.end = end;
+        a.origin = origin;
+        a.chunk_len = L;
+        a.nchunks = nch;
+        a.visits = visits;
+        a.chunk_exit = chunk_exit;
+        if (mapscan) {
+            uint16_t* elems = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
+            uint16_t* excl = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
+            uint16_t* centry = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
+            uint16_t* mtot = static_cast<uint16_t*>(ar.take(16));
+            void* mtmp = ar.take(exclusive_scan_monoid_tmp_bytes(nch));
+            rc = monoid_prefix(ctx, dfa, seq, begin, end, origin, L, nch, elems, excl, mtot, mtmp, &launches);
+            if (rc) return rc;
+            rc = launch_chunk_entry(ctx, excl, nch, dfa->d_action, h.nq, 0, entry, centry, &launches);
+            if (rc) return rc;
+            a.chunk_entry = centry;
+        } else {
+            a.lookback = h.sync_depth;
+            a.base_pos = begin;
+            a.base_state_ptr = entry;
+            a.any_state = h.start_internal;
+        }
+        KS_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
+        rc = dispatch(ctx, dfa, dfa->scan, plan, a, kModeCount, &launches);
+        if (rc) return rc;
+        KS_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
+    }
+    rc = launch_finalize_counts(ctx, visits, h.n_accept, dfa->d_acc_out_off, dfa->d_acc_out_ids, d_counts,
+                                nullptr, nullptr, &launches);
+    if (rc) return rc;
+    ctx->async_launches += launches + 2;
     return KS_OK;
 }
 

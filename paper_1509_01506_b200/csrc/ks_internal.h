@@ -150,6 +150,8 @@ struct ks_dfa {
     uint16_t* d_prod = nullptr;
     uint16_t* d_act0 = nullptr;
     uint16_t* d_action = nullptr;   // nm x nq
+    int32_t* d_new_of_old = nullptr;
+    int32_t* d_old_of_new = nullptr;
     void* d_blob = nullptr;   // single allocation backing the above
     bool tables_in_smem = true;
 };

@@ -312,3 +312,39 @@ def test_count_host_ascii_small_pieces_and_whitespace():
     text = b"\n".join(data[i:i + 61] for i in range(0, 200_000, 61))
     want = O.ref_sequential_count(w.dfa, ks.encode_bytes(text))[0]
     assert ctx.count_host_ascii(dh, text).tolist() == want.tolist()
+
+
+# ---------------------------------------------------------------- multi-GPU building blocks (on one GPU)
+
+@pytest.mark.parametrize("config,n,world", [(3, 1 << 20, 3), (4, 1 << 19, 2), (5, 300_000, 4), (1, 5000, 3)])
+def test_sharded_async_matches_sequential(config, n, world):
+    """The NCCL path's device pieces, emulated rank by rank on one GPU: each
+    shard's boundary map (ks_segment_map_async), the entry composed on the
+    device from the 'gathered' maps, the shard scan (ks_count_shard_async);
+    the summed counts equal one sequential pass."""
+    import torch
+    from paper_1509_01506_b200.distributed import shard_bounds
+
+    w = workloads.make(config, n)
+    codes = ks.encode_bytes(w.ascii.tobytes())
+    ctx = _native.DeviceContext(0)
+    dh = ctx.dfa(w.dfa)
+    bounds = shard_bounds(codes.size, world)
+    shards = [ctx.upload_codes(codes[b:e]) for b, e in bounds]
+    nq, ne = w.dfa.state_count, w.dfa.n_expressions
+    maps = torch.empty((world, nq), dtype=torch.int32, device="cuda")
+    for r, sh in enumerate(shards):
+        ctx.segment_map_async(dh, sh, 0, sh.length, maps[r].data_ptr())
+    ctx.synchronize()
+    total = np.zeros(ne, dtype=np.int64)
+    for r, sh in enumerate(shards):
+        c = torch.zeros(max(ne, 1), dtype=torch.int64, device="cuda")
+        ctx.count_shard_async(dh, sh, 0, sh.length, maps.data_ptr(), r, c.data_ptr())
+        ctx.synchronize()
+        total += c.cpu().numpy()[:ne]
+        # the gathered map of shard r is the host map
+        b, e = bounds[r]
+        want_map = ctx.segment_map(dh, sh, 0, sh.length)
+        assert maps[r].cpu().numpy().tolist() == want_map.tolist()
+    want = O.ref_sequential_count(w.dfa, codes)[0]
+    assert total.tolist() == want.tolist()
