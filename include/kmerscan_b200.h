@@ -67,6 +67,8 @@ typedef struct ks_stats {
     int32_t chunks;          /* lane chunks in the main scan                */
     int64_t chunk_len;       /* bases per lane chunk                        */
     int64_t rows;            /* locate rows produced                        */
+    int64_t h2d_bytes;       /* host->device bytes the call copied          */
+    int64_t d2h_bytes;       /* device->host bytes the call copied          */
 } ks_stats;
 
 /* ---- context ------------------------------------------------------------ */
@@ -136,11 +138,22 @@ KS_API int ks_count_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int
 KS_API int ks_async_wait(ks_ctx* ctx, float* scan_ms_total, int32_t* calls, int32_t* launches);
 
 /* Counts straight from a HOST buffer of raw ASCII (the end-to-end call):
- * pieces are copied host->device on a copy stream while the previous piece
- * is encoded and scanned (each piece entering in the state the previous one
- * left), so transfer, encode and scan overlap.  Same result as
- * ks_seq_upload_ascii + ks_count; input with whitespace falls back to that
- * path.  Pinned host memory gives full PCIe bandwidth. */
+ * host worker threads pack each 64 MiB piece into the device tile-slot
+ * format (2-bit bases + OTHER bitmap, 0.25-0.375 B/base on the wire) in
+ * pinned staging, the copy stream moves it while the previous piece is
+ * scanned, and each piece enters in the state the previous one left.  Same
+ * result as ks_seq_upload_ascii + ks_count; input with whitespace falls back
+ * to that path.  KS_HOST_THREADS caps the packer threads; KS_DEVICE_ENCODE=1
+ * copies raw ASCII and encodes on the device instead. */
+/* The host packer on its own (CPU only, no context): blocks of `bytes` in
+ * tile-slot order for units of 2^lb 64-base blocks, 32 units per tile --
+ * block g lands in slot ((g>>lb)>>5 << (5+lb)) | (g & (2^lb-1)) << 5 | (g>>lb) & 31.
+ * `bases` holds 2*slots words, `nmask` `slots` words, slots = ceil(n/64)
+ * rounded up to whole tiles.  *flags gets bit0 = whitespace seen, bit1 =
+ * OTHER seen. */
+KS_API int ks_pack_host_ascii(const uint8_t* bytes, int64_t n_bytes, int32_t lb, uint64_t* bases,
+                              uint64_t* nmask, int32_t* flags);
+
 KS_API int ks_count_host_ascii(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int64_t n_bytes,
                                int64_t* counts_out);
 

@@ -50,7 +50,8 @@ class DfaInfo(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("scan_ms", C.c_float), ("total_ms", C.c_float),
                 ("kernel_launches", C.c_int32), ("chunks", C.c_int32),
-                ("chunk_len", C.c_int64), ("rows", C.c_int64)]
+                ("chunk_len", C.c_int64), ("rows", C.c_int64),
+                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64)]
 
 
 EXPORTED = (
@@ -59,7 +60,7 @@ EXPORTED = (
     "ks_seq_upload_codes", "ks_seq_upload_ascii", "ks_seq_encode_device", "ks_seq_length",
     "ks_seq_download_codes", "ks_seq_download_softmask", "ks_seq_free", "ks_count", "ks_locate",
     "ks_count_host_ascii", "ks_count_async", "ks_async_wait", "ks_segment_map_async",
-    "ks_count_shard_async",
+    "ks_count_shard_async", "ks_pack_host_ascii",
     "ks_scan_range", "ks_segment_map", "ks_speculate", "ks_free",
 )
 
@@ -97,6 +98,7 @@ def _declare(lib) -> None:
         "ks_locate": (C.c_int, [_P, _P, _P, _i64p, C.POINTER(_i64p), _i64p]),
         "ks_count_host_ascii": (C.c_int, [_P, _P, _u8p, C.c_int64, _i64p]),
         "ks_count_async": (C.c_int, [_P, _P, _P, _i64p]),
+        "ks_pack_host_ascii": (C.c_int, [_u8p, C.c_int64, C.c_int32, _P, _P, _i32p]),
         "ks_segment_map_async": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, _P]),
         "ks_count_shard_async": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, _P, C.c_int32, _P]),
         "ks_async_wait": (C.c_int, [_P, C.POINTER(C.c_float), _i32p, _i32p]),
@@ -409,6 +411,22 @@ def _take_rows(rows_p, n: int) -> np.ndarray:
 
 _contexts: dict[int, DeviceContext] = {}
 _ctx_lock = threading.Lock()
+
+
+def pack_host_ascii(data, lb: int) -> tuple[np.ndarray, np.ndarray, int]:
+    """The streaming count's host packer on its own (no GPU needed): returns
+    (bases uint64[2*slots], nmask uint64[slots], flags) in tile-slot order."""
+    arr = np.ascontiguousarray(np.frombuffer(bytes(data), dtype=np.uint8) if isinstance(data, (bytes, bytearray))
+                               else np.asarray(data, dtype=np.uint8))
+    tile = 32 << lb
+    slots = max(-(-((arr.size + 63) // 64) // tile) * tile, 1)
+    bases = np.zeros(2 * slots, dtype=np.uint64)
+    nmask = np.zeros(slots, dtype=np.uint64)
+    flags = C.c_int32()
+    buf = arr if arr.size else np.zeros(1, dtype=np.uint8)
+    _check(library().ks_pack_host_ascii(_ptr(buf, C.c_uint8), int(arr.size), int(lb), bases.ctypes.data,
+                                        nmask.ctypes.data, C.byref(flags)))
+    return bases, nmask, int(flags.value)
 
 
 def context(device: int = 0) -> DeviceContext:

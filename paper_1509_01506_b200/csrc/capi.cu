@@ -20,6 +20,7 @@
 #include <type_traits>
 #include <vector>
 
+#include "host_pack.h"
 #include "scan_kernels.cuh"
 
 namespace ks {
@@ -42,6 +43,8 @@ int encode_ascii_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, ks_se
                         int* launches);
 int pack_codes_device(ks_ctx* ctx, const uint8_t* d_codes, int64_t n, ks_seq* seq, int* d_flag,
                       int* launches);
+int scatter_tile_masks_device(ks_ctx* ctx, const uint64_t* d_compact, const int32_t* d_ids, int n_tiles,
+                              int tile_words, uint64_t* d_nmask, int* launches);
 int encode_piece_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, ks_seq* seq, uint32_t* kept,
                         int* ws_flag, int* launches);
 int unpack_codes_device(ks_ctx* ctx, const ks_seq* seq, uint8_t* d_out);
@@ -576,15 +579,20 @@ void seq_destroy(ks_seq* s) {
     delete s;
 }
 
-// Streaming count from a host buffer (ks_count_host_ascii).  Piece i is
-// copied into device buffer i%2 on the copy stream while piece i-1 is encoded
-// and scanned on the compute stream; every piece enters in the state the
-// previous piece left (a device-resident uint16), visits accumulate.
+// Streaming count from a host buffer (ks_count_host_ascii).  Default wire
+// format: host worker threads pack piece i (AVX-512, host_pack.cpp) straight
+// into the tile-slot layout in pinned staging slot i%3, the copy stream moves
+// 0.25-0.375 B/base into device buffer i%2, and the compute stream scans it
+// while piece i+1 is packed.  KS_DEVICE_ENCODE=1 instead copies raw ASCII
+// (1 B/base) and encodes on the device.  Every piece enters in the state the
+// previous piece left (a device-resident uint16); visits accumulate.
 int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int64_t n_bytes,
                       int64_t* counts_out, bool* fallback) {
     const HostDfa& h = dfa->host;
     *fallback = false;
-    const int64_t piece = std::min<int64_t>(std::max<int64_t>(n_bytes, 64), int64_t(64) << 20);
+    const bool host_pack = std::getenv("KS_DEVICE_ENCODE") == nullptr;
+    static const int64_t piece_mb = std::getenv("KS_PIECE_MB") ? std::atoll(std::getenv("KS_PIECE_MB")) : 64;
+    const int64_t piece = std::min<int64_t>(std::max<int64_t>(n_bytes, 64), piece_mb << 20);
     const int64_t npieces = (n_bytes + piece - 1) / piece;
     // piece buffers: 2 x (input bytes + packed tiled sequence)
     ks_seq tmpl;
@@ -592,7 +600,10 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
     const int64_t tile_blocks = int64_t(32) << tmpl.lb;
     const int64_t blocks = (piece + 63) / 64;
     const int64_t slots = ((blocks + tile_blocks - 1) / tile_blocks + 1) * tile_blocks;
-    const size_t in_bytes = up(size_t(piece) + 64);
+    const int64_t ntiles = slots / tile_blocks;
+    // device input region per buffer: raw ASCII (device encode) or the
+    // compacted OTHER bitmaps + their tile ids (host pack)
+    const size_t in_bytes = host_pack ? up(size_t(slots) * 8 + size_t(ntiles) * 4 + 64) : up(size_t(piece) + 64);
     const size_t seq_bytes = up(size_t(slots) * 32);
     const size_t need = 2 * (in_bytes + seq_bytes);
     if (ctx->sbuf_bytes < need) {
@@ -606,6 +617,20 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
     if (!ctx->copy_stream) {
         KS_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
         for (auto& e : ctx->sev) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (auto& e : ctx->hev) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    // staging slot: bases (16 B per block slot), compacted OTHER bitmaps (<= 8 B per slot), tile ids
+    const size_t wire = up(size_t(slots) * 24 + size_t(ntiles) * 4);
+    if (host_pack) {
+        if (ctx->hstage_bytes < 3 * wire) {
+            KS_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+            if (ctx->hstage) KS_CUDA(cudaFreeHost(ctx->hstage));
+            ctx->hstage = nullptr;
+            ctx->hstage_bytes = 0;
+            KS_CUDA(cudaMallocHost(&ctx->hstage, 3 * wire));
+            ctx->hstage_bytes = 3 * wire;
+        }
+        if (!ctx->pool) ctx->pool = new HostPool(host_pack_threads());
     }
     uint8_t* din[2];
     ks_seq pseq[2];
@@ -656,17 +681,64 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
     KS_CUDA(cudaEventRecord(ctx->sev[3], ctx->stream));
     const ScanPlan plan = plan_for(ctx, dfa, dfa->scan);
     int launches = 0;
+    int64_t h2d = 2;   // the entry state
     for (int64_t i = 0; i < npieces; ++i) {
         const int b = int(i & 1);
         const int64_t off = i * piece;
         const int64_t len = std::min(piece, n_bytes - off);
-        KS_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->sev[2 + b], 0));
-        KS_CUDA(cudaMemcpyAsync(din[b], bytes + off, size_t(len), cudaMemcpyHostToDevice, ctx->copy_stream));
-        KS_CUDA(cudaEventRecord(ctx->sev[b], ctx->copy_stream));
-        KS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->sev[b], 0));
-        rc = encode_piece_device(ctx, din[b], len, &pseq[b], kept, ws_flag, &launches);
-        if (rc) return rc;
-        KS_CUDA(cudaEventRecord(ctx->sev[2 + b], ctx->stream));  // din[b] consumed
+        if (host_pack) {
+            const int st = int(i % 3);
+            uint64_t* hb = reinterpret_cast<uint64_t*>(static_cast<char*>(ctx->hstage) + st * wire);
+            uint64_t* hn = hb + 2 * slots;
+            int32_t* hid = reinterpret_cast<int32_t*>(hn + slots);
+            if (i >= 3) KS_CUDA(cudaEventSynchronize(ctx->hev[st]));   // staging slot free again
+            const int64_t nt = ((len + 63) / 64 + tile_blocks - 1) / tile_blocks;   // tiles in this piece
+            const int64_t used = nt * tile_blocks;
+            const int64_t per_task = 4;   // tiles
+            std::atomic<int> fl{0};
+            std::atomic<int32_t> ncomp{0};
+            const uint8_t* src = bytes + off;
+            ctx->pool->run((nt + per_task - 1) / per_task, [&](int64_t t) {
+                const PackFlags f = pack_ascii_tiles(src, len, t * per_task, std::min(nt, (t + 1) * per_task),
+                                                     tmpl.lb, hb, hn, hid, &ncomp);
+                if (f.whitespace) fl.fetch_or(1);
+            });
+            if (fl.load() & 1) {   // whitespace: positions shift, use the compacting path
+                KS_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+                KS_CUDA(cudaStreamSynchronize(ctx->stream));
+                *fallback = true;
+                return KS_OK;
+            }
+            const int nc = ncomp.load();
+            uint64_t* d_comp = reinterpret_cast<uint64_t*>(din[b]);
+            int32_t* d_ids = reinterpret_cast<int32_t*>(din[b] + size_t(slots) * 8);
+            KS_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->sev[2 + b], 0));
+            KS_CUDA(cudaMemcpyAsync(pseq[b].d_bases, hb, size_t(used) * 16, cudaMemcpyHostToDevice,
+                                    ctx->copy_stream));
+            KS_CUDA(cudaMemsetAsync(pseq[b].d_nmask, 0, size_t(used) * 8, ctx->copy_stream));
+            h2d += used * 16;
+            if (nc > 0) {
+                KS_CUDA(cudaMemcpyAsync(d_comp, hn, size_t(nc) * tile_blocks * 8, cudaMemcpyHostToDevice,
+                                        ctx->copy_stream));
+                KS_CUDA(cudaMemcpyAsync(d_ids, hid, size_t(nc) * 4, cudaMemcpyHostToDevice, ctx->copy_stream));
+                h2d += int64_t(nc) * (tile_blocks * 8 + 4);
+            }
+            KS_CUDA(cudaEventRecord(ctx->hev[st], ctx->copy_stream));
+            KS_CUDA(cudaEventRecord(ctx->sev[b], ctx->copy_stream));
+            KS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->sev[b], 0));
+            rc = scatter_tile_masks_device(ctx, d_comp, d_ids, nc, int(tile_blocks), pseq[b].d_nmask, &launches);
+            if (rc) return rc;
+            pseq[b].n = len;
+        } else {
+            KS_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->sev[2 + b], 0));
+            KS_CUDA(cudaMemcpyAsync(din[b], bytes + off, size_t(len), cudaMemcpyHostToDevice, ctx->copy_stream));
+            h2d += len;
+            KS_CUDA(cudaEventRecord(ctx->sev[b], ctx->copy_stream));
+            KS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->sev[b], 0));
+            rc = encode_piece_device(ctx, din[b], len, &pseq[b], kept, ws_flag, &launches);
+            if (rc) return rc;
+            KS_CUDA(cudaEventRecord(ctx->sev[2 + b], ctx->stream));  // din[b] consumed
+        }
         int64_t o2, L2, nch;
         geometry(&pseq[b], 0, len, &o2, &L2, &nch);
         ScanArgs a = base_args(dfa, dfa->scan, &pseq[b]);
@@ -692,6 +764,7 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
         rc = dispatch(ctx, dfa, dfa->scan, plan, a, kModeCount, &launches);
         if (rc) return rc;
         KS_CUDA(cudaMemcpyAsync(state, chunk_exit + (nch - 1), 2, cudaMemcpyDeviceToDevice, ctx->stream));
+        if (host_pack) KS_CUDA(cudaEventRecord(ctx->sev[2 + b], ctx->stream));  // device buffer b consumed
     }
     rc = launch_finalize_counts(ctx, visits, h.n_accept, dfa->d_acc_out_off, dfa->d_acc_out_ids, counts,
                                 nullptr, nullptr, &launches);
@@ -706,6 +779,8 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
     }
     std::memcpy(counts_out, pin, size_t(h.ne) * 8);
     ctx->stats.kernel_launches = launches;
+    ctx->stats.h2d_bytes = h2d;
+    ctx->stats.d2h_bytes = int64_t(h.ne) * 8 + 4;
     return KS_OK;
 }
 
@@ -758,6 +833,11 @@ int ks_close(ks_ctx* ctx) {
     if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->sbuf) cudaFree(ctx->sbuf);
+    if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
+    delete ctx->pool;
+    if (ctx->hstage) cudaFreeHost(ctx->hstage);
+    for (auto& ev : ctx->hev)
+        if (ev) cudaEventDestroy(ev);
     if (ctx->copy_stream) {
         cudaStreamSynchronize(ctx->copy_stream);
         cudaStreamDestroy(ctx->copy_stream);
@@ -1063,6 +1143,17 @@ int ks_async_wait(ks_ctx* ctx, float* scan_ms_total, int32_t* calls, int32_t* la
     if (launches) *launches = ctx->async_launches;
     ctx->n_async = 0;
     ctx->async_launches = 0;
+    return KS_OK;
+}
+
+int ks_pack_host_ascii(const uint8_t* bytes, int64_t n_bytes, int32_t lb, uint64_t* bases, uint64_t* nmask,
+                       int32_t* flags) {
+    if (n_bytes < 0 || (n_bytes > 0 && (!bytes || !bases || !nmask)) || lb < 0 || lb > 12)
+        return fail(KS_E_INVALID, "bad argument");
+    const int64_t tb = int64_t(32) << lb;
+    const int64_t used = (n_bytes + 63) / 64 + tb - 1 - ((n_bytes + 63) / 64 + tb - 1) % tb;
+    const PackFlags f = pack_ascii_blocks(bytes, n_bytes, 0, used, lb, bases, nmask);
+    if (flags) *flags = (f.whitespace ? 1 : 0) | (f.other ? 2 : 0);
     return KS_OK;
 }
 

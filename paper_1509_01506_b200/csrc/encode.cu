@@ -266,6 +266,24 @@ int encode_piece_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, ks_se
     return KS_OK;
 }
 
+// Host-packed wire format (host_pack.h): OTHER bitmaps arrive only for the
+// tiles that hold OTHER, compacted; one CTA copies each into place.
+__global__ void scatter_tile_masks_kernel(const uint64_t* __restrict__ compact, const int32_t* __restrict__ ids,
+                                          int tile_words, uint64_t* __restrict__ nmask) {
+    const uint64_t* src = compact + size_t(blockIdx.x) * tile_words;
+    uint64_t* dst = nmask + size_t(ids[blockIdx.x]) * tile_words;
+    for (int i = threadIdx.x; i < tile_words; i += blockDim.x) dst[i] = src[i];
+}
+
+int scatter_tile_masks_device(ks_ctx* ctx, const uint64_t* d_compact, const int32_t* d_ids, int n_tiles,
+                              int tile_words, uint64_t* d_nmask, int* launches) {
+    if (n_tiles <= 0) return KS_OK;
+    scatter_tile_masks_kernel<<<n_tiles, 256, 0, ctx->stream>>>(d_compact, d_ids, tile_words, d_nmask);
+    if (launches) ++*launches;
+    KS_CUDA(cudaGetLastError());
+    return KS_OK;
+}
+
 int pack_codes_device(ks_ctx* ctx, const uint8_t* d_codes, int64_t n, ks_seq* seq, int* d_flag,
                       int* launches) {
     const int64_t nb = (n + 63) / 64;

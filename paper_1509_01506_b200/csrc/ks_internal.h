@@ -11,6 +11,8 @@
 
 namespace ks {
 
+class HostPool;
+
 // ---------------------------------------------------------------- errors
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
@@ -133,6 +135,11 @@ struct ks_ctx {
     cudaEvent_t sev[4] = {nullptr, nullptr, nullptr, nullptr};
     void* sbuf = nullptr;
     size_t sbuf_bytes = 0;
+    // host-packed wire format: worker pool + pinned staging ring
+    ks::HostPool* pool = nullptr;
+    void* hstage = nullptr;
+    size_t hstage_bytes = 0;
+    cudaEvent_t hev[3] = {nullptr, nullptr, nullptr};
     // ks_count_async: one event pair per call until ks_async_wait
     std::vector<cudaEvent_t> aev;
     int n_async = 0;

@@ -5,6 +5,7 @@ import hashlib
 
 import numpy as np
 import pytest
+import torch
 
 import paper_1509_01506_b200 as ks
 from paper_1509_01506_b200 import _native, workloads
@@ -288,8 +289,11 @@ def test_match_chunk_reduce_roundtrip(toy_dfa):
 
 # ---------------------------------------------------------------- streaming host input
 
+@pytest.mark.parametrize("encode", ["host", "device"])
 @pytest.mark.parametrize("config,n", [(3, (1 << 20) + 12345), (2, 300_001), (5, 200_003), (1, 0), (1, 1)])
-def test_count_host_ascii_matches(config, n, monkeypatch):
+def test_count_host_ascii_matches(config, n, encode, monkeypatch):
+    if encode == "device":
+        monkeypatch.setenv("KS_DEVICE_ENCODE", "1")
     w = workloads.make(config, max(n, 1))
     data = w.ascii.tobytes()[:n]
     ctx = _native.context(0)
@@ -312,6 +316,30 @@ def test_count_host_ascii_small_pieces_and_whitespace():
     text = b"\n".join(data[i:i + 61] for i in range(0, 200_000, 61))
     want = O.ref_sequential_count(w.dfa, ks.encode_bytes(text))[0]
     assert ctx.count_host_ascii(dh, text).tolist() == want.tolist()
+
+
+@pytest.mark.parametrize("encode", ["host", "device"])
+def test_count_host_ascii_many_pieces(encode, monkeypatch):
+    """Five 64 MiB pieces: the 3-slot pinned staging ring wraps, the device
+    double buffer alternates, the entry state crosses every piece boundary
+    (cuts fall inside units), and OTHER appears in some pieces only (nmask
+    copied vs zero-filled)."""
+    if encode == "device":
+        monkeypatch.setenv("KS_DEVICE_ENCODE", "1")
+    piece = 64 << 20
+    w = workloads.make(3, 4 * piece + 777_777)
+    buf = bytearray(w.ascii.tobytes())
+    rng = np.random.default_rng(5)
+    for p in rng.integers(piece, 2 * piece, size=1000).tolist() + [3 * piece - 1, 3 * piece, 4 * piece + 5]:
+        buf[p] = ord("N")
+    data = bytes(buf)
+    want = O.ref_sequential_count(w.dfa, ks.encode_bytes(data))[0]
+    ctx = _native.context(0)
+    dh = ctx.dfa(w.dfa)
+    pinned = torch.empty(len(data), dtype=torch.uint8, pin_memory=True)
+    pinned.numpy()[:] = np.frombuffer(data, dtype=np.uint8)
+    assert ctx.count_host_ascii(dh, pinned.numpy()).tolist() == want.tolist()
+    assert ctx.count_host_ascii(dh, data).tolist() == want.tolist()   # pageable input too
 
 
 # ---------------------------------------------------------------- multi-GPU building blocks (on one GPU)

@@ -8,6 +8,7 @@ import subprocess
 import sys
 from pathlib import Path
 
+import numpy as np
 import pytest
 
 from paper_1509_01506_b200 import _native
@@ -64,3 +65,64 @@ def test_product_never_imports_oracle():
     for path in (REPO / "paper_1509_01506_b200").rglob("*.py"):
         text = path.read_text()
         assert not re.search(r"^\s*(from|import)\s+oracle", text, flags=re.M), path
+
+
+def _blk_slot(g, lb):
+    u = g >> lb
+    return ((u >> 5) << (5 + lb)) | ((g & ((1 << lb) - 1)) << 5) | (u & 31)
+
+
+def _pack_reference(data: bytes, lb: int):
+    """Straight restatement of the wire format (encode.cu header) in numpy."""
+    x = np.frombuffer(data, dtype=np.uint8).astype(np.int64)
+    lx = x | 0x20
+    base = np.isin(lx, [ord(c) for c in "acgt"])
+    ws = np.isin(x, [9, 10, 13, 32])
+    code = np.where(base, ((x >> 1) ^ (x >> 2)) & 3, 0)
+    other = ~base & ~ws
+    nblk = (x.size + 63) // 64
+    tile = 32 << lb
+    slots = max(-(-nblk // tile) * tile, 1)
+    bases = np.zeros(2 * slots, dtype=np.uint64)
+    nmask = np.zeros(slots, dtype=np.uint64)
+    for g in range(nblk):
+        s = _blk_slot(g, lb)
+        c = code[64 * g: 64 * g + 64]
+        o = other[64 * g: 64 * g + 64]
+        for i in range(c.size):
+            bases[2 * s + (i >> 5)] |= np.uint64(int(c[i]) << (2 * (i & 31)))
+            nmask[s] |= np.uint64(int(o[i]) << i)
+    return bases, nmask, int(ws.any()) | (int(other.any()) << 1)
+
+
+@pytest.mark.parametrize("n,lb,alphabet", [
+    (0, 0, b"acgt"), (1, 0, b"acgt"), (63, 1, b"ACGTacgt"), (64, 0, b"acgtN"), (4097, 2, b"acgtACGTnNx-"),
+    (70_000, 4, b"acgt"), (70_001, 3, b"acgt \n"), (9000, 1, b"\x00\xffacgt\t\r"),
+])
+@pytest.mark.parametrize("scalar", [False, True])
+def test_host_packer_matches_wire_format(n, lb, alphabet, scalar, monkeypatch):
+    """ks_pack_host_ascii (AVX-512 and scalar paths, run in a subprocess for
+    the scalar switch) reproduces the documented wire format bit for bit."""
+    rng = np.random.default_rng(n * 7 + lb)
+    data = bytes(np.frombuffer(alphabet, dtype=np.uint8)[rng.integers(0, len(alphabet), size=n)])
+    want = _pack_reference(data, lb)
+    if scalar:
+        code = ("import sys, numpy as np; from paper_1509_01506_b200 import _native;"
+                f"b, m, f = _native.pack_host_ascii(open(sys.argv[1], 'rb').read(), {lb});"
+                "np.save(sys.argv[2], np.concatenate([b, m, np.array([f], dtype=np.uint64)]))")
+        import tempfile
+        with tempfile.TemporaryDirectory() as d:
+            Path(d, "in").write_bytes(data)
+            env = dict(__import__("os").environ, KS_HOST_SCALAR="1")
+            subprocess.run([sys.executable, "-c", code, str(Path(d, "in")), str(Path(d, "out.npy"))],
+                           check=True, env=env, cwd=REPO)
+            out = np.load(Path(d, "out.npy"))
+        k = want[0].size
+        got = (out[:k], out[k:-1], int(out[-1]))
+    else:
+        got = _native.pack_host_ascii(data, lb)
+    assert got[2] == want[2]
+    nblk = (n + 63) // 64
+    slots = [_blk_slot(g, lb) for g in range(nblk)]
+    assert np.array_equal(got[1][slots], want[1][slots])
+    assert np.array_equal(got[0].reshape(-1, 2)[slots], want[0].reshape(-1, 2)[slots])
