@@ -152,8 +152,8 @@ __device__ __forceinline__ void rewalk(const Ctx& c, Lane<MODE>& L, uint32_t v, 
 // accepts.
 template <int K, int MODE>
 __device__ __forceinline__ void resolve(const Ctx& c, Lane<MODE>& L, uint32_t a) {
-    if constexpr (K == 2) {
-        const uint32_t e = lds16(c.tk + a);
+    if constexpr (K == 2) {   // ring value = address | entry << 17: no table re-read
+        const uint32_t e = a >> 17;
         if (e & 0x2000u) record<MODE>(c, L, 0, step1<MODE>(c, (a >> 1) & 0xFFFu, (a >> 13) & 3u));
         if (e & 0x4000u) record<MODE>(c, L, 0, (e >> 1) & 0xFFFu);
     } else {
@@ -171,9 +171,33 @@ __device__ __forceinline__ void drain(const Ctx& c, Lane<MODE>& L, unsigned am, 
     rp = rp0;
 }
 
+// Register ring (K = 2 count/rows, high hit rates): a flagged step keeps
+// (table address << 15) | entry in r0 (the previous one shifts to r1) and
+// the lanes drain every 2 steps, so hits cost no shared-memory ring traffic
+// and the entry is never re-read: bit 14 names the final state, bit 13 says
+// the intermediate state accepts (re-derived with one 1-base lookup).
+template <int MODE>
+__device__ __forceinline__ void resolve_reg(const Ctx& c, Lane<MODE>& L, uint32_t v) {
+    if (v & 0x4000u) record<MODE>(c, L, 0, (v >> 1) & 0xFFFu);
+    if (v & 0x2000u) {
+        const uint32_t a = v >> 15;
+        record<MODE>(c, L, 0, step1<MODE>(c, (a >> 1) & 0xFFFu, (a >> 13) & 3u));
+    }
+}
+
+template <int MODE>
+__device__ __forceinline__ void drain_reg(const Ctx& c, Lane<MODE>& L, unsigned am, uint32_t r0, uint32_t r1,
+                                          uint32_t cnt) {
+    const uint32_t kmax = __reduce_max_sync(am, cnt);
+    if (kmax) {
+        if (cnt) resolve_reg<MODE>(c, L, r0);
+        if (kmax > 1 && cnt > 1) resolve_reg<MODE>(c, L, r1);
+    }
+}
+
 // One full, OTHER-free 64-base block.  `live` lanes record hits; others ride
 // along in the sink state.
-template <int K, int MODE>
+template <int K, int MODE, bool REG>
 __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint32_t s, const uint4& xb,
                                                int64_t p0, unsigned am, uint32_t rp0, uint32_t& rp,
                                                uint32_t ring_stride) {
@@ -184,13 +208,25 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
     constexpr uint32_t FM = ((1u << (2 * K)) - 1u) << LC;  // field mask
     constexpr bool RING = MODE == kModeCount || MODE == kModeRows;
     uint32_t e = s << 1;  // entry form of the current state (no flag)
+    uint32_t r0 = 0, r1 = 0, cnt = 0;
 #pragma unroll
     for (int j = 0; j < NL; ++j) {
         const uint32_t a = bitsel<FM>(field<K>(xb, j), e);
         e = lds16(c.tk + a);
-        if constexpr (RING) {
+        if constexpr (REG) {
+            static_assert(K == 2 && RING, "register ring is K = 2 count/rows only");
             if (e & 0x8000u) {
-                sts32(rp, a);
+                r1 = r0;
+                r0 = (a << 15) | (e & 0x7FFFu);
+                ++cnt;
+            }
+            if (j & 1) {
+                drain_reg<MODE>(c, L, am, r0, r1, cnt);
+                cnt = 0;
+            }
+        } else if constexpr (RING) {
+            if (e & 0x8000u) {
+                sts32(rp, K == 2 ? a + (e << 17) : a);
                 rp += ring_stride;
             }
             if ((j % kRing) == kRing - 1 || j == NL - 1) drain<K, MODE>(c, L, am, rp0, rp, ring_stride);
@@ -217,7 +253,7 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
 
 extern __shared__ __align__(128) unsigned char f_smem[];
 
-template <int K, int MODE>
+template <int K, int MODE, bool REG>
 __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     constexpr bool RING = MODE == kModeCount || MODE == kModeRows;
     constexpr bool DIRECT = MODE == kModeCountDirect;
@@ -342,8 +378,8 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
             const bool fast = !has || (k >= kfl && k < kfh && (clean || (alln && resets)));
             if (__all_sync(am, fast)) {
                 const bool live = has && !alln;
-                const uint32_t s2 = fast_block<K, MODE>(c, L, live ? s : sink, wb, p0, am, rp0, rp,
-                                                        ring_stride);
+                const uint32_t s2 = fast_block<K, MODE, REG>(c, L, live ? s : sink, wb, p0, am, rp0, rp,
+                                                             ring_stride);
                 if (live) {
                     s = s2;
                 } else if (has) {
@@ -404,24 +440,28 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
 using FastFn = void (*)(const ScanArgs);
 
 template <int K>
-FastFn pick_mode(int mode) {
+FastFn pick_mode(int mode, bool reg) {
+    if constexpr (K == 2) {
+        if (reg && mode == kModeCount) return scan_fast_kernel<2, kModeCount, true>;
+        if (reg && mode == kModeRows) return scan_fast_kernel<2, kModeRows, true>;
+    }
     switch (mode) {
         case kModeCountDirect:
-            if constexpr (K == 2) return scan_fast_kernel<2, kModeCountDirect>;
+            if constexpr (K == 2) return scan_fast_kernel<2, kModeCountDirect, false>;
             return nullptr;
-        case kModeCount: return scan_fast_kernel<K, kModeCount>;
-        case kModeRows: return scan_fast_kernel<K, kModeRows>;
-        case kModeEmit: return scan_fast_kernel<K, kModeEmit>;
-        case kModeMap: return scan_fast_kernel<K, kModeMap>;
+        case kModeCount: return scan_fast_kernel<K, kModeCount, false>;
+        case kModeRows: return scan_fast_kernel<K, kModeRows, false>;
+        case kModeEmit: return scan_fast_kernel<K, kModeEmit, false>;
+        case kModeMap: return scan_fast_kernel<K, kModeMap, false>;
     }
     return nullptr;
 }
 
-FastFn pick(int mode, int k) {
+FastFn pick(int mode, int k, bool reg) {
     switch (k) {
-        case 2: return pick_mode<2>(mode);
-        case 3: return pick_mode<3>(mode);
-        case 4: return pick_mode<4>(mode);
+        case 2: return pick_mode<2>(mode, reg);
+        case 3: return pick_mode<3>(mode, reg);
+        case 4: return pick_mode<4>(mode, reg);
     }
     return nullptr;
 }
@@ -442,7 +482,7 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
     if (a.end <= a.begin || a.nchunks <= 0) return KS_OK;
     const bool ring = mode == kModeCount || mode == kModeRows || mode == kModeCountDirect;
     a.hist_smem = ring ? 1 : 0;
-    FastFn fn = pick(mode, k);
+    FastFn fn = pick(mode, k, a.reg_ring != 0);
     if (!fn) return fail(KS_E_INVALID, "fast scan: bad mode/stride");
     const size_t smem = fast_smem_bytes(mode, a.t1_pad, ring ? a.n_accept : 0, kFastThreads);
     if (smem > ctx->smem_optin) return fail(KS_E_UNSUPPORTED, "fast scan: shared memory budget exceeded");

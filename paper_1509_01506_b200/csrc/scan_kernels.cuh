@@ -49,6 +49,7 @@ struct ScanArgs {
     int32_t nq = 0, n_accept = 0, reset_state = -1;
     int32_t tk_pad = 0, t1_pad = 0;  // uint16 entries, multiples of 8
     int32_t hist_smem = 0;           // histogram in shared memory
+    int32_t reg_ring = 0;            // fast kernel, K = 2: deferred hits in registers (scan_fast.cu)
     // outputs
     unsigned long long* visits = nullptr;   // n_accept, global accumulation
     uint16_t* chunk_exit = nullptr;         // per chunk exit state (optional)
