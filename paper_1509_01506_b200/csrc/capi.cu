@@ -234,9 +234,11 @@ int dispatch(ks_ctx* ctx, const ks_dfa* dfa, const DevTable& T, const ScanPlan& 
             if (direct && fast_smem_bytes(kModeCountDirectId, 0, T.n_accept, fast_threads()) <= ctx->smem_optin)
                 mode = kModeCountDirectId;
         }
-        if (T.fast_k == 2 && (mode == kModeCount || mode == kModeRows)) {
-            const char* env = std::getenv("KS_REG_RING");
-            a.reg_ring = env && *env ? *env == '1' : 0;   // measured slower on C3 (0.571 vs 0.456 ms)
+        if (mode == kModeCount || mode == kModeRows) {
+            const char* env = std::getenv("KS_FAST_VAR");
+            const int var = env && *env ? std::atoi(env) : 0;
+            if (variant_smem_bytes(var, mode, T.fast_k, a.t1_pad, T.n_accept, fast_threads()) <= ctx->smem_optin)
+                a.fast_variant = var;
         }
         return launch_scan_fast(ctx, a, mode, T.fast_k, launches);
     }

@@ -21,13 +21,29 @@
 // The lane/chunk/entry-state logic is the one of scan.cu (lookback, uniform
 // or per-chunk entry states).
 #include <algorithm>
+#include <cstdlib>
 
 #include "scan_kernels.cuh"
 
 namespace ks {
 namespace {
 
-constexpr int kRing = 8;  // steps between ring drains (ring depth)
+constexpr int kRing = 8;      // minimum ring depth (deferred hits per lane)
+constexpr int kRingMax = 32;  // the ring takes what shared memory is left, up to this
+// steps between ring-fill checks: every 2nd step at K = 2 (high hit rates),
+// every 8th otherwise (the vote is pure overhead when hits are rare)
+__host__ __device__ constexpr int chk_steps(int k) { return k == 2 ? 2 : 8; }
+// Kernel variants (template V), count/rows modes:
+//   kVarRing  : deferred hits resolved with the 1-base table (in shared memory);
+//   kVarPairs : K = 2 count mode -- a hit whose intermediate state accepts
+//               bumps a (first base, previous state) counter instead of
+//               re-deriving the state; the pairs are mapped to states once
+//               per CTA at the end.  Its 64 KiB of counters leave a shallow
+//               ring (1-base table read through L1): measured slower on C3
+//               (0.54 vs 0.43 ms), kept selectable with KS_FAST_VAR=1.
+constexpr int kVarRing = 0;
+constexpr int kVarPairs = 1;
+__host__ __device__ constexpr bool t1_in_smem(int v) { return v != kVarPairs; }
 // Count mode with direct shared-memory histograms instead of the ring (K = 2,
 // high hit rates): bit 13 of an entry = the intermediate state is accepting
 // (counted per (first base, previous state) and resolved at the end), bit 14
@@ -103,6 +119,7 @@ struct Ctx {
     int64_t* rows;
     int64_t row_base;
     uint32_t n_accept;
+    uint32_t ring_thr;  // drain when a lane holds this many ring bytes (depth - chk_steps(K) entries)
 };
 
 template <int MODE>
@@ -127,21 +144,21 @@ __device__ __forceinline__ void record(const Ctx& c, Lane<MODE>& L, int64_t pos,
     }
 }
 
-template <int MODE>
+template <int MODE, int V = kVarRing>
 __device__ __forceinline__ uint32_t step1(const Ctx& c, uint32_t s, uint32_t sym) {
-    if constexpr (MODE == kModeCountDirect) return __ldg(c.t1g + s * 5u + sym);
+    if constexpr (MODE == kModeCountDirect || !t1_in_smem(V)) return __ldg(c.t1g + s * 5u + sym);
     return lds16(c.t1 + (s * 5u + sym) * 2u);
 }
 
 // Re-walk one deferred K-step (ring value = its table byte address).
-template <int K, int MODE>
+template <int K, int MODE, int V = kVarRing>
 __device__ __forceinline__ void rewalk(const Ctx& c, Lane<MODE>& L, uint32_t v, int64_t pos) {
     constexpr int LC = 17 - 2 * K;
     uint32_t s = (v >> 1) & ((1u << (LC - 1)) - 1u);
     const uint32_t w = v >> LC;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-        s = step1<MODE>(c, s, (w >> (2 * i)) & 3u);
+        s = step1<MODE, V>(c, s, (w >> (2 * i)) & 3u);
         if (s < c.n_accept) record<MODE>(c, L, pos + i, s);
     }
 }
@@ -150,54 +167,45 @@ __device__ __forceinline__ void rewalk(const Ctx& c, Lane<MODE>& L, uint32_t v, 
 // 13/14 say which of the two states accepts: re-reading the entry gives the
 // final state directly and the intermediate one is only re-derived when it
 // accepts.
-template <int K, int MODE>
+template <int K, int MODE, int V>
 __device__ __forceinline__ void resolve(const Ctx& c, Lane<MODE>& L, uint32_t a) {
-    if constexpr (K == 2) {   // ring value = address | entry << 17: no table re-read
+    if constexpr (V == kVarPairs) {   // count only: intermediate hits by (first base, previous state)
         const uint32_t e = a >> 17;
-        if (e & 0x2000u) record<MODE>(c, L, 0, step1<MODE>(c, (a >> 1) & 0xFFFu, (a >> 13) & 3u));
+        if (e & 0x2000u) red_shared_add(c.hist2 + ((a & 0x7FFEu) << 1), 1u);
+        if (e & 0x4000u) red_shared_add(c.hist + ((e & 0x1FFEu) << 1), 1u);
+    } else if constexpr (K == 2) {   // ring value = address | entry << 17: no table re-read
+        const uint32_t e = a >> 17;
+        if (e & 0x2000u) record<MODE>(c, L, 0, step1<MODE, V>(c, (a >> 1) & 0xFFFu, (a >> 13) & 3u));
         if (e & 0x4000u) record<MODE>(c, L, 0, (e >> 1) & 0xFFFu);
     } else {
-        rewalk<K, MODE>(c, L, a, 0);
+        rewalk<K, MODE, V>(c, L, a, 0);
     }
 }
 
-template <int K, int MODE>
+template <int K, int MODE, int V>
 __device__ __forceinline__ void drain(const Ctx& c, Lane<MODE>& L, unsigned am, uint32_t rp0,
                                       uint32_t& rp, uint32_t ring_stride) {
     const uint32_t cnt = (rp - rp0) / kRingStride;
     const uint32_t kmax = __reduce_max_sync(am, cnt);  // warp-uniform trip count
     for (uint32_t k = 0; k < kmax; ++k)
-        if (k < cnt) resolve<K, MODE>(c, L, lds32(rp0 + k * ring_stride));
+        if (k < cnt) resolve<K, MODE, V>(c, L, lds32(rp0 + k * ring_stride));
     rp = rp0;
 }
 
-// Register ring (K = 2 count/rows, high hit rates): a flagged step keeps
-// (table address << 15) | entry in r0 (the previous one shifts to r1) and
-// the lanes drain every 2 steps, so hits cost no shared-memory ring traffic
-// and the entry is never re-read: bit 14 names the final state, bit 13 says
-// the intermediate state accepts (re-derived with one 1-base lookup).
-template <int MODE>
-__device__ __forceinline__ void resolve_reg(const Ctx& c, Lane<MODE>& L, uint32_t v) {
-    if (v & 0x4000u) record<MODE>(c, L, 0, (v >> 1) & 0xFFFu);
-    if (v & 0x2000u) {
-        const uint32_t a = v >> 15;
-        record<MODE>(c, L, 0, step1<MODE>(c, (a >> 1) & 0xFFFu, (a >> 13) & 3u));
-    }
-}
-
-template <int MODE>
-__device__ __forceinline__ void drain_reg(const Ctx& c, Lane<MODE>& L, unsigned am, uint32_t r0, uint32_t r1,
-                                          uint32_t cnt) {
-    const uint32_t kmax = __reduce_max_sync(am, cnt);
-    if (kmax) {
-        if (cnt) resolve_reg<MODE>(c, L, r0);
-        if (kmax > 1 && cnt > 1) resolve_reg<MODE>(c, L, r1);
-    }
+// Out-of-line drain for the adaptive drain sites inside the unrolled block
+// loop (one copy of the resolve code instead of one per site).
+template <int K, int MODE, int V>
+__device__ __noinline__ uint32_t drain_out(const Ctx c, uint32_t rp0, uint32_t cnt) {
+    Lane<MODE> L;
+    const uint32_t kmax = __reduce_max_sync(0xffffffffu, cnt);
+    for (uint32_t k = 0; k < kmax; ++k)
+        if (k < cnt) resolve<K, MODE, V>(c, L, lds32(rp0 + k * kRingStride));
+    return L.nrows;
 }
 
 // One full, OTHER-free 64-base block.  `live` lanes record hits; others ride
 // along in the sink state.
-template <int K, int MODE, bool REG>
+template <int K, int MODE, int V>
 __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint32_t s, const uint4& xb,
                                                int64_t p0, unsigned am, uint32_t rp0, uint32_t& rp,
                                                uint32_t ring_stride) {
@@ -208,30 +216,25 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
     constexpr uint32_t FM = ((1u << (2 * K)) - 1u) << LC;  // field mask
     constexpr bool RING = MODE == kModeCount || MODE == kModeRows;
     uint32_t e = s << 1;  // entry form of the current state (no flag)
-    uint32_t r0 = 0, r1 = 0, cnt = 0;
 #pragma unroll
     for (int j = 0; j < NL; ++j) {
         const uint32_t a = bitsel<FM>(field<K>(xb, j), e);
         e = lds16(c.tk + a);
-        if constexpr (REG) {
-            static_assert(K == 2 && RING, "register ring is K = 2 count/rows only");
-            if (e & 0x8000u) {
-                r1 = r0;
-                r0 = (a << 15) | (e & 0x7FFFu);
-                ++cnt;
-            }
-            if (j & 1) {
-                drain_reg<MODE>(c, L, am, r0, r1, cnt);
-                cnt = 0;
-            }
-        } else if constexpr (RING) {
+        if constexpr (RING) {
             if (e & 0x8000u) {
                 sts32(rp, K == 2 ? a + (e << 17) : a);
                 rp += ring_stride;
             }
-            if ((j % kRing) == kRing - 1 || j == NL - 1) drain<K, MODE>(c, L, am, rp0, rp, ring_stride);
+            // drain only when some lane's ring is nearly full (checked every
+            // chk_steps(K) steps): drains then run with full lanes, and ring entries
+            // (table addresses) are position-free, so they may cross blocks
+            constexpr int CHK = chk_steps(K);
+            if ((j % CHK) == CHK - 1 && __any_sync(am, rp - rp0 >= c.ring_thr)) {
+                L.nrows += drain_out<K, MODE, V>(c, rp0, (rp - rp0) / kRingStride);
+                rp = rp0;
+            }
         } else if constexpr (MODE == kModeEmit) {
-            if (e & 0x8000u) rewalk<K, MODE>(c, L, a, p0 + K * j);
+            if (e & 0x8000u) rewalk<K, MODE, V>(c, L, a, p0 + K * j);
         } else if constexpr (MODE == kModeCountDirect) {
             static_assert(K == 2, "direct counting is K = 2 only");
             red_shared_inc_if(c.hist2 + ((a & 0x7FFEu) << 1), e & 0x2000u);
@@ -242,7 +245,7 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
 #pragma unroll
     for (int r = NL * K; r < 64; ++r) {  // K == 3 leaves one base
         const uint32_t sym = uint32_t(r < 32 ? w0 >> (2 * r) : w1 >> (2 * (r - 32))) & 3u;
-        s = step1<MODE>(c, s, sym);
+        s = step1<MODE, V>(c, s, sym);
         if constexpr (MODE != kModeMap) {
             if (s < c.n_accept) record<MODE>(c, L, p0 + r, s);
         }
@@ -253,24 +256,26 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
 
 extern __shared__ __align__(128) unsigned char f_smem[];
 
-template <int K, int MODE, bool REG>
+template <int K, int MODE, int V>
 __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     constexpr bool RING = MODE == kModeCount || MODE == kModeRows;
-    constexpr bool DIRECT = MODE == kModeCountDirect;
-    constexpr bool HIST = RING || DIRECT;
+    constexpr bool PAIRS = MODE == kModeCountDirect || V == kVarPairs;   // (first base, state) counters
+    constexpr bool T1S = !PAIRS && t1_in_smem(V);                        // 1-base table in shared memory
+    constexpr bool HIST = RING || MODE == kModeCountDirect;
     constexpr int TK_BYTES = 1 << 17;
     constexpr int H2_WORDS = 4 << 12;  // (first base, state) for K = 2
-    // layout: table | t1 (not in direct mode) | ring (ring modes) | hist | hist2 (direct)
+    static_assert(V != kVarPairs || (K == 2 && MODE == kModeCount), "pair counters: K = 2 count only");
+    // layout: table | t1 (T1S) | ring (ring modes) | hist | hist2 (PAIRS)
     unsigned char* p_t1 = f_smem + TK_BYTES;
-    unsigned char* p_ring = p_t1 + (DIRECT ? 0 : size_t(a.t1_pad) * 2);
+    unsigned char* p_ring = p_t1 + (T1S ? size_t(a.t1_pad) * 2 : 0);
     unsigned int* s_hist = reinterpret_cast<unsigned int*>(
-        p_ring + (RING ? size_t(kRing) * 4 * blockDim.x : 0));
+        p_ring + (RING ? size_t(a.ring_depth) * 4 * blockDim.x : 0));
     unsigned int* s_hist2 = s_hist + ((a.n_accept + 3) & ~3);
     {
         const uint4* src = reinterpret_cast<const uint4*>(a.tk);
         uint4* dst = reinterpret_cast<uint4*>(f_smem);
         for (int i = threadIdx.x; i < TK_BYTES / 16; i += blockDim.x) dst[i] = __ldg(src + i);
-        if constexpr (!DIRECT) {
+        if constexpr (T1S) {
             src = reinterpret_cast<const uint4*>(a.t1);
             dst = reinterpret_cast<uint4*>(p_t1);
             for (int i = threadIdx.x; i < a.t1_pad / 8; i += blockDim.x) dst[i] = __ldg(src + i);
@@ -278,7 +283,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     }
     if constexpr (HIST)
         for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x) s_hist[i] = 0u;
-    if constexpr (DIRECT)
+    if constexpr (PAIRS)
         for (int i = threadIdx.x; i < H2_WORDS; i += blockDim.x) s_hist2[i] = 0u;
     __syncthreads();
 
@@ -294,6 +299,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     c.rows = a.rows;
     c.row_base = a.row_base;
     c.n_accept = opaque(uint32_t(a.n_accept));
+    c.ring_thr = uint32_t(a.ring_depth - chk_steps(K)) * kRingStride;
     const uint32_t sink = uint32_t(a.nq);  // the sink state Z
     const uint32_t ring_stride = kRingStride;
     const uint32_t rp0 = smem_addr(p_ring) + 4u * threadIdx.x;
@@ -339,7 +345,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                 const int q = int(p & 63);
                 const uint32_t word = q < 16 ? xb.x : q < 32 ? xb.y : q < 48 ? xb.z : xb.w;
                 const uint32_t sym = ((xm >> q) & 1ull) ? 4u : (word >> (2 * (q & 15))) & 3u;
-                s = step1<MODE>(c, s, sym);
+                s = step1<MODE, V>(c, s, sym);
             }
         }
         Lane<MODE> L;
@@ -378,8 +384,8 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
             const bool fast = !has || (k >= kfl && k < kfh && (clean || (alln && resets)));
             if (__all_sync(am, fast)) {
                 const bool live = has && !alln;
-                const uint32_t s2 = fast_block<K, MODE, REG>(c, L, live ? s : sink, wb, p0, am, rp0, rp,
-                                                             ring_stride);
+                const uint32_t s2 = fast_block<K, MODE, V>(c, L, live ? s : sink, wb, p0, am, rp0, rp,
+                                                           ring_stride);
                 if (live) {
                     s = s2;
                 } else if (has) {
@@ -402,7 +408,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                     const uint32_t sym = ((wm >> q) & 1ull)
                                              ? 4u
                                              : uint32_t((q < 32 ? w0 >> (2 * q) : w1 >> (2 * (q - 32)))) & 3u;
-                    s = step1<MODE>(c, s, sym);
+                    s = step1<MODE, V>(c, s, sym);
                     if constexpr (MODE != kModeMap) {
                         if (s < c.n_accept) record<MODE>(c, L, p0 + q, s);
                     }
@@ -413,6 +419,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                 wm = nm;
             }
         }
+        if constexpr (MODE == kModeRows) drain<K, MODE, V>(c, L, am, rp0, rp, ring_stride);   // rows are per chunk
         if (active) {
             if (a.chunk_exit) a.chunk_exit[ch] = uint16_t(s);
             if constexpr (MODE == kModeRows) a.chunk_rows[ch] = L.nrows;
@@ -422,48 +429,57 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
         }
     }
 
+    if constexpr (MODE == kModeCount) {   // the ring's leftovers
+        Lane<MODE> L;
+        drain<K, MODE, V>(c, L, am, rp0, rp, ring_stride);
+    }
     if constexpr (HIST) {
         __syncthreads();
+        if constexpr (PAIRS) {  // (first base, previous state) -> intermediate state, folded in shared memory
+            for (int i = threadIdx.x; i < H2_WORDS; i += blockDim.x) {
+                const unsigned int n = s_hist2[i];
+                if (n) red_shared_add(smem_addr(s_hist) + 4u * __ldg(a.t1 + (i & 0xFFF) * 5 + (i >> 12)), n);
+            }
+            __syncthreads();
+        }
         for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x)
             if (s_hist[i]) atomicAdd(&a.visits[i], (unsigned long long)s_hist[i]);
-    }
-    if constexpr (DIRECT) {  // resolve (first base, previous state) -> intermediate state
-        for (int i = threadIdx.x; i < H2_WORDS; i += blockDim.x) {
-            const unsigned int n = s_hist2[i];
-            if (!n) continue;
-            const uint32_t s1 = __ldg(a.t1 + (i & 0xFFF) * 5 + (i >> 12));
-            atomicAdd(&a.visits[s1], (unsigned long long)n);
-        }
     }
 }
 
 using FastFn = void (*)(const ScanArgs);
 
 template <int K>
-FastFn pick_mode(int mode, bool reg) {
+FastFn pick_mode(int mode, int var) {
     if constexpr (K == 2) {
-        if (reg && mode == kModeCount) return scan_fast_kernel<2, kModeCount, true>;
-        if (reg && mode == kModeRows) return scan_fast_kernel<2, kModeRows, true>;
+        if (var == kVarPairs && mode == kModeCount) return scan_fast_kernel<2, kModeCount, kVarPairs>;
     }
     switch (mode) {
         case kModeCountDirect:
-            if constexpr (K == 2) return scan_fast_kernel<2, kModeCountDirect, false>;
+            if constexpr (K == 2) return scan_fast_kernel<2, kModeCountDirect, kVarRing>;
             return nullptr;
-        case kModeCount: return scan_fast_kernel<K, kModeCount, false>;
-        case kModeRows: return scan_fast_kernel<K, kModeRows, false>;
-        case kModeEmit: return scan_fast_kernel<K, kModeEmit, false>;
-        case kModeMap: return scan_fast_kernel<K, kModeMap, false>;
+        case kModeCount: return scan_fast_kernel<K, kModeCount, kVarRing>;
+        case kModeRows: return scan_fast_kernel<K, kModeRows, kVarRing>;
+        case kModeEmit: return scan_fast_kernel<K, kModeEmit, kVarRing>;
+        case kModeMap: return scan_fast_kernel<K, kModeMap, kVarRing>;
     }
     return nullptr;
 }
 
-FastFn pick(int mode, int k, bool reg) {
+FastFn pick(int mode, int k, int var) {
     switch (k) {
-        case 2: return pick_mode<2>(mode, reg);
-        case 3: return pick_mode<3>(mode, reg);
-        case 4: return pick_mode<4>(mode, reg);
+        case 2: return pick_mode<2>(mode, var);
+        case 3: return pick_mode<3>(mode, var);
+        case 4: return pick_mode<4>(mode, var);
     }
     return nullptr;
+}
+
+// Variant actually used for (mode, k): falls back to kVarRing where the
+// requested one does not apply.
+int effective_variant(int var, int mode, int k) {
+    if (var == kVarPairs) return (k == 2 && mode == kModeCount) ? kVarPairs : kVarRing;
+    return kVarRing;
 }
 
 }  // namespace
@@ -476,15 +492,40 @@ size_t fast_smem_bytes(int mode, int32_t t1_pad, int32_t hist_words, int threads
            size_t(hist_words) * 4;
 }
 
+// Shared memory of a variant without its ring, and the ring depth that fits.
+size_t variant_fixed_bytes(int var, int mode, int k, int32_t t1_pad, int32_t hist_words) {
+    const int v = effective_variant(var, mode, k);
+    if (mode == kModeCountDirect) return fast_smem_bytes(mode, t1_pad, hist_words, 0);
+    return size_t(1 << 17) + (t1_in_smem(v) ? size_t(t1_pad) * 2 : 0) + size_t((hist_words + 3) & ~3) * 4 +
+           (v == kVarPairs ? size_t(4 << 12) * 4 : 0);
+}
+
+int ring_depth_for(size_t fixed, size_t optin, int threads) {
+    if (optin <= fixed) return 0;
+    return int(std::min<size_t>(kRingMax, (optin - fixed) / (size_t(4) * threads)));
+}
+
+size_t variant_smem_bytes(int var, int mode, int k, int32_t t1_pad, int32_t hist_words, int threads) {
+    return variant_fixed_bytes(var, mode, k, t1_pad, hist_words) + size_t(kRing) * 4 * threads;
+}
+
 int fast_threads() { return kFastThreads; }
 
 int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
     if (a.end <= a.begin || a.nchunks <= 0) return KS_OK;
     const bool ring = mode == kModeCount || mode == kModeRows || mode == kModeCountDirect;
     a.hist_smem = ring ? 1 : 0;
-    FastFn fn = pick(mode, k, a.reg_ring != 0);
+    const int var = effective_variant(a.fast_variant, mode, k);
+    FastFn fn = pick(mode, k, var);
     if (!fn) return fail(KS_E_INVALID, "fast scan: bad mode/stride");
-    const size_t smem = fast_smem_bytes(mode, a.t1_pad, ring ? a.n_accept : 0, kFastThreads);
+    size_t smem = variant_fixed_bytes(var, mode, k, a.t1_pad, ring ? a.n_accept : 0);
+    if (mode == kModeCount || mode == kModeRows) {
+        a.ring_depth = ring_depth_for(smem, ctx->smem_optin, kFastThreads);
+        if (const char* env = std::getenv("KS_RING_DEPTH"))   // tuning knob
+            a.ring_depth = std::min(a.ring_depth, std::max(chk_steps(k) + 1, std::atoi(env)));
+        if (a.ring_depth < chk_steps(k) + 1) return fail(KS_E_UNSUPPORTED, "fast scan: no room for the hit ring");
+        smem += size_t(a.ring_depth) * 4 * kFastThreads;
+    }
     if (smem > ctx->smem_optin) return fail(KS_E_UNSUPPORTED, "fast scan: shared memory budget exceeded");
     {  // the attribute is per function and device; set it once per size
         static thread_local const void* last_fn[16];
