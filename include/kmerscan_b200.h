@@ -104,7 +104,8 @@ KS_API int ks_dfa_free(ks_dfa* dfa);
 KS_API int ks_seq_upload_codes(ks_ctx* ctx, const uint8_t* codes, int64_t n, ks_seq** out);
 /* Raw ASCII bytes -> device encode (alphabet.py:20-37 / ingest.py:67-69):
  * case fold, whitespace (SP,TAB,CR,LF) dropped, every other byte OTHER.
- * fasta != 0 additionally drops lines starting with '>' (ingest.py:65-66). */
+ * fasta != 0 additionally drops lines starting with '>' (ingest.py:65-66,
+ * lines split at CR, LF, CRLF), on the device. */
 KS_API int ks_seq_upload_ascii(ks_ctx* ctx, const uint8_t* bytes, int64_t n_bytes,
                         int32_t fasta, ks_seq** out);
 /* Same, input already resident in device memory (not copied, not retained). */
@@ -143,8 +144,20 @@ KS_API int ks_async_wait(ks_ctx* ctx, float* scan_ms_total, int32_t* calls, int3
  * pinned staging, the copy stream moves it while the previous piece is
  * scanned, and each piece enters in the state the previous one left.  Same
  * result as ks_seq_upload_ascii + ks_count; input with whitespace falls back
- * to that path.  KS_HOST_THREADS caps the packer threads; KS_DEVICE_ENCODE=1
- * copies raw ASCII and encodes on the device instead. */
+ * to the device-encode stream of ks_count_host_bytes.  KS_HOST_THREADS caps
+ * the packer threads; KS_DEVICE_ENCODE=1 copies raw ASCII and encodes on the
+ * device instead. */
+KS_API int ks_count_host_ascii(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int64_t n_bytes,
+                               int64_t* counts_out);
+
+/* Same for raw (fasta = 0) or FASTA (fasta != 0) file bytes: FASTA and
+ * whitespace-bearing input stream raw bytes over PCIe into double device
+ * buffers and are encoded + compacted there (header-line state carried
+ * across pieces) while the next piece copies.  Replaces load_sequence +
+ * run(count) (ingest.py:54-70, engine.py:207). */
+KS_API int ks_count_host_bytes(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int64_t n_bytes,
+                               int32_t fasta, int64_t* counts_out);
+
 /* The host packer on its own (CPU only, no context): blocks of `bytes` in
  * tile-slot order for units of 2^lb 64-base blocks, 32 units per tile --
  * block g lands in slot ((g>>lb)>>5 << (5+lb)) | (g & (2^lb-1)) << 5 | (g>>lb) & 31.
@@ -153,9 +166,6 @@ KS_API int ks_async_wait(ks_ctx* ctx, float* scan_ms_total, int32_t* calls, int3
  * OTHER seen. */
 KS_API int ks_pack_host_ascii(const uint8_t* bytes, int64_t n_bytes, int32_t lb, uint64_t* bases,
                               uint64_t* nmask, int32_t* flags);
-
-KS_API int ks_count_host_ascii(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int64_t n_bytes,
-                               int64_t* counts_out);
 
 /* Range form used by match_chunk (engine.py:94-134) and by sharded scans:
  * scan positions [begin, end) of seq entering at `entry_state` (original

@@ -60,7 +60,7 @@ EXPORTED = (
     "ks_seq_upload_codes", "ks_seq_upload_ascii", "ks_seq_encode_device", "ks_seq_length",
     "ks_seq_download_codes", "ks_seq_download_softmask", "ks_seq_free", "ks_count", "ks_locate",
     "ks_count_host_ascii", "ks_count_async", "ks_async_wait", "ks_segment_map_async",
-    "ks_count_shard_async", "ks_pack_host_ascii",
+    "ks_count_shard_async", "ks_pack_host_ascii", "ks_count_host_bytes",
     "ks_scan_range", "ks_segment_map", "ks_speculate", "ks_free",
 )
 
@@ -97,6 +97,7 @@ def _declare(lib) -> None:
         "ks_count": (C.c_int, [_P, _P, _P, _i64p]),
         "ks_locate": (C.c_int, [_P, _P, _P, _i64p, C.POINTER(_i64p), _i64p]),
         "ks_count_host_ascii": (C.c_int, [_P, _P, _u8p, C.c_int64, _i64p]),
+        "ks_count_host_bytes": (C.c_int, [_P, _P, _u8p, C.c_int64, C.c_int32, _i64p]),
         "ks_count_async": (C.c_int, [_P, _P, _P, _i64p]),
         "ks_pack_host_ascii": (C.c_int, [_u8p, C.c_int64, C.c_int32, _P, _P, _i32p]),
         "ks_segment_map_async": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, _P]),
@@ -260,20 +261,21 @@ class DeviceContext:
                                                  C.byref(h)))
         return SeqHandle(self, h)
 
-    def upload_ascii(self, data) -> SeqHandle:
+    def upload_ascii(self, data, fasta: bool = False) -> SeqHandle:
+        """Raw (or FASTA) bytes -> device encode (ks_seq_upload_ascii)."""
         arr = np.frombuffer(data, dtype=np.uint8) if isinstance(data, (bytes, bytearray, memoryview)) \
             else np.ascontiguousarray(np.asarray(data, dtype=np.uint8))
         buf = arr if arr.size else np.zeros(1, dtype=np.uint8)
         h = _P()
         with self.lock:
-            _check(library().ks_seq_upload_ascii(self.handle, _ptr(buf, C.c_uint8), int(arr.size), 0,
-                                                 C.byref(h)))
+            _check(library().ks_seq_upload_ascii(self.handle, _ptr(buf, C.c_uint8), int(arr.size),
+                                                 int(bool(fasta)), C.byref(h)))
         return SeqHandle(self, h)
 
-    def encode_device(self, device_ptr: int, n_bytes: int) -> SeqHandle:
+    def encode_device(self, device_ptr: int, n_bytes: int, fasta: bool = False) -> SeqHandle:
         h = _P()
         with self.lock:
-            _check(library().ks_seq_encode_device(self.handle, _P(device_ptr), int(n_bytes), 0,
+            _check(library().ks_seq_encode_device(self.handle, _P(device_ptr), int(n_bytes), int(bool(fasta)),
                                                   C.byref(h)))
         return SeqHandle(self, h)
 
@@ -328,16 +330,16 @@ class DeviceContext:
         _check(library().ks_async_wait(self.handle, C.byref(ms), C.byref(calls), C.byref(launches)))
         return {"scan_ms_total": ms.value, "calls": calls.value, "kernel_launches": launches.value}
 
-    def count_host_ascii(self, dfa: DfaHandle, data) -> np.ndarray:
-        """End-to-end count from a host ASCII buffer (pipelined H2D + encode
-        + scan; pinned memory gives full PCIe bandwidth)."""
+    def count_host_ascii(self, dfa: DfaHandle, data, fasta: bool = False) -> np.ndarray:
+        """End-to-end count from a host buffer of raw (or FASTA) bytes:
+        pipelined pack/copy/encode + scan (ks_count_host_bytes)."""
         arr = np.frombuffer(data, dtype=np.uint8) if isinstance(data, (bytes, bytearray, memoryview)) \
             else np.ascontiguousarray(np.asarray(data, dtype=np.uint8))
         buf = arr if arr.size else np.zeros(1, dtype=np.uint8)
         counts = np.zeros(max(dfa.n_expressions, 1), dtype=np.int64)
         with self.lock:
-            _check(library().ks_count_host_ascii(self.handle, dfa.handle, _ptr(buf, C.c_uint8), int(arr.size),
-                                                 _ptr(counts, C.c_int64)))
+            _check(library().ks_count_host_bytes(self.handle, dfa.handle, _ptr(buf, C.c_uint8), int(arr.size),
+                                                 int(bool(fasta)), _ptr(counts, C.c_int64)))
         return counts[: dfa.n_expressions]
 
     def locate(self, dfa: DfaHandle, seq: SeqHandle) -> tuple[np.ndarray, np.ndarray]:

@@ -39,14 +39,14 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 // encode.cu / spec.cu
 size_t encode_scratch_bytes(int64_t n_bytes);
-int encode_ascii_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, ks_seq* seq, void* scratch,
+int encode_compact_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, bool fasta, int* d_carry,
+                          ks_seq* seq, void* scratch, int64_t* d_total, int* launches);
+int encode_ascii_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, bool fasta, ks_seq* seq, void* scratch,
                         int* launches);
 int pack_codes_device(ks_ctx* ctx, const uint8_t* d_codes, int64_t n, ks_seq* seq, int* d_flag,
                       int* launches);
 int scatter_tile_masks_device(ks_ctx* ctx, const uint64_t* d_compact, const int32_t* d_ids, int n_tiles,
                               int tile_words, uint64_t* d_nmask, int* launches);
-int encode_piece_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, ks_seq* seq, uint32_t* kept,
-                        int* ws_flag, int* launches);
 int unpack_codes_device(ks_ctx* ctx, const ks_seq* seq, uint8_t* d_out);
 int linear_softmask_device(ks_ctx* ctx, const ks_seq* seq, uint64_t* d_out);
 int launch_speculate(ks_ctx* ctx, const SeqView& seq, int32_t n_chunks, const int64_t* d_cbeg,
@@ -585,30 +585,38 @@ void seq_destroy(ks_seq* s) {
     delete s;
 }
 
-// Streaming count from a host buffer (ks_count_host_ascii).  Default wire
-// format: host worker threads pack piece i (AVX-512, host_pack.cpp) straight
-// into the tile-slot layout in pinned staging slot i%3, the copy stream moves
-// 0.25-0.375 B/base into device buffer i%2, and the compute stream scans it
-// while piece i+1 is packed.  KS_DEVICE_ENCODE=1 instead copies raw ASCII
-// (1 B/base) and encodes on the device.  Every piece enters in the state the
-// previous piece left (a device-resident uint16); visits accumulate.
-int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int64_t n_bytes,
-                      int64_t* counts_out, bool* fallback) {
+// Streaming count from a host buffer (ks_count_host_bytes).  Two wire
+// formats, both double-buffered on the device, every piece entering in the
+// state the previous piece left (a device-resident uint16), visits
+// accumulating across pieces:
+//  * host pack (raw input without whitespace, the default): host worker
+//    threads pack piece i (AVX-512, host_pack.cpp) straight into the
+//    tile-slot layout in pinned staging slot i%3; the copy stream moves
+//    0.25-0.375 B/base while piece i+1 is packed and piece i-1 scanned.  A
+//    piece holding whitespace sets *fallback (positions would shift).
+//  * device encode (FASTA, whitespace, or KS_DEVICE_ENCODE=1): raw bytes go
+//    over PCIe (1 B/base) into buffer i%2 while the previous piece is
+//    encoded -- line state (FASTA headers) carried across pieces on the
+//    device -- compacted and scanned.  One host sync per piece reads the
+//    piece's retained length for the scan geometry; the next piece's copy is
+//    already queued, so the link never idles.
+int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int64_t n_bytes, bool fasta,
+                      bool host_pack, int64_t* counts_out, bool* fallback) {
     const HostDfa& h = dfa->host;
     *fallback = false;
-    const bool host_pack = std::getenv("KS_DEVICE_ENCODE") == nullptr;
-    static const int64_t piece_mb = std::getenv("KS_PIECE_MB") ? std::atoll(std::getenv("KS_PIECE_MB")) : 64;
-    const int64_t piece = std::min<int64_t>(std::max<int64_t>(n_bytes, 64), piece_mb << 20);
+    // piece size: 64 MiB; KS_PIECE_KB overrides (tests use small pieces to cross many boundaries)
+    const char* pk = std::getenv("KS_PIECE_KB");
+    const int64_t piece_bytes = pk && std::atoll(pk) > 0 ? std::atoll(pk) << 10 : int64_t(64) << 20;
+    const int64_t piece = std::min<int64_t>(std::max<int64_t>(n_bytes, 64), piece_bytes);
     const int64_t npieces = (n_bytes + piece - 1) / piece;
-    // piece buffers: 2 x (input bytes + packed tiled sequence)
     ks_seq tmpl;
     tmpl.lb = choose_lb(ctx, piece);
     const int64_t tile_blocks = int64_t(32) << tmpl.lb;
     const int64_t blocks = (piece + 63) / 64;
     const int64_t slots = ((blocks + tile_blocks - 1) / tile_blocks + 1) * tile_blocks;
     const int64_t ntiles = slots / tile_blocks;
-    // device input region per buffer: raw ASCII (device encode) or the
-    // compacted OTHER bitmaps + their tile ids (host pack)
+    // device input region per buffer: the compacted OTHER bitmaps + their tile
+    // ids (host pack) or the raw bytes (device encode)
     const size_t in_bytes = host_pack ? up(size_t(slots) * 8 + size_t(ntiles) * 4 + 64) : up(size_t(piece) + 64);
     const size_t seq_bytes = up(size_t(slots) * 32);
     const size_t need = 2 * (in_bytes + seq_bytes);
@@ -654,17 +662,18 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
     geometry(&pseq[0], 0, piece, &origin, &L, &nch_max);
     const bool mapscan = h.strategy == KS_STRATEGY_MAPSCAN;
     Arena ar;
-    size_t scratch = size_t(h.n_accept) * 8 + size_t(std::max(h.ne, 1)) * 8 + size_t(nch_max) * 2 +
-                     size_t(blocks + 1) * 4 + 16 * kAlign;
+    size_t scratch = size_t(h.n_accept) * 8 + size_t(std::max(h.ne, 1)) * 8 + size_t(nch_max) * 2 + 16 * kAlign;
     if (mapscan) scratch += size_t(nch_max) * 6 + exclusive_scan_monoid_tmp_bytes(nch_max) + 4 * kAlign;
+    if (!host_pack) scratch += encode_scratch_bytes(piece) + 2 * kAlign;
     int rc = ensure_scratch(ctx, scratch, &ar);
     if (rc) return rc;
     unsigned long long* visits = static_cast<unsigned long long*>(ar.take(size_t(h.n_accept) * 8));
     unsigned long long* counts = static_cast<unsigned long long*>(ar.take(size_t(std::max(h.ne, 1)) * 8));
     uint16_t* chunk_exit = static_cast<uint16_t*>(ar.take(size_t(nch_max) * 2 + 2));
-    uint32_t* kept = static_cast<uint32_t*>(ar.take(size_t(blocks + 1) * 4));
-    int* ws_flag = static_cast<int*>(ar.take(16));
     uint16_t* state = static_cast<uint16_t*>(ar.take(16));
+    int* d_carry = static_cast<int*>(ar.take(16));           // FASTA line state between pieces
+    int64_t* d_total = static_cast<int64_t*>(ar.take(16));   // retained symbols of the piece
+    void* enc_scratch = host_pack ? nullptr : ar.take(encode_scratch_bytes(piece));
     uint16_t *elems = nullptr, *excl = nullptr, *centry = nullptr, *mtot = nullptr;
     void* mtmp = nullptr;
     if (mapscan) {
@@ -677,10 +686,11 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
     rc = ensure_pinned(ctx, size_t(std::max(h.ne, 1)) * 8 + 64);
     if (rc) return rc;
     char* pin = static_cast<char*>(ctx->pinned);
+    int64_t* pin_total = reinterpret_cast<int64_t*>(pin + size_t(std::max(h.ne, 1)) * 8 + 16);
     *reinterpret_cast<uint16_t*>(pin) = uint16_t(h.start_internal);
     if (h.n_accept > 0) KS_CUDA(cudaMemsetAsync(visits, 0, size_t(h.n_accept) * 8, ctx->stream));
     KS_CUDA(cudaMemsetAsync(counts, 0, size_t(std::max(h.ne, 1)) * 8, ctx->stream));
-    KS_CUDA(cudaMemsetAsync(ws_flag, 0, 16, ctx->stream));
+    KS_CUDA(cudaMemsetAsync(d_carry, 0, 16, ctx->stream));
     KS_CUDA(cudaMemcpyAsync(state, pin, 2, cudaMemcpyHostToDevice, ctx->stream));
     // the copy stream must not overwrite a buffer before the compute stream is done with it
     KS_CUDA(cudaEventRecord(ctx->sev[2], ctx->stream));
@@ -688,10 +698,26 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
     const ScanPlan plan = plan_for(ctx, dfa, dfa->scan);
     int launches = 0;
     int64_t h2d = 2;   // the entry state
+    int64_t d2h = 0;
+    auto issue_raw_copy = [&](int64_t i) -> int {   // device-encode mode: raw piece i -> din[i % 2]
+        const int b = int(i & 1);
+        const int64_t off = i * piece;
+        const int64_t len = std::min(piece, n_bytes - off);
+        KS_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->sev[2 + b], 0));
+        KS_CUDA(cudaMemcpyAsync(din[b], bytes + off, size_t(len), cudaMemcpyHostToDevice, ctx->copy_stream));
+        KS_CUDA(cudaEventRecord(ctx->sev[b], ctx->copy_stream));
+        h2d += len;
+        return KS_OK;
+    };
+    if (!host_pack && npieces > 0) {
+        rc = issue_raw_copy(0);
+        if (rc) return rc;
+    }
     for (int64_t i = 0; i < npieces; ++i) {
         const int b = int(i & 1);
         const int64_t off = i * piece;
         const int64_t len = std::min(piece, n_bytes - off);
+        int64_t nsym = len;   // symbols this piece contributes
         if (host_pack) {
             const int st = int(i % 3);
             uint64_t* hb = reinterpret_cast<uint64_t*>(static_cast<char*>(ctx->hstage) + st * wire);
@@ -734,59 +760,60 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
             KS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->sev[b], 0));
             rc = scatter_tile_masks_device(ctx, d_comp, d_ids, nc, int(tile_blocks), pseq[b].d_nmask, &launches);
             if (rc) return rc;
-            pseq[b].n = len;
         } else {
-            KS_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->sev[2 + b], 0));
-            KS_CUDA(cudaMemcpyAsync(din[b], bytes + off, size_t(len), cudaMemcpyHostToDevice, ctx->copy_stream));
-            h2d += len;
-            KS_CUDA(cudaEventRecord(ctx->sev[b], ctx->copy_stream));
+            if (i + 1 < npieces) {   // keep the link busy: the next piece's copy goes first
+                rc = issue_raw_copy(i + 1);
+                if (rc) return rc;
+            }
             KS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->sev[b], 0));
-            rc = encode_piece_device(ctx, din[b], len, &pseq[b], kept, ws_flag, &launches);
+            rc = encode_compact_device(ctx, din[b], len, fasta, d_carry, &pseq[b], enc_scratch, d_total,
+                                       &launches);
             if (rc) return rc;
             KS_CUDA(cudaEventRecord(ctx->sev[2 + b], ctx->stream));  // din[b] consumed
+            KS_CUDA(cudaMemcpyAsync(pin_total, d_total, 8, cudaMemcpyDeviceToHost, ctx->stream));
+            KS_CUDA(cudaStreamSynchronize(ctx->stream));
+            d2h += 8;
+            nsym = *pin_total;
         }
-        int64_t o2, L2, nch;
-        geometry(&pseq[b], 0, len, &o2, &L2, &nch);
-        ScanArgs a = base_args(dfa, dfa->scan, &pseq[b]);
-        a.begin = 0;
-        a.end = len;
-        a.origin = o2;
-        a.chunk_len = L2;
-        a.nchunks = nch;
-        a.visits = visits;
-        a.chunk_exit = chunk_exit;
-        if (mapscan) {
-            rc = monoid_prefix(ctx, dfa, &pseq[b], 0, len, o2, L2, nch, elems, excl, mtot, mtmp, &launches);
+        pseq[b].n = nsym;
+        if (nsym > 0) {
+            int64_t o2, L2, nch;
+            geometry(&pseq[b], 0, nsym, &o2, &L2, &nch);
+            ScanArgs a = base_args(dfa, dfa->scan, &pseq[b]);
+            a.begin = 0;
+            a.end = nsym;
+            a.origin = o2;
+            a.chunk_len = L2;
+            a.nchunks = nch;
+            a.visits = visits;
+            a.chunk_exit = chunk_exit;
+            if (mapscan) {
+                rc = monoid_prefix(ctx, dfa, &pseq[b], 0, nsym, o2, L2, nch, elems, excl, mtot, mtmp, &launches);
+                if (rc) return rc;
+                rc = launch_chunk_entry(ctx, excl, nch, dfa->d_action, h.nq, 0, state, centry, &launches);
+                if (rc) return rc;
+                a.chunk_entry = centry;
+            } else {
+                a.lookback = h.sync_depth;
+                a.base_pos = 0;
+                a.base_state_ptr = state;
+                a.any_state = h.start_internal;
+            }
+            rc = dispatch(ctx, dfa, dfa->scan, plan, a, kModeCount, &launches);
             if (rc) return rc;
-            rc = launch_chunk_entry(ctx, excl, nch, dfa->d_action, h.nq, 0, state, centry, &launches);
-            if (rc) return rc;
-            a.chunk_entry = centry;
-        } else {
-            a.lookback = h.sync_depth;
-            a.base_pos = 0;
-            a.base_state_ptr = state;
-            a.any_state = h.start_internal;
+            KS_CUDA(cudaMemcpyAsync(state, chunk_exit + (nch - 1), 2, cudaMemcpyDeviceToDevice, ctx->stream));
         }
-        rc = dispatch(ctx, dfa, dfa->scan, plan, a, kModeCount, &launches);
-        if (rc) return rc;
-        KS_CUDA(cudaMemcpyAsync(state, chunk_exit + (nch - 1), 2, cudaMemcpyDeviceToDevice, ctx->stream));
         if (host_pack) KS_CUDA(cudaEventRecord(ctx->sev[2 + b], ctx->stream));  // device buffer b consumed
     }
     rc = launch_finalize_counts(ctx, visits, h.n_accept, dfa->d_acc_out_off, dfa->d_acc_out_ids, counts,
                                 nullptr, nullptr, &launches);
     if (rc) return rc;
     KS_CUDA(cudaMemcpyAsync(pin, counts, size_t(h.ne) * 8, cudaMemcpyDeviceToHost, ctx->stream));
-    KS_CUDA(cudaMemcpyAsync(pin + size_t(std::max(h.ne, 1)) * 8, ws_flag, 4, cudaMemcpyDeviceToHost,
-                            ctx->stream));
     KS_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (*reinterpret_cast<int*>(pin + size_t(std::max(h.ne, 1)) * 8)) {
-        *fallback = true;
-        return KS_OK;
-    }
     std::memcpy(counts_out, pin, size_t(h.ne) * 8);
     ctx->stats.kernel_launches = launches;
     ctx->stats.h2d_bytes = h2d;
-    ctx->stats.d2h_bytes = int64_t(h.ne) * 8 + 4;
+    ctx->stats.d2h_bytes = d2h + int64_t(h.ne) * 8;
     return KS_OK;
 }
 
@@ -1028,8 +1055,6 @@ int ks_seq_upload_codes(ks_ctx* ctx, const uint8_t* codes, int64_t n, ks_seq** o
 }
 
 static int encode_common(ks_ctx* ctx, const uint8_t* d_bytes, int64_t n_bytes, int32_t fasta, ks_seq** out) {
-    if (fasta)
-        return fail(KS_E_UNSUPPORTED, "device FASTA header removal is not implemented; strip headers on the host");
     ks_seq* s = nullptr;
     int rc = seq_alloc(ctx, n_bytes, &s);
     if (rc) return rc;
@@ -1042,7 +1067,8 @@ static int encode_common(ks_ctx* ctx, const uint8_t* d_bytes, int64_t n_bytes, i
         return rc;
     }
     int launches = 0;
-    rc = encode_ascii_device(ctx, d_bytes, n_bytes, s, ar.take(encode_scratch_bytes(n_bytes)), &launches);
+    rc = encode_ascii_device(ctx, d_bytes, n_bytes, fasta != 0, s, ar.take(encode_scratch_bytes(n_bytes)),
+                             &launches);
     if (rc) {
         seq_destroy(s);
         return rc;
@@ -1060,13 +1086,11 @@ int ks_seq_encode_device(ks_ctx* ctx, const uint8_t* d_bytes, int64_t n_bytes, i
 int ks_seq_upload_ascii(ks_ctx* ctx, const uint8_t* bytes, int64_t n_bytes, int32_t fasta, ks_seq** out) {
     if (!ctx || !out || n_bytes < 0 || (n_bytes > 0 && !bytes)) return fail(KS_E_INVALID, "bad argument");
     DeviceGuard guard(ctx->device);
-    if (fasta)
-        return fail(KS_E_UNSUPPORTED, "device FASTA header removal is not implemented; strip headers on the host");
     uint8_t* d_in = nullptr;
     KS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_in), size_t(n_bytes) + 64, ctx->stream));
     cudaError_t e = n_bytes ? cudaMemcpyAsync(d_in, bytes, size_t(n_bytes), cudaMemcpyHostToDevice, ctx->stream)
                             : cudaSuccess;
-    int rc = e == cudaSuccess ? encode_common(ctx, d_in, n_bytes, 0, out) : cuda_fail(e, "ascii upload");
+    int rc = e == cudaSuccess ? encode_common(ctx, d_in, n_bytes, fasta, out) : cuda_fail(e, "ascii upload");
     cudaFreeAsync(d_in, ctx->stream);
     cudaStreamSynchronize(ctx->stream);
     return rc;
@@ -1163,7 +1187,7 @@ int ks_pack_host_ascii(const uint8_t* bytes, int64_t n_bytes, int32_t lb, uint64
     return KS_OK;
 }
 
-int ks_count_host_ascii(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int64_t n_bytes,
+int ks_count_host_bytes(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int64_t n_bytes, int32_t fasta,
                         int64_t* counts_out) {
     if (!ctx || !dfa || !counts_out || n_bytes < 0 || (n_bytes > 0 && !bytes))
         return fail(KS_E_INVALID, "bad argument");
@@ -1176,15 +1200,14 @@ int ks_count_host_ascii(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, in
     ctx->stats = ks_stats{};
     KS_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
     bool fallback = false;
-    int rc = stream_count_impl(ctx, dfa, bytes, n_bytes, counts_out, &fallback);
+    const bool host_pack = !fasta && std::getenv("KS_DEVICE_ENCODE") == nullptr;
+    int rc = stream_count_impl(ctx, dfa, bytes, n_bytes, fasta != 0, host_pack, counts_out, &fallback);
     if (rc) return rc;
-    if (fallback) {  // whitespace present: compacting encode of the whole input
-        ks_seq* seq = nullptr;
-        rc = ks_seq_upload_ascii(ctx, bytes, n_bytes, 0, &seq);
+    if (fallback) {  // whitespace in raw input: the device-encode stream compacts it
+        ctx->stats = ks_stats{};
+        KS_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+        rc = stream_count_impl(ctx, dfa, bytes, n_bytes, false, false, counts_out, &fallback);
         if (rc) return rc;
-        rc = scan_impl(ctx, dfa, seq, 0, seq->n, -1, 0, counts_out, nullptr, nullptr, nullptr);
-        ks_seq_free(seq);
-        return rc;
     }
     KS_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
     KS_CUDA(cudaEventSynchronize(ctx->ev[3]));
@@ -1192,6 +1215,11 @@ int ks_count_host_ascii(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, in
     cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[3]);
     ctx->stats.total_ms = ms;
     return KS_OK;
+}
+
+int ks_count_host_ascii(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int64_t n_bytes,
+                        int64_t* counts_out) {
+    return ks_count_host_bytes(ctx, dfa, bytes, n_bytes, 0, counts_out);
 }
 
 int ks_scan_range(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end,

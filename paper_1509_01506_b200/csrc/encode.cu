@@ -9,7 +9,10 @@
 // One thread packs one 64-base block: 64 input bytes -> 16 B + 8 B + 8 B.
 // Whitespace-free input (the common case) is written in place in a single
 // pass; otherwise per-block kept counts are scanned and a compaction pass
-// ORs each block's bits into their shifted output position.
+// ORs each block's bits into their shifted output position.  FASTA input
+// (ingest.py:65-66: lines starting with '>' dropped, CR/LF/CRLF line ends)
+// adds one pass: each block's last line terminator, an exclusive running-max
+// scan of those, and from it the line state at every block start.
 #include <algorithm>
 
 #include "scan_kernels.cuh"
@@ -35,13 +38,42 @@ __device__ __forceinline__ void classify(uint32_t x, uint32_t& code, bool& other
     if (!base) code = 0;
 }
 
-// Encode the 64 bytes of block b (bytes past n_bytes are treated as dropped).
-__device__ __forceinline__ Packed pack_block(const uint8_t* in, int64_t n_bytes, int64_t b,
-                                             bool compact) {
-    Packed r{0, 0, 0, 0, 0};
+// FASTA line state (reference ingest.py:65-66 via bytes.splitlines: CR, LF
+// and CRLF end lines; a line whose first byte is '>' is dropped whole).
+// `carry` codes the state before the first byte of a piece: 0 = at a line
+// start, 1 = inside a sequence line, 2 = inside a header line.
+struct LineState {
+    bool at_ls;   // the previous byte ended a line (or input start)
+    bool in_hdr;  // inside a header line
+};
+
+__device__ __forceinline__ bool is_term(uint32_t x) { return x == '\n' || x == '\r'; }
+
+// State at the start of block b: from the last line terminator before the
+// block (lt_excl[b], exclusive running max) or, when the piece has none, the
+// carry.
+__device__ __forceinline__ LineState block_start_state(const uint8_t* in, int64_t b, const int64_t* lt_excl,
+                                                       int carry) {
+    LineState st;
+    if (b == 0) {
+        st.at_ls = carry == 0;
+        st.in_hdr = carry == 2;
+        return st;
+    }
+    const int64_t t = lt_excl[b];
+    st.at_ls = t == (b << 6) - 1;
+    if (st.at_ls) st.in_hdr = false;
+    else if (t >= 0) st.in_hdr = in[t + 1] == '>';
+    else st.in_hdr = carry == 0 ? in[0] == '>' : carry == 2;
+    return st;
+}
+
+__device__ __forceinline__ int carry_of(const LineState& st) { return st.at_ls ? 0 : st.in_hdr ? 2 : 1; }
+
+// Load the 64 bytes of block b as 16 words; bytes past n_bytes read as SP.
+__device__ __forceinline__ void load_block(const uint8_t* in, int64_t n_bytes, int64_t b, uint32_t words[16]) {
     const int64_t p0 = b << 6;
     const int lim = int(min64(64, n_bytes - p0));
-    uint32_t words[16];
     if (lim == 64 && ((reinterpret_cast<uintptr_t>(in) & 15) == 0)) {
         const uint4* src = reinterpret_cast<const uint4*>(in + p0);
 #pragma unroll
@@ -65,6 +97,23 @@ __device__ __forceinline__ Packed pack_block(const uint8_t* in, int64_t n_bytes,
             words[q] = w;
         }
     }
+}
+
+// Encode the 64 bytes of block b (bytes past n_bytes are treated as dropped).
+// FASTA: `st` enters as the line state at the block start and leaves as the
+// state after its last real byte.
+template <bool FASTA = false>
+__device__ __forceinline__ Packed pack_block(const uint8_t* in, int64_t n_bytes, int64_t b, bool compact,
+                                             LineState* st = nullptr) {
+    Packed r{0, 0, 0, 0, 0};
+    uint32_t words[16];
+    load_block(in, n_bytes, b, words);
+    const int lim = int(min64(64, n_bytes - (b << 6)));
+    bool at_ls = false, in_hdr = false;
+    if constexpr (FASTA) {
+        at_ls = st->at_ls;
+        in_hdr = st->in_hdr;
+    }
     int o = 0;  // output slot within the block (== i when nothing is dropped)
 #pragma unroll
     for (int i = 0; i < 64; ++i) {
@@ -72,6 +121,18 @@ __device__ __forceinline__ Packed pack_block(const uint8_t* in, int64_t n_bytes,
         uint32_t code;
         bool other, lower, ws;
         classify(x, code, other, lower, ws);
+        if constexpr (FASTA) {
+            if (i < lim) {
+                if (is_term(x)) {
+                    at_ls = true;
+                    in_hdr = false;
+                } else {
+                    if (at_ls) in_hdr = x == '>';
+                    at_ls = false;
+                    ws |= in_hdr;   // header bytes are dropped like whitespace
+                }
+            }
+        }
         const int slot = compact ? o : i;
         if (!ws) {
             if (slot < 32) r.w0 |= uint64_t(code) << (2 * slot);
@@ -81,8 +142,46 @@ __device__ __forceinline__ Packed pack_block(const uint8_t* in, int64_t n_bytes,
             ++o;
         }
     }
+    if constexpr (FASTA) {
+        st->at_ls = at_ls;
+        st->in_hdr = in_hdr;
+    }
     r.kept = uint32_t(o);
     return r;
+}
+
+// Last line terminator of each block (global position, -1 if none).
+__global__ void last_term_kernel(const uint8_t* in, int64_t n_bytes, int64_t n_blocks, int64_t* lt) {
+    for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < n_blocks;
+         b += int64_t(gridDim.x) * blockDim.x) {
+        uint32_t words[16];
+        load_block(in, n_bytes, b, words);
+        int last = -1;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+            const uint32_t x = (words[i >> 2] >> (8 * (i & 3))) & 0xffu;
+            if (is_term(x)) last = i;   // SP padding past the end never matches
+        }
+        lt[b] = last < 0 ? -1 : (b << 6) + last;
+    }
+}
+
+// Kept (retained) symbols per block; the last block also records the line
+// state after the input (FASTA carry out).
+template <bool FASTA>
+__global__ void kept_kernel(const uint8_t* in, int64_t n_bytes, int64_t n_blocks, const int64_t* lt_excl,
+                            const int* carry, uint32_t* kept, int* carry_out) {
+    const int c = FASTA && carry ? *carry : 0;
+    for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < n_blocks;
+         b += int64_t(gridDim.x) * blockDim.x) {
+        LineState st{};
+        if constexpr (FASTA) st = block_start_state(in, b, lt_excl, c);
+        const Packed r = pack_block<FASTA>(in, n_bytes, b, true, &st);
+        kept[b] = r.kept;
+        if constexpr (FASTA) {
+            if (b == n_blocks - 1) *carry_out = carry_of(st);
+        }
+    }
 }
 
 __global__ void encode_inplace_kernel(const uint8_t* in, int64_t n_bytes, int64_t n_blocks, int lb,
@@ -120,12 +219,16 @@ __device__ __forceinline__ void or_bits(uint64_t* a, int64_t bit, uint64_t v, in
                  (unsigned long long)(v >> (64 - sh)));
 }
 
+template <bool FASTA>
 __global__ void encode_compact_kernel(const uint8_t* in, int64_t n_bytes, int64_t n_blocks, int lb,
-                                      const int64_t* out_pos, uint64_t* bases, uint64_t* nmask,
-                                      uint64_t* soft) {
+                                      const int64_t* out_pos, const int64_t* lt_excl, const int* carry,
+                                      uint64_t* bases, uint64_t* nmask, uint64_t* soft) {
+    const int c = FASTA && carry ? *carry : 0;
     for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < n_blocks;
          b += int64_t(gridDim.x) * blockDim.x) {
-        Packed r = pack_block(in, n_bytes, b, true);
+        LineState st{};
+        if constexpr (FASTA) st = block_start_state(in, b, lt_excl, c);
+        Packed r = pack_block<FASTA>(in, n_bytes, b, true, &st);
         const int64_t o = out_pos[b];
         const int k = int(r.kept);
         // bases: 2k bits starting at bit 2*o; split into the two 64-bit halves
@@ -197,72 +300,110 @@ int grid_for(const ks_ctx* ctx, int64_t items, int threads) {
 
 }  // namespace
 
-// Encode n_bytes of device ASCII into seq (whose arrays are sized for n_bytes
-// bases).  Sets seq->n to the retained symbol count.  `scratch` must hold
-// kept counts + offsets (encode_scratch_bytes).
+// Scratch of encode_compact_device for n_bytes of input.
 size_t encode_scratch_bytes(int64_t n_bytes) {
     const int64_t nb = (n_bytes + 63) / 64 + 1;
-    return align16(size_t(nb) * 4) + align16(size_t(nb) * 8) + exclusive_scan_rows_tmp_bytes(nb) + 64;
+    return align16(size_t(nb) * 4) + 3 * align16(size_t(nb) * 8) + exclusive_scan_rows_tmp_bytes(nb) + 128;
 }
 
-int encode_ascii_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, ks_seq* seq,
-                        void* scratch, int* launches) {
+// Compacting encode of n_bytes of device ASCII into seq, no host sync: every
+// block's retained count, an exclusive scan for its output position, then
+// each block ORs its bits into place.  FASTA additionally drops header lines:
+// the last line terminator before each block comes from an exclusive
+// running-max scan, so every block knows its line state.  d_carry (FASTA,
+// may be null = input start) holds the line state before d_in[0] and
+// receives the state after the last byte.  *d_total = retained symbols.
+int encode_compact_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, bool fasta, int* d_carry,
+                          ks_seq* seq, void* scratch, int64_t* d_total, int* launches) {
     const int64_t nb = (n_bytes + 63) / 64;
     char* p = static_cast<char*>(scratch);
     uint32_t* kept = reinterpret_cast<uint32_t*>(p);
     p += align16(size_t(nb + 1) * 4);
     int64_t* pos = reinterpret_cast<int64_t*>(p);
     p += align16(size_t(nb + 1) * 8);
-    int* flag = reinterpret_cast<int*>(p);
+    int64_t* lt = reinterpret_cast<int64_t*>(p);
+    p += align16(size_t(nb + 1) * 8);
+    int64_t* lt_excl = reinterpret_cast<int64_t*>(p);
+    p += align16(size_t(nb + 1) * 8);
+    int* carry_next = reinterpret_cast<int*>(p);
+    int64_t* lt_total = reinterpret_cast<int64_t*>(p + 16);
     p += 64;
     void* tmp = p;
-    int64_t* d_total = reinterpret_cast<int64_t*>(flag + 4);
-    KS_CUDA(cudaMemsetAsync(flag, 0, 64, ctx->stream));
     if (nb == 0) {
-        seq->n = 0;
+        KS_CUDA(cudaMemsetAsync(d_total, 0, sizeof(int64_t), ctx->stream));
         return KS_OK;
     }
     const int threads = 256;
-    encode_inplace_kernel<<<grid_for(ctx, nb, threads), threads, 0, ctx->stream>>>(
-        d_in, n_bytes, nb, seq->lb, seq->d_bases, seq->d_nmask, seq->d_soft, kept, flag);
+    const int grid = grid_for(ctx, nb, threads);
+    if (fasta) {
+        last_term_kernel<<<grid, threads, 0, ctx->stream>>>(d_in, n_bytes, nb, lt);
+        if (launches) ++*launches;
+        KS_CUDA(cudaGetLastError());
+        int rc = exclusive_scan_max(ctx, lt, nb, lt_excl, lt_total, tmp, launches);
+        if (rc != KS_OK) return rc;
+        kept_kernel<true><<<grid, threads, 0, ctx->stream>>>(d_in, n_bytes, nb, lt_excl, d_carry, kept, carry_next);
+    } else {
+        kept_kernel<false><<<grid, threads, 0, ctx->stream>>>(d_in, n_bytes, nb, nullptr, nullptr, kept, nullptr);
+    }
     if (launches) ++*launches;
     KS_CUDA(cudaGetLastError());
-    int any_ws = 0;
-    KS_CUDA(cudaMemcpyAsync(&any_ws, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    KS_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (!any_ws) {
-        seq->n = n_bytes;
-        return KS_OK;
-    }
     int rc = exclusive_scan_rows(ctx, kept, nb, pos, d_total, tmp, launches);
     if (rc != KS_OK) return rc;
     const size_t words = size_t(seq->n_blocks);
     KS_CUDA(cudaMemsetAsync(seq->d_bases, 0, words * 16, ctx->stream));
     KS_CUDA(cudaMemsetAsync(seq->d_nmask, 0, words * 8, ctx->stream));
-    KS_CUDA(cudaMemsetAsync(seq->d_soft, 0, words * 8, ctx->stream));
-    encode_compact_kernel<<<grid_for(ctx, nb, threads), threads, 0, ctx->stream>>>(
-        d_in, n_bytes, nb, seq->lb, pos, seq->d_bases, seq->d_nmask, seq->d_soft);
+    if (seq->d_soft) KS_CUDA(cudaMemsetAsync(seq->d_soft, 0, words * 8, ctx->stream));
+    if (fasta)
+        encode_compact_kernel<true><<<grid, threads, 0, ctx->stream>>>(d_in, n_bytes, nb, seq->lb, pos, lt_excl, d_carry,
+                                                                       seq->d_bases, seq->d_nmask, seq->d_soft);
+    else
+        encode_compact_kernel<false><<<grid, threads, 0, ctx->stream>>>(d_in, n_bytes, nb, seq->lb, pos, nullptr,
+                                                                        nullptr, seq->d_bases, seq->d_nmask,
+                                                                        seq->d_soft);
     if (launches) ++*launches;
     KS_CUDA(cudaGetLastError());
+    if (fasta && d_carry)
+        KS_CUDA(cudaMemcpyAsync(d_carry, carry_next, sizeof(int), cudaMemcpyDeviceToDevice, ctx->stream));
+    return KS_OK;
+}
+
+// Encode n_bytes of device ASCII into seq (whose arrays are sized for n_bytes
+// bases).  Sets seq->n to the retained symbol count (host sync).  Raw input
+// without whitespace is written in place in one pass; anything else takes
+// the compacting path.  `scratch` holds encode_scratch_bytes(n_bytes).
+int encode_ascii_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, bool fasta, ks_seq* seq,
+                        void* scratch, int* launches) {
+    const int64_t nb = (n_bytes + 63) / 64;
+    if (nb == 0) {
+        seq->n = 0;
+        return KS_OK;
+    }
+    char* p = static_cast<char*>(scratch);
+    uint32_t* kept = reinterpret_cast<uint32_t*>(p);
+    int* flag = reinterpret_cast<int*>(static_cast<char*>(scratch) + encode_scratch_bytes(n_bytes) - 64);
+    int64_t* d_total = reinterpret_cast<int64_t*>(flag + 4);
+    int rc;
+    if (!fasta) {
+        KS_CUDA(cudaMemsetAsync(flag, 0, 64, ctx->stream));
+        const int threads = 256;
+        encode_inplace_kernel<<<grid_for(ctx, nb, threads), threads, 0, ctx->stream>>>(
+            d_in, n_bytes, nb, seq->lb, seq->d_bases, seq->d_nmask, seq->d_soft, kept, flag);
+        if (launches) ++*launches;
+        KS_CUDA(cudaGetLastError());
+        int any_ws = 0;
+        KS_CUDA(cudaMemcpyAsync(&any_ws, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        KS_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (!any_ws) {
+            seq->n = n_bytes;
+            return KS_OK;
+        }
+    }
+    rc = encode_compact_device(ctx, d_in, n_bytes, fasta, nullptr, seq, scratch, d_total, launches);
+    if (rc != KS_OK) return rc;
     int64_t total = 0;
     KS_CUDA(cudaMemcpyAsync(&total, d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
     KS_CUDA(cudaStreamSynchronize(ctx->stream));
     seq->n = total;
-    return KS_OK;
-}
-
-// Whitespace-free fast path only, no host synchronisation: any whitespace
-// sets *ws_flag (the caller must then fall back to encode_ascii_device).
-int encode_piece_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, ks_seq* seq, uint32_t* kept,
-                        int* ws_flag, int* launches) {
-    const int64_t nb = (n_bytes + 63) / 64;
-    seq->n = n_bytes;
-    if (nb == 0) return KS_OK;
-    const int threads = 256;
-    encode_inplace_kernel<<<grid_for(ctx, nb, threads), threads, 0, ctx->stream>>>(
-        d_in, n_bytes, nb, seq->lb, seq->d_bases, seq->d_nmask, seq->d_soft, kept, ws_flag);
-    if (launches) ++*launches;
-    KS_CUDA(cudaGetLastError());
     return KS_OK;
 }
 

@@ -26,6 +26,12 @@ struct AddOp {
     __device__ __forceinline__ T operator()(T a, T b) const { return a + b; }
 };
 
+struct MaxOp {   // last-terminator positions for FASTA line state (encode.cu)
+    using T = long long;
+    __device__ __forceinline__ T identity() const { return -1; }
+    __device__ __forceinline__ T operator()(T a, T b) const { return a > b ? a : b; }
+};
+
 struct MonoidOp {
     using T = unsigned int;
     const uint16_t* prod;
@@ -42,6 +48,10 @@ __device__ typename Op::T load_item(const void* in, int64_t i, int64_t n, const 
 template <>
 __device__ long long load_item<AddOp>(const void* in, int64_t i, int64_t n, const AddOp& op) {
     return i < n ? (long long)static_cast<const uint32_t*>(in)[i] : op.identity();
+}
+template <>
+__device__ long long load_item<MaxOp>(const void* in, int64_t i, int64_t n, const MaxOp& op) {
+    return i < n ? static_cast<const long long*>(in)[i] : op.identity();
 }
 template <>
 __device__ unsigned int load_item<MonoidOp>(const void* in, int64_t i, int64_t n, const MonoidOp& op) {
@@ -159,6 +169,13 @@ int exclusive_scan_rows(ks_ctx* ctx, const uint32_t* in, int64_t n, int64_t* out
                         int64_t* d_total, void* tmp, int* launches) {
     AddOp op;
     return run_scan<AddOp, long long>(ctx, in, n, op, reinterpret_cast<long long*>(out_excl),
+                                      reinterpret_cast<long long*>(d_total), tmp, launches);
+}
+
+int exclusive_scan_max(ks_ctx* ctx, const int64_t* in, int64_t n, int64_t* out_excl, int64_t* d_total,
+                       void* tmp, int* launches) {
+    MaxOp op;
+    return run_scan<MaxOp, long long>(ctx, in, n, op, reinterpret_cast<long long*>(out_excl),
                                       reinterpret_cast<long long*>(d_total), tmp, launches);
 }
 

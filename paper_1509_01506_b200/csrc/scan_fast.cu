@@ -32,7 +32,7 @@ constexpr int kRing = 8;      // minimum ring depth (deferred hits per lane)
 constexpr int kRingMax = 32;  // the ring takes what shared memory is left, up to this
 // steps between ring-fill checks: every 2nd step at K = 2 (high hit rates),
 // every 8th otherwise (the vote is pure overhead when hits are rare)
-__host__ __device__ constexpr int chk_steps(int k) { return k == 2 ? 2 : 8; }
+__host__ __device__ constexpr int chk_steps(int k) { return k == 2 ? 4 : 8; }
 // Kernel variants (template V), count/rows modes:
 //   kVarRing  : deferred hits resolved with the 1-base table (in shared memory);
 //   kVarPairs : K = 2 count mode -- a hit whose intermediate state accepts

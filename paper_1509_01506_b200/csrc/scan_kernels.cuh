@@ -91,6 +91,9 @@ int fast_threads();
 int exclusive_scan_rows(ks_ctx* ctx, const uint32_t* in, int64_t n, int64_t* out_excl,
                         int64_t* d_total, void* tmp, int* launches);
 size_t exclusive_scan_rows_tmp_bytes(int64_t n);
+// exclusive running maximum (identity -1); tmp sized like the rows scan
+int exclusive_scan_max(ks_ctx* ctx, const int64_t* in, int64_t n, int64_t* out_excl, int64_t* d_total,
+                       void* tmp, int* launches);
 int exclusive_scan_monoid(ks_ctx* ctx, const uint16_t* in, int64_t n, const uint16_t* prod,
                           int32_t nm, uint16_t* out_excl, uint16_t* d_total, void* tmp,
                           int* launches);

@@ -154,17 +154,20 @@ def run(dfa: Dfa, seq: Sequence, cfg: EngineConfig = EngineConfig()) -> MatchRep
     return MatchReport(counts, total, locations, metadata, dstats)
 
 
-def scan_bytes(dfa: Dfa, data, mode: str = "count", device: int = 0):
-    """Raw-mode ASCII bytes (host buffer) -> (counts, rows | None) with the
-    encode on the device (ks_seq_upload_ascii): the same result as
-    ``run(dfa, Sequence(encode_bytes(data)))`` without the host encode."""
+def scan_bytes(dfa: Dfa, data, mode: str = "count", device: int = 0, fmt: str = "raw"):
+    """Raw or FASTA file bytes (host buffer) -> (counts, rows | None) with the
+    ingest on the device: the same result as ``run(dfa, seq)`` for the
+    Sequence ``load_sequence`` would build (`ingest.py:54-70`), without the
+    host encode.  Counts stream the input through ks_count_host_bytes."""
     if mode not in ("count", "locate"):
         raise ValueError(f"unknown mode {mode!r}")
+    if fmt not in ("raw", "fasta"):
+        raise ValueError(f"unknown format {fmt!r}")
     ctx = _native.context(device)
     dh = ctx.dfa(dfa)
     if mode == "count":  # pipelined host->device copy, encode and scan
-        return ctx.count_host_ascii(dh, data), None
-    sh = ctx.upload_ascii(data)
+        return ctx.count_host_ascii(dh, data, fasta=fmt == "fasta"), None
+    sh = ctx.upload_ascii(data, fasta=fmt == "fasta")
     try:
         return ctx.locate(dh, sh)
     finally:

@@ -376,3 +376,86 @@ def test_sharded_async_matches_sequential(config, n, world):
         assert maps[r].cpu().numpy().tolist() == want_map.tolist()
     want = O.ref_sequential_count(w.dfa, codes)[0]
     assert total.tolist() == want.tolist()
+
+
+# ---------------------------------------------------------------- device ingest (FASTA / whitespace)
+
+FASTA_CASES = [
+    b">s1 demo\nctacat\n",
+    b">h\r\nACGT\r\nacgN\r\n>h2\r\nTTTT",
+    b">h\rAC\rGT\r>x\r\rnn",
+    b"acgt\n>not a header at file start? yes it is\nggg\n",
+    b"ac>gt\n>hdr\n>hdr2\nA C\tG T\n\n\n",
+    b">only header without newline",
+    b"",
+    b"\n\n\r\n",
+    b"no header at all\nACGTTT\n",
+    b">" + b"x" * 300 + b"\n" + b"acgt" * 70 + b"\n>" + b"y" * 130 + b"\r\n" + b"TTGCA" * 40,
+]
+
+
+def _fasta_expected(data: bytes) -> np.ndarray:
+    from paper_1509_01506_b200.ingest import strip_fasta_headers
+    return ks.encode_bytes(strip_fasta_headers(data))
+
+
+def _random_fasta(rng, n_records: int, line: int) -> bytes:
+    parts = []
+    for r in range(n_records):
+        parts.append(b">" + bytes(rng.choice(list(b"abc xyz>"), size=int(rng.integers(0, 150)))) +
+                     rng.choice([b"\n", b"\r\n", b"\r"]))
+        body = bytes(rng.choice(list(b"acgtACGTnN-"), size=int(rng.integers(0, 3000))))
+        for i in range(0, len(body), line):
+            parts.append(body[i:i + line] + rng.choice([b"\n", b"\r\n", b"\r", b" \n"]))
+    return b"".join(parts)
+
+
+@pytest.mark.parametrize("k", range(len(FASTA_CASES)))
+def test_device_fasta_ingest_cases(k):
+    data = FASTA_CASES[k]
+    ctx = _native.context(0)
+    sh = ctx.upload_ascii(data, fasta=True)
+    assert sh.codes().tolist() == _fasta_expected(data).tolist()
+    raw = ctx.upload_ascii(data, fasta=False)
+    assert raw.codes().tolist() == ks.encode_bytes(data).tolist()
+
+
+@pytest.mark.parametrize("seed,line", [(1, 60), (2, 80), (3, 61), (4, 200), (5, 7)])
+def test_device_fasta_ingest_random(seed, line):
+    rng = np.random.default_rng(seed)
+    data = _random_fasta(rng, 40, line)
+    ctx = _native.context(0)
+    assert ctx.upload_ascii(data, fasta=True).codes().tolist() == _fasta_expected(data).tolist()
+
+
+@pytest.mark.parametrize("piece_kb", [1, 3, 64])
+@pytest.mark.parametrize("fmt", ["fasta", "raw"])
+def test_count_host_bytes_streams_fasta_and_whitespace(piece_kb, fmt, monkeypatch):
+    """Many small pieces: the header-line state and the DFA state cross every
+    piece boundary (cuts fall inside headers, CRLF pairs and sequence lines)."""
+    monkeypatch.setenv("KS_PIECE_KB", str(piece_kb))
+    rng = np.random.default_rng(piece_kb)
+    data = _random_fasta(rng, 60, 61)
+    w = workloads.make(3, 4096)
+    ctx = _native.context(0)
+    dh = ctx.dfa(w.dfa)
+    sym = _fasta_expected(data) if fmt == "fasta" else ks.encode_bytes(data)
+    want = O.ref_sequential_count(w.dfa, sym)[0]
+    assert ctx.count_host_ascii(dh, data, fasta=fmt == "fasta").tolist() == want.tolist()
+    counts, rows = ks.scan_bytes(w.dfa, data, "locate", fmt=fmt)
+    assert counts.tolist() == want.tolist()
+    ref = O.ref_scan_rows(w.dfa, sym, 0, len(sym), w.dfa.start)[2]
+    assert np.array_equal(rows, ref)
+
+
+def test_load_sequence_device_matches_host(tmp_path):
+    rng = np.random.default_rng(7)
+    for name, fmt in (("a.fa", "fasta"), ("b.txt", "raw")):
+        path = tmp_path / name
+        path.write_bytes(_random_fasta(rng, 20, 70))
+        dev = ks.load_sequence_device(path, fmt)
+        host = ks.load_sequence(path, fmt)
+        assert dev.symbols.tolist() == host.symbols.tolist() and dev.length == host.length
+        w = workloads.make(2, 4096)
+        assert ks.run(w.dfa, dev).per_expression_counts.tolist() == \
+            ks.run(w.dfa, host).per_expression_counts.tolist()
