@@ -151,6 +151,10 @@ int synchronisation_depth(const std::vector<uint16_t>& t1, int nq) {
             if (work > budget) return -1;
         }
         if (next.empty()) return k + 1;
+        // a level that maps onto itself never shrinks (e.g. permutation columns)
+        if (next.size() == level.size() &&
+            std::all_of(level.begin(), level.end(), [&](const std::vector<uint16_t>& v) { return next.count(v); }))
+            return -1;
         level.assign(next.begin(), next.end());
     }
     return -1;
@@ -283,7 +287,7 @@ int compile_dfa(const int32_t* trans, int nq, const int32_t* out_off, const int3
     if (force_strategy == KS_STRATEGY_MAPSCAN)
         return fail(KS_E_INVALID, "dfa: MAPSCAN forced but the transition monoid exceeds 4096 maps");
     return fail(KS_E_UNSUPPORTED,
-                "dfa: automaton is neither definite (depth <= 64) nor has a transition monoid "
+                "dfa: automaton is neither definite (depth <= 2048) nor has a transition monoid "
                 "<= 4096 maps; the speculative map-scan strategy is not implemented yet");
 }
 

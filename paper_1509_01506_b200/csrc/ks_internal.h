@@ -28,7 +28,7 @@ int cuda_fail(cudaError_t e, const char* what);
 constexpr int kMaxStates = 32767;        // uint16 entries, bit 15 = hit flag
 constexpr uint16_t kFlag = 0x8000u;
 constexpr uint16_t kStateMask = 0x7FFFu;
-constexpr int kMaxSyncDepth = 64;        // lookback must fit in one 64-base block
+constexpr int kMaxSyncDepth = 2048;      // longest lookback (AC automata: the longest literal)
 constexpr int kMaxMonoid = 4096;         // product table <= 32 MiB
 constexpr int kBlockBases = 64;          // bases per packed block (one nmask word)
 constexpr int kScanThreads = 512;

@@ -459,3 +459,34 @@ def test_load_sequence_device_matches_host(tmp_path):
         w = workloads.make(2, 4096)
         assert ks.run(w.dfa, dev).per_expression_counts.tolist() == \
             ks.run(w.dfa, host).per_expression_counts.tolist()
+
+
+# ---------------------------------------------------------------- long literals (lookback > 64 bases)
+
+@pytest.mark.parametrize("lengths", [(70, 90), (150, 300), (1000, 1500)])
+def test_long_literals_lookback(lengths):
+    """Literals longer than a 64-base block: the synchronisation depth is the
+    longest literal and the lookback spans several blocks (and, for the last
+    case, the whole previous unit)."""
+    rng = np.random.default_rng(lengths[0])
+    lits = ["".join(rng.choice(list("acgt"), size=int(rng.integers(*lengths)))) for _ in range(6)]
+    text = "\n".join(lits[:3] + [f"{lits[3]}|{lits[4]}", lits[5][:40]]) + "\n"
+    dfa = ks.build_dfa(ks.expand_to_literals(ks.parse_expressions(text)))
+    n = 1 << 20
+    sym = rng.integers(0, 4, size=n).astype(np.uint8)
+    for k in range(300):   # plant occurrences, some overlapping unit boundaries
+        lit = lits[k % len(lits)]
+        p = int(rng.integers(0, n - len(lit)))
+        sym[p:p + len(lit)] = [("acgt".index(c)) for c in lit]
+    sym[rng.integers(0, n, size=50)] = 4
+    seq = ks.Sequence(sym)
+    ctx = _native.context(0)
+    dh = ctx.dfa(dfa)
+    info = dh.info
+    assert info["strategy_name"] == "lookback" and info["sync_depth"] >= lengths[0]
+    want = O.ref_sequential_count(dfa, sym)[0]
+    assert ctx.count(dh, ctx.seq(seq)).tolist() == want.tolist()
+    assert want.sum() >= 150   # planted (some overwritten by later plants or N)
+    rep = ks.run(dfa, seq, ks.EngineConfig(workers=7, mode="locate"))
+    ref = O.ref_scan_rows(dfa, sym, 0, n, dfa.start)[2]
+    assert np.array_equal(rep.locations, ref)
