@@ -223,7 +223,7 @@ def run_ours(args) -> None:
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
-    dh = ctx.dfa(wl.dfa)
+    dh = ctx.dfa(wl.dfa, strategy={"auto": 0, "lookback": 1, "mapscan": 2, "speculate": 3}[args.strategy])
     ascii_host = torch.from_numpy(wl.ascii).pin_memory()
     sh = ctx.upload_ascii(ascii_host.numpy())        # resident packed sequence
     scanner = DeviceShardScanner(ctx, dh, sh, row_base=rank * n)
@@ -370,6 +370,8 @@ def main() -> None:
     ap.add_argument("--bases", type=int, default=None, help="override bases per GPU")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--strategy", default="auto", choices=["auto", "lookback", "mapscan", "speculate"],
+                    help="force a scan strategy (exploration; the contract line uses auto)")
     ap.add_argument("--cpu-sample", type=int, default=256 << 20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],

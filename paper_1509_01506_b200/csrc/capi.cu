@@ -266,6 +266,28 @@ int monoid_prefix(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t beg
 }
 
 // True internal state of the sequence at position pos (state after pos bases).
+// SPECULATE entries of every chunk of [begin, end) (spec.cu), map memory in
+// ctx->spec_buf (grow-only, <= 256 MiB per segment of chunks).
+int spec_entries(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end, int64_t origin,
+                 int64_t L, int64_t nch, int32_t entry_val, const uint16_t* entry_ptr, uint16_t* centry,
+                 uint16_t* d_exit, int* launches) {
+    const HostDfa& h = dfa->host;
+    const int64_t per_chunk = int64_t(h.pss_max) * 2 + 4;
+    const int64_t seg = std::max<int64_t>(1, std::min<int64_t>(nch, (int64_t(256) << 20) / per_chunk));
+    const size_t bytes = speculate_entries_bytes(seg, h.pss_max) + 64 * kAlign;
+    if (ctx->spec_bytes < bytes) {
+        KS_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (ctx->spec_buf) KS_CUDA(cudaFree(ctx->spec_buf));
+        ctx->spec_buf = nullptr;
+        ctx->spec_bytes = 0;
+        KS_CUDA(cudaMalloc(&ctx->spec_buf, bytes));
+        ctx->spec_bytes = bytes;
+    }
+    return speculate_entries(ctx, view_of(seq), begin, end, origin, L, nch, dfa->scan.t1, h.nq, dfa->d_pss,
+                             dfa->d_pss_off, dfa->d_pss_inv, h.pss_max, entry_val, entry_ptr, centry, d_exit,
+                             ctx->spec_buf, seg, launches);
+}
+
 int true_state_at(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t pos, int* out,
                   int* launches) {
     const HostDfa& h = dfa->host;
@@ -290,6 +312,19 @@ int true_state_at(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t pos
     }
     int64_t origin, L, nch;
     geometry(seq, 0, pos, &origin, &L, &nch);
+    if (h.strategy == KS_STRATEGY_SPECULATE) {
+        int rc = ensure_scratch(ctx, size_t(nch) * 2 + 4096, &ar);
+        if (rc) return rc;
+        uint16_t* centry = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
+        uint16_t* d = static_cast<uint16_t*>(ar.take(16));
+        rc = spec_entries(ctx, dfa, seq, 0, pos, origin, L, nch, h.start_internal, nullptr, centry, d, launches);
+        if (rc) return rc;
+        uint16_t v = 0;
+        KS_CUDA(cudaMemcpyAsync(&v, d, 2, cudaMemcpyDeviceToHost, ctx->stream));
+        KS_CUDA(cudaStreamSynchronize(ctx->stream));
+        *out = v;
+        return KS_OK;
+    }
     int rc = ensure_scratch(ctx, size_t(nch) * 4 + exclusive_scan_monoid_tmp_bytes(nch) + 4096, &ar);
     if (rc) return rc;
     uint16_t* elems = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
@@ -321,7 +356,7 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
     KS_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
 
     int entry = entry_orig >= 0 ? h.new_of_old[entry_orig] : -1;
-    if (entry < 0 && h.strategy == KS_STRATEGY_MAPSCAN) {
+    if (entry < 0 && h.strategy != KS_STRATEGY_LOOKBACK) {
         int rc = true_state_at(ctx, dfa, seq, begin, &entry, &launches);
         if (rc) return rc;
     }
@@ -332,9 +367,11 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
     if (end == begin) nch = 0;
 
     const bool mapscan = h.strategy == KS_STRATEGY_MAPSCAN;
+    const bool spec = h.strategy == KS_STRATEGY_SPECULATE;
     size_t need = size_t(h.n_accept) * 8 + size_t(std::max(h.ne, 1)) * 8 + size_t(nch) * 2 + 4096;
     if (locate) need += size_t(nch) * 4 + size_t(nch + 1) * 8 + exclusive_scan_rows_tmp_bytes(nch) + 8 * kAlign;
     if (mapscan) need += size_t(nch) * 6 + exclusive_scan_monoid_tmp_bytes(nch) + 4 * kAlign;
+    if (spec) need += size_t(nch) * 2 + 2 * kAlign;
     Arena ar;
     int rc = ensure_scratch(ctx, need, &ar);
     if (rc) return rc;
@@ -363,6 +400,7 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
         mtot = static_cast<uint16_t*>(ar.take(16));
         mtmp = ar.take(exclusive_scan_monoid_tmp_bytes(nch));
     }
+    if (spec) centry = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
     KS_CUDA(cudaMemsetAsync(blk, 0, size_t(h.n_accept) * 8 + res_bytes, ctx->stream));
 
     ScanArgs a = base_args(dfa, dfa->scan, seq);
@@ -399,6 +437,11 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
         rc = monoid_prefix(ctx, dfa, seq, begin, end, origin, L, nch, elems, excl, mtot, mtmp, &launches);
         if (rc) return rc;
         rc = launch_chunk_entry(ctx, excl, nch, dfa->d_action, h.nq, entry, nullptr, centry, &launches);
+        if (rc) return rc;
+        a.chunk_entry = centry;
+    }
+    if (spec && nch > 0) {
+        rc = spec_entries(ctx, dfa, seq, begin, end, origin, L, nch, entry, nullptr, centry, nullptr, &launches);
         if (rc) return rc;
         a.chunk_entry = centry;
     }
@@ -661,9 +704,11 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
     int64_t origin, L, nch_max;
     geometry(&pseq[0], 0, piece, &origin, &L, &nch_max);
     const bool mapscan = h.strategy == KS_STRATEGY_MAPSCAN;
+    const bool spec = h.strategy == KS_STRATEGY_SPECULATE;
     Arena ar;
     size_t scratch = size_t(h.n_accept) * 8 + size_t(std::max(h.ne, 1)) * 8 + size_t(nch_max) * 2 + 16 * kAlign;
     if (mapscan) scratch += size_t(nch_max) * 6 + exclusive_scan_monoid_tmp_bytes(nch_max) + 4 * kAlign;
+    if (spec) scratch += size_t(nch_max) * 2 + 2 * kAlign;
     if (!host_pack) scratch += encode_scratch_bytes(piece) + 2 * kAlign;
     int rc = ensure_scratch(ctx, scratch, &ar);
     if (rc) return rc;
@@ -683,6 +728,7 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
         mtot = static_cast<uint16_t*>(ar.take(16));
         mtmp = ar.take(exclusive_scan_monoid_tmp_bytes(nch_max));
     }
+    if (spec) centry = static_cast<uint16_t*>(ar.take(size_t(nch_max) * 2));
     rc = ensure_pinned(ctx, size_t(std::max(h.ne, 1)) * 8 + 64);
     if (rc) return rc;
     char* pin = static_cast<char*>(ctx->pinned);
@@ -793,6 +839,10 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
                 rc = launch_chunk_entry(ctx, excl, nch, dfa->d_action, h.nq, 0, state, centry, &launches);
                 if (rc) return rc;
                 a.chunk_entry = centry;
+            } else if (spec) {
+                rc = spec_entries(ctx, dfa, &pseq[b], 0, nsym, o2, L2, nch, -1, state, centry, nullptr, &launches);
+                if (rc) return rc;
+                a.chunk_entry = centry;
             } else {
                 a.lookback = h.sync_depth;
                 a.base_pos = 0;
@@ -866,6 +916,7 @@ int ks_close(ks_ctx* ctx) {
     if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->sbuf) cudaFree(ctx->sbuf);
+    if (ctx->spec_buf) cudaFree(ctx->spec_buf);
     if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
     delete ctx->pool;
     if (ctx->hstage) cudaFreeHost(ctx->hstage);
@@ -939,6 +990,11 @@ int ks_dfa_upload_ex(ks_ctx* ctx, const int32_t* transitions, int32_t n_states, 
             d->d_act0 = reinterpret_cast<uint16_t*>(place(h.act0.data(), h.act0.size() * 2));
             d->d_action = reinterpret_cast<uint16_t*>(place(h.action.data(), h.action.size() * 2));
         }
+        if (h.strategy == KS_STRATEGY_SPECULATE) {
+            d->d_pss = reinterpret_cast<uint16_t*>(place(h.pss.data(), h.pss.size() * 2));
+            d->d_pss_off = reinterpret_cast<int32_t*>(place(h.pss_off.data(), h.pss_off.size() * 4));
+            d->d_pss_inv = reinterpret_cast<int16_t*>(place(h.pss_inv.data(), h.pss_inv.size() * 2));
+        }
         return up(off);
     };
     const size_t bytes = layout(nullptr, true);
@@ -978,6 +1034,11 @@ int ks_dfa_upload_ex(ks_ctx* ctx, const int32_t* transitions, int32_t n_states, 
         rebase(d->d_prod);
         rebase(d->d_act0);
         rebase(d->d_action);
+    }
+    if (h.strategy == KS_STRATEGY_SPECULATE) {
+        rebase(d->d_pss);
+        rebase(d->d_pss_off);
+        rebase(d->d_pss_inv);
     }
     const size_t smem_scan = d->scan.tk_bytes + d->scan.t1_bytes;
     const size_t smem_mono = h.strategy == KS_STRATEGY_MAPSCAN ? d->mono.tk_bytes + d->mono.t1_bytes : 0;
@@ -1238,12 +1299,12 @@ int ks_segment_map(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t be
     const HostDfa& h = dfa->host;
     std::vector<uint16_t> img(h.nq);
     int launches = 0;
-    if (h.strategy == KS_STRATEGY_LOOKBACK) {
+    if (h.strategy != KS_STRATEGY_MAPSCAN) {   // SPECULATE: every state walks the segment
         Arena ar;
         int rc = ensure_scratch(ctx, size_t(h.nq) * 2 + 1024, &ar);
         if (rc) return rc;
         uint16_t* d = static_cast<uint16_t*>(ar.take(size_t(h.nq) * 2));
-        if (end - begin >= h.sync_depth) {
+        if (h.strategy == KS_STRATEGY_LOOKBACK && end - begin >= h.sync_depth) {
             walk_kernel<<<1, 32, 0, ctx->stream>>>(view_of(seq), end - h.sync_depth, end, dfa->scan.t1, 1,
                                                      h.start_internal, d);
             KS_CUDA(cudaGetLastError());
@@ -1289,8 +1350,8 @@ int ks_segment_map_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
     const HostDfa& h = dfa->host;
     const int threads = 256;
     const int blocks = std::max(1, std::min((h.nq + threads - 1) / threads, 1024));
-    if (h.strategy == KS_STRATEGY_LOOKBACK) {
-        const bool uniform = end - begin >= h.sync_depth;
+    if (h.strategy != KS_STRATEGY_MAPSCAN) {   // SPECULATE: every state walks the segment
+        const bool uniform = h.strategy == KS_STRATEGY_LOOKBACK && end - begin >= h.sync_depth;
         segment_map_kernel<<<uniform ? 1 : blocks, threads, 0, ctx->stream>>>(
             view_of(seq), uniform ? end - h.sync_depth : begin, end, dfa->scan.t1, h.nq,
             uniform ? h.start_internal : -1, dfa->d_new_of_old, dfa->d_old_of_new, d_map_out);
@@ -1328,9 +1389,11 @@ int ks_count_shard_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
     int64_t origin, L, nch;
     geometry(seq, begin, end, &origin, &L, &nch);
     const bool mapscan = h.strategy == KS_STRATEGY_MAPSCAN;
+    const bool spec = h.strategy == KS_STRATEGY_SPECULATE;
     Arena ar;
     size_t need = size_t(h.n_accept) * 8 + size_t(nch) * 2 + 64 * kAlign;
     if (mapscan) need += size_t(nch) * 6 + exclusive_scan_monoid_tmp_bytes(nch);
+    if (spec) need += size_t(nch) * 2;
     int rc = ensure_scratch(ctx, need, &ar);
     if (rc) return rc;
     unsigned long long* visits = static_cast<unsigned long long*>(ar.take(size_t(h.n_accept) * 8));
@@ -1360,6 +1423,11 @@ int ks_count_shard_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
             rc = monoid_prefix(ctx, dfa, seq, begin, end, origin, L, nch, elems, excl, mtot, mtmp, &launches);
             if (rc) return rc;
             rc = launch_chunk_entry(ctx, excl, nch, dfa->d_action, h.nq, 0, entry, centry, &launches);
+            if (rc) return rc;
+            a.chunk_entry = centry;
+        } else if (spec) {
+            uint16_t* centry = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
+            rc = spec_entries(ctx, dfa, seq, begin, end, origin, L, nch, -1, entry, centry, nullptr, &launches);
             if (rc) return rc;
             a.chunk_entry = centry;
         } else {

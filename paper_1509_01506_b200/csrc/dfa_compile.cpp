@@ -286,9 +286,27 @@ int compile_dfa(const int32_t* trans, int nq, const int32_t* out_off, const int3
     }
     if (force_strategy == KS_STRATEGY_MAPSCAN)
         return fail(KS_E_INVALID, "dfa: MAPSCAN forced but the transition monoid exceeds 4096 maps");
-    return fail(KS_E_UNSUPPORTED,
-                "dfa: automaton is neither definite (depth <= 2048) nor has a transition monoid "
-                "<= 4096 maps; the speculative map-scan strategy is not implemented yet");
+    // SPECULATE: candidate entry states per preceding symbol (the image of its
+    // column, engine.py:80-91) and their inverse index
+    h->strategy = KS_STRATEGY_SPECULATE;
+    h->pss_off.assign(6, 0);
+    h->pss.clear();
+    h->pss_inv.assign(size_t(5) * nq, int16_t(-1));
+    h->pss_max = 0;
+    std::vector<char> seen(nq);
+    for (int x = 0; x < 5; ++x) {
+        std::fill(seen.begin(), seen.end(), 0);
+        for (int q = 0; q < nq; ++q) seen[t.t1[size_t(q) * 5 + x]] = 1;
+        int k = 0;
+        for (int q = 0; q < nq; ++q)
+            if (seen[q]) {
+                h->pss_inv[size_t(x) * nq + q] = int16_t(k++);
+                h->pss.push_back(uint16_t(q));
+            }
+        h->pss_off[x + 1] = int32_t(h->pss.size());
+        h->pss_max = std::max(h->pss_max, k);
+    }
+    return KS_OK;
 }
 
 }  // namespace ks

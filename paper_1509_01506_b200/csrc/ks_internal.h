@@ -67,6 +67,11 @@ struct HostDfa {
     std::vector<uint16_t> prod;         // nm x nm: element(a then b)
     std::vector<uint16_t> act0;         // nm: internal state reached from START
     std::vector<uint16_t> action;       // nm x nq: internal state reached from q
+    // SPECULATE
+    std::vector<uint16_t> pss;          // candidate entry states after symbol x: pss[pss_off[x]..pss_off[x+1])
+    std::vector<int32_t> pss_off;       // 6
+    std::vector<int16_t> pss_inv;       // 5 x nq: index of q in pss of x, or -1
+    int pss_max = 0;
 };
 
 int compile_dfa(const int32_t* trans, int nq, const int32_t* out_off, const int32_t* out_ids,
@@ -140,6 +145,9 @@ struct ks_ctx {
     void* hstage = nullptr;
     size_t hstage_bytes = 0;
     cudaEvent_t hev[3] = {nullptr, nullptr, nullptr};
+    // SPECULATE chunk maps (grow-only, separate from `scratch`)
+    void* spec_buf = nullptr;
+    size_t spec_bytes = 0;
     // ks_count_async: one event pair per call until ks_async_wait
     std::vector<cudaEvent_t> aev;
     int n_async = 0;
@@ -157,6 +165,9 @@ struct ks_dfa {
     uint16_t* d_prod = nullptr;
     uint16_t* d_act0 = nullptr;
     uint16_t* d_action = nullptr;   // nm x nq
+    uint16_t* d_pss = nullptr;      // SPECULATE candidate sets (HostDfa::pss)
+    int32_t* d_pss_off = nullptr;
+    int16_t* d_pss_inv = nullptr;
     int32_t* d_new_of_old = nullptr;
     int32_t* d_old_of_new = nullptr;
     void* d_blob = nullptr;   // single allocation backing the above

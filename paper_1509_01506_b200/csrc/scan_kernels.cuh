@@ -104,6 +104,15 @@ int launch_finalize_counts(ks_ctx* ctx, const unsigned long long* visits, int32_
                            const int32_t* acc_out_off, const int32_t* acc_out_ids,
                            unsigned long long* counts, const uint16_t* exit_src, uint16_t* exit_dst,
                            int* launches);
+// SPECULATE strategy (spec.cu): entry state of every chunk of [begin, end)
+// from per-chunk candidate maps, processed seg_chunks chunks at a time in
+// `buf` (speculate_entries_bytes).  The range's entry is entry_val (>= 0) or
+// *entry_ptr; *d_exit (optional) receives the state after `end`.
+size_t speculate_entries_bytes(int64_t seg_chunks, int32_t pss_max);
+int speculate_entries(ks_ctx* ctx, const SeqView& seq, int64_t begin, int64_t end, int64_t origin, int64_t L,
+                      int64_t nch, const uint16_t* t1, int32_t nq, const uint16_t* pss, const int32_t* pss_off,
+                      const int16_t* inv, int32_t pss_max, int32_t entry_val, const uint16_t* entry_ptr,
+                      uint16_t* centry, uint16_t* d_exit, void* buf, int64_t seg_chunks, int* launches);
 int launch_chunk_entry(ks_ctx* ctx, const uint16_t* excl, int64_t n, const uint16_t* action,
                        int32_t nq, int32_t entry, const uint16_t* entry_ptr, uint16_t* chunk_entry,
                        int* launches);

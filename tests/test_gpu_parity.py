@@ -490,3 +490,87 @@ def test_long_literals_lookback(lengths):
     rep = ks.run(dfa, seq, ks.EngineConfig(workers=7, mode="locate"))
     ref = O.ref_scan_rows(dfa, sym, 0, n, dfa.start)[2]
     assert np.array_equal(rep.locations, ref)
+
+
+# ---------------------------------------------------------------- SPECULATE strategy (generic automata)
+
+def _wild_dfa(nq=200, seed=3):
+    """Three permutation columns (the generated group is huge, so no small
+    monoid), one merging column, OTHER -> 0: neither definite nor MAPSCAN."""
+    rng = np.random.default_rng(seed)
+    trans = np.empty((nq, 5), dtype=np.int32)
+    for c in range(3):
+        trans[:, c] = rng.permutation(nq)
+    trans[:, 3] = rng.integers(0, nq, nq)
+    trans[:, 4] = 0
+    outs = [sorted(rng.integers(0, 4, int(rng.integers(0, 3))).tolist()) if rng.random() < 0.2 else []
+            for _ in range(nq)]
+    off = np.zeros(nq + 1, dtype=np.int32)
+    off[1:] = np.cumsum([len(o) for o in outs])
+    ids = np.array([e for o in outs for e in o], dtype=np.int32)
+    return ks.Dfa(trans, off, ids, tuple(str(i) for i in range(4)), 4)
+
+
+@pytest.mark.parametrize("n", [1, 1000, 300_001])
+def test_speculate_generic_automaton(n):
+    dfa = _wild_dfa()
+    ctx = _native.context(0)
+    dh = ctx.dfa(dfa)
+    assert dh.info["strategy_name"] == "speculate"
+    rng = np.random.default_rng(n)
+    codes = rng.integers(0, 4, n).astype(np.uint8)
+    codes[rng.random(n) < 0.0005] = 4
+    want, rows = O.ref_run(dfa, codes, 1, 10, True)[:2]
+    got, grows = ctx.locate(dh, ctx.upload_codes(codes))
+    assert got.tolist() == want.tolist()
+    assert np.array_equal(grows, rows)
+    rep = ks.run(dfa, ks.Sequence(codes), ks.EngineConfig(workers=5, mode="locate"))
+    assert rep.per_expression_counts.tolist() == want.tolist()
+    assert np.array_equal(rep.locations, rows)
+    # ranges entering in given states and the exit state
+    sh = ctx.upload_codes(codes)
+    for b, e, q in ((0, n, 7), (n // 3, n, -1), (n // 2, n // 2 + 5000, 11)):
+        e = min(e, n)
+        q0 = q if q >= 0 else (int(O.ref_sequential_count(dfa, codes[:b])[1]) if b else 0)
+        wc, wl = O.ref_sequential_count(dfa, codes[b:e], state=q0)
+        c, last, _ = ctx.scan_range(dh, sh, b, e, q)
+        assert c.tolist() == wc.tolist() and last == wl
+
+
+@pytest.mark.parametrize("config", [1, 2, 3, 5])
+def test_speculate_forced_on_config_automata(config):
+    """The generic strategy forced onto the config automata (definite and
+    MAPSCAN ones) must give their results too."""
+    w = workloads.make(config, 200_003)
+    ctx = _native.context(0)
+    dh = ctx.dfa(w.dfa, strategy=_native.STRATEGY_SPECULATE)
+    assert dh.info["strategy_name"] == "speculate"
+    sym = ks.encode_bytes(w.ascii.tobytes())
+    want = O.ref_sequential_count(w.dfa, sym)[0]
+    assert ctx.count(dh, ctx.seq(ks.Sequence(sym))).tolist() == want.tolist()
+    assert ctx.count_host_ascii(dh, w.ascii.tobytes()).tolist() == want.tolist()
+
+
+def test_speculate_streamed_and_sharded(monkeypatch):
+    monkeypatch.setenv("KS_PIECE_KB", "16")
+    dfa = _wild_dfa(97, seed=9)
+    rng = np.random.default_rng(2)
+    data = bytes(np.frombuffer(b"acgtN", dtype=np.uint8)[rng.choice(5, 100_000, p=[.25, .25, .25, .2499, .0001])])
+    sym = ks.encode_bytes(data)
+    want = O.ref_sequential_count(dfa, sym)[0]
+    ctx = _native.context(0)
+    dh = ctx.dfa(dfa)
+    assert dh.info["strategy_name"] == "speculate"
+    assert ctx.count_host_ascii(dh, data).tolist() == want.tolist()
+    assert ctx.count_host_ascii(dh, data, fasta=True).tolist() == want.tolist()
+    # segment maps (every state walks the shard) composed like the NCCL path
+    sh = ctx.upload_codes(sym)
+    cuts = [0, 30_001, 64_000, len(sym)]
+    state, total = 0, np.zeros_like(want)
+    for b, e in zip(cuts[:-1], cuts[1:]):
+        m = ctx.segment_map(dh, sh, b, e)
+        c, last, _ = ctx.scan_range(dh, sh, b, e, state)
+        assert last == m[state]
+        total += c
+        state = int(m[state])
+    assert total.tolist() == want.tolist()
