@@ -227,19 +227,6 @@ int dispatch(ks_ctx* ctx, const ks_dfa* dfa, const DevTable& T, const ScanPlan& 
         a.tk = T.tkc;
         a.t1 = T.t1z;
         a.t1_pad = int32_t(T.t1z_bytes / 2);
-        // high hit rates: count with direct histograms instead of the ring
-        if (mode == kModeCount && T.fast_k == 2) {
-            const char* env = std::getenv("KS_DIRECT");
-            const bool direct = env && *env ? *env == '1' : false;  // measured: the ring wins on C3 (0.478 vs 0.489 ms)
-            if (direct && fast_smem_bytes(kModeCountDirectId, 0, T.n_accept, fast_threads()) <= ctx->smem_optin)
-                mode = kModeCountDirectId;
-        }
-        if (mode == kModeCount || mode == kModeRows) {
-            const char* env = std::getenv("KS_FAST_VAR");
-            const int var = env && *env ? std::atoi(env) : 0;
-            if (variant_smem_bytes(var, mode, T.fast_k, a.t1_pad, T.n_accept, fast_threads()) <= ctx->smem_optin)
-                a.fast_variant = var;
-        }
         return launch_scan_fast(ctx, a, mode, T.fast_k, launches);
     }
     return launch_scan(ctx, a, mode, T.stride, dfa->tables_in_smem, launches);

@@ -10,11 +10,16 @@
 //     per K bases the critical path is SHF -> LOP3 -> LDS.
 //   * the 1-base table (|Q|+1) x 5 (row-major, OTHER column included) for
 //     re-walks, OTHER blocks and the lookback;
-//   * a per-lane ring of deferred hits: a flagged step only stores its table
-//     address (predicated STS, no divergence); every 8 steps each lane
-//     re-walks its own ring entries with the 1-base table and histograms the
-//     accepting states it enters (shared atomics).  This replaces the
-//     reference's per-symbol CSR output loop (_kernels.py:26-28, 80-84).
+//   * a per-lane ring of deferred hits, as deep as the shared memory left
+//     allows (C3: 13): a flagged step only stores its table address (K = 2:
+//     address | entry << 17) with a predicated STS, no divergence; every
+//     chk_steps(K) steps the warp votes whether some lane's ring is nearly
+//     full and only then calls the out-of-line drain, which resolves every
+//     lane's entries (K = 2: the final state from the stored entry, the
+//     intermediate one by one 1-base lookup; K > 2: a re-walk) into a
+//     shared-memory histogram of accepting-state visits (shared atomics).
+//     This replaces the reference's per-symbol CSR output loop
+//     (_kernels.py:26-28, 80-84).
 //   * a "sink" state Z = |Q| whose row never flags: lanes of a warp that
 //     have no work for a block (N-run blocks, finished chunks) ride the fast
 //     path in Z instead of diverging.
@@ -30,25 +35,9 @@ namespace {
 
 constexpr int kRing = 8;      // minimum ring depth (deferred hits per lane)
 constexpr int kRingMax = 32;  // the ring takes what shared memory is left, up to this
-// steps between ring-fill checks: every 2nd step at K = 2 (high hit rates),
+// steps between ring-fill checks: every 4th step at K = 2 (high hit rates),
 // every 8th otherwise (the vote is pure overhead when hits are rare)
 __host__ __device__ constexpr int chk_steps(int k) { return k == 2 ? 4 : 8; }
-// Kernel variants (template V), count/rows modes:
-//   kVarRing  : deferred hits resolved with the 1-base table (in shared memory);
-//   kVarPairs : K = 2 count mode -- a hit whose intermediate state accepts
-//               bumps a (first base, previous state) counter instead of
-//               re-deriving the state; the pairs are mapped to states once
-//               per CTA at the end.  Its 64 KiB of counters leave a shallow
-//               ring (1-base table read through L1): measured slower on C3
-//               (0.54 vs 0.43 ms), kept selectable with KS_FAST_VAR=1.
-constexpr int kVarRing = 0;
-constexpr int kVarPairs = 1;
-__host__ __device__ constexpr bool t1_in_smem(int v) { return v != kVarPairs; }
-// Count mode with direct shared-memory histograms instead of the ring (K = 2,
-// high hit rates): bit 13 of an entry = the intermediate state is accepting
-// (counted per (first base, previous state) and resolved at the end), bit 14
-// = the final state is accepting (counted per state).  No re-walks at all.
-constexpr int kModeCountDirect = 4;
 constexpr int kFastThreads = 1024;
 constexpr uint32_t kRingStride = 4u * kFastThreads;  // bytes between ring slots
 
@@ -74,12 +63,6 @@ __device__ __forceinline__ uint32_t bitsel(uint32_t f, uint32_t e) {
 }
 __device__ __forceinline__ void red_shared_add(uint32_t addr, uint32_t v) {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
-// Predicated shared-memory increment (no branch around it).
-__device__ __forceinline__ void red_shared_inc_if(uint32_t addr, uint32_t cond) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %1, 0;\n\t@p red.shared.add.u32 [%0], 1;\n\t}"
-        ::"r"(addr), "r"(cond) : "memory");
 }
 // Keep a value in a register (stops the compiler from re-deriving shared
 // window bases / reloading constants inside the drain loops).
@@ -110,8 +93,6 @@ __device__ __forceinline__ uint32_t field(const uint4& x, int j) {
 struct Ctx {
     uint32_t tk;        // shared address of the K-stride table
     uint32_t t1;        // shared address of the 1-base table
-    const uint16_t* t1g;  // the same table in global memory (direct mode)
-    uint32_t hist2;     // direct mode: (first base, previous state) counters
     uint32_t hist;      // shared address of the visit histogram (count/rows)
     const uint16_t* outcnt;
     const int32_t* off;
@@ -130,7 +111,7 @@ struct Lane {
 
 template <int MODE>
 __device__ __forceinline__ void record(const Ctx& c, Lane<MODE>& L, int64_t pos, uint32_t s) {
-    if constexpr (MODE == kModeCount || MODE == kModeRows || MODE == kModeCountDirect) {
+    if constexpr (MODE == kModeCount || MODE == kModeRows) {
         red_shared_add(c.hist + 4u * s, 1u);
         if constexpr (MODE == kModeRows) L.nrows += __ldg(&c.outcnt[s]);
     } else if constexpr (MODE == kModeEmit) {
@@ -144,68 +125,62 @@ __device__ __forceinline__ void record(const Ctx& c, Lane<MODE>& L, int64_t pos,
     }
 }
 
-template <int MODE, int V = kVarRing>
 __device__ __forceinline__ uint32_t step1(const Ctx& c, uint32_t s, uint32_t sym) {
-    if constexpr (MODE == kModeCountDirect || !t1_in_smem(V)) return __ldg(c.t1g + s * 5u + sym);
     return lds16(c.t1 + (s * 5u + sym) * 2u);
 }
 
 // Re-walk one deferred K-step (ring value = its table byte address).
-template <int K, int MODE, int V = kVarRing>
+template <int K, int MODE>
 __device__ __forceinline__ void rewalk(const Ctx& c, Lane<MODE>& L, uint32_t v, int64_t pos) {
     constexpr int LC = 17 - 2 * K;
     uint32_t s = (v >> 1) & ((1u << (LC - 1)) - 1u);
     const uint32_t w = v >> LC;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-        s = step1<MODE, V>(c, s, (w >> (2 * i)) & 3u);
+        s = step1(c, s, (w >> (2 * i)) & 3u);
         if (s < c.n_accept) record<MODE>(c, L, pos + i, s);
     }
 }
 
-// Count/rows resolution of one deferred step.  For K = 2 the entry's bits
-// 13/14 say which of the two states accepts: re-reading the entry gives the
-// final state directly and the intermediate one is only re-derived when it
-// accepts.
-template <int K, int MODE, int V>
+// Count/rows resolution of one deferred step.  For K = 2 the ring value is
+// address | entry << 17 and the entry's bits 13/14 say which of the two
+// states accepts: the final state comes straight from the entry, the
+// intermediate one is re-derived (one 1-base lookup) only when it accepts.
+template <int K, int MODE>
 __device__ __forceinline__ void resolve(const Ctx& c, Lane<MODE>& L, uint32_t a) {
-    if constexpr (V == kVarPairs) {   // count only: intermediate hits by (first base, previous state)
+    if constexpr (K == 2) {
         const uint32_t e = a >> 17;
-        if (e & 0x2000u) red_shared_add(c.hist2 + ((a & 0x7FFEu) << 1), 1u);
-        if (e & 0x4000u) red_shared_add(c.hist + ((e & 0x1FFEu) << 1), 1u);
-    } else if constexpr (K == 2) {   // ring value = address | entry << 17: no table re-read
-        const uint32_t e = a >> 17;
-        if (e & 0x2000u) record<MODE>(c, L, 0, step1<MODE, V>(c, (a >> 1) & 0xFFFu, (a >> 13) & 3u));
+        if (e & 0x2000u) record<MODE>(c, L, 0, step1(c, (a >> 1) & 0xFFFu, (a >> 13) & 3u));
         if (e & 0x4000u) record<MODE>(c, L, 0, (e >> 1) & 0xFFFu);
     } else {
-        rewalk<K, MODE, V>(c, L, a, 0);
+        rewalk<K, MODE>(c, L, a, 0);
     }
 }
 
-template <int K, int MODE, int V>
+template <int K, int MODE>
 __device__ __forceinline__ void drain(const Ctx& c, Lane<MODE>& L, unsigned am, uint32_t rp0,
                                       uint32_t& rp, uint32_t ring_stride) {
     const uint32_t cnt = (rp - rp0) / kRingStride;
     const uint32_t kmax = __reduce_max_sync(am, cnt);  // warp-uniform trip count
     for (uint32_t k = 0; k < kmax; ++k)
-        if (k < cnt) resolve<K, MODE, V>(c, L, lds32(rp0 + k * ring_stride));
+        if (k < cnt) resolve<K, MODE>(c, L, lds32(rp0 + k * ring_stride));
     rp = rp0;
 }
 
 // Out-of-line drain for the adaptive drain sites inside the unrolled block
 // loop (one copy of the resolve code instead of one per site).
-template <int K, int MODE, int V>
+template <int K, int MODE>
 __device__ __noinline__ uint32_t drain_out(const Ctx c, uint32_t rp0, uint32_t cnt) {
     Lane<MODE> L;
     const uint32_t kmax = __reduce_max_sync(0xffffffffu, cnt);
     for (uint32_t k = 0; k < kmax; ++k)
-        if (k < cnt) resolve<K, MODE, V>(c, L, lds32(rp0 + k * kRingStride));
+        if (k < cnt) resolve<K, MODE>(c, L, lds32(rp0 + k * kRingStride));
     return L.nrows;
 }
 
 // One full, OTHER-free 64-base block.  `live` lanes record hits; others ride
 // along in the sink state.
-template <int K, int MODE, int V>
+template <int K, int MODE>
 __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint32_t s, const uint4& xb,
                                                int64_t p0, unsigned am, uint32_t rp0, uint32_t& rp,
                                                uint32_t ring_stride) {
@@ -230,22 +205,18 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
             // (table addresses) are position-free, so they may cross blocks
             constexpr int CHK = chk_steps(K);
             if ((j % CHK) == CHK - 1 && __any_sync(am, rp - rp0 >= c.ring_thr)) {
-                L.nrows += drain_out<K, MODE, V>(c, rp0, (rp - rp0) / kRingStride);
+                L.nrows += drain_out<K, MODE>(c, rp0, (rp - rp0) / kRingStride);
                 rp = rp0;
             }
         } else if constexpr (MODE == kModeEmit) {
-            if (e & 0x8000u) rewalk<K, MODE, V>(c, L, a, p0 + K * j);
-        } else if constexpr (MODE == kModeCountDirect) {
-            static_assert(K == 2, "direct counting is K = 2 only");
-            red_shared_inc_if(c.hist2 + ((a & 0x7FFEu) << 1), e & 0x2000u);
-            red_shared_inc_if(c.hist + ((e & 0x1FFEu) << 1), e & 0x4000u);
+            if (e & 0x8000u) rewalk<K, MODE>(c, L, a, p0 + K * j);
         }
     }
     s = (e >> 1) & ((1u << (LC - 1)) - 1u);
 #pragma unroll
     for (int r = NL * K; r < 64; ++r) {  // K == 3 leaves one base
         const uint32_t sym = uint32_t(r < 32 ? w0 >> (2 * r) : w1 >> (2 * (r - 32))) & 3u;
-        s = step1<MODE, V>(c, s, sym);
+        s = step1(c, s, sym);
         if constexpr (MODE != kModeMap) {
             if (s < c.n_accept) record<MODE>(c, L, p0 + r, s);
         }
@@ -256,43 +227,31 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
 
 extern __shared__ __align__(128) unsigned char f_smem[];
 
-template <int K, int MODE, int V>
+template <int K, int MODE>
 __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     constexpr bool RING = MODE == kModeCount || MODE == kModeRows;
-    constexpr bool PAIRS = MODE == kModeCountDirect || V == kVarPairs;   // (first base, state) counters
-    constexpr bool T1S = !PAIRS && t1_in_smem(V);                        // 1-base table in shared memory
-    constexpr bool HIST = RING || MODE == kModeCountDirect;
     constexpr int TK_BYTES = 1 << 17;
-    constexpr int H2_WORDS = 4 << 12;  // (first base, state) for K = 2
-    static_assert(V != kVarPairs || (K == 2 && MODE == kModeCount), "pair counters: K = 2 count only");
-    // layout: table | t1 (T1S) | ring (ring modes) | hist | hist2 (PAIRS)
+    // layout: table | t1 | ring (count/rows) | hist (count/rows)
     unsigned char* p_t1 = f_smem + TK_BYTES;
-    unsigned char* p_ring = p_t1 + (T1S ? size_t(a.t1_pad) * 2 : 0);
+    unsigned char* p_ring = p_t1 + size_t(a.t1_pad) * 2;
     unsigned int* s_hist = reinterpret_cast<unsigned int*>(
         p_ring + (RING ? size_t(a.ring_depth) * 4 * blockDim.x : 0));
-    unsigned int* s_hist2 = s_hist + ((a.n_accept + 3) & ~3);
     {
         const uint4* src = reinterpret_cast<const uint4*>(a.tk);
         uint4* dst = reinterpret_cast<uint4*>(f_smem);
         for (int i = threadIdx.x; i < TK_BYTES / 16; i += blockDim.x) dst[i] = __ldg(src + i);
-        if constexpr (T1S) {
-            src = reinterpret_cast<const uint4*>(a.t1);
-            dst = reinterpret_cast<uint4*>(p_t1);
-            for (int i = threadIdx.x; i < a.t1_pad / 8; i += blockDim.x) dst[i] = __ldg(src + i);
-        }
+        src = reinterpret_cast<const uint4*>(a.t1);
+        dst = reinterpret_cast<uint4*>(p_t1);
+        for (int i = threadIdx.x; i < a.t1_pad / 8; i += blockDim.x) dst[i] = __ldg(src + i);
     }
-    if constexpr (HIST)
+    if constexpr (RING)
         for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x) s_hist[i] = 0u;
-    if constexpr (PAIRS)
-        for (int i = threadIdx.x; i < H2_WORDS; i += blockDim.x) s_hist2[i] = 0u;
     __syncthreads();
 
     Ctx c;
     c.tk = smem_addr(f_smem);
     c.t1 = opaque(smem_addr(p_t1));
     c.hist = opaque(smem_addr(s_hist));
-    c.hist2 = smem_addr(s_hist2);
-    c.t1g = a.t1;
     c.outcnt = a.acc_outcnt;
     c.off = a.acc_out_off;
     c.ids = a.acc_out_ids;
@@ -345,7 +304,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                 const int q = int(p & 63);
                 const uint32_t word = q < 16 ? xb.x : q < 32 ? xb.y : q < 48 ? xb.z : xb.w;
                 const uint32_t sym = ((xm >> q) & 1ull) ? 4u : (word >> (2 * (q & 15))) & 3u;
-                s = step1<MODE, V>(c, s, sym);
+                s = step1(c, s, sym);
             }
         }
         Lane<MODE> L;
@@ -384,8 +343,8 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
             const bool fast = !has || (k >= kfl && k < kfh && (clean || (alln && resets)));
             if (__all_sync(am, fast)) {
                 const bool live = has && !alln;
-                const uint32_t s2 = fast_block<K, MODE, V>(c, L, live ? s : sink, wb, p0, am, rp0, rp,
-                                                           ring_stride);
+                const uint32_t s2 = fast_block<K, MODE>(c, L, live ? s : sink, wb, p0, am, rp0, rp,
+                                                        ring_stride);
                 if (live) {
                     s = s2;
                 } else if (has) {
@@ -408,7 +367,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                     const uint32_t sym = ((wm >> q) & 1ull)
                                              ? 4u
                                              : uint32_t((q < 32 ? w0 >> (2 * q) : w1 >> (2 * (q - 32)))) & 3u;
-                    s = step1<MODE, V>(c, s, sym);
+                    s = step1(c, s, sym);
                     if constexpr (MODE != kModeMap) {
                         if (s < c.n_accept) record<MODE>(c, L, p0 + q, s);
                     }
@@ -419,7 +378,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                 wm = nm;
             }
         }
-        if constexpr (MODE == kModeRows) drain<K, MODE, V>(c, L, am, rp0, rp, ring_stride);   // rows are per chunk
+        if constexpr (MODE == kModeRows) drain<K, MODE>(c, L, am, rp0, rp, ring_stride);   // rows are per chunk
         if (active) {
             if (a.chunk_exit) a.chunk_exit[ch] = uint16_t(s);
             if constexpr (MODE == kModeRows) a.chunk_rows[ch] = L.nrows;
@@ -431,17 +390,10 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
 
     if constexpr (MODE == kModeCount) {   // the ring's leftovers
         Lane<MODE> L;
-        drain<K, MODE, V>(c, L, am, rp0, rp, ring_stride);
+        drain<K, MODE>(c, L, am, rp0, rp, ring_stride);
     }
-    if constexpr (HIST) {
+    if constexpr (RING) {
         __syncthreads();
-        if constexpr (PAIRS) {  // (first base, previous state) -> intermediate state, folded in shared memory
-            for (int i = threadIdx.x; i < H2_WORDS; i += blockDim.x) {
-                const unsigned int n = s_hist2[i];
-                if (n) red_shared_add(smem_addr(s_hist) + 4u * __ldg(a.t1 + (i & 0xFFF) * 5 + (i >> 12)), n);
-            }
-            __syncthreads();
-        }
         for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x)
             if (s_hist[i]) atomicAdd(&a.visits[i], (unsigned long long)s_hist[i]);
     }
@@ -450,54 +402,23 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
 using FastFn = void (*)(const ScanArgs);
 
 template <int K>
-FastFn pick_mode(int mode, int var) {
-    if constexpr (K == 2) {
-        if (var == kVarPairs && mode == kModeCount) return scan_fast_kernel<2, kModeCount, kVarPairs>;
-    }
+FastFn pick_mode(int mode) {
     switch (mode) {
-        case kModeCountDirect:
-            if constexpr (K == 2) return scan_fast_kernel<2, kModeCountDirect, kVarRing>;
-            return nullptr;
-        case kModeCount: return scan_fast_kernel<K, kModeCount, kVarRing>;
-        case kModeRows: return scan_fast_kernel<K, kModeRows, kVarRing>;
-        case kModeEmit: return scan_fast_kernel<K, kModeEmit, kVarRing>;
-        case kModeMap: return scan_fast_kernel<K, kModeMap, kVarRing>;
+        case kModeCount: return scan_fast_kernel<K, kModeCount>;
+        case kModeRows: return scan_fast_kernel<K, kModeRows>;
+        case kModeEmit: return scan_fast_kernel<K, kModeEmit>;
+        case kModeMap: return scan_fast_kernel<K, kModeMap>;
     }
     return nullptr;
 }
 
-FastFn pick(int mode, int k, int var) {
+FastFn pick(int mode, int k) {
     switch (k) {
-        case 2: return pick_mode<2>(mode, var);
-        case 3: return pick_mode<3>(mode, var);
-        case 4: return pick_mode<4>(mode, var);
+        case 2: return pick_mode<2>(mode);
+        case 3: return pick_mode<3>(mode);
+        case 4: return pick_mode<4>(mode);
     }
     return nullptr;
-}
-
-// Variant actually used for (mode, k): falls back to kVarRing where the
-// requested one does not apply.
-int effective_variant(int var, int mode, int k) {
-    if (var == kVarPairs) return (k == 2 && mode == kModeCount) ? kVarPairs : kVarRing;
-    return kVarRing;
-}
-
-}  // namespace
-
-size_t fast_smem_bytes(int mode, int32_t t1_pad, int32_t hist_words, int threads) {
-    if (mode == kModeCountDirect)
-        return size_t(1 << 17) + size_t((hist_words + 3) & ~3) * 4 + size_t(4 << 12) * 4;
-    const bool ring = mode == kModeCount || mode == kModeRows;
-    return size_t(1 << 17) + size_t(t1_pad) * 2 + (ring ? size_t(kRing) * 4 * threads : 0) +
-           size_t(hist_words) * 4;
-}
-
-// Shared memory of a variant without its ring, and the ring depth that fits.
-size_t variant_fixed_bytes(int var, int mode, int k, int32_t t1_pad, int32_t hist_words) {
-    const int v = effective_variant(var, mode, k);
-    if (mode == kModeCountDirect) return fast_smem_bytes(mode, t1_pad, hist_words, 0);
-    return size_t(1 << 17) + (t1_in_smem(v) ? size_t(t1_pad) * 2 : 0) + size_t((hist_words + 3) & ~3) * 4 +
-           (v == kVarPairs ? size_t(4 << 12) * 4 : 0);
 }
 
 int ring_depth_for(size_t fixed, size_t optin, int threads) {
@@ -505,21 +426,29 @@ int ring_depth_for(size_t fixed, size_t optin, int threads) {
     return int(std::min<size_t>(kRingMax, (optin - fixed) / (size_t(4) * threads)));
 }
 
-size_t variant_smem_bytes(int var, int mode, int k, int32_t t1_pad, int32_t hist_words, int threads) {
-    return variant_fixed_bytes(var, mode, k, t1_pad, hist_words) + size_t(kRing) * 4 * threads;
+}  // namespace
+
+// Shared memory without the hit ring (the ring takes what is left).
+size_t fast_fixed_bytes(int32_t t1_pad, int32_t hist_words) {
+    return size_t(1 << 17) + size_t(t1_pad) * 2 + size_t((hist_words + 3) & ~3) * 4;
+}
+
+// Smallest configuration the fast kernel accepts (ring of kRing entries).
+size_t fast_smem_bytes(int mode, int32_t t1_pad, int32_t hist_words, int threads) {
+    const bool ring = mode == kModeCount || mode == kModeRows;
+    return fast_fixed_bytes(t1_pad, ring ? hist_words : 0) + (ring ? size_t(kRing) * 4 * threads : 0);
 }
 
 int fast_threads() { return kFastThreads; }
 
 int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
     if (a.end <= a.begin || a.nchunks <= 0) return KS_OK;
-    const bool ring = mode == kModeCount || mode == kModeRows || mode == kModeCountDirect;
+    const bool ring = mode == kModeCount || mode == kModeRows;
     a.hist_smem = ring ? 1 : 0;
-    const int var = effective_variant(a.fast_variant, mode, k);
-    FastFn fn = pick(mode, k, var);
+    FastFn fn = pick(mode, k);
     if (!fn) return fail(KS_E_INVALID, "fast scan: bad mode/stride");
-    size_t smem = variant_fixed_bytes(var, mode, k, a.t1_pad, ring ? a.n_accept : 0);
-    if (mode == kModeCount || mode == kModeRows) {
+    size_t smem = fast_fixed_bytes(a.t1_pad, ring ? a.n_accept : 0);
+    if (ring) {
         a.ring_depth = ring_depth_for(smem, ctx->smem_optin, kFastThreads);
         if (const char* env = std::getenv("KS_RING_DEPTH"))   // tuning knob
             a.ring_depth = std::min(a.ring_depth, std::max(chk_steps(k) + 1, std::atoi(env)));

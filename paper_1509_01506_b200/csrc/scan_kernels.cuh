@@ -27,7 +27,7 @@
 
 namespace ks {
 
-enum ScanMode : int { kModeCount = 0, kModeRows = 1, kModeEmit = 2, kModeMap = 3, kModeCountDirectId = 4 };
+enum ScanMode : int { kModeCount = 0, kModeRows = 1, kModeEmit = 2, kModeMap = 3 };
 
 struct ScanArgs {
     SeqView seq;
@@ -49,7 +49,6 @@ struct ScanArgs {
     int32_t nq = 0, n_accept = 0, reset_state = -1;
     int32_t tk_pad = 0, t1_pad = 0;  // uint16 entries, multiples of 8
     int32_t hist_smem = 0;           // histogram in shared memory
-    int32_t fast_variant = 0;        // fast kernel variant (scan_fast.cu kVar*)
     int32_t ring_depth = 0;          // fast kernel: deferred hits per lane (set by launch_scan_fast)
     // outputs
     unsigned long long* visits = nullptr;   // n_accept, global accumulation
@@ -83,7 +82,6 @@ void chunk_geometry(int64_t begin, int64_t end, int64_t threads, int64_t* origin
 
 // Fast shared-memory kernel for tables with a fast form (csrc/scan_fast.cu).
 int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches);
-size_t variant_smem_bytes(int var, int mode, int k, int32_t t1_pad, int32_t hist_words, int threads);
 size_t fast_smem_bytes(int mode, int32_t t1_pad, int32_t hist_words, int threads);
 int fast_threads();
 

@@ -31,8 +31,6 @@ def main():
         "chunk2k": {"KS_CHUNK_LEN": "2048"},
         "chunk16k": {"KS_CHUNK_LEN": "16384"},
         "generic_k1": {"KS_DISABLE_FAST": "1", "KS_FORCE_STRIDE": "1"},
-        "direct": {"KS_DIRECT": "1"},
-        "ring": {"KS_DIRECT": "0"},
         "chunk64": {"KS_CHUNK_LEN": "64"},
         "chunk128": {"KS_CHUNK_LEN": "128"},
         "chunk256": {"KS_CHUNK_LEN": "256"},
