@@ -400,15 +400,17 @@ class DeviceContext:
 
 
 def _take_rows(rows_p, n: int) -> np.ndarray:
+    """(n, 2) int64 view of library-allocated rows, without a copy: the
+    buffer is handed back to ks_free when the array is garbage collected."""
     lib = library()
-    try:
-        if n == 0:
-            return np.empty((0, 2), dtype=np.int64)
-        arr = np.ctypeslib.as_array(rows_p, shape=(n, 2)).copy()
-        return arr
-    finally:
+    if n == 0 or not rows_p:
         if rows_p:
             lib.ks_free(C.cast(rows_p, _P))
+        return np.empty((0, 2), dtype=np.int64)
+    addr = C.cast(rows_p, C.c_void_p).value
+    holder = (C.c_int64 * (2 * n)).from_address(addr)
+    weakref.finalize(holder, lib.ks_free, C.c_void_p(addr))
+    return np.frombuffer(holder, dtype=np.int64).reshape(n, 2)
 
 
 _contexts: dict[int, DeviceContext] = {}

@@ -433,7 +433,31 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
         a.chunk_entry = centry;
     }
     if (locate) a.chunk_rows = chunk_rows;
-    rc = dispatch(ctx, dfa, dfa->scan, plan, a, locate ? kModeRows : kModeCount, &launches);
+    // locate on the fast kernel: one pass that logs every accepting visit
+    // (position, chunk, rank inside the chunk); rows are scattered from the
+    // log once the chunk offsets are known.  A log overflow falls back to the
+    // two-pass form (row counts, then an emitting re-scan).
+    const int64_t cap = std::max<int64_t>(int64_t(1) << 16, std::min<int64_t>((end - begin) / 64, int64_t(4) << 20));
+    // hit-dense automata (expected visits beyond the log) go straight to two passes
+    const bool use_log = locate && plan.fast && nch > 0 && dfa->scan.hit_rate * double(end - begin) < 0.5 * double(cap);
+    unsigned long long* log_n = nullptr;
+    if (use_log) {
+        const size_t bytes = size_t(cap) * sizeof(LogEntry) + 64;
+        if (ctx->log_bytes < bytes) {
+            KS_CUDA(cudaStreamSynchronize(ctx->stream));
+            if (ctx->log_buf) KS_CUDA(cudaFree(ctx->log_buf));
+            ctx->log_buf = nullptr;
+            ctx->log_bytes = 0;
+            KS_CUDA(cudaMalloc(&ctx->log_buf, bytes));
+            ctx->log_bytes = bytes;
+        }
+        log_n = reinterpret_cast<unsigned long long*>(static_cast<char*>(ctx->log_buf) + size_t(cap) * sizeof(LogEntry));
+        KS_CUDA(cudaMemsetAsync(log_n, 0, 8, ctx->stream));
+        a.log = static_cast<LogEntry*>(ctx->log_buf);
+        a.log_n = log_n;
+        a.log_cap = cap;
+    }
+    rc = dispatch(ctx, dfa, dfa->scan, plan, a, use_log ? kModeLog : locate ? kModeRows : kModeCount, &launches);
     if (rc) return rc;
     KS_CUDA(cudaEventRecord(ev_b, ctx->stream));
     rc = launch_finalize_counts(ctx, visits, h.n_accept, dfa->d_acc_out_off, dfa->d_acc_out_ids, counts,
@@ -452,10 +476,21 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
         rc = exclusive_scan_rows(ctx, chunk_rows, nch, row_off, row_off + nch, rows_tmp, &launches);
         if (rc) return rc;
         KS_CUDA(cudaMemcpyAsync(&total_rows, row_off + nch, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        unsigned long long logged = 0;
+        if (use_log) KS_CUDA(cudaMemcpyAsync(&logged, log_n, 8, cudaMemcpyDeviceToHost, ctx->stream));
         KS_CUDA(cudaStreamSynchronize(ctx->stream));
-        if (total_rows > 0) {
+        if (total_rows > 0 && use_log && logged <= (unsigned long long)a.log_cap) {
+            KS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_rows), size_t(total_rows) * 16, ctx->stream));
+            rc = launch_log_scatter(ctx, a.log, int64_t(logged), row_off, dfa->d_acc_out_off, dfa->d_acc_out_ids,
+                                    d_rows, &launches);
+            if (rc) {
+                cudaFreeAsync(d_rows, ctx->stream);
+                return rc;
+            }
+        } else if (total_rows > 0) {
             KS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_rows), size_t(total_rows) * 16, ctx->stream));
             ScanArgs e = a;
+            e.log = nullptr;
             e.chunk_rows = nullptr;
             e.chunk_row_off = row_off;
             e.rows = d_rows;
@@ -484,8 +519,16 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
             return fail(KS_E_NOMEM, "host allocation of match rows failed");
         }
         if (total_rows > 0) {
-            cudaError_t ce = cudaMemcpyAsync(host_rows, d_rows, size_t(total_rows) * 16,
-                                             cudaMemcpyDeviceToHost, ctx->stream);
+            // large results: page-lock the destination so the copy runs at DMA speed
+            const size_t rbytes = size_t(total_rows) * 16;
+            bool registered = false;
+            if (rbytes >= (size_t(32) << 20))
+                registered = cudaHostRegister(host_rows, rbytes, cudaHostRegisterDefault) == cudaSuccess;
+            cudaError_t ce = cudaMemcpyAsync(host_rows, d_rows, rbytes, cudaMemcpyDeviceToHost, ctx->stream);
+            if (registered) {
+                if (ce == cudaSuccess) ce = cudaStreamSynchronize(ctx->stream);
+                cudaHostUnregister(host_rows);
+            }
             if (ce != cudaSuccess) {
                 std::free(host_rows);
                 cudaFreeAsync(d_rows, ctx->stream);
@@ -892,6 +935,13 @@ int ks_open(int device, ks_ctx** out) {
     }
     c->stream = c->own_stream;
     for (auto& ev : c->ev) cudaEventCreate(&ev);
+    // keep freed stream-ordered allocations (match rows, upload staging) in
+    // the pool instead of returning them to the driver at every sync
+    cudaMemPool_t pool = nullptr;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t keep = 1ull << 32;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     *out = c;
     return KS_OK;
 }
@@ -904,6 +954,7 @@ int ks_close(ks_ctx* ctx) {
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->sbuf) cudaFree(ctx->sbuf);
     if (ctx->spec_buf) cudaFree(ctx->spec_buf);
+    if (ctx->log_buf) cudaFree(ctx->log_buf);
     if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
     delete ctx->pool;
     if (ctx->hstage) cudaFreeHost(ctx->hstage);

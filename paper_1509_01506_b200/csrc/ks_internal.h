@@ -148,6 +148,9 @@ struct ks_ctx {
     // SPECULATE chunk maps (grow-only, separate from `scratch`)
     void* spec_buf = nullptr;
     size_t spec_bytes = 0;
+    // single-pass locate log (grow-only)
+    void* log_buf = nullptr;
+    size_t log_bytes = 0;
     // ks_count_async: one event pair per call until ks_async_wait
     std::vector<cudaEvent_t> aev;
     int n_async = 0;

@@ -101,12 +101,16 @@ struct Ctx {
     int64_t row_base;
     uint32_t n_accept;
     uint32_t ring_thr;  // drain when a lane holds this many ring bytes (depth - chk_steps(K) entries)
+    LogEntry* log;
+    unsigned long long* log_n;
+    int64_t log_cap;
 };
 
 template <int MODE>
 struct Lane {
     uint32_t nrows = 0;
     int64_t cur = 0;
+    uint32_t ch = 0;
 };
 
 template <int MODE>
@@ -121,6 +125,20 @@ __device__ __forceinline__ void record(const Ctx& c, Lane<MODE>& L, int64_t pos,
             r.x = c.row_base + pos + 1;
             r.y = __ldg(&c.ids[k]);
             reinterpret_cast<longlong2*>(c.rows)[L.cur] = r;
+        }
+    } else if constexpr (MODE == kModeLog) {
+        red_shared_add(c.hist + 4u * s, 1u);
+        const uint32_t local = L.nrows;
+        L.nrows += __ldg(&c.outcnt[s]);
+        const unsigned long long i = atomicAdd(c.log_n, 1ull);
+        if (i < (unsigned long long)c.log_cap) {
+            LogEntry e;
+            e.pos1 = c.row_base + pos + 1;
+            e.chunk = L.ch;
+            e.local = local;
+            e.state = s;
+            e.pad = 0;
+            c.log[i] = e;
         }
     }
 }
@@ -208,7 +226,7 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
                 L.nrows += drain_out<K, MODE>(c, rp0, (rp - rp0) / kRingStride);
                 rp = rp0;
             }
-        } else if constexpr (MODE == kModeEmit) {
+        } else if constexpr (MODE == kModeEmit || MODE == kModeLog) {
             if (e & 0x8000u) rewalk<K, MODE>(c, L, a, p0 + K * j);
         }
     }
@@ -230,8 +248,9 @@ extern __shared__ __align__(128) unsigned char f_smem[];
 template <int K, int MODE>
 __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     constexpr bool RING = MODE == kModeCount || MODE == kModeRows;
+    constexpr bool HIST = RING || MODE == kModeLog;
     constexpr int TK_BYTES = 1 << 17;
-    // layout: table | t1 | ring (count/rows) | hist (count/rows)
+    // layout: table | t1 | ring (count/rows) | hist (count/rows/log)
     unsigned char* p_t1 = f_smem + TK_BYTES;
     unsigned char* p_ring = p_t1 + size_t(a.t1_pad) * 2;
     unsigned int* s_hist = reinterpret_cast<unsigned int*>(
@@ -244,7 +263,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
         dst = reinterpret_cast<uint4*>(p_t1);
         for (int i = threadIdx.x; i < a.t1_pad / 8; i += blockDim.x) dst[i] = __ldg(src + i);
     }
-    if constexpr (RING)
+    if constexpr (HIST)
         for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x) s_hist[i] = 0u;
     __syncthreads();
 
@@ -259,6 +278,9 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     c.row_base = a.row_base;
     c.n_accept = opaque(uint32_t(a.n_accept));
     c.ring_thr = uint32_t(a.ring_depth - chk_steps(K)) * kRingStride;
+    c.log = a.log;
+    c.log_n = a.log_n;
+    c.log_cap = a.log_cap;
     const uint32_t sink = uint32_t(a.nq);  // the sink state Z
     const uint32_t ring_stride = kRingStride;
     const uint32_t rp0 = smem_addr(p_ring) + 4u * threadIdx.x;
@@ -309,6 +331,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
         }
         Lane<MODE> L;
         if constexpr (MODE == kModeEmit) L.cur = active ? a.chunk_row_off[ch] : 0;
+        L.ch = uint32_t(ch);
 
         // block k of this unit sits at slot ubase + 32 k
         const int64_t ubase = (t << (5 + lb)) | lane;
@@ -351,7 +374,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                     s = uint32_t(a.reset_state);
                     if constexpr (MODE != kModeMap) {
                         if (s < c.n_accept) {
-                            if constexpr (MODE == kModeEmit) {
+                            if constexpr (MODE == kModeEmit || MODE == kModeLog) {
                                 for (int q = 0; q < 64; ++q) record<MODE>(c, L, p0 + q, s);
                             } else {  // count / rows / direct
                                 red_shared_add(c.hist + 4u * s, 64u);
@@ -381,7 +404,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
         if constexpr (MODE == kModeRows) drain<K, MODE>(c, L, am, rp0, rp, ring_stride);   // rows are per chunk
         if (active) {
             if (a.chunk_exit) a.chunk_exit[ch] = uint16_t(s);
-            if constexpr (MODE == kModeRows) a.chunk_rows[ch] = L.nrows;
+            if constexpr (MODE == kModeRows || MODE == kModeLog) a.chunk_rows[ch] = L.nrows;
             if constexpr (MODE == kModeEmit) {
                 if (L.cur != a.chunk_row_off[ch + 1]) atomicExch(a.error, 1);
             }
@@ -392,7 +415,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
         Lane<MODE> L;
         drain<K, MODE>(c, L, am, rp0, rp, ring_stride);
     }
-    if constexpr (RING) {
+    if constexpr (HIST) {
         __syncthreads();
         for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x)
             if (s_hist[i]) atomicAdd(&a.visits[i], (unsigned long long)s_hist[i]);
@@ -408,8 +431,25 @@ FastFn pick_mode(int mode) {
         case kModeRows: return scan_fast_kernel<K, kModeRows>;
         case kModeEmit: return scan_fast_kernel<K, kModeEmit>;
         case kModeMap: return scan_fast_kernel<K, kModeMap>;
+        case kModeLog: return scan_fast_kernel<K, kModeLog>;
     }
     return nullptr;
+}
+
+__global__ void log_scatter_kernel(const LogEntry* __restrict__ log, int64_t n, const int64_t* __restrict__ row_off,
+                                   const int32_t* __restrict__ off, const int32_t* __restrict__ ids,
+                                   int64_t* __restrict__ rows) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const LogEntry e = log[i];
+        const int64_t base = row_off[e.chunk] + e.local;
+        const int k0 = off[e.state], k1 = off[e.state + 1];
+        for (int k = k0; k < k1; ++k) {
+            longlong2 r;
+            r.x = e.pos1;
+            r.y = ids[k];
+            reinterpret_cast<longlong2*>(rows)[base + (k - k0)] = r;
+        }
+    }
 }
 
 FastFn pick(int mode, int k) {
@@ -441,13 +481,25 @@ size_t fast_smem_bytes(int mode, int32_t t1_pad, int32_t hist_words, int threads
 
 int fast_threads() { return kFastThreads; }
 
+int launch_log_scatter(ks_ctx* ctx, const LogEntry* log, int64_t n, const int64_t* row_off,
+                       const int32_t* acc_out_off, const int32_t* acc_out_ids, int64_t* rows, int* launches) {
+    if (n <= 0) return KS_OK;
+    const int threads = 256;
+    const int blocks = int(max64(1, min64((n + threads - 1) / threads, int64_t(ctx->num_sms) * 8)));
+    log_scatter_kernel<<<blocks, threads, 0, ctx->stream>>>(log, n, row_off, acc_out_off, acc_out_ids, rows);
+    if (launches) ++*launches;
+    KS_CUDA(cudaGetLastError());
+    return KS_OK;
+}
+
 int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
     if (a.end <= a.begin || a.nchunks <= 0) return KS_OK;
     const bool ring = mode == kModeCount || mode == kModeRows;
-    a.hist_smem = ring ? 1 : 0;
+    const bool hist = ring || mode == kModeLog;
+    a.hist_smem = hist ? 1 : 0;
     FastFn fn = pick(mode, k);
     if (!fn) return fail(KS_E_INVALID, "fast scan: bad mode/stride");
-    size_t smem = fast_fixed_bytes(a.t1_pad, ring ? a.n_accept : 0);
+    size_t smem = fast_fixed_bytes(a.t1_pad, hist ? a.n_accept : 0);
     if (ring) {
         a.ring_depth = ring_depth_for(smem, ctx->smem_optin, kFastThreads);
         if (const char* env = std::getenv("KS_RING_DEPTH"))   // tuning knob

@@ -27,7 +27,18 @@
 
 namespace ks {
 
-enum ScanMode : int { kModeCount = 0, kModeRows = 1, kModeEmit = 2, kModeMap = 3 };
+enum ScanMode : int { kModeCount = 0, kModeRows = 1, kModeEmit = 2, kModeMap = 3, kModeLog = 4 };
+
+// One accepting-state visit of a locate pass (kModeLog, fast kernel): where
+// its rows start inside its chunk; log_scatter turns it into rows once the
+// chunk offsets are known.  Single-pass locate while hits fit the log.
+struct LogEntry {
+    int64_t pos1;     // row offset (row_base + position + 1)
+    uint32_t chunk;   // chunk index of the launch
+    uint32_t local;   // rows of this chunk before this visit
+    uint32_t state;   // internal accepting state
+    uint32_t pad;
+};
 
 struct ScanArgs {
     SeqView seq;
@@ -61,6 +72,9 @@ struct ScanArgs {
     int64_t* rows = nullptr;
     int64_t row_base = 0;                   // row offset = position + 1 + row_base
     int32_t* error = nullptr;               // set to 1 on an internal invariant failure
+    LogEntry* log = nullptr;                // kModeLog
+    unsigned long long* log_n = nullptr;    // kModeLog: visits appended (may exceed log_cap)
+    int64_t log_cap = 0;
 };
 
 inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -84,6 +98,9 @@ void chunk_geometry(int64_t begin, int64_t end, int64_t threads, int64_t* origin
 int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches);
 size_t fast_smem_bytes(int mode, int32_t t1_pad, int32_t hist_words, int threads);
 int fast_threads();
+// rows of the logged visits: rows[row_off[chunk] + local + k] = (pos1, id_k)
+int launch_log_scatter(ks_ctx* ctx, const LogEntry* log, int64_t n, const int64_t* row_off,
+                       const int32_t* acc_out_off, const int32_t* acc_out_ids, int64_t* rows, int* launches);
 
 // Prefix scans (csrc/prefix_scan.cu).
 int exclusive_scan_rows(ks_ctx* ctx, const uint32_t* in, int64_t n, int64_t* out_excl,
