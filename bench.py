@@ -320,6 +320,24 @@ def run_ours(args) -> None:
     e2e_s = statistics.median(e2e_times[1:])
     e2e_val = world * n / e2e_s / 1e9  # every rank does the same in parallel
 
+    # configs that also extract match positions (C1, C2, C4): time ks_locate
+    # (count + sorted (offset, id) rows landed in host memory) on the resident
+    # shard; rank-local rows carry global offsets
+    locate = None
+    if args.config in (1, 2, 4):
+        loc_times = []
+        for i in range(4):
+            torch.cuda.synchronize()
+            l0 = time.perf_counter()
+            lc, lrows = ctx.locate(dh, sh)
+            loc_times.append(time.perf_counter() - l0)
+        if world == 1 and (not np.array_equal(lc, ref_counts) or lrows.shape[0] != int(ref_counts.sum())):
+            raise RuntimeError("locate counts differ")
+        loc_s = statistics.median(loc_times[1:])
+        locate = {"value": world * n / loc_s / 1e9, "unit": UNIT, "ms_per_step": loc_s * 1e3,
+                  "rows_per_gpu": int(lrows.shape[0]),
+                  "path": "ks_locate: single-pass visit log + scatter (or rows/emit passes), rows D2H"}
+
     if rank == 0:
         peaks = measured_peaks()
         achieved = n / (scan_ms / 1e3) / 1e9
@@ -352,6 +370,7 @@ def run_ours(args) -> None:
                              "packing the next and scanning the previous; counts D2H"),
                     "host_threads": host_threads()},
             "gpu_launches": launches[0],
+            **({"locate": locate} if locate else {}),
             "clocks": clocks.summary(),
         }
         if not args.no_cpu_baseline:
