@@ -367,6 +367,22 @@ int encode_compact_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, boo
     return KS_OK;
 }
 
+// Whitespace-free encode of a raw piece in place, no host sync: any
+// whitespace sets *ws_flag (the caller then redoes the input on a compacting
+// path).  Used for the raw pieces of the streamed count.
+int encode_raw_piece(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, ks_seq* seq, uint32_t* kept, int* ws_flag,
+                     int* launches) {
+    const int64_t nb = (n_bytes + 63) / 64;
+    seq->n = n_bytes;
+    if (nb == 0) return KS_OK;
+    const int threads = 256;
+    encode_inplace_kernel<<<grid_for(ctx, nb, threads), threads, 0, ctx->stream>>>(
+        d_in, n_bytes, nb, seq->lb, seq->d_bases, seq->d_nmask, seq->d_soft, kept, ws_flag);
+    if (launches) ++*launches;
+    KS_CUDA(cudaGetLastError());
+    return KS_OK;
+}
+
 // Encode n_bytes of device ASCII into seq (whose arrays are sized for n_bytes
 // bases).  Sets seq->n to the retained symbol count (host sync).  Raw input
 // without whitespace is written in place in one pass; anything else takes

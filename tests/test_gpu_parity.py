@@ -340,6 +340,12 @@ def test_count_host_ascii_many_pieces(encode, monkeypatch):
     pinned.numpy()[:] = np.frombuffer(data, dtype=np.uint8)
     assert ctx.count_host_ascii(dh, pinned.numpy()).tolist() == want.tolist()
     assert ctx.count_host_ascii(dh, data).tolist() == want.tolist()   # pageable input too
+    # whitespace only inside a piece that travels raw (pinned input, piece 2):
+    # detected on the device, the call redoes the input on the compacting path
+    pinned.numpy()[2 * piece + 12345] = ord("\n")
+    text = pinned.numpy().tobytes()
+    want_ws = O.ref_sequential_count(w.dfa, ks.encode_bytes(text))[0]
+    assert ctx.count_host_ascii(dh, pinned.numpy()).tolist() == want_ws.tolist()
 
 
 # ---------------------------------------------------------------- multi-GPU building blocks (on one GPU)
