@@ -3,6 +3,7 @@ test_oracle_bench.py).  Harness-logic tests run on CPU; anything that scans
 runs on the GPU (marked)."""
 
 import json
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -179,3 +180,41 @@ def test_pattern_parallel_and_exhaustive(toy_exprs, toy_dfa):
         assert 0 < r["converged_runs"] <= r["speculative_runs"]
     r = ks.exhaustive_reconciliation_check(toy_dfa, 3, window=0)
     assert r["converged_runs"] == 0
+
+
+# ------------------------------------------------------------ reference transcripts
+# tests/golden/cli/cases.json: argv, exit code and stdout of the REAL reference
+# CLI (tests/golden/make_cli_golden.py).  The drop-in must match byte for byte.
+
+GOLDEN_CLI = Path(__file__).resolve().parent / "golden" / "cli"
+
+
+def _cli_cases(pred):
+    cases = json.loads((GOLDEN_CLI / "cases.json").read_text())
+    return [c for c in cases if pred(c)]
+
+
+def _run_case(case, capsys, monkeypatch):
+    monkeypatch.chdir(GOLDEN_CLI)
+    code = cli.main(case["argv"])
+    cap = capsys.readouterr()
+    return code, cap.out, cap.err
+
+
+@pytest.mark.parametrize("case", _cli_cases(lambda c: c["argv"][0] == "dump-dfa" or c["code"] != 0),
+                         ids=lambda c: " ".join(c["argv"][:3]))
+def test_cli_matches_reference_transcript_cpu(case, capsys, monkeypatch):
+    """dump-dfa and the error paths never touch the GPU."""
+    code, out, err = _run_case(case, capsys, monkeypatch)
+    assert code == case["code"] and out == case["stdout"]
+    if case["code"]:
+        assert err == case["stderr"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", _cli_cases(lambda c: c["argv"][0] in ("count", "locate") and c["code"] == 0),
+                         ids=lambda c: " ".join(c["argv"]))
+def test_cli_matches_reference_transcript_gpu(case, capsys, monkeypatch):
+    code, out, err = _run_case(case, capsys, monkeypatch)
+    assert code == 0 and err == ""
+    assert out == case["stdout"]
