@@ -48,6 +48,10 @@ CASES = [
     ["dump-dfa", "--patterns", "pats.txt", "--minimized"],
     ["count", "--patterns", "bad.txt", "--input", "seq.fa"],
     ["count", "--patterns", "pats.txt", "--input", "missing.fa"],
+    ["bench", "--patterns", "pats.txt", "--synthetic-size", "64K", "--workers", "1,3", "--repeat", "2",
+     "--pattern-based"],
+    ["bench", "--patterns", "classes.txt", "--input", "seq.fa", "--workers", "2", "--repeat", "1",
+     "--output-format", "json"],
 ]
 
 

@@ -211,10 +211,27 @@ def test_cli_matches_reference_transcript_cpu(case, capsys, monkeypatch):
         assert err == case["stderr"]
 
 
+def _untimed(argv, text: str):
+    """bench output without its timings (everything else must match)."""
+    if argv[0] != "bench":
+        return text
+    if "--output-format" in argv:
+        doc = json.loads(text)
+        for r in doc["results"]:
+            for k in ("seconds", "median_seconds", "min_seconds"):
+                r.pop(k)
+        return doc
+    keep = []
+    for line in text.splitlines():
+        f = line.split("\t")
+        keep.append(f[:2] if line.startswith("# median") else f[:3] if len(f) == 4 and not line.startswith("#") else f)
+    return keep
+
+
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", _cli_cases(lambda c: c["argv"][0] in ("count", "locate") and c["code"] == 0),
+@pytest.mark.parametrize("case", _cli_cases(lambda c: c["argv"][0] in ("count", "locate", "bench") and c["code"] == 0),
                          ids=lambda c: " ".join(c["argv"]))
 def test_cli_matches_reference_transcript_gpu(case, capsys, monkeypatch):
     code, out, err = _run_case(case, capsys, monkeypatch)
     assert code == 0 and err == ""
-    assert out == case["stdout"]
+    assert _untimed(case["argv"], out) == _untimed(case["argv"], case["stdout"])
