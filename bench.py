@@ -252,6 +252,11 @@ def run_ours(args) -> None:
             dist.all_reduce(counts_dev)
             out_pin.copy_(counts_dev, non_blocking=True)
             return
+        out_np[:ne] = host_step()
+
+    def host_step() -> np.ndarray:
+        """The exchange with host-side composition (gloo dry runs, and the
+        cross-check of the device-composed NCCL path)."""
         m = torch.from_numpy(scanner.segment_map(0, n).astype(np.int64)).to(cdev)
         launches[0] += 1
         dist.all_gather(maps_buf, m)
@@ -262,13 +267,17 @@ def run_ours(args) -> None:
         scan_ms_sum[0] += ctx.stats()["scan_ms"]
         counts_t.copy_(torch.from_numpy(counts))
         dist.all_reduce(counts_t)
-        out_np[:ne] = counts_t.cpu().numpy()
+        return counts_t.cpu().numpy()
 
     scan_ms_sum = [0.0]
     for _ in range(args.warmup):
         step()
     ctx.async_wait()
     ref_counts = out_np[:ne].copy()
+    if world > 1 and args.dist_backend == "nccl":
+        # device-composed entries + NCCL must equal the host-composed exchange
+        if not np.array_equal(host_step(), ref_counts):
+            raise RuntimeError("NCCL path counts differ from the host-composed exchange")
     launches[0] = 0
     scan_ms_sum[0] = 0.0
     ev0 = torch.cuda.Event(enable_timing=True)
