@@ -167,6 +167,14 @@ KS_API int ks_count_host_bytes(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* by
 KS_API int ks_pack_host_ascii(const uint8_t* bytes, int64_t n_bytes, int32_t lb, uint64_t* bases,
                               uint64_t* nmask, int32_t* flags);
 
+/* The host side of the FASTA / whitespace stream on its own (CPU only): the
+ * whole buffer as one task starting at a line start.  Per 64-byte block g:
+ * bases[2g..2g+1] 2-bit codes, special[g] a mask of non-base positions --
+ * code 01 = dropped (whitespace, header line, past the end), code 00 =
+ * OTHER.  *kept = retained symbols. */
+KS_API int ks_pack_host_wire(const uint8_t* bytes, int64_t n_bytes, int32_t fasta, uint64_t* bases,
+                             uint64_t* special, int64_t* kept);
+
 /* Range form used by match_chunk (engine.py:94-134) and by sharded scans:
  * scan positions [begin, end) of seq entering at `entry_state` (original
  * state id; -1 = the true state of the sequence at `begin`, derived on

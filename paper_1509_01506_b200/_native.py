@@ -60,7 +60,7 @@ EXPORTED = (
     "ks_seq_upload_codes", "ks_seq_upload_ascii", "ks_seq_encode_device", "ks_seq_length",
     "ks_seq_download_codes", "ks_seq_download_softmask", "ks_seq_free", "ks_count", "ks_locate",
     "ks_count_host_ascii", "ks_count_async", "ks_async_wait", "ks_segment_map_async",
-    "ks_count_shard_async", "ks_pack_host_ascii", "ks_count_host_bytes",
+    "ks_count_shard_async", "ks_pack_host_ascii", "ks_count_host_bytes", "ks_pack_host_wire",
     "ks_scan_range", "ks_segment_map", "ks_speculate", "ks_free",
 )
 
@@ -100,6 +100,7 @@ def _declare(lib) -> None:
         "ks_count_host_bytes": (C.c_int, [_P, _P, _u8p, C.c_int64, C.c_int32, _i64p]),
         "ks_count_async": (C.c_int, [_P, _P, _P, _i64p]),
         "ks_pack_host_ascii": (C.c_int, [_u8p, C.c_int64, C.c_int32, _P, _P, _i32p]),
+        "ks_pack_host_wire": (C.c_int, [_u8p, C.c_int64, C.c_int32, _P, _P, _i64p]),
         "ks_segment_map_async": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, _P]),
         "ks_count_shard_async": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, _P, C.c_int32, _P]),
         "ks_async_wait": (C.c_int, [_P, C.POINTER(C.c_float), _i32p, _i32p]),
@@ -431,6 +432,20 @@ def pack_host_ascii(data, lb: int) -> tuple[np.ndarray, np.ndarray, int]:
     _check(library().ks_pack_host_ascii(_ptr(buf, C.c_uint8), int(arr.size), int(lb), bases.ctypes.data,
                                         nmask.ctypes.data, C.byref(flags)))
     return bases, nmask, int(flags.value)
+
+
+def pack_host_wire(data, fasta: bool) -> tuple[np.ndarray, np.ndarray, int]:
+    """Host side of the FASTA/whitespace stream (no GPU needed): (bases
+    uint64[2*blocks], special uint64[blocks], retained symbols)."""
+    arr = np.ascontiguousarray(np.frombuffer(bytes(data), dtype=np.uint8))
+    nb = max((arr.size + 63) // 64, 1)
+    bases = np.zeros(2 * nb, dtype=np.uint64)
+    special = np.zeros(nb, dtype=np.uint64)
+    kept = C.c_int64()
+    buf = arr if arr.size else np.zeros(1, dtype=np.uint8)
+    _check(library().ks_pack_host_wire(_ptr(buf, C.c_uint8), int(arr.size), int(bool(fasta)), bases.ctypes.data,
+                                       special.ctypes.data, C.byref(kept)))
+    return bases, special, int(kept.value)
 
 
 def context(device: int = 0) -> DeviceContext:

@@ -45,6 +45,8 @@ int encode_ascii_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, bool 
                         int* launches);
 int pack_codes_device(ks_ctx* ctx, const uint8_t* d_codes, int64_t n, ks_seq* seq, int* d_flag,
                       int* launches);
+int wire_compact_device(ks_ctx* ctx, const uint64_t* d_lin, const uint64_t* d_special, int64_t n_blocks, ks_seq* seq,
+                        uint32_t* kept, int64_t* pos, void* tmp, int64_t* d_total, int* launches);
 int encode_raw_piece(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, ks_seq* seq, uint32_t* kept, int* ws_flag,
                      int* launches);
 int scatter_tile_masks_device(ks_ctx* ctx, const uint64_t* d_compact, const int32_t* d_ids, int n_tiles,
@@ -675,8 +677,12 @@ void seq_destroy(ks_seq* s) {
 //    device -- compacted and scanned.  One host sync per piece reads the
 //    piece's retained length for the scan geometry; the next piece's copy is
 //    already queued, so the link never idles.
+enum StreamMode { kStreamPacked = 0, kStreamWire = 1, kStreamDevice = 2 };
+
 int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int64_t n_bytes, bool fasta,
-                      bool host_pack, int64_t* counts_out, bool* fallback) {
+                      int stream_mode, int64_t* counts_out, bool* fallback) {
+    const bool host_pack = stream_mode == kStreamPacked;
+    const bool wire = stream_mode == kStreamWire;
     const HostDfa& h = dfa->host;
     *fallback = false;
     // piece size: 64 MiB; KS_PIECE_KB overrides (tests use small pieces to cross many boundaries)
@@ -706,7 +712,8 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
     auto raw_piece = [&](int64_t i) { return raw_every > 0 && (i % raw_every) == raw_every - 2; };
     const size_t in_bytes = host_pack ? up(std::max(size_t(slots) * 8 + size_t(ntiles) * 4 + 64,
                                                     raw_every > 0 ? size_t(piece) + 64 : size_t(0)))
-                                      : up(size_t(piece) + 64);
+                            : wire ? up(size_t(blocks) * 24 + 64)   // linear codes + special masks
+                                   : up(size_t(piece) + 64);
     const size_t seq_bytes = up(size_t(slots) * 32);
     const size_t need = 2 * (in_bytes + seq_bytes);
     if (ctx->sbuf_bytes < need) {
@@ -723,15 +730,15 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
         for (auto& e : ctx->hev) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     // staging slot: bases (16 B per block slot), compacted OTHER bitmaps (<= 8 B per slot), tile ids
-    const size_t wire = up(size_t(slots) * 24 + size_t(ntiles) * 4);
-    if (host_pack) {
-        if (ctx->hstage_bytes < 3 * wire) {
+    const size_t stage = wire ? up(size_t(blocks) * 24) : up(size_t(slots) * 24 + size_t(ntiles) * 4);
+    if (host_pack || wire) {
+        if (ctx->hstage_bytes < 3 * stage) {
             KS_CUDA(cudaStreamSynchronize(ctx->copy_stream));
             if (ctx->hstage) KS_CUDA(cudaFreeHost(ctx->hstage));
             ctx->hstage = nullptr;
             ctx->hstage_bytes = 0;
-            KS_CUDA(cudaMallocHost(&ctx->hstage, 3 * wire));
-            ctx->hstage_bytes = 3 * wire;
+            KS_CUDA(cudaMallocHost(&ctx->hstage, 3 * stage));
+            ctx->hstage_bytes = 3 * stage;
         }
         if (!ctx->pool) ctx->pool = new HostPool(host_pack_threads());
     }
@@ -755,7 +762,8 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
     size_t scratch = size_t(h.n_accept) * 8 + size_t(std::max(h.ne, 1)) * 8 + size_t(nch_max) * 2 + 16 * kAlign;
     if (mapscan) scratch += size_t(nch_max) * 6 + exclusive_scan_monoid_tmp_bytes(nch_max) + 4 * kAlign;
     if (spec) scratch += size_t(nch_max) * 2 + 2 * kAlign;
-    if (!host_pack) scratch += encode_scratch_bytes(piece) + 2 * kAlign;
+    if (stream_mode == kStreamDevice) scratch += encode_scratch_bytes(piece) + 2 * kAlign;
+    if (wire) scratch += size_t(blocks + 1) * 12 + exclusive_scan_rows_tmp_bytes(blocks + 1) + 4 * kAlign;
     if (raw_every > 0) scratch += size_t(blocks + 1) * 4 + 2 * kAlign;
     int rc = ensure_scratch(ctx, scratch, &ar);
     if (rc) return rc;
@@ -765,7 +773,10 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
     uint16_t* state = static_cast<uint16_t*>(ar.take(16));
     int* d_carry = static_cast<int*>(ar.take(16));           // FASTA line state between pieces
     int64_t* d_total = static_cast<int64_t*>(ar.take(16));   // retained symbols of the piece
-    void* enc_scratch = host_pack ? nullptr : ar.take(encode_scratch_bytes(piece));
+    void* enc_scratch = stream_mode == kStreamDevice ? ar.take(encode_scratch_bytes(piece)) : nullptr;
+    uint32_t* w_kept = wire ? static_cast<uint32_t*>(ar.take(size_t(blocks + 1) * 4)) : nullptr;
+    int64_t* w_pos = wire ? static_cast<int64_t*>(ar.take(size_t(blocks + 1) * 8)) : nullptr;
+    void* w_tmp = wire ? ar.take(exclusive_scan_rows_tmp_bytes(blocks + 1)) : nullptr;
     uint32_t* kept = raw_every > 0 ? static_cast<uint32_t*>(ar.take(size_t(blocks + 1) * 4)) : nullptr;
     int* ws_flag = static_cast<int*>(ar.take(16));           // raw pieces of the host-pack stream
     uint16_t *elems = nullptr, *excl = nullptr, *centry = nullptr, *mtot = nullptr;
@@ -794,6 +805,7 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
     const ScanPlan plan = plan_for(ctx, dfa, dfa->scan);
     int launches = 0;
     int64_t h2d = 2;   // the entry state
+    int line_state = 0;   // wire mode, FASTA: line state before the next piece (input start = line start)
     int64_t d2h = 0;
     auto issue_raw_copy = [&](int64_t i) -> int {   // device-encode mode: raw piece i -> din[i % 2]
         const int b = int(i & 1);
@@ -805,7 +817,7 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
         h2d += len;
         return KS_OK;
     };
-    if (!host_pack && npieces > 0) {
+    if (stream_mode == kStreamDevice && npieces > 0) {
         rc = issue_raw_copy(0);
         if (rc) return rc;
     }
@@ -824,7 +836,7 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
             if (rc) return rc;
         } else if (host_pack) {
             const int st = int(i % 3);
-            uint64_t* hb = reinterpret_cast<uint64_t*>(static_cast<char*>(ctx->hstage) + st * wire);
+            uint64_t* hb = reinterpret_cast<uint64_t*>(static_cast<char*>(ctx->hstage) + st * stage);
             uint64_t* hn = hb + 2 * slots;
             int32_t* hid = reinterpret_cast<int32_t*>(hn + slots);
             if (i >= 3) KS_CUDA(cudaEventSynchronize(ctx->hev[st]));   // staging slot free again
@@ -864,6 +876,53 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
             KS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->sev[b], 0));
             rc = scatter_tile_masks_device(ctx, d_comp, d_ids, nc, int(tile_blocks), pseq[b].d_nmask, &launches);
             if (rc) return rc;
+        } else if (wire) {
+            const int st = int(i % 3);
+            const int64_t nbk = (len + 63) / 64;
+            char* sp = static_cast<char*>(ctx->hstage) + st * stage;
+            uint64_t* hb = reinterpret_cast<uint64_t*>(sp);
+            uint64_t* hs = reinterpret_cast<uint64_t*>(sp + size_t(nbk) * 16);
+            if (i >= 3) KS_CUDA(cudaEventSynchronize(ctx->hev[st]));   // staging slot free again
+            // 256 KiB of input per task (KS_WIRE_TASK_BLOCKS: tests cut tasks small)
+            const char* tb = std::getenv("KS_WIRE_TASK_BLOCKS");
+            const int64_t kTaskBlocks = tb && std::atoll(tb) > 0 ? std::atoll(tb) : 4096;
+            const int64_t ntask = (nbk + kTaskBlocks - 1) / kTaskBlocks;
+            std::vector<WireTask> res(static_cast<size_t>(ntask));
+            const uint8_t* src = bytes + off;
+            const int first_state = line_state;
+            ctx->pool->run(ntask, [&](int64_t t) {
+                const int64_t b0 = t * kTaskBlocks, b1 = std::min(nbk, b0 + kTaskBlocks);
+                int ss = 1;
+                if (fasta) {
+                    if (t == 0) ss = first_state;
+                    else ss = (src[(b0 << 6) - 1] == '\n' || src[(b0 << 6) - 1] == '\r') ? 0 : -1;
+                }
+                res[size_t(t)] = pack_wire_task(src, len, b0, b1, fasta, ss, hb, hs);
+            });
+            // resolve the tasks that assumed "sequence line" at their start
+            int64_t kept = 0;
+            for (int64_t t = 0; t < ntask; ++t) {
+                WireTask& r = res[size_t(t)];
+                if (!r.exact && line_state == 2) {
+                    const int64_t b0 = t * kTaskBlocks, b1 = std::min(nbk, b0 + kTaskBlocks);
+                    wire_drop_prefix(b0, b1, r.first_term, hb, hs);
+                    r.kept -= r.prefix_kept;
+                }
+                kept += r.kept;
+                if (r.exact || r.first_term >= 0) line_state = r.end_state;
+            }
+            const size_t wire_bytes = size_t(nbk) * 24;
+            KS_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->sev[2 + b], 0));
+            KS_CUDA(cudaMemcpyAsync(din[b], sp, wire_bytes, cudaMemcpyHostToDevice, ctx->copy_stream));
+            h2d += int64_t(wire_bytes);
+            KS_CUDA(cudaEventRecord(ctx->hev[st], ctx->copy_stream));
+            KS_CUDA(cudaEventRecord(ctx->sev[b], ctx->copy_stream));
+            KS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->sev[b], 0));
+            const uint64_t* d_lin = reinterpret_cast<const uint64_t*>(din[b]);
+            rc = wire_compact_device(ctx, d_lin, d_lin + 2 * nbk, nbk, &pseq[b], w_kept, w_pos, w_tmp, d_total,
+                                     &launches);
+            if (rc) return rc;
+            nsym = kept;
         } else {
             if (i + 1 < npieces) {   // keep the link busy: the next piece's copy goes first
                 rc = issue_raw_copy(i + 1);
@@ -911,7 +970,7 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
             if (rc) return rc;
             KS_CUDA(cudaMemcpyAsync(state, chunk_exit + (nch - 1), 2, cudaMemcpyDeviceToDevice, ctx->stream));
         }
-        if (host_pack) KS_CUDA(cudaEventRecord(ctx->sev[2 + b], ctx->stream));  // device buffer b consumed
+        if (host_pack || wire) KS_CUDA(cudaEventRecord(ctx->sev[2 + b], ctx->stream));  // device buffer b consumed
     }
     rc = launch_finalize_counts(ctx, visits, h.n_accept, dfa->d_acc_out_off, dfa->d_acc_out_ids, counts,
                                 nullptr, nullptr, &launches);
@@ -1320,6 +1379,15 @@ int ks_pack_host_ascii(const uint8_t* bytes, int64_t n_bytes, int32_t lb, uint64
     return KS_OK;
 }
 
+int ks_pack_host_wire(const uint8_t* bytes, int64_t n_bytes, int32_t fasta, uint64_t* bases, uint64_t* special,
+                      int64_t* kept) {
+    if (n_bytes < 0 || (n_bytes > 0 && (!bytes || !bases || !special)) || !kept)
+        return fail(KS_E_INVALID, "bad argument");
+    const WireTask t = pack_wire_task(bytes, n_bytes, 0, (n_bytes + 63) / 64, fasta != 0, 0, bases, special);
+    *kept = t.kept;
+    return KS_OK;
+}
+
 int ks_count_host_bytes(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int64_t n_bytes, int32_t fasta,
                         int64_t* counts_out) {
     if (!ctx || !dfa || !counts_out || n_bytes < 0 || (n_bytes > 0 && !bytes))
@@ -1333,13 +1401,15 @@ int ks_count_host_bytes(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, in
     ctx->stats = ks_stats{};
     KS_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
     bool fallback = false;
-    const bool host_pack = !fasta && std::getenv("KS_DEVICE_ENCODE") == nullptr;
-    int rc = stream_count_impl(ctx, dfa, bytes, n_bytes, fasta != 0, host_pack, counts_out, &fallback);
+    const bool device_encode = std::getenv("KS_DEVICE_ENCODE") != nullptr;
+    const int second = device_encode ? kStreamDevice : kStreamWire;   // input with whitespace / FASTA
+    const int first = fasta ? second : device_encode ? kStreamDevice : kStreamPacked;
+    int rc = stream_count_impl(ctx, dfa, bytes, n_bytes, fasta != 0, first, counts_out, &fallback);
     if (rc) return rc;
     if (fallback) {  // whitespace in raw input: the device-encode stream compacts it
         ctx->stats = ks_stats{};
         KS_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
-        rc = stream_count_impl(ctx, dfa, bytes, n_bytes, false, false, counts_out, &fallback);
+        rc = stream_count_impl(ctx, dfa, bytes, n_bytes, false, second, counts_out, &fallback);
         if (rc) return rc;
     }
     KS_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));

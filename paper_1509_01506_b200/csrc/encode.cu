@@ -423,6 +423,78 @@ int encode_ascii_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, bool 
     return KS_OK;
 }
 
+// Host wire form (host_pack.h pack_wire_task): per 64-byte block 2 words of
+// 2-bit codes and a special mask; a special position with code 01 is
+// dropped, with code 00 it is OTHER.  Blocks are compacted into the
+// tile-slot layout like encode_compact_kernel does for ASCII.
+__device__ __forceinline__ uint64_t even_bits(uint64_t w) {   // bit 2i of w -> bit i
+    uint64_t x = w & 0x5555555555555555ull;
+    x = (x | (x >> 1)) & 0x3333333333333333ull;
+    x = (x | (x >> 2)) & 0x0F0F0F0F0F0F0F0Full;
+    x = (x | (x >> 4)) & 0x00FF00FF00FF00FFull;
+    x = (x | (x >> 8)) & 0x0000FFFF0000FFFFull;
+    x = (x | (x >> 16)) & 0x00000000FFFFFFFFull;
+    return x;
+}
+
+__device__ __forceinline__ uint64_t wire_drop(const uint64_t* lin, const uint64_t* special, int64_t b) {
+    return special[b] & (even_bits(lin[2 * b]) | (even_bits(lin[2 * b + 1]) << 32));
+}
+
+__global__ void wire_kept_kernel(const uint64_t* __restrict__ lin, const uint64_t* __restrict__ special,
+                                 int64_t n_blocks, uint32_t* kept) {
+    for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < n_blocks;
+         b += int64_t(gridDim.x) * blockDim.x)
+        kept[b] = 64u - uint32_t(__popcll(wire_drop(lin, special, b)));
+}
+
+__global__ void wire_compact_kernel(const uint64_t* __restrict__ lin, const uint64_t* __restrict__ special,
+                                    int64_t n_blocks, const int64_t* pos, int lb, uint64_t* bases, uint64_t* nmask) {
+    for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < n_blocks;
+         b += int64_t(gridDim.x) * blockDim.x) {
+        const uint64_t w0 = lin[2 * b], w1 = lin[2 * b + 1];
+        const uint64_t drop = wire_drop(lin, special, b);
+        const uint64_t oth = special[b] & ~drop;
+        uint64_t keep = ~drop;
+        uint64_t r0 = 0, r1 = 0, rn = 0;
+        int o = 0;
+        while (keep) {
+            const int i = __ffsll(keep) - 1;
+            keep &= keep - 1;
+            const uint64_t code = ((oth >> i) & 1ull) ? 0ull : (i < 32 ? w0 >> (2 * i) : w1 >> (2 * (i - 32))) & 3u;
+            if (o < 32) r0 |= code << (2 * o);
+            else r1 |= code << (2 * (o - 32));
+            rn |= ((oth >> i) & 1ull) << o;
+            ++o;
+        }
+        const int64_t p = pos[b];
+        or_bits(bases, 2 * p, r0, std::min(64, 2 * o), 2, lb);
+        if (o > 32) or_bits(bases, 2 * p + 64, r1, 2 * (o - 32), 2, lb);
+        or_bits(nmask, p, rn, o, 1, lb);
+    }
+}
+
+// Compact n_blocks wire blocks into seq (bases + nmask; soft-mask untouched).
+// `kept`/`pos`/`tmp` are scratch of n_blocks + 1 entries and the rows scan.
+int wire_compact_device(ks_ctx* ctx, const uint64_t* d_lin, const uint64_t* d_special, int64_t n_blocks, ks_seq* seq,
+                        uint32_t* kept, int64_t* pos, void* tmp, int64_t* d_total, int* launches) {
+    if (n_blocks <= 0) return KS_OK;
+    const int threads = 256;
+    const int grid = grid_for(ctx, n_blocks, threads);
+    wire_kept_kernel<<<grid, threads, 0, ctx->stream>>>(d_lin, d_special, n_blocks, kept);
+    KS_CUDA(cudaGetLastError());
+    int rc = exclusive_scan_rows(ctx, kept, n_blocks, pos, d_total, tmp, launches);
+    if (rc != KS_OK) return rc;
+    const size_t words = size_t(seq->n_blocks);
+    KS_CUDA(cudaMemsetAsync(seq->d_bases, 0, words * 16, ctx->stream));
+    KS_CUDA(cudaMemsetAsync(seq->d_nmask, 0, words * 8, ctx->stream));
+    wire_compact_kernel<<<grid, threads, 0, ctx->stream>>>(d_lin, d_special, n_blocks, pos, seq->lb, seq->d_bases,
+                                                           seq->d_nmask);
+    KS_CUDA(cudaGetLastError());
+    if (launches) *launches += 2;
+    return KS_OK;
+}
+
 // Host-packed wire format (host_pack.h): OTHER bitmaps arrive only for the
 // tiles that hold OTHER, compacted; one CTA copies each into place.
 __global__ void scatter_tile_masks_kernel(const uint64_t* __restrict__ compact, const int32_t* __restrict__ ids,

@@ -230,6 +230,186 @@ void stream_copy(void* dst, const void* src, size_t bytes) {
 
 }  // namespace
 
+// ------------------------------------------------------------ wire format for compaction on the device
+
+namespace {
+
+struct BlockMasks {
+    uint64_t w0, w1;   // 2-bit codes of all 64 bytes (non-bases 0)
+    uint64_t base, ws, term, gt;
+};
+
+inline void block_masks_scalar(const uint8_t* p, int lim, BlockMasks* m) {
+    uint64_t w0 = 0, w1 = 0, base = 0, ws = 0, term = 0, gt = 0;
+    for (int i = 0; i < lim; ++i) {
+        const uint8_t x = p[i];
+        const uint8_t c = kLut.v[x];
+        const uint64_t bit = uint64_t(1) << i;
+        if (!(c & 12)) {
+            base |= bit;
+            if (i < 32) w0 |= uint64_t(c & 3) << (2 * i);
+            else w1 |= uint64_t(c & 3) << (2 * (i - 32));
+        }
+        if (c & 8) ws |= bit;
+        if (x == '\n' || x == '\r') term |= bit;
+        if (x == '>') gt |= bit;
+    }
+    *m = BlockMasks{w0, w1, base, ws, term, gt};
+}
+
+// Spread the 32 bits of v to the even bit positions of a 64-bit word.
+inline uint64_t spread_even(uint32_t v) {
+    uint64_t x = v;
+    x = (x | (x << 16)) & 0x0000FFFF0000FFFFull;
+    x = (x | (x << 8)) & 0x00FF00FF00FF00FFull;
+    x = (x | (x << 4)) & 0x0F0F0F0F0F0F0F0Full;
+    x = (x | (x << 2)) & 0x3333333333333333ull;
+    x = (x | (x << 1)) & 0x5555555555555555ull;
+    return x;
+}
+
+// Mark dropped positions: code 01 and the special bit.
+inline void mark_dropped(uint64_t d, uint64_t* w0, uint64_t* w1, uint64_t* sp) {
+    const uint64_t m0 = spread_even(uint32_t(d)), m1 = spread_even(uint32_t(d >> 32));
+    *w0 = (*w0 & ~(m0 * 3)) | m0;
+    *w1 = (*w1 & ~(m1 * 3)) | m1;
+    *sp |= d;
+}
+
+// Header bytes of a block: from each line start holding '>' up to the next
+// line terminator -- one carry chain per header run (F + S).  Updates the
+// line state across the block.
+inline uint64_t header_mask(const BlockMasks& m, uint64_t valid, int lim, bool* at_ls, bool* in_hdr) {
+    const uint64_t F = ~m.term & valid;
+    const uint64_t ls = (m.term << 1) | (*at_ls ? 1u : 0u);
+    const uint64_t S = (ls & m.gt & F) | (*in_hdr ? 1u : 0u);
+    const uint64_t hdr = ((F + S) ^ F) & F;
+    *at_ls = (m.term >> (lim - 1)) & 1;
+    *in_hdr = (hdr >> (lim - 1)) & 1;
+    return hdr;
+}
+
+inline int popc64(uint64_t v) { return __builtin_popcountll(v); }
+
+// Per-block bookkeeping shared by both task loops: returns the drop mask.
+struct WireLoop {
+    WireTask t;
+    bool at_ls, in_hdr;
+    bool fasta;
+    explicit WireLoop(bool fa, int start_state) : at_ls(start_state == 0), in_hdr(start_state == 2), fasta(fa) {
+        t.exact = start_state >= 0;
+    }
+    inline uint64_t drop_of(const BlockMasks& m, int lim) {
+        const uint64_t valid = lim == 64 ? ~uint64_t(0) : (uint64_t(1) << lim) - 1;
+        const uint64_t hdr = fasta && lim > 0 ? header_mask(m, valid, lim, &at_ls, &in_hdr) : 0;
+        return m.ws | hdr | ~valid;
+    }
+    inline void account(const BlockMasks& m, uint64_t d, int64_t b) {
+        const int k = 64 - popc64(d);
+        t.kept += k;
+        if (fasta && !t.exact && t.first_term < 0) {
+            if (m.term) {
+                const int ft = __builtin_ctzll(m.term);
+                t.first_term = (b << 6) + ft;
+                t.prefix_kept += popc64(~d & ((uint64_t(1) << ft) - 1));
+            } else {
+                t.prefix_kept += k;
+            }
+        }
+    }
+    inline WireTask finish() {
+        t.end_state = at_ls ? 0 : in_hdr ? 2 : 1;
+        return t;
+    }
+};
+
+WireTask wire_task_scalar(const uint8_t* in, int64_t n_bytes, int64_t b0, int64_t b1, bool fasta, int start_state,
+                          uint64_t* bases, uint64_t* special) {
+    WireLoop L(fasta, start_state);
+    for (int64_t b = b0; b < b1; ++b) {
+        const int lim = int(std::max<int64_t>(0, std::min<int64_t>(64, n_bytes - (b << 6))));
+        BlockMasks m;
+        block_masks_scalar(in + (b << 6), lim, &m);
+        const uint64_t d = L.drop_of(m, lim);
+        uint64_t w0 = m.w0, w1 = m.w1, sp = ~m.base;
+        if (d) mark_dropped(d, &w0, &w1, &sp);
+        bases[2 * b] = w0;
+        bases[2 * b + 1] = w1;
+        special[b] = sp;
+        L.account(m, d, b);
+    }
+    return L.finish();
+}
+
+// AVX-512 classification (the nibble LUTs of pack_avx512), BMI2 pdep to
+// mark dropped codes, streaming stores (the staging is only read by the DMA).
+__attribute__((target("avx512f,avx512bw,bmi2"))) WireTask wire_task_avx512(const uint8_t* in, int64_t n_bytes,
+                                                                            int64_t b0, int64_t b1, bool fasta,
+                                                                            int start_state, uint64_t* bases,
+                                                                            uint64_t* special) {
+    WireLoop L(fasta, start_state);
+    const __m512i kf = _mm512_set1_epi8(0x0f), k2 = _mm512_set1_epi8(0x02);
+    const __m512i lut_base = _mm512_broadcast_i32x4(_mm_setr_epi8(-1, 6, -1, 6, 7, -1, -1, 6, -1, -1, -1, -1, -1, -1, -1, -1));
+    const __m512i lut_code = _mm512_broadcast_i32x4(_mm_setr_epi8(0, 0, 1, 1, 3, 3, 2, 2, 2, 2, 3, 3, 1, 1, 0, 0));
+    const __m512i lut_ws = _mm512_broadcast_i32x4(_mm_setr_epi8(2, -1, -1, -1, -1, -1, -1, -1, -1, 0, 0, -1, -1, 0, -1, -1));
+    const __m512i m16 = _mm512_set1_epi16(0x0401), m32 = _mm512_set1_epi32(0x00100001);
+    const __m512i klf = _mm512_set1_epi8('\n'), kcr = _mm512_set1_epi8('\r'), kgt = _mm512_set1_epi8('>');
+    for (int64_t b = b0; b < b1; ++b) {
+        const int lim = int(std::max<int64_t>(0, std::min<int64_t>(64, n_bytes - (b << 6))));
+        BlockMasks m;
+        if (lim == 64) {
+            const uint8_t* p = in + (b << 6);
+            _mm_prefetch(reinterpret_cast<const char*>(p + 8192), _MM_HINT_T0);
+            const __m512i x = _mm512_loadu_si512(p);
+            const __m512i lo = _mm512_and_si512(x, kf);
+            const __m512i hi4 = _mm512_and_si512(_mm512_srli_epi16(x, 4), kf);
+            const __mmask64 base = _mm512_cmpeq_epi8_mask(_mm512_shuffle_epi8(lut_base, lo), _mm512_or_si512(hi4, k2));
+            const __mmask64 ws = _mm512_cmpeq_epi8_mask(_mm512_shuffle_epi8(lut_ws, lo), hi4);
+            const __mmask64 term = _mm512_cmpeq_epi8_mask(x, klf) | _mm512_cmpeq_epi8_mask(x, kcr);
+            const __mmask64 gt = _mm512_cmpeq_epi8_mask(x, kgt);
+            const __m512i code = _mm512_maskz_mov_epi8(base, _mm512_shuffle_epi8(lut_code, lo));
+            const __m128i packed = _mm512_cvtepi32_epi8(_mm512_madd_epi16(_mm512_maddubs_epi16(code, m16), m32));
+            m = BlockMasks{uint64_t(_mm_cvtsi128_si64(packed)), uint64_t(_mm_extract_epi64(packed, 1)),
+                           uint64_t(base), uint64_t(ws), uint64_t(term), uint64_t(gt)};
+        } else {
+            block_masks_scalar(in + (b << 6), lim, &m);
+        }
+        const uint64_t d = L.drop_of(m, lim);
+        uint64_t w0 = m.w0, w1 = m.w1, sp = ~m.base;
+        if (d) {
+            const uint64_t m0 = _pdep_u64(d, 0x5555555555555555ull);
+            const uint64_t m1 = _pdep_u64(d >> 32, 0x5555555555555555ull);
+            w0 = (w0 & ~(m0 * 3)) | m0;
+            w1 = (w1 & ~(m1 * 3)) | m1;
+            sp |= d;
+        }
+        _mm_stream_si64(reinterpret_cast<long long*>(bases + 2 * b), (long long)w0);
+        _mm_stream_si64(reinterpret_cast<long long*>(bases + 2 * b + 1), (long long)w1);
+        _mm_stream_si64(reinterpret_cast<long long*>(special + b), (long long)sp);
+        L.account(m, d, b);
+    }
+    _mm_sfence();
+    return L.finish();
+}
+
+}  // namespace
+
+WireTask pack_wire_task(const uint8_t* in, int64_t n_bytes, int64_t b0, int64_t b1, bool fasta, int start_state,
+                        uint64_t* bases, uint64_t* special) {
+    static const bool simd = has_avx512bw() && __builtin_cpu_supports("bmi2");
+    return simd ? wire_task_avx512(in, n_bytes, b0, b1, fasta, start_state, bases, special)
+                : wire_task_scalar(in, n_bytes, b0, b1, fasta, start_state, bases, special);
+}
+
+void wire_drop_prefix(int64_t b0, int64_t b1, int64_t first_term, uint64_t* bases, uint64_t* special) {
+    const int64_t end = first_term < 0 ? (b1 << 6) : first_term;
+    for (int64_t b = b0; b < b1 && (b << 6) < end; ++b) {
+        const int64_t upto = std::min<int64_t>(64, end - (b << 6));
+        const uint64_t d = upto == 64 ? ~uint64_t(0) : (uint64_t(1) << upto) - 1;
+        mark_dropped(d, &bases[2 * b], &bases[2 * b + 1], &special[b]);
+    }
+}
+
 PackFlags pack_ascii_tiles(const uint8_t* in, int64_t n_bytes, int64_t t0, int64_t t1, int lb,
                            uint64_t* bases, uint64_t* nm_compact, int32_t* tile_ids,
                            std::atomic<int32_t>* n_compact) {

@@ -64,4 +64,26 @@ PackFlags pack_ascii_tiles(const uint8_t* in, int64_t n_bytes, int64_t t0, int64
                            uint64_t* bases, uint64_t* nm_compact, int32_t* tile_ids,
                            std::atomic<int32_t>* n_compact);
 
+// Wire form for input with whitespace or FASTA headers (the device
+// compacts, encode.cu wire_compact_kernel): blocks [b0, b1) of `in` in
+// linear order, 24 B per 64 input bytes -- 2 words of 2-bit codes and a
+// "special" mask.  A special position is OTHER when its code is 00 and
+// dropped (whitespace, header line, past the end) when its code is 01.
+// start_state: the line state before block b0 when known (0 line start,
+// 1 sequence line, 2 header line), else -1: then the task assumes "sequence
+// line" and reports what its first line contributed, so the caller can drop
+// it once the true state is resolved.
+struct WireTask {
+    int64_t kept = 0;          // retained symbols
+    int64_t prefix_kept = 0;   // of them, before the first line terminator (assumed start only)
+    int64_t first_term = -1;   // byte index of the first line terminator (assumed start only), -1 none
+    int end_state = 1;         // line state after the last byte
+    bool exact = true;         // the start state was known
+};
+WireTask pack_wire_task(const uint8_t* in, int64_t n_bytes, int64_t b0, int64_t b1, bool fasta, int start_state,
+                        uint64_t* bases, uint64_t* special);
+// The assumed start was a header line after all: drop everything before the
+// first terminator (or all of [b0, b1) when there is none).
+void wire_drop_prefix(int64_t b0, int64_t b1, int64_t first_term, uint64_t* bases, uint64_t* special);
+
 }  // namespace ks

@@ -454,6 +454,28 @@ def test_count_host_bytes_streams_fasta_and_whitespace(piece_kb, fmt, monkeypatc
     assert np.array_equal(rows, ref)
 
 
+@pytest.mark.parametrize("task_blocks,piece_kb", [(1, 7), (2, 64), (3, 1), (4096, 64 * 1024)])
+@pytest.mark.parametrize("encode", ["host", "device"])
+def test_fasta_stream_tasks_and_pieces(task_blocks, piece_kb, encode, monkeypatch):
+    """Host wire packing of FASTA: tiny tasks so that header lines, CRLF pairs
+    and sequence lines straddle task and piece boundaries; a header line
+    longer than a task; a file that does not end with a newline."""
+    monkeypatch.setenv("KS_WIRE_TASK_BLOCKS", str(task_blocks))
+    monkeypatch.setenv("KS_PIECE_KB", str(piece_kb))
+    if encode == "device":
+        monkeypatch.setenv("KS_DEVICE_ENCODE", "1")
+    rng = np.random.default_rng(task_blocks * 7 + piece_kb)
+    data = (_random_fasta(rng, 25, 61) + b">" + b"h" * 700 + b"\r\n" + _random_fasta(rng, 10, 200) +
+            b"acgt\r>not a header\racgtNN>x\n\n>last header, no newline")
+    w = workloads.make(3, 4096)
+    ctx = _native.context(0)
+    dh = ctx.dfa(w.dfa)
+    want = O.ref_sequential_count(w.dfa, _fasta_expected(data))[0]
+    assert ctx.count_host_ascii(dh, data, fasta=True).tolist() == want.tolist()
+    want_raw = O.ref_sequential_count(w.dfa, ks.encode_bytes(data))[0]
+    assert ctx.count_host_ascii(dh, data).tolist() == want_raw.tolist()
+
+
 def test_load_sequence_device_matches_host(tmp_path):
     rng = np.random.default_rng(7)
     for name, fmt in (("a.fa", "fasta"), ("b.txt", "raw")):

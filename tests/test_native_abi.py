@@ -126,3 +126,53 @@ def test_host_packer_matches_wire_format(n, lb, alphabet, scalar, monkeypatch):
     slots = [_blk_slot(g, lb) for g in range(nblk)]
     assert np.array_equal(got[1][slots], want[1][slots])
     assert np.array_equal(got[0].reshape(-1, 2)[slots], want[0].reshape(-1, 2)[slots])
+
+
+def _wire_decode(bases, special, n_bytes):
+    """Retained symbol codes (0..4) of a wire buffer, by the documented rules."""
+    out = []
+    for g in range((n_bytes + 63) // 64):
+        for i in range(64):
+            code = (int(bases[2 * g + (i >> 5)]) >> (2 * (i & 31))) & 3
+            if (int(special[g]) >> i) & 1:
+                if code == 1:
+                    continue        # dropped
+                out.append(4)       # OTHER
+            else:
+                out.append(code)
+    return np.array(out, dtype=np.uint8)
+
+
+WIRE_CASES = [
+    b">s1 demo\nctacat\n", b">h\r\nACGT\r\nacgN\r\n>h2\r\nTTTT", b">h\rAC\rGT\r>x\r\rnn",
+    b"ac>gt\n>hdr\n>hdr2\nA C\tG T\n\n\n", b"", b">" + b"x" * 300 + b"\n" + b"acgt" * 70 + b"\n>y\r\n" + b"TTGCA" * 40,
+]
+
+
+@pytest.mark.parametrize("k", range(len(WIRE_CASES)))
+@pytest.mark.parametrize("fasta", [True, False])
+def test_host_wire_packer(k, fasta):
+    """ks_pack_host_wire against ingest's own host normalisation (the
+    reference's load_sequence rules), AVX-512 and scalar paths."""
+    from paper_1509_01506_b200.ingest import strip_fasta_headers
+    import paper_1509_01506_b200 as ks
+    data = WIRE_CASES[k]
+    rng = np.random.default_rng(k)
+    data += bytes(rng.choice(list(b"acgtN \n\r>"), size=int(rng.integers(0, 3000))))
+    want = ks.encode_bytes(strip_fasta_headers(data) if fasta else data)
+    bases, special, kept = _native.pack_host_wire(data, fasta)
+    assert kept == want.size
+    assert _wire_decode(bases, special, len(data)).tolist() == want.tolist()
+    code = ("import sys, numpy as np; from paper_1509_01506_b200 import _native;"
+            f"b, s, k = _native.pack_host_wire(open(sys.argv[1], 'rb').read(), {fasta});"
+            "np.save(sys.argv[2], np.concatenate([b, s, np.array([k], dtype=np.uint64)]))")
+    import os
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        Path(d, "in").write_bytes(data)
+        subprocess.run([sys.executable, "-c", code, str(Path(d, "in")), str(Path(d, "out.npy"))], check=True,
+                       env=dict(os.environ, KS_HOST_SCALAR="1"), cwd=REPO)
+        out = np.load(Path(d, "out.npy"))
+    assert int(out[-1]) == want.size
+    nb = special.size
+    assert _wire_decode(out[:2 * nb], out[2 * nb:3 * nb], len(data)).tolist() == want.tolist()
