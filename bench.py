@@ -201,6 +201,10 @@ def run_ours(args) -> None:
     from paper_1509_01506_b200.distributed import DeviceShardScanner, compose_entry
 
     world, rank, local = dist_env()
+    if world > 1 and "KS_HOST_THREADS" not in os.environ:
+        # ranks of one node share the host cores for the end-to-end packers
+        per_node = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+        os.environ["KS_HOST_THREADS"] = str(max(1, len(os.sched_getaffinity(0)) // max(per_node, 1)))
     ngpu = torch.cuda.device_count()
     local = local % max(ngpu, 1)  # (gloo dry runs may put several ranks on one GPU)
     torch.cuda.set_device(local)
