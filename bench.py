@@ -385,8 +385,9 @@ def run_ours(args) -> None:
                     "d2h_bytes_per_step": e2e_stats["d2h_bytes"], "seconds_per_step": e2e_s,
                     "input_bytes_per_step": n,
                     "path": ("ks_count_host_ascii: pinned host ASCII in; host threads pack 64 MiB pieces to "
-                             "2-bit tile slots in pinned staging; H2D of the packed piece overlapped with "
-                             "packing the next and scanning the previous; counts D2H"),
+                             "2-bit tile slots in pinned staging (every 6th piece goes raw and is encoded on "
+                             "the device); H2D of a piece overlapped with packing the next and scanning the "
+                             "previous; counts D2H"),
                     "host_threads": host_threads()},
             "gpu_launches": launches[0],
             **({"locate": locate} if locate else {}),
