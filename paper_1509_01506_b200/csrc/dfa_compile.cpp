@@ -69,8 +69,8 @@ void build_stride_table(CompiledTable* t, size_t budget) {
     t->fast_k = 0;
     t->tkc.clear();
     t->t1z.clear();
-    if (nq + 1 <= 4096 && !(std::getenv("KS_DISABLE_FAST") && *std::getenv("KS_DISABLE_FAST") == '1')) {
-        const int fk = nq + 1 <= 256 ? 4 : (nq + 1 <= 1024 ? 3 : 2);
+    if (nq <= 4096 && !(std::getenv("KS_DISABLE_FAST") && *std::getenv("KS_DISABLE_FAST") == '1')) {
+        const int fk = nq <= 256 ? 4 : (nq <= 1024 ? 3 : 2);
         const int sb = 16 - 2 * fk;  // state bits
         const int fw = 1 << (2 * fk);
         const int z = nq;

@@ -43,8 +43,8 @@ struct CompiledTable {
     int reset_state = -1;            // internal id all states enter on OTHER, or -1
     std::vector<uint16_t> t1;        // nq x 5 single-symbol table (internal ids)
     std::vector<uint16_t> tk;        // nq x 4^K, entry = next | (hit on path ? kFlag : 0)
-    // fast form (nq + 1 <= 4096): 128 KiB column-major K-stride table with a
-    // sink state Z = nq; entry at [(w << (16 - 2K)) + s] = (next << 1) | hit
+    // fast form (nq <= 4096): 128 KiB column-major K-stride table with a
+    // row nq (unused padding); entry at [(w << (16 - 2K)) + s] = (next << 1) | hit
     int fast_k = 0;                  // 0 = not eligible
     double hit_rate = 0;             // accepting-state visits per base on uniform random input
     std::vector<uint16_t> tkc;       // 65536 entries

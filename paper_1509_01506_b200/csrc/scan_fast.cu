@@ -20,9 +20,9 @@
 //     shared-memory histogram of accepting-state visits (shared atomics).
 //     This replaces the reference's per-symbol CSR output loop
 //     (_kernels.py:26-28, 80-84).
-//   * a "sink" state Z = |Q| whose row never flags: lanes of a warp that
-//     have no work for a block (N-run blocks, finished chunks) ride the fast
-//     path in Z instead of diverging.
+//   * lanes of a warp that have no work for a block (N-run blocks, finished
+//     chunks) ride the fast path with their hit mask cleared instead of
+//     diverging (no sink state: |Q| = 1024 keeps K = 3).
 // The lane/chunk/entry-state logic is the one of scan.cu (lookback, uniform
 // or per-chunk entry states).
 #include <algorithm>
@@ -196,12 +196,13 @@ __device__ __noinline__ uint32_t drain_out(const Ctx c, uint32_t rp0, uint32_t c
     return L.nrows;
 }
 
-// One full, OTHER-free 64-base block.  `live` lanes record hits; others ride
-// along in the sink state.
+// One full, OTHER-free 64-base block.  Live lanes (lm = 0x8000) record
+// hits; the others (lm = 0: no work for this block) ride along from any
+// state without recording, so the warp never diverges.
 template <int K, int MODE>
-__device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint32_t s, const uint4& xb,
-                                               int64_t p0, unsigned am, uint32_t rp0, uint32_t& rp,
-                                               uint32_t ring_stride) {
+__device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint32_t s, uint32_t lm,
+                                               const uint4& xb, int64_t p0, unsigned am, uint32_t rp0,
+                                               uint32_t& rp, uint32_t ring_stride) {
     const uint64_t w0 = (uint64_t(xb.y) << 32) | xb.x;
     const uint64_t w1 = (uint64_t(xb.w) << 32) | xb.z;
     constexpr int NL = 64 / K;
@@ -214,7 +215,7 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
         const uint32_t a = bitsel<FM>(field<K>(xb, j), e);
         e = lds16(c.tk + a);
         if constexpr (RING) {
-            if (e & 0x8000u) {
+            if (e & lm) {
                 sts32(rp, K == 2 ? a + (e << 17) : a);
                 rp += ring_stride;
             }
@@ -227,7 +228,7 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
                 rp = rp0;
             }
         } else if constexpr (MODE == kModeEmit || MODE == kModeLog) {
-            if (e & 0x8000u) rewalk<K, MODE>(c, L, a, p0 + K * j);
+            if (e & lm) rewalk<K, MODE>(c, L, a, p0 + K * j);
         }
     }
     s = (e >> 1) & ((1u << (LC - 1)) - 1u);
@@ -236,7 +237,7 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
         const uint32_t sym = uint32_t(r < 32 ? w0 >> (2 * r) : w1 >> (2 * (r - 32))) & 3u;
         s = step1(c, s, sym);
         if constexpr (MODE != kModeMap) {
-            if (s < c.n_accept) record<MODE>(c, L, p0 + r, s);
+            if (lm && s < c.n_accept) record<MODE>(c, L, p0 + r, s);
         }
     }
     return s;
@@ -281,7 +282,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     c.log = a.log;
     c.log_n = a.log_n;
     c.log_cap = a.log_cap;
-    const uint32_t sink = uint32_t(a.nq);  // the sink state Z
+    const uint32_t idle = 0;  // state of lanes without work (their hits are masked)
     const uint32_t ring_stride = kRingStride;
     const uint32_t rp0 = smem_addr(p_ring) + 4u * threadIdx.x;
     uint32_t rp = rp0;
@@ -304,7 +305,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
         const int64_t cb = active ? max64(a.begin, u * a.chunk_len) : 0;
         const int64_t ce = active ? min64(a.end, (u + 1) * a.chunk_len) : 0;
 
-        uint32_t s = sink;
+        uint32_t s = idle;
         if (!active) {
         } else if (a.chunk_entry) {
             s = a.chunk_entry[ch];
@@ -366,8 +367,8 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
             const bool fast = !has || (k >= kfl && k < kfh && (clean || (alln && resets)));
             if (__all_sync(am, fast)) {
                 const bool live = has && !alln;
-                const uint32_t s2 = fast_block<K, MODE>(c, L, live ? s : sink, wb, p0, am, rp0, rp,
-                                                        ring_stride);
+                const uint32_t s2 = fast_block<K, MODE>(c, L, live ? s : idle, live ? 0x8000u : 0u, wb, p0, am,
+                                                        rp0, rp, ring_stride);
                 if (live) {
                     s = s2;
                 } else if (has) {
