@@ -184,20 +184,72 @@ __global__ void kept_kernel(const uint8_t* in, int64_t n_bytes, int64_t n_blocks
     }
 }
 
+// In-place encode (no whitespace expected), four lanes per 64-byte block:
+// each lane classifies 16 bytes with byte-SIMD compares (__vcmpeq4 & co.),
+// the quad assembles the block with two xor-shuffles, lane 0 stores it.  A
+// warp reads 512 contiguous bytes per iteration.  Any whitespace sets
+// *any_ws (the caller then takes the compacting path).
+__device__ __forceinline__ uint32_t msb4(uint32_t m) {   // 4 byte masks (0x00 / 0xFF) -> 4 bits
+    return (((m >> 7) & 0x01010101u) * 0x01020408u) >> 24;
+}
+__device__ __forceinline__ uint32_t pack4(uint32_t code) {   // 4 bytes holding 0..3 -> 8 bits
+    const uint32_t c = (code | (code >> 6)) & 0x000F000Fu;
+    return (c | (c >> 12)) & 0xFFu;
+}
+
 __global__ void encode_inplace_kernel(const uint8_t* in, int64_t n_bytes, int64_t n_blocks, int lb,
-                                      uint64_t* bases, uint64_t* nmask, uint64_t* soft,
-                                      uint32_t* kept, int* any_ws) {
-    for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < n_blocks;
-         b += int64_t(gridDim.x) * blockDim.x) {
-        Packed r = pack_block(in, n_bytes, b, false);
-        const int lim = int(min64(64, n_bytes - (b << 6)));
-        const int64_t slot = blk_slot(b, lb);
-        reinterpret_cast<ulonglong2*>(bases)[slot] = make_ulonglong2(r.w0, r.w1);
-        nmask[slot] = r.n;
-        soft[slot] = r.soft;
-        kept[b] = r.kept;
-        if (int(r.kept) != lim) atomicOr(any_ws, 1);
+                                      uint64_t* bases, uint64_t* nmask, uint64_t* soft, int* any_ws) {
+    const int lane = threadIdx.x & 31, q = lane & 3;
+    const int64_t stride = (int64_t(gridDim.x) * blockDim.x) >> 2;
+    bool saw_ws = false;
+    for (int64_t b0 = (int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31)) >> 2; b0 < n_blocks; b0 += stride) {
+        const int64_t b = b0 + (lane >> 2);   // warp-uniform loop; b may pass the end
+        const int64_t p = (b << 6) + 16 * q;
+        uint32_t x[4] = {0x20202020u, 0x20202020u, 0x20202020u, 0x20202020u};   // SP padding
+        uint32_t valid = 0;
+        if (b < n_blocks) {
+            if (p + 16 <= n_bytes && (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(in + p));
+                x[0] = v.x, x[1] = v.y, x[2] = v.z, x[3] = v.w;
+                valid = 0xFFFFu;
+            } else {
+                for (int i = 0; i < 16 && p + i < n_bytes; ++i) {
+                    x[i >> 2] = (x[i >> 2] & ~(0xFFu << (8 * (i & 3)))) | (uint32_t(in[p + i]) << (8 * (i & 3)));
+                    valid |= 1u << i;
+                }
+            }
+        }
+        uint32_t codes = 0, oth = 0, ws = 0, low = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t w = x[k], lw = w | 0x20202020u;
+            const uint32_t base = __vcmpeq4(lw, 0x61616161u) | __vcmpeq4(lw, 0x63636363u) |
+                                  __vcmpeq4(lw, 0x67676767u) | __vcmpeq4(lw, 0x74747474u);
+            const uint32_t wsm = __vcmpeq4(w, 0x20202020u) | __vcmpeq4(w, 0x09090909u) |
+                                 __vcmpeq4(w, 0x0D0D0D0Du) | __vcmpeq4(w, 0x0A0A0A0Au);
+            const uint32_t lower = __vcmpgeu4(w, 0x61616161u) & __vcmpleu4(w, 0x7A7A7A7Au);
+            codes |= pack4(((w >> 1) ^ (w >> 2)) & 0x03030303u & base) << (8 * k);
+            oth |= msb4(~base & ~wsm) << (4 * k);
+            ws |= msb4(wsm) << (4 * k);
+            low |= msb4(lower) << (4 * k);
+        }
+        saw_ws |= (ws & valid) != 0;
+        // quad assembly: lane q holds bases 16q .. 16q + 15
+        const uint64_t mine = uint64_t(codes) | (uint64_t(__shfl_down_sync(0xffffffffu, codes, 1, 4)) << 32);
+        const uint64_t hi = __shfl_down_sync(0xffffffffu, mine, 2, 4);
+        uint64_t n = uint64_t(oth & valid) << (16 * q), sm = uint64_t(low & valid) << (16 * q);
+        n |= __shfl_xor_sync(0xffffffffu, n, 1, 4);
+        n |= __shfl_xor_sync(0xffffffffu, n, 2, 4);
+        sm |= __shfl_xor_sync(0xffffffffu, sm, 1, 4);
+        sm |= __shfl_xor_sync(0xffffffffu, sm, 2, 4);
+        if (q == 0 && b < n_blocks) {
+            const int64_t slot = blk_slot(b, lb);
+            reinterpret_cast<ulonglong2*>(bases)[slot] = make_ulonglong2(mine, hi);
+            nmask[slot] = n;
+            soft[slot] = sm;
+        }
     }
+    if (saw_ws) atomicOr(any_ws, 1);
 }
 
 // Storage word of linear 64-bit word w of a stream with `per_block` words
@@ -376,8 +428,8 @@ int encode_raw_piece(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, ks_seq* 
     seq->n = n_bytes;
     if (nb == 0) return KS_OK;
     const int threads = 256;
-    encode_inplace_kernel<<<grid_for(ctx, nb, threads), threads, 0, ctx->stream>>>(
-        d_in, n_bytes, nb, seq->lb, seq->d_bases, seq->d_nmask, seq->d_soft, kept, ws_flag);
+    encode_inplace_kernel<<<grid_for(ctx, nb * 4, threads), threads, 0, ctx->stream>>>(
+        d_in, n_bytes, nb, seq->lb, seq->d_bases, seq->d_nmask, seq->d_soft, ws_flag);
     if (launches) ++*launches;
     KS_CUDA(cudaGetLastError());
     return KS_OK;
@@ -402,8 +454,8 @@ int encode_ascii_device(ks_ctx* ctx, const uint8_t* d_in, int64_t n_bytes, bool 
     if (!fasta) {
         KS_CUDA(cudaMemsetAsync(flag, 0, 64, ctx->stream));
         const int threads = 256;
-        encode_inplace_kernel<<<grid_for(ctx, nb, threads), threads, 0, ctx->stream>>>(
-            d_in, n_bytes, nb, seq->lb, seq->d_bases, seq->d_nmask, seq->d_soft, kept, flag);
+        encode_inplace_kernel<<<grid_for(ctx, nb * 4, threads), threads, 0, ctx->stream>>>(
+            d_in, n_bytes, nb, seq->lb, seq->d_bases, seq->d_nmask, seq->d_soft, flag);
         if (launches) ++*launches;
         KS_CUDA(cudaGetLastError());
         int any_ws = 0;
