@@ -41,11 +41,11 @@ int stride_for(int nq, size_t budget) {
         int k = std::atoi(force);
         if (k >= 1 && k <= 4) return k;
     }
-    for (int k = 4; k >= 1; --k) {
+    for (int k = 4; k >= 2; --k) {
         size_t bytes = size_t(nq) * (size_t(1) << (2 * k)) * 2 + size_t(nq) * 5 * 2;
         if (bytes <= budget) return k;
     }
-    return 1;
+    return 1;   // K = 1 scans the 1-base table itself (no stride table)
 }
 
 void build_stride_table(CompiledTable* t, size_t budget) {
@@ -53,8 +53,8 @@ void build_stride_table(CompiledTable* t, size_t budget) {
     const int k = stride_for(nq, budget);
     t->stride = k;
     const int words = 1 << (2 * k);
-    t->tk.assign(size_t(nq) * words, 0);
-    for (int s = 0; s < nq; ++s) {
+    t->tk.assign(k == 1 ? 0 : size_t(nq) * words, 0);
+    for (int s = 0; s < (k == 1 ? 0 : nq); ++s) {
         for (int w = 0; w < words; ++w) {
             int x = s;
             bool hit = false;

@@ -98,6 +98,16 @@ __device__ __forceinline__ uint32_t fast_block(uint32_t s, uint64_t w0, uint64_t
                                                Sink<MODE>& sink) {
     constexpr int W = 2 * K;
     constexpr int NL = 64 / K;
+    if constexpr (K == 1) {   // large automata: the 1-base table itself, hits by the accepting-first ids
+#pragma unroll 16
+        for (int j = 0; j < 64; ++j) {
+            s = T.one(s * 5u + bits128(w0, w1, 2 * j, 2));
+            if constexpr (MODE != kModeMap) {
+                if (live && s < uint32_t(n_accept)) sink.hit(p0 + j, s);
+            }
+        }
+        return s;
+    }
 #pragma unroll
     for (int j = 0; j < NL; ++j) {
         const uint32_t word = bits128(w0, w1, W * j, W);
