@@ -94,7 +94,9 @@ void build_stride_table(CompiledTable* t, size_t budget) {
                 // lookup's input field, so they never reach an address.
                 uint32_t v = uint32_t(x << 1) | (hit ? 0x8000u : 0u);
                 if (fk == 2) v |= (first_hit ? 0x2000u : 0u) | (x < t->n_accept ? 0x4000u : 0u);
-                t->tkc[(size_t(w) << sb) + s] = uint16_t(v);
+                // K >= 3: row-swizzled (scan_fast.cu swizzled())
+                const int row = fk >= 3 ? (s ^ (w & 31)) : s;
+                t->tkc[(size_t(w) << sb) + row] = uint16_t(v);
             }
         }
     }
