@@ -617,3 +617,35 @@ def test_locate_log_and_overflow_fallback(n):
     ref_counts, _, ref_rows = O.ref_scan_rows(w.dfa, sym, 0, n, w.dfa.start)
     assert counts.tolist() == ref_counts.tolist()
     assert np.array_equal(rows, ref_rows)
+
+
+# ---------------------------------------------------------------- full-size properties (C3, 1 GiB)
+
+def test_full_size_c3_properties(monkeypatch):
+    """At the benchmark's own size, size-independent properties (no oracle):
+    resident count == streamed count (host-packed wire, raw pieces) ==
+    streamed count with device encoding; additivity over 7 ranges whose
+    entry states come from composed segment maps; locate rows == counts."""
+    w = workloads.make(3)
+    ctx = _native.context(0)
+    dh = ctx.dfa(w.dfa)
+    pinned = torch.empty(w.n, dtype=torch.uint8, pin_memory=True)
+    pinned.numpy()[:] = w.ascii
+    sh = ctx.upload_ascii(pinned.numpy())
+    whole = ctx.count(dh, sh)
+    assert ctx.count_host_ascii(dh, pinned.numpy()).tolist() == whole.tolist()
+    monkeypatch.setenv("KS_DEVICE_ENCODE", "1")
+    assert ctx.count_host_ascii(dh, pinned.numpy()).tolist() == whole.tolist()
+    monkeypatch.delenv("KS_DEVICE_ENCODE")
+    cuts = sorted(set([0, w.n] + [int(x) for x in np.random.default_rng(3).integers(1, w.n, 6)]))
+    state, total = 0, np.zeros_like(whole)
+    for b, e in zip(cuts[:-1], cuts[1:]):
+        m = ctx.segment_map(dh, sh, b, e)
+        c, last, _ = ctx.scan_range(dh, sh, b, e, state)
+        assert last == m[state]
+        total += c
+        state = int(m[state])
+    assert total.tolist() == whole.tolist()
+    counts, rows = ctx.locate(dh, sh)
+    assert counts.tolist() == whole.tolist() and rows.shape[0] == int(whole.sum())
+    assert np.all(np.diff(rows[:, 0]) >= 0)
