@@ -393,8 +393,9 @@ def run_ours(args) -> None:
             **({"locate": locate} if locate else {}),
             "clocks": clocks.summary(),
         }
-        if not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(wl, args.cpu_sample)
+        # the CPU baseline is timed at N = 1 only (its rank would idle the others)
+        line["cpu_baseline"] = (cpu_baseline(wl, args.cpu_sample)
+                                if world == 1 and not args.no_cpu_baseline else None)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
