@@ -74,6 +74,19 @@ __device__ __forceinline__ uint32_t opaque(uint32_t x) {
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return uint32_t(__cvta_generic_to_shared(p));
 }
+// Bulk (non-tensor TMA) copy global -> shared, completion counted in bytes on mbar.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity0(uint32_t mbar) {
+    asm volatile(
+        "{\n\t.reg .pred done;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], 0;\n\t"
+        "@!done bra WAIT_%=;\n\t}"
+        ::"r"(mbar) : "memory");
+}
 
 // K input bases of step j shifted so they start at bit LC; bits outside
 // [LC, LC + 2K) are garbage (removed by the bit-select).  x0..x3 are the
@@ -278,16 +291,28 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     unsigned char* p_ring = p_t1 + size_t(a.t1_pad) * 2;
     unsigned int* s_hist = reinterpret_cast<unsigned int*>(
         p_ring + (RING ? size_t(a.ring_depth) * 4 * blockDim.x : 0));
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(a.tk);
-        uint4* dst = reinterpret_cast<uint4*>(f_smem);
-        for (int i = threadIdx.x; i < TK_BYTES / 16; i += blockDim.x) dst[i] = __ldg(src + i);
-        src = reinterpret_cast<const uint4*>(a.t1);
-        dst = reinterpret_cast<uint4*>(p_t1);
-        for (int i = threadIdx.x; i < a.t1_pad / 8; i += blockDim.x) dst[i] = __ldg(src + i);
+    // stage the tables with bulk copies (TMA engine, UBLKCP) completing on an
+    // mbarrier, while the threads clear the histogram
+    __shared__ __align__(8) unsigned long long tables_ready;
+    const uint32_t mbar = smem_addr(&tables_ready);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t t1_bytes = uint32_t(a.t1_pad) * 2u;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                     ::"r"(mbar), "r"(uint32_t(TK_BYTES) + t1_bytes) : "memory");
+        constexpr uint32_t kPart = 32768;   // bytes per bulk copy
+        for (uint32_t o = 0; o < uint32_t(TK_BYTES); o += kPart)
+            bulk_g2s(smem_addr(f_smem) + o, reinterpret_cast<const char*>(a.tk) + o, kPart, mbar);
+        for (uint32_t o = 0; o < t1_bytes; o += kPart)
+            bulk_g2s(smem_addr(p_t1) + o, reinterpret_cast<const char*>(a.t1) + o, min(kPart, t1_bytes - o), mbar);
     }
     if constexpr (HIST)
         for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x) s_hist[i] = 0u;
+    mbar_wait_parity0(mbar);
     __syncthreads();
 
     Ctx c;
@@ -485,6 +510,7 @@ FastFn pick(int mode, int k) {
 }
 
 int ring_depth_for(size_t fixed, size_t optin, int threads) {
+    fixed += 64;   // the static mbarrier of the table staging
     if (optin <= fixed) return 0;
     return int(std::min<size_t>(kRingMax, (optin - fixed) / (size_t(4) * threads)));
 }
@@ -530,7 +556,7 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
         if (a.ring_depth < chk_steps(k) + 1) return fail(KS_E_UNSUPPORTED, "fast scan: no room for the hit ring");
         smem += size_t(a.ring_depth) * 4 * kFastThreads;
     }
-    if (smem > ctx->smem_optin) return fail(KS_E_UNSUPPORTED, "fast scan: shared memory budget exceeded");
+    if (smem + 64 > ctx->smem_optin) return fail(KS_E_UNSUPPORTED, "fast scan: shared memory budget exceeded");
     {  // the attribute is per function and device; set it once per size
         static thread_local const void* last_fn[16];
         static thread_local size_t last_smem[16];
