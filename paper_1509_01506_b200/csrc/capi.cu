@@ -204,7 +204,7 @@ ScanPlan plan_for(const ks_ctx* ctx, const ks_dfa* dfa, const DevTable& T) {
     ScanPlan p;
     const int32_t A = T.n_accept;
     if (T.fast_k > 0 && dfa->tables_in_smem &&
-        fast_smem_bytes(kModeCount, int32_t(T.t1z_bytes / 2), A, fast_threads()) <= ctx->smem_optin) {
+        fast_smem_bytes(kModeCount, int32_t(T.t1z_bytes / 2), A, fast_threads()) + 256 <= ctx->smem_optin) {
         p.fast = true;  // the fast kernel keeps its visit histogram in shared memory
         p.hist_smem = true;
         return p;

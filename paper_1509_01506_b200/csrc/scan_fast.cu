@@ -510,7 +510,7 @@ FastFn pick(int mode, int k) {
 }
 
 int ring_depth_for(size_t fixed, size_t optin, int threads) {
-    fixed += 64;   // the static mbarrier of the table staging
+    fixed += 256;   // the static mbarrier of the table staging (+ alignment of the dynamic region)
     if (optin <= fixed) return 0;
     return int(std::min<size_t>(kRingMax, (optin - fixed) / (size_t(4) * threads)));
 }
@@ -556,7 +556,7 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
         if (a.ring_depth < chk_steps(k) + 1) return fail(KS_E_UNSUPPORTED, "fast scan: no room for the hit ring");
         smem += size_t(a.ring_depth) * 4 * kFastThreads;
     }
-    if (smem + 64 > ctx->smem_optin) return fail(KS_E_UNSUPPORTED, "fast scan: shared memory budget exceeded");
+    if (smem + 256 > ctx->smem_optin) return fail(KS_E_UNSUPPORTED, "fast scan: shared memory budget exceeded");
     {  // the attribute is per function and device; set it once per size
         static thread_local const void* last_fn[16];
         static thread_local size_t last_smem[16];
