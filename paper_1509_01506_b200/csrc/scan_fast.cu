@@ -359,8 +359,26 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
         } else if (a.uniform_entry >= 0) {
             s = uint32_t(a.uniform_entry);
         } else {
-            const int64_t lbp = max64(a.base_pos, cb - a.lookback);
+            int64_t lbp = max64(a.base_pos, cb - a.lookback);
             s = uint32_t(lbp == a.base_pos ? (a.base_state_ptr ? int32_t(*a.base_state_ptr) : a.base_state) : a.any_state);
+            if (lbp > a.base_pos && (cb & 63) == 0 && a.lookback <= 64 && a.lookback % K == 0) {
+                // whole K-steps over the tail of the previous block, when it has no OTHER there
+                const int64_t slot = blk_slot((cb >> 6) - 1, lb);
+                const uint64_t xm = __ldg(nmask + slot);
+                if (a.lookback == 0 || (xm >> (64 - a.lookback)) == 0) {
+                    const uint4 xb = __ldg(bases4 + slot);
+                    const uint64_t w0 = (uint64_t(xb.y) << 32) | xb.x, w1 = (uint64_t(xb.w) << 32) | xb.z;
+                    constexpr int LC = 17 - 2 * K;
+                    for (int q = 64 - a.lookback; q < 64; q += K) {
+                        const uint64_t v = q == 0 ? w0 : q < 32 ? (w0 >> (2 * q)) | (w1 << (64 - 2 * q))
+                                                               : w1 >> (2 * (q - 32));
+                        const uint32_t wv = uint32_t(v) & ((1u << (2 * K)) - 1u);
+                        const uint32_t row = swizzled(K) ? (s ^ (wv & 31u)) : s;
+                        s = (lds16(c.tk + ((wv << LC) | (row << 1))) >> 1) & ((1u << (LC - 1)) - 1u);
+                    }
+                    lbp = cb;   // done
+                }
+            }
             int64_t lbk = -1;
             uint4 xb = make_uint4(0, 0, 0, 0);
             uint64_t xm = 0;
