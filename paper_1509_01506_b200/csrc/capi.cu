@@ -404,12 +404,22 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
         a.log_n = log_n;
         a.log_cap = cap;
     }
+    // plain counts on the fast kernel: its last CTA finalizes (one launch per call)
+    const bool fused = !locate && plan.fast && nch > 0;
+    if (fused) {
+        a.fin_counts = counts;
+        a.fin_exit_src = chunk_exit + (nch - 1);
+        a.fin_exit_dst = exit_slot;
+        a.fin_done = reinterpret_cast<unsigned int*>(err + 1);   // zeroed with the result block
+    }
     rc = dispatch(ctx, dfa, dfa->scan, plan, a, use_log ? kModeLog : locate ? kModeRows : kModeCount, &launches);
     if (rc) return rc;
     KS_CUDA(cudaEventRecord(ev_b, ctx->stream));
-    rc = launch_finalize_counts(ctx, visits, h.n_accept, dfa->d_acc_out_off, dfa->d_acc_out_ids, counts,
-                                nch > 0 ? chunk_exit + (nch - 1) : nullptr, exit_slot, &launches);
-    if (rc) return rc;
+    if (!fused) {
+        rc = launch_finalize_counts(ctx, visits, h.n_accept, dfa->d_acc_out_off, dfa->d_acc_out_ids, counts,
+                                    nch > 0 ? chunk_exit + (nch - 1) : nullptr, exit_slot, &launches);
+        if (rc) return rc;
+    }
     if (async_dst) {
         if (h.ne > 0)
             KS_CUDA(cudaMemcpyAsync(async_dst, counts, size_t(h.ne) * 8, cudaMemcpyDeviceToHost, ctx->stream));

@@ -486,6 +486,25 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
         for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x)
             if (s_hist[i]) atomicAdd(&a.visits[i], (unsigned long long)s_hist[i]);
     }
+    if constexpr (MODE == kModeCount) {
+        if (a.fin_counts) {   // fused finalize: the last CTA to finish converts visits to counts
+            __shared__ unsigned int is_last;
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) is_last = atomicAdd(a.fin_done, 1u) == gridDim.x - 1;
+            __syncthreads();
+            if (is_last) {
+                __threadfence();
+                if (threadIdx.x == 0 && a.fin_exit_src) *a.fin_exit_dst = __ldcg(a.fin_exit_src);
+                for (int st = threadIdx.x; st < a.n_accept; st += blockDim.x) {
+                    const unsigned long long v = __ldcg(&a.visits[st]);
+                    if (!v) continue;
+                    for (int k = __ldg(&a.acc_out_off[st]); k < __ldg(&a.acc_out_off[st + 1]); ++k)
+                        atomicAdd(&a.fin_counts[__ldg(&a.acc_out_ids[k])], v);
+                }
+            }
+        }
+    }
 }
 
 using FastFn = void (*)(const ScanArgs);

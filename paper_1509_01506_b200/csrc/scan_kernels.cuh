@@ -72,6 +72,12 @@ struct ScanArgs {
     int64_t* rows = nullptr;
     int64_t row_base = 0;                   // row offset = position + 1 + row_base
     int32_t* error = nullptr;               // set to 1 on an internal invariant failure
+    // fast kernel, count mode: the last CTA turns visits into counts (fused
+    // finalize_counts; fin_done must be zero at launch)
+    unsigned long long* fin_counts = nullptr;
+    const uint16_t* fin_exit_src = nullptr;
+    uint16_t* fin_exit_dst = nullptr;
+    unsigned int* fin_done = nullptr;
     LogEntry* log = nullptr;                // kModeLog
     unsigned long long* log_n = nullptr;    // kModeLog: visits appended (may exceed log_cap)
     int64_t log_cap = 0;
