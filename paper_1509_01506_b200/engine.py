@@ -109,13 +109,14 @@ def _speculation_metadata(ctx, dh, sh, dfa, seq, plan: ChunkPlan, cfg: EngineCon
             data.append(pss)
             offs.append(offs[-1] + int(pss.size))
         conv, _ = ctx.speculate(dh, sh, begins, ends, offs, np.concatenate(data), cfg.window)
-        for k in range(len(begins)):
-            for c in conv[offs[k] + 1: offs[k + 1]]:
-                speculative += 1
-                if c < 0:
-                    unconverged += 1
-                else:
-                    steps[int(c)] += 1
+        offs_a = np.asarray(offs, dtype=np.int64)
+        spec = np.ones(conv.size, dtype=bool)
+        spec[offs_a[:-1]] = False            # R0 (pss[0]) of every chunk is not speculative
+        runs = np.asarray(conv)[spec]
+        speculative = int(runs.size)
+        unconverged = int(np.count_nonzero(runs < 0))
+        vals, cnts = np.unique(runs[runs >= 0], return_counts=True)
+        steps.update({int(v): int(c) for v, c in zip(vals, cnts)})
     return {
         "input_length": plan.bounds[-1][1],
         "workers": cfg.workers,
