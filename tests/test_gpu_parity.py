@@ -649,3 +649,23 @@ def test_full_size_c3_properties(monkeypatch):
     counts, rows = ctx.locate(dh, sh)
     assert counts.tolist() == whole.tolist() and rows.shape[0] == int(whole.sum())
     assert np.all(np.diff(rows[:, 0]) >= 0)
+
+
+@pytest.mark.parametrize("data", [b"\n" * 1000, b" \t\r\n" * 5000, b">only a header\n", b">h\n" * 3000,
+                                  b"N" * 100_000, b"acgt", b"x", b"a" * 64, b"a" * 65, b"\n" + b"acgt" * 40000])
+@pytest.mark.parametrize("fasta", [False, True])
+def test_degenerate_inputs(data, fasta):
+    """Inputs that compact to nothing or to a handful of symbols, through the
+    streamed count, the device ingest and run()."""
+    from paper_1509_01506_b200.ingest import strip_fasta_headers
+    w = workloads.make(2, 4096)
+    ctx = _native.context(0)
+    dh = ctx.dfa(w.dfa)
+    sym = ks.encode_bytes(strip_fasta_headers(data) if fasta else data)
+    want = O.ref_sequential_count(w.dfa, sym)[0]
+    assert ctx.count_host_ascii(dh, data, fasta=fasta).tolist() == want.tolist()
+    sh = ctx.upload_ascii(data, fasta=fasta)
+    assert sh.length == sym.size
+    assert ctx.count(dh, sh).tolist() == want.tolist()
+    rep = ks.run(w.dfa, ks.Sequence(sym), ks.EngineConfig(workers=3, mode="locate"))
+    assert rep.per_expression_counts.tolist() == want.tolist()
