@@ -198,7 +198,11 @@ KS_API int ks_segment_map(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int
  * all-gather.  ks_count_shard_async composes START through the gathered maps
  * d_maps[0..rank) (int32[world][n_states]) on the device, scans
  * [begin, end) from that state and writes the shard's per-expression counts
- * into d_counts (uint64[n_expressions], the NCCL all-reduce payload). */
+ * into d_counts (uint64[n_expressions], the NCCL all-reduce payload).
+ * Halo mode (rank > 0, d_maps == NULL, definite automata only): the caller
+ * loaded at least sync_depth bases of the previous shard in front of
+ * `begin`, the entry state is recovered by lookback and no map exchange is
+ * needed -- one all-reduce per step. */
 KS_API int ks_segment_map_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin,
                                 int64_t end, int32_t* d_map_out);
 KS_API int ks_count_shard_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin,

@@ -322,7 +322,9 @@ class DeviceContext:
     def count_shard_async(self, dfa: DfaHandle, seq: SeqHandle, begin: int, end: int, d_maps: int,
                           rank: int, d_counts: int) -> None:
         """Scan a shard from the state composed on the device out of the
-        gathered maps of ranks < rank; counts (uint64) into device memory."""
+        gathered maps of ranks < rank (d_maps = 0 with rank > 0: halo mode,
+        the bases before `begin` are the previous shard's tail); counts
+        (uint64) into device memory."""
         _check(library().ks_count_shard_async(self.handle, dfa.handle, seq.handle, int(begin), int(end),
                                               _P(d_maps), int(rank), _P(d_counts)))
 

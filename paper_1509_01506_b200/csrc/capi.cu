@@ -1091,10 +1091,15 @@ int ks_segment_map_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
 
 int ks_count_shard_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end,
                          const int32_t* d_maps, int32_t rank, unsigned long long* d_counts) {
-    if (!ctx || !dfa || !seq || !d_counts || (rank > 0 && !d_maps)) return fail(KS_E_INVALID, "null argument");
+    if (!ctx || !dfa || !seq || !d_counts) return fail(KS_E_INVALID, "null argument");
     if (begin < 0 || end < begin || end > seq->n) return fail(KS_E_INVALID, "range out of bounds");
     DeviceGuard guard(ctx->device);
     const HostDfa& h = dfa->host;
+    // halo mode (rank > 0, no maps): the bases before `begin` are the previous
+    // shard's tail, at least the synchronisation depth long (LOOKBACK only)
+    const bool halo = rank > 0 && !d_maps;
+    if (halo && (h.strategy != KS_STRATEGY_LOOKBACK || begin < h.sync_depth))
+        return fail(KS_E_INVALID, "shard without maps needs a definite automaton and a halo of sync_depth bases");
     int64_t origin, L, nch;
     geometry(seq, begin, end, &origin, &L, &nch);
     const bool mapscan = h.strategy == KS_STRATEGY_MAPSCAN;
@@ -1111,8 +1116,10 @@ int ks_count_shard_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
     int launches = 0;
     if (h.n_accept > 0) KS_CUDA(cudaMemsetAsync(visits, 0, size_t(h.n_accept) * 8, ctx->stream));
     KS_CUDA(cudaMemsetAsync(d_counts, 0, size_t(std::max(h.ne, 1)) * 8, ctx->stream));
-    compose_entry_kernel<<<1, 1, 0, ctx->stream>>>(d_maps, h.nq, rank, 0, dfa->d_new_of_old, entry);
-    KS_CUDA(cudaGetLastError());
+    if (!halo) {
+        compose_entry_kernel<<<1, 1, 0, ctx->stream>>>(d_maps, h.nq, rank, 0, dfa->d_new_of_old, entry);
+        KS_CUDA(cudaGetLastError());
+    }
     if (nch > 0) {
         const ScanPlan plan = plan_for(ctx, dfa, dfa->scan);
         ScanArgs a = base_args(dfa, dfa->scan, seq);
@@ -1141,8 +1148,9 @@ int ks_count_shard_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
             a.chunk_entry = centry;
         } else {
             a.lookback = h.sync_depth;
-            a.base_pos = begin;
-            a.base_state_ptr = entry;
+            a.base_pos = halo ? 0 : begin;   // halo: every chunk, the first included, looks back
+            a.base_state = h.start_internal;
+            a.base_state_ptr = halo ? nullptr : entry;
             a.any_state = h.start_internal;
         }
         KS_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));

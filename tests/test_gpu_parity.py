@@ -384,6 +384,34 @@ def test_sharded_async_matches_sequential(config, n, world):
     assert total.tolist() == want.tolist()
 
 
+@pytest.mark.parametrize("config,n,world", [(3, 1 << 20, 3), (4, 1 << 19, 4), (2, 300_000, 2)])
+def test_sharded_halo_matches_sequential(config, n, world):
+    """Halo mode of the multi-GPU step (definite automata): each shard is
+    loaded with the previous shard's last bases in front, scanned from
+    `halo` without any map exchange; the summed counts equal one pass."""
+    import torch
+    from paper_1509_01506_b200.distributed import shard_bounds
+
+    w = workloads.make(config, n)
+    codes = ks.encode_bytes(w.ascii.tobytes())
+    ctx = _native.DeviceContext(0)
+    dh = ctx.dfa(w.dfa)
+    depth = dh.info["sync_depth"]
+    halo = -(-max(depth, 1) // 64) * 64
+    total = np.zeros(w.dfa.n_expressions, dtype=np.int64)
+    for r, (b, e) in enumerate(shard_bounds(codes.size, world)):
+        h = min(halo, b)
+        sh = ctx.upload_codes(codes[b - h:e])
+        c = torch.zeros(max(w.dfa.n_expressions, 1), dtype=torch.int64, device="cuda")
+        ctx.count_shard_async(dh, sh, h, h + (e - b), 0, r, c.data_ptr())
+        ctx.synchronize()
+        total += c.cpu().numpy()[: w.dfa.n_expressions]
+    assert total.tolist() == O.ref_sequential_count(w.dfa, codes)[0].tolist()
+    with pytest.raises(ValueError):   # a halo shorter than the synchronisation depth is refused
+        ctx.count_shard_async(dh, ctx.upload_codes(codes[:4096]), depth - 1, 4096, 0, 1,
+                              torch.zeros(64, dtype=torch.int64, device="cuda").data_ptr())
+
+
 # ---------------------------------------------------------------- device ingest (FASTA / whitespace)
 
 FASTA_CASES = [
