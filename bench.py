@@ -418,8 +418,12 @@ def run_ours(args) -> None:
             "clocks": clocks.summary(),
         }
         # the CPU baseline is timed at N = 1 only (its rank would idle the others)
-        line["cpu_baseline"] = (cpu_baseline(wl, args.cpu_sample)
-                                if world == 1 and not args.no_cpu_baseline else None)
+        line["cpu_baseline"] = None
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                line["cpu_baseline"] = cpu_baseline(wl, args.cpu_sample)
+            except Exception as exc:   # the reported baseline must not sink the measurement
+                line["cpu_baseline"] = {"error": f"{type(exc).__name__}: {exc}"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
