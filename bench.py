@@ -437,7 +437,7 @@ def main() -> None:
     ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--bases", type=int, default=None, help="override bases per GPU")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--strategy", default="auto", choices=["auto", "lookback", "mapscan", "speculate"],
                     help="force a scan strategy (exploration; the contract line uses auto)")
     ap.add_argument("--cpu-sample", type=int, default=256 << 20)
