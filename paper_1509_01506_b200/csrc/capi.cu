@@ -67,25 +67,27 @@ int ensure_pinned(ks_ctx* ctx, size_t bytes) {
 namespace {
 
 // ------------------------------------------------------------ tiny kernels
-__global__ void walk_kernel(SeqView seq, int64_t begin, int64_t end, const uint16_t* t1, int32_t nq,
-                            int32_t uniform_start, uint16_t* out) {
+template <class T>   // T: uint16_t tables, uint32_t for wide automata
+__global__ void walk_kernel(SeqView seq, int64_t begin, int64_t end, const T* t1, int32_t nq,
+                            int32_t uniform_start, uint32_t* out) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nq) return;
     uint32_t s = uniform_start >= 0 ? uint32_t(uniform_start) : uint32_t(q);
-    for (int64_t p = begin; p < end; ++p) s = t1[s * 5u + seq_sym(seq, p)];
-    out[q] = uint16_t(s);
+    for (int64_t p = begin; p < end; ++p) s = t1[size_t(s) * 5 + seq_sym(seq, p)];
+    out[q] = s;
 }
 
 // map_out[q_orig] = original id of walking [begin, end) from q (all q), or of
 // walking [end - D, end) from any state (uniform) for definite automata.
-__global__ void segment_map_kernel(SeqView seq, int64_t begin, int64_t end, const uint16_t* t1, int32_t nq,
+template <class T>
+__global__ void segment_map_kernel(SeqView seq, int64_t begin, int64_t end, const T* t1, int32_t nq,
                                    int32_t uniform_start, const int32_t* new_of_old, const int32_t* old_of_new,
                                    int32_t* map_out) {
     __shared__ uint32_t shared_state;
     if (uniform_start >= 0) {
         if (threadIdx.x == 0 && blockIdx.x == 0) {
             uint32_t s = uint32_t(uniform_start);
-            for (int64_t p = begin; p < end; ++p) s = t1[s * 5u + seq_sym(seq, p)];
+            for (int64_t p = begin; p < end; ++p) s = t1[size_t(s) * 5 + seq_sym(seq, p)];
             shared_state = s;
         }
         __syncthreads();
@@ -95,7 +97,7 @@ __global__ void segment_map_kernel(SeqView seq, int64_t begin, int64_t end, cons
     }
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
         uint32_t s = uint32_t(new_of_old[q]);
-        for (int64_t p = begin; p < end; ++p) s = t1[s * 5u + seq_sym(seq, p)];
+        for (int64_t p = begin; p < end; ++p) s = t1[size_t(s) * 5 + seq_sym(seq, p)];
         map_out[q] = old_of_new[s];
     }
 }
@@ -118,6 +120,22 @@ __global__ void compose_entry_kernel(const int32_t* maps, int32_t nq, int32_t ra
 
 }  // namespace
 
+// Walk [begin, end) from every state (uniform_start < 0, nlanes = |Q|) or
+// from one state; internal ids into out (uint32).
+int launch_walk(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end, int32_t nlanes,
+                int32_t uniform_start, uint32_t* out) {
+    const int threads = nlanes == 1 ? 32 : 128;
+    const int blocks = (nlanes + threads - 1) / threads;
+    if (dfa->host.wide)
+        walk_kernel<uint32_t><<<blocks, threads, 0, ctx->stream>>>(view_of(seq), begin, end, dfa->scan.t1w, nlanes,
+                                                                     uniform_start, out);
+    else
+        walk_kernel<uint16_t><<<blocks, threads, 0, ctx->stream>>>(view_of(seq), begin, end, dfa->scan.t1, nlanes,
+                                                                     uniform_start, out);
+    KS_CUDA(cudaGetLastError());
+    return KS_OK;
+}
+
 SeqView view_of(const ks_seq* s) {
     SeqView v;
     v.bases = s->d_bases;
@@ -131,6 +149,7 @@ ScanArgs base_args(const ks_dfa* dfa, const DevTable& T, const ks_seq* seq) {
     ScanArgs a;
     a.seq = view_of(seq);
     a.t1 = T.t1;
+    a.t1w = T.t1w;
     a.tk = T.tk;
     a.nq = T.nq;
     a.n_accept = T.n_accept;
@@ -169,6 +188,7 @@ void geometry(const ks_seq* seq, int64_t begin, int64_t end, int64_t* origin, in
 
 int dispatch(ks_ctx* ctx, const ks_dfa* dfa, const DevTable& T, const ScanPlan& p, ScanArgs a, int mode,
              int* launches) {
+    if (dfa->host.wide) return launch_scan_wide(ctx, a, mode, launches);
     a.hist_smem = p.hist_smem ? 1 : 0;
     if (p.fast) {
         a.tk = T.tkc;
@@ -233,15 +253,15 @@ int true_state_at(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t pos
     if (h.strategy == KS_STRATEGY_LOOKBACK) {
         int rc = ensure_scratch(ctx, 4096, &ar);
         if (rc) return rc;
-        uint16_t* d = static_cast<uint16_t*>(ar.take(16));
+        uint32_t* d = static_cast<uint32_t*>(ar.take(16));
         const int64_t lb = std::max<int64_t>(0, pos - h.sync_depth);
-        walk_kernel<<<1, 32, 0, ctx->stream>>>(view_of(seq), lb, pos, dfa->scan.t1, 1, h.start_internal, d);
+        rc = launch_walk(ctx, dfa, seq, lb, pos, 1, h.start_internal, d);
+        if (rc) return rc;
         if (launches) ++*launches;
-        KS_CUDA(cudaGetLastError());
-        uint16_t v = 0;
-        KS_CUDA(cudaMemcpyAsync(&v, d, 2, cudaMemcpyDeviceToHost, ctx->stream));
+        uint32_t v = 0;
+        KS_CUDA(cudaMemcpyAsync(&v, d, 4, cudaMemcpyDeviceToHost, ctx->stream));
         KS_CUDA(cudaStreamSynchronize(ctx->stream));
-        *out = v;
+        *out = int(v);
         return KS_OK;
     }
     int64_t origin, L, nch;
@@ -315,8 +335,9 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
     unsigned long long* visits = reinterpret_cast<unsigned long long*>(blk);
     unsigned long long* counts = reinterpret_cast<unsigned long long*>(blk + size_t(h.n_accept) * 8);
     int32_t* err = reinterpret_cast<int32_t*>(counts + std::max(h.ne, 1));
-    uint16_t* exit_slot = reinterpret_cast<uint16_t*>(err + 2);
-    uint16_t* chunk_exit = static_cast<uint16_t*>(ar.take(size_t(nch) * 2 + 2));
+    uint16_t* exit_slot = reinterpret_cast<uint16_t*>(err + 2);   // uint32 for wide automata
+    void* exit_region = ar.take(size_t(nch) * 4 + 4);
+    uint16_t* chunk_exit = static_cast<uint16_t*>(exit_region);
     uint32_t* chunk_rows = nullptr;
     int64_t* row_off = nullptr;
     void* rows_tmp = nullptr;
@@ -344,7 +365,8 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
     a.chunk_len = L;
     a.nchunks = nch;
     a.visits = visits;
-    a.chunk_exit = chunk_exit;
+    a.chunk_exit = h.wide ? nullptr : chunk_exit;
+    a.chunk_exit32 = h.wide ? static_cast<uint32_t*>(exit_region) : nullptr;
     a.error = err;
     a.row_base = row_base;
     if (h.strategy == KS_STRATEGY_LOOKBACK) {
@@ -417,8 +439,10 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
     KS_CUDA(cudaEventRecord(ev_b, ctx->stream));
     if (!fused) {
         rc = launch_finalize_counts(ctx, visits, h.n_accept, dfa->d_acc_out_off, dfa->d_acc_out_ids, counts,
-                                    nch > 0 ? chunk_exit + (nch - 1) : nullptr, exit_slot, &launches);
+                                    nch > 0 && !h.wide ? chunk_exit + (nch - 1) : nullptr, exit_slot, &launches);
         if (rc) return rc;
+        if (h.wide && nch > 0)
+            KS_CUDA(cudaMemcpyAsync(exit_slot, a.chunk_exit32 + (nch - 1), 4, cudaMemcpyDeviceToDevice, ctx->stream));
     }
     if (async_dst) {
         if (h.ne > 0)
@@ -508,7 +532,7 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
     std::memcpy(counts_out, pin, size_t(h.ne) * 8);
     if (exit_out) {
         int ex;
-        if (nch > 0) ex = *pin_exit;
+        if (nch > 0) ex = h.wide ? int(*reinterpret_cast<uint32_t*>(pin_exit)) : int(*pin_exit);
         else if (entry >= 0) ex = entry;
         else {
             rc = true_state_at(ctx, dfa, seq, begin, &ex, &launches);
@@ -551,6 +575,7 @@ int upload_table(const CompiledTable& t, DevTable* d, char* blob, size_t* off, b
     d->t1_bytes = align16(t.t1.size() * 2);
     d->tk = reinterpret_cast<const uint16_t*>(place(t.tk.data(), t.tk.size() * 2));
     d->t1 = reinterpret_cast<const uint16_t*>(place(t.t1.data(), t.t1.size() * 2));
+    if (!t.t1w.empty()) d->t1w = reinterpret_cast<const uint32_t*>(place(t.t1w.data(), t.t1w.size() * 4));
     d->fast_k = t.fast_k;
     d->hit_rate = t.hit_rate;
     d->t1z_bytes = align16(t.t1z.size() * 2);
@@ -774,6 +799,7 @@ int ks_dfa_upload_ex(ks_ctx* ctx, const int32_t* transitions, int32_t n_states, 
     };
     rebase(d->scan.tk);
     rebase(d->scan.t1);
+    rebase(d->scan.t1w);
     rebase(d->scan.tkc);
     rebase(d->scan.t1z);
     rebase(d->d_acc_out_off);
@@ -797,7 +823,7 @@ int ks_dfa_upload_ex(ks_ctx* ctx, const int32_t* transitions, int32_t n_states, 
     }
     const size_t smem_scan = d->scan.tk_bytes + d->scan.t1_bytes;
     const size_t smem_mono = h.strategy == KS_STRATEGY_MAPSCAN ? d->mono.tk_bytes + d->mono.t1_bytes : 0;
-    d->tables_in_smem = std::max(smem_scan, smem_mono) + 1024 <= ctx->smem_optin;
+    d->tables_in_smem = !h.wide && std::max(smem_scan, smem_mono) + 1024 <= ctx->smem_optin;
     if (const char* g = std::getenv("KS_FORCE_GLOBAL_TABLES"); g && *g == '1') d->tables_in_smem = false;
     *out = d;
     return KS_OK;
@@ -1006,26 +1032,24 @@ int ks_segment_map(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t be
     if (begin < 0 || end < begin || end > seq->n) return fail(KS_E_INVALID, "segment out of bounds");
     DeviceGuard guard(ctx->device);
     const HostDfa& h = dfa->host;
-    std::vector<uint16_t> img(h.nq);
+    std::vector<uint32_t> img(h.nq);
     int launches = 0;
     if (h.strategy != KS_STRATEGY_MAPSCAN) {   // SPECULATE: every state walks the segment
         Arena ar;
-        int rc = ensure_scratch(ctx, size_t(h.nq) * 2 + 1024, &ar);
+        int rc = ensure_scratch(ctx, size_t(h.nq) * 4 + 1024, &ar);
         if (rc) return rc;
-        uint16_t* d = static_cast<uint16_t*>(ar.take(size_t(h.nq) * 2));
+        uint32_t* d = static_cast<uint32_t*>(ar.take(size_t(h.nq) * 4));
         if (h.strategy == KS_STRATEGY_LOOKBACK && end - begin >= h.sync_depth) {
-            walk_kernel<<<1, 32, 0, ctx->stream>>>(view_of(seq), end - h.sync_depth, end, dfa->scan.t1, 1,
-                                                     h.start_internal, d);
-            KS_CUDA(cudaGetLastError());
-            uint16_t v = 0;
-            KS_CUDA(cudaMemcpyAsync(&v, d, 2, cudaMemcpyDeviceToHost, ctx->stream));
+            rc = launch_walk(ctx, dfa, seq, end - h.sync_depth, end, 1, h.start_internal, d);
+            if (rc) return rc;
+            uint32_t v = 0;
+            KS_CUDA(cudaMemcpyAsync(&v, d, 4, cudaMemcpyDeviceToHost, ctx->stream));
             KS_CUDA(cudaStreamSynchronize(ctx->stream));
             std::fill(img.begin(), img.end(), v);
         } else {
-            walk_kernel<<<(h.nq + 127) / 128, 128, 0, ctx->stream>>>(view_of(seq), begin, end, dfa->scan.t1,
-                                                                       h.nq, -1, d);
-            KS_CUDA(cudaGetLastError());
-            KS_CUDA(cudaMemcpyAsync(img.data(), d, size_t(h.nq) * 2, cudaMemcpyDeviceToHost, ctx->stream));
+            rc = launch_walk(ctx, dfa, seq, begin, end, h.nq, -1, d);
+            if (rc) return rc;
+            KS_CUDA(cudaMemcpyAsync(img.data(), d, size_t(h.nq) * 4, cudaMemcpyDeviceToHost, ctx->stream));
             KS_CUDA(cudaStreamSynchronize(ctx->stream));
         }
     } else {
@@ -1061,9 +1085,14 @@ int ks_segment_map_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
     const int blocks = std::max(1, std::min((h.nq + threads - 1) / threads, 1024));
     if (h.strategy != KS_STRATEGY_MAPSCAN) {   // SPECULATE: every state walks the segment
         const bool uniform = h.strategy == KS_STRATEGY_LOOKBACK && end - begin >= h.sync_depth;
-        segment_map_kernel<<<uniform ? 1 : blocks, threads, 0, ctx->stream>>>(
-            view_of(seq), uniform ? end - h.sync_depth : begin, end, dfa->scan.t1, h.nq,
-            uniform ? h.start_internal : -1, dfa->d_new_of_old, dfa->d_old_of_new, d_map_out);
+        if (h.wide)
+            segment_map_kernel<uint32_t><<<uniform ? 1 : blocks, threads, 0, ctx->stream>>>(
+                view_of(seq), uniform ? end - h.sync_depth : begin, end, dfa->scan.t1w, h.nq,
+                uniform ? h.start_internal : -1, dfa->d_new_of_old, dfa->d_old_of_new, d_map_out);
+        else
+            segment_map_kernel<uint16_t><<<uniform ? 1 : blocks, threads, 0, ctx->stream>>>(
+                view_of(seq), uniform ? end - h.sync_depth : begin, end, dfa->scan.t1, h.nq,
+                uniform ? h.start_internal : -1, dfa->d_new_of_old, dfa->d_old_of_new, d_map_out);
         KS_CUDA(cudaGetLastError());
         return KS_OK;
     }
@@ -1098,6 +1127,8 @@ int ks_count_shard_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
     // halo mode (rank > 0, no maps): the bases before `begin` are the previous
     // shard's tail, at least the synchronisation depth long (LOOKBACK only)
     const bool halo = rank > 0 && !d_maps;
+    if (h.wide && rank > 0 && !halo)
+        return fail(KS_E_UNSUPPORTED, "wide automata shard in halo mode only (no map exchange)");
     if (halo && (h.strategy != KS_STRATEGY_LOOKBACK || begin < h.sync_depth))
         return fail(KS_E_INVALID, "shard without maps needs a definite automaton and a halo of sync_depth bases");
     int64_t origin, L, nch;
@@ -1180,32 +1211,37 @@ int ks_speculate(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int32_t n_ch
             return fail(KS_E_INVALID, "chunk out of bounds");
     }
     const int64_t total = pss_off[n_chunks];
-    std::vector<uint16_t> pss(size_t(std::max<int64_t>(total, 1)));
+    std::vector<uint32_t> pss(size_t(std::max<int64_t>(total, 1)));   // internal ids
     for (int64_t i = 0; i < total; ++i) {
         if (pss_data[i] < 0 || pss_data[i] >= h.nq) return fail(KS_E_INVALID, "pss state out of range");
-        pss[i] = uint16_t(h.new_of_old[pss_data[i]]);
+        pss[i] = uint32_t(h.new_of_old[pss_data[i]]);
     }
+    std::vector<uint16_t> pss16;
+    if (!h.wide) pss16.assign(pss.begin(), pss.end());
+    const size_t id_bytes = h.wide ? 4 : 2;
     const size_t task_bytes = speculate_task_bytes(n_chunks, pss_off);
     const size_t delta_bytes = delta_out ? size_t(total) * size_t(std::max(h.ne, 1)) * 8 : 0;
     Arena ar;
-    int rc = ensure_scratch(ctx, size_t(n_chunks) * 16 + size_t(n_chunks + 1) * 8 + size_t(total) * 6 +
+    int rc = ensure_scratch(ctx, size_t(n_chunks) * 16 + size_t(n_chunks + 1) * 8 + size_t(total) * 8 +
                                      task_bytes + delta_bytes + 16 * 1024,
                             &ar);
     if (rc) return rc;
     int64_t* d_cb = static_cast<int64_t*>(ar.take(size_t(n_chunks) * 8));
     int64_t* d_ce = static_cast<int64_t*>(ar.take(size_t(n_chunks) * 8));
     int64_t* d_off = static_cast<int64_t*>(ar.take(size_t(n_chunks + 1) * 8));
-    uint16_t* d_pss = static_cast<uint16_t*>(ar.take(size_t(total) * 2 + 2));
+    void* d_pss = ar.take(size_t(total) * id_bytes + 4);
     int32_t* d_conv = static_cast<int32_t*>(ar.take(size_t(total) * 4 + 4));
     void* d_tasks = ar.take(task_bytes);
     long long* d_delta = delta_out ? static_cast<long long*>(ar.take(delta_bytes)) : nullptr;
     KS_CUDA(cudaMemcpyAsync(d_cb, chunk_begin, size_t(n_chunks) * 8, cudaMemcpyHostToDevice, ctx->stream));
     KS_CUDA(cudaMemcpyAsync(d_ce, chunk_end, size_t(n_chunks) * 8, cudaMemcpyHostToDevice, ctx->stream));
     KS_CUDA(cudaMemcpyAsync(d_off, pss_off, size_t(n_chunks + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
-    KS_CUDA(cudaMemcpyAsync(d_pss, pss.data(), size_t(total) * 2, cudaMemcpyHostToDevice, ctx->stream));
+    KS_CUDA(cudaMemcpyAsync(d_pss, h.wide ? static_cast<const void*>(pss.data()) : static_cast<const void*>(pss16.data()),
+                            size_t(total) * id_bytes, cudaMemcpyHostToDevice, ctx->stream));
     if (d_delta) KS_CUDA(cudaMemsetAsync(d_delta, 0, delta_bytes, ctx->stream));
     int launches = 0;
-    rc = launch_speculate(ctx, view_of(seq), n_chunks, d_cb, d_ce, d_off, d_pss, pss_off, window, dfa->scan.t1,
+    rc = launch_speculate(ctx, view_of(seq), n_chunks, d_cb, d_ce, d_off, d_pss, h.wide, pss_off, window,
+                          h.wide ? static_cast<const void*>(dfa->scan.t1w) : static_cast<const void*>(dfa->scan.t1),
                           h.n_accept, dfa->d_acc_out_off, dfa->d_acc_out_ids, h.ne, d_conv, d_delta, d_tasks,
                           &launches);
     if (rc) return rc;

@@ -28,9 +28,10 @@ namespace ks {
 namespace {
 
 struct VecHash {
-    size_t operator()(const std::vector<uint16_t>& v) const noexcept {
+    template <class T>
+    size_t operator()(const std::vector<T>& v) const noexcept {
         uint64_t h = 1469598103934665603ull ^ v.size();
-        for (uint16_t x : v) h = (h ^ x) * 1099511628211ull;
+        for (T x : v) h = (h ^ x) * 1099511628211ull;
         return static_cast<size_t>(h);
     }
 };
@@ -121,24 +122,25 @@ void build_stride_table(CompiledTable* t, size_t budget) {
 }
 
 // Smallest D with |delta(Q, w)| == 1 for all |w| == D, or -1.
-int synchronisation_depth(const std::vector<uint16_t>& t1, int nq) {
+template <class T>
+int synchronisation_depth(const std::vector<T>& t1, int nq) {
     if (nq <= 1) return 0;
-    std::vector<std::vector<uint16_t>> level(1);
+    std::vector<std::vector<T>> level(1);
     level[0].resize(nq);
-    std::iota(level[0].begin(), level[0].end(), uint16_t(0));
+    std::iota(level[0].begin(), level[0].end(), T(0));
     std::vector<uint32_t> stamp(nq, 0);
     uint32_t tick = 0;
     int64_t work = 0;
     const int64_t budget = 200000000;
-    std::vector<uint16_t> img;
+    std::vector<T> img;
     for (int k = 0; k < kMaxSyncDepth; ++k) {
-        std::unordered_set<std::vector<uint16_t>, VecHash> next;
+        std::unordered_set<std::vector<T>, VecHash> next;
         for (const auto& set : level) {
             for (int c = 0; c < 5; ++c) {
                 ++tick;
                 img.clear();
-                for (uint16_t q : set) {
-                    uint16_t x = t1[size_t(q) * 5 + c];
+                for (T q : set) {
+                    T x = t1[size_t(q) * 5 + c];
                     if (stamp[x] != tick) {
                         stamp[x] = tick;
                         img.push_back(x);
@@ -155,7 +157,7 @@ int synchronisation_depth(const std::vector<uint16_t>& t1, int nq) {
         if (next.empty()) return k + 1;
         // a level that maps onto itself never shrinks (e.g. permutation columns)
         if (next.size() == level.size() &&
-            std::all_of(level.begin(), level.end(), [&](const std::vector<uint16_t>& v) { return next.count(v); }))
+            std::all_of(level.begin(), level.end(), [&](const std::vector<T>& v) { return next.count(v); }))
             return -1;
         level.assign(next.begin(), next.end());
     }
@@ -220,9 +222,7 @@ bool build_monoid(const CompiledTable& t, int start, HostDfa* h) {
 int compile_dfa(const int32_t* trans, int nq, const int32_t* out_off, const int32_t* out_ids,
                 int ne, int force_strategy, size_t smem_budget, HostDfa* h) {
     if (!trans || !out_off || nq < 1) return fail(KS_E_INVALID, "dfa: empty transition table");
-    if (nq > kMaxStates)
-        return fail(KS_E_UNSUPPORTED, "dfa: " + std::to_string(nq) +
-                                          " states exceed the device limit of 32767");
+    if (nq > (1 << 30)) return fail(KS_E_UNSUPPORTED, "dfa: too many states");
     if (ne < 0) return fail(KS_E_INVALID, "dfa: negative expression count");
     if (out_off[0] != 0) return fail(KS_E_INVALID, "dfa: out_offsets[0] must be 0");
     for (int s = 0; s < nq; ++s) {
@@ -264,6 +264,28 @@ int compile_dfa(const int32_t* trans, int nq, const int32_t* out_off, const int3
     CompiledTable& t = h->scan;
     t.nq = nq;
     t.n_accept = h->n_accept;
+    if (nq > kMaxStates) {
+        // wide automata: 32-bit ids, definite only (every build_dfa automaton
+        // is), scanned one base at a time from the 1-base table in L1/L2
+        if (force_strategy != 0 && force_strategy != KS_STRATEGY_LOOKBACK)
+            return fail(KS_E_UNSUPPORTED, "dfa: automata above 32767 states scan with the LOOKBACK strategy only");
+        h->wide = true;
+        t.stride = 1;
+        t.t1w.resize(size_t(nq) * 5);
+        for (int s = 0; s < nq; ++s)
+            for (int c = 0; c < 5; ++c)
+                t.t1w[size_t(h->new_of_old[s]) * 5 + c] = uint32_t(h->new_of_old[trans[size_t(s) * 5 + c]]);
+        const uint32_t r = t.t1w[4];
+        bool resets = true;
+        for (int s = 1; s < nq && resets; ++s) resets = t.t1w[size_t(s) * 5 + 4] == r;
+        t.reset_state = resets ? int(r) : -1;
+        h->sync_depth = synchronisation_depth(t.t1w, nq);
+        if (h->sync_depth < 0)
+            return fail(KS_E_UNSUPPORTED, "dfa: automata above 32767 states must be definite "
+                                          "(synchronise within 2048 symbols)");
+        h->strategy = KS_STRATEGY_LOOKBACK;
+        return KS_OK;
+    }
     t.t1.resize(size_t(nq) * 5);
     for (int s = 0; s < nq; ++s)
         for (int c = 0; c < 5; ++c)

@@ -42,6 +42,7 @@ struct CompiledTable {
     int stride = 1;                  // K: bases per stride-table lookup
     int reset_state = -1;            // internal id all states enter on OTHER, or -1
     std::vector<uint16_t> t1;        // nq x 5 single-symbol table (internal ids)
+    std::vector<uint32_t> t1w;       // the same with 32-bit ids (automata above kMaxStates)
     std::vector<uint16_t> tk;        // nq x 4^K, entry = next | (hit on path ? kFlag : 0)
     // fast form (nq <= 4096): 128 KiB column-major K-stride table with a
     // row nq (unused padding); entry at [(w << (16 - 2K)) + s] = (next << 1) | hit
@@ -53,6 +54,7 @@ struct CompiledTable {
 
 struct HostDfa {
     int nq = 0, ne = 0, n_accept = 0;
+    bool wide = false;                  // > kMaxStates states: 32-bit ids, LOOKBACK, generic K = 1 scan
     int strategy = 0;
     int sync_depth = -1;
     int start_internal = 0;
@@ -80,6 +82,7 @@ int compile_dfa(const int32_t* trans, int nq, const int32_t* out_off, const int3
 // ---------------------------------------------------------------- device views
 struct DevTable {
     const uint16_t* t1 = nullptr;   // nq x 5
+    const uint32_t* t1w = nullptr;  // nq x 5, 32-bit ids (wide automata)
     const uint16_t* tk = nullptr;   // nq x 4^K
     int nq = 0, n_accept = 0, stride = 1, reset_state = -1;
     size_t tk_bytes = 0, t1_bytes = 0;

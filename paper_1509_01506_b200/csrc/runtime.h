@@ -85,8 +85,8 @@ int scatter_tile_masks_device(ks_ctx* ctx, const uint64_t* d_compact, const int3
 int unpack_codes_device(ks_ctx* ctx, const ks_seq* seq, uint8_t* d_out);
 int linear_softmask_device(ks_ctx* ctx, const ks_seq* seq, uint64_t* d_out);
 int launch_speculate(ks_ctx* ctx, const SeqView& seq, int32_t n_chunks, const int64_t* d_cbeg,
-                     const int64_t* d_cend, const int64_t* d_pss_off, const uint16_t* d_pss,
-                     const int64_t* h_pss_off, int32_t window, const uint16_t* t1, int32_t n_accept,
+                     const int64_t* d_cend, const int64_t* d_pss_off, const void* d_pss, bool wide,
+                     const int64_t* h_pss_off, int32_t window, const void* t1, int32_t n_accept,
                      const int32_t* off, const int32_t* ids, int32_t ne, int32_t* d_conv,
                      long long* d_delta, void* d_tasks_buf, int* launches);
 size_t speculate_task_bytes(int32_t n_chunks, const int64_t* h_pss_off);

@@ -240,6 +240,54 @@ __global__ void __launch_bounds__(1024, 1) scan_kernel(const ScanArgs a) {
     }
 }
 
+// Wide automata (> 32767 states, 32-bit ids): one thread per chunk, one
+// 1-base lookup per symbol (__ldg, the table lives in L2), entry states by
+// lookback only (definite automata), hits as in scan_kernel.
+template <int MODE>
+__global__ void __launch_bounds__(256) scan_wide_kernel(const ScanArgs a) {
+    extern __shared__ __align__(16) unsigned int w_hist[];
+    const bool hist_smem = (MODE == kModeCount || MODE == kModeRows) && a.hist_smem;
+    if (hist_smem) {
+        for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x) w_hist[i] = 0u;
+        __syncthreads();
+    }
+    const uint32_t n_accept = uint32_t(a.n_accept);
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < a.nchunks; c += stride) {
+        const int64_t cb = max64(a.begin, a.origin + c * a.chunk_len);
+        const int64_t ce = min64(a.end, a.origin + (c + 1) * a.chunk_len);
+        const int64_t lb = max64(a.base_pos, cb - a.lookback);
+        uint32_t s = uint32_t(lb == a.base_pos ? a.base_state : a.any_state);
+        for (int64_t p = lb; p < cb; ++p) s = __ldg(&a.t1w[size_t(s) * 5 + seq_sym(a.seq, p)]);
+        Sink<MODE> sink;
+        sink.shist = hist_smem ? w_hist : nullptr;
+        sink.visits = a.visits;
+        sink.outcnt = a.acc_outcnt;
+        sink.off = a.acc_out_off;
+        sink.ids = a.acc_out_ids;
+        sink.rows = a.rows;
+        sink.row_base = a.row_base;
+        sink.nrows = 0;
+        sink.cur = (MODE == kModeEmit) ? a.chunk_row_off[c] : 0;
+        for (int64_t p = cb; p < ce; ++p) {
+            s = __ldg(&a.t1w[size_t(s) * 5 + seq_sym(a.seq, p)]);
+            if constexpr (MODE != kModeMap) {
+                if (s < n_accept) sink.hit(p, s);
+            }
+        }
+        if (a.chunk_exit32) a.chunk_exit32[c] = s;
+        if constexpr (MODE == kModeRows) a.chunk_rows[c] = sink.nrows;
+        if constexpr (MODE == kModeEmit) {
+            if (sink.cur != a.chunk_row_off[c + 1]) atomicExch(a.error, 1);
+        }
+    }
+    if (hist_smem) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x)
+            if (w_hist[i]) atomicAdd(&a.visits[i], (unsigned long long)w_hist[i]);
+    }
+}
+
 using ScanFn = void (*)(const ScanArgs);
 
 template <int K, bool SM>
@@ -364,6 +412,30 @@ int launch_finalize_counts(ks_ctx* ctx, const unsigned long long* visits, int32_
     const int blocks = std::max(1, std::min((n_accept + threads - 1) / threads, 1024));
     finalize_counts_kernel<<<blocks, threads, 0, ctx->stream>>>(visits, n_accept, acc_out_off,
                                                                   acc_out_ids, counts, exit_src, exit_dst);
+    if (launches) ++*launches;
+    KS_CUDA(cudaGetLastError());
+    return KS_OK;
+}
+
+int launch_scan_wide(ks_ctx* ctx, ScanArgs a, int mode, int* launches) {
+    if (a.end <= a.begin || a.nchunks <= 0) return KS_OK;
+    ScanFn fn = mode == kModeCount ? scan_wide_kernel<kModeCount>
+              : mode == kModeRows  ? scan_wide_kernel<kModeRows>
+              : mode == kModeEmit  ? scan_wide_kernel<kModeEmit>
+                                   : nullptr;
+    if (!fn) return fail(KS_E_UNSUPPORTED, "wide automata: mode not supported");
+    size_t smem = 0;
+    a.hist_smem = 0;
+    if ((mode == kModeCount || mode == kModeRows) && size_t(a.n_accept) * 4 <= 96 * 1024) {
+        a.hist_smem = 1;
+        smem = size_t(a.n_accept) * 4;
+        if (smem > 48 * 1024)
+            KS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    }
+    const int threads = 256;
+    const int blocks = int(max64(1, min64((a.nchunks + threads - 1) / threads, int64_t(ctx->num_sms) * 8)));
+    fn<<<blocks, threads, smem, ctx->stream>>>(a);
     if (launches) ++*launches;
     KS_CUDA(cudaGetLastError());
     return KS_OK;

@@ -56,6 +56,8 @@ struct ScanArgs {
     int32_t any_state = 0;
     // automaton
     const uint16_t* t1 = nullptr;    // nq x 5 (global)
+    const uint32_t* t1w = nullptr;   // nq x 5, 32-bit ids (wide automata, scan_wide_kernel)
+    uint32_t* chunk_exit32 = nullptr;   // wide automata: per chunk exit state (optional)
     const uint16_t* tk = nullptr;    // nq x 4^K (global)
     int32_t nq = 0, n_accept = 0, reset_state = -1;
     int32_t tk_pad = 0, t1_pad = 0;  // uint16 entries, multiples of 8
@@ -91,6 +93,9 @@ __host__ __device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return
 // Launch one scan over [a.begin, a.end); fills chunk geometry, grid and smem.
 // Returns KS_OK or a KS_E_* code (error text set).
 int launch_scan(ks_ctx* ctx, ScanArgs a, int mode, int stride, bool smem_tables, int* launches);
+// Automata above kMaxStates (32-bit ids): one base per lookup from the
+// 1-base table through L1/L2, lookback entries only.
+int launch_scan_wide(ks_ctx* ctx, ScanArgs a, int mode, int* launches);
 
 // Chunk geometry used by launch_scan for a span (so callers can size arrays).
 void scan_geometry(const ks_ctx* ctx, int64_t begin, int64_t end, int stride, bool smem_tables,

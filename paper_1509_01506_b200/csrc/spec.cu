@@ -35,9 +35,10 @@ __device__ __forceinline__ void add_outputs(long long* row, uint32_t s, int32_t 
         atomicAdd(reinterpret_cast<unsigned long long*>(&row[ids[k]]), (unsigned long long)v);
 }
 
+template <class T>   // state id type of the tables: uint16_t, uint32_t for wide automata
 __global__ void speculate_kernel(SeqView seq, const int64_t* cbeg, const int64_t* cend,
-                                 const int64_t* pss_off, const uint16_t* pss, int32_t window,
-                                 const SpecTask* tasks, int32_t ntasks, const uint16_t* t1,
+                                 const int64_t* pss_off, const T* pss, int32_t window,
+                                 const SpecTask* tasks, int32_t ntasks, const T* t1,
                                  int32_t n_accept, const int32_t* off, const int32_t* ids,
                                  int32_t ne, int32_t* conv_out, long long* delta) {
     const int lane = threadIdx.x & 31;
@@ -54,7 +55,7 @@ __global__ void speculate_kernel(SeqView seq, const int64_t* cbeg, const int64_t
     int32_t conv = -1;
     for (int64_t j = 0; j < weff; ++j) {
         const uint32_t sym = seq_sym(seq, cb + j);
-        s = t1[s * 5u + sym];
+        s = t1[size_t(s) * 5 + sym];
         const uint32_t s0 = __shfl_sync(0xffffffffu, s, 0);
         const unsigned same = __match_any_sync(0xffffffffu, s) & 1u;
         if (live && conv < 0) {
@@ -75,8 +76,8 @@ __global__ void speculate_kernel(SeqView seq, const int64_t* cbeg, const int64_t
 }  // namespace
 
 int launch_speculate(ks_ctx* ctx, const SeqView& seq, int32_t n_chunks, const int64_t* d_cbeg,
-                     const int64_t* d_cend, const int64_t* d_pss_off, const uint16_t* d_pss,
-                     const int64_t* h_pss_off, int32_t window, const uint16_t* t1,
+                     const int64_t* d_cend, const int64_t* d_pss_off, const void* d_pss, bool wide,
+                     const int64_t* h_pss_off, int32_t window, const void* t1,
                      int32_t n_accept, const int32_t* off, const int32_t* ids, int32_t ne,
                      int32_t* d_conv, long long* d_delta, void* d_tasks_buf, int* launches) {
     std::vector<SpecTask> tasks;
@@ -95,9 +96,16 @@ int launch_speculate(ks_ctx* ctx, const SeqView& seq, int32_t n_chunks, const in
     const int threads = 256;
     const int64_t total = int64_t(tasks.size()) * 32;
     const int blocks = int((total + threads - 1) / threads);
-    speculate_kernel<<<blocks, threads, 0, ctx->stream>>>(
-        seq, d_cbeg, d_cend, d_pss_off, d_pss, window, static_cast<const SpecTask*>(d_tasks_buf),
-        int32_t(tasks.size()), t1, n_accept, off, ids, ne, d_conv, d_delta);
+    if (wide)
+        speculate_kernel<uint32_t><<<blocks, threads, 0, ctx->stream>>>(
+            seq, d_cbeg, d_cend, d_pss_off, static_cast<const uint32_t*>(d_pss), window,
+            static_cast<const SpecTask*>(d_tasks_buf), int32_t(tasks.size()), static_cast<const uint32_t*>(t1),
+            n_accept, off, ids, ne, d_conv, d_delta);
+    else
+        speculate_kernel<uint16_t><<<blocks, threads, 0, ctx->stream>>>(
+            seq, d_cbeg, d_cend, d_pss_off, static_cast<const uint16_t*>(d_pss), window,
+            static_cast<const SpecTask*>(d_tasks_buf), int32_t(tasks.size()), static_cast<const uint16_t*>(t1),
+            n_accept, off, ids, ne, d_conv, d_delta);
     if (launches) ++*launches;
     KS_CUDA(cudaGetLastError());
     // the task list lives in pageable host memory: finish before it goes away

@@ -372,6 +372,14 @@ int ks_count_host_bytes(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, in
         std::memset(counts_out, 0, size_t(dfa->host.ne) * 8);
         return KS_OK;
     }
+    if (dfa->host.wide) {   // wide automata: one device upload + the plain scan (no streaming form)
+        ks_seq* seq = nullptr;
+        int rc = ks_seq_upload_ascii(ctx, bytes, n_bytes, fasta, &seq);
+        if (rc) return rc;
+        rc = ks_count(ctx, dfa, seq, counts_out);
+        ks_seq_free(seq);
+        return rc;
+    }
     ctx->stats = ks_stats{};
     KS_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
     bool fallback = false;

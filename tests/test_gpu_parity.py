@@ -697,3 +697,65 @@ def test_degenerate_inputs(data, fasta):
     assert ctx.count(dh, sh).tolist() == want.tolist()
     rep = ks.run(w.dfa, ks.Sequence(sym), ks.EngineConfig(workers=3, mode="locate"))
     assert rep.per_expression_counts.tolist() == want.tolist()
+
+
+# ---------------------------------------------------------------- wide automata (> 32767 states)
+
+@pytest.fixture(scope="module")
+def wide_dfa():
+    rng = np.random.default_rng(5)
+    lits = set()
+    while len(lits) < 4600:
+        lits.add("".join(rng.choice(list("acgt"), size=int(rng.integers(12, 17)))))
+    text = "\n".join(sorted(lits)[:2300]) + "\n" + "|".join(sorted(lits)[2300:2400]) + "\n" + \
+        "\n".join(sorted(lits)[2400:]) + "\n"
+    dfa = ks.build_dfa(ks.expand_to_literals(ks.parse_expressions(text)))
+    assert dfa.state_count > 32767
+    return dfa, sorted(lits)
+
+
+def test_wide_automaton(wide_dfa):
+    """Automata above the 16-bit state range: 32-bit ids, LOOKBACK, the wide
+    scan kernel -- counts, sorted rows, ranges, run() with metadata, the
+    streamed call (which falls back to one upload) and the halo shard."""
+    import torch
+
+    dfa, lits = wide_dfa
+    rng = np.random.default_rng(9)
+    n = 1 << 20
+    sym = rng.integers(0, 4, n).astype(np.uint8)
+    for k in range(400):
+        lit = lits[int(rng.integers(0, len(lits)))]
+        p = int(rng.integers(0, n - len(lit)))
+        sym[p:p + len(lit)] = ["acgt".index(c) for c in lit]
+    sym[rng.integers(0, n, 40)] = 4
+    ctx = _native.context(0)
+    dh = ctx.dfa(dfa)
+    assert dh.info["strategy_name"] == "lookback"
+    want, rows, meta = O.ref_run(dfa, sym, 6, 10, True)
+    sh = ctx.upload_codes(sym)
+    got, grows = ctx.locate(dh, sh)
+    assert got.tolist() == want.tolist() and np.array_equal(grows, rows) and want.sum() >= 300
+    assert ctx.count(dh, sh).tolist() == want.tolist()
+    rep = ks.run(dfa, ks.Sequence(sym), ks.EngineConfig(workers=6, mode="locate"))
+    assert rep.per_expression_counts.tolist() == want.tolist() and np.array_equal(rep.locations, rows)
+    for key in ("pss_sizes", "speculative_runs", "converged_runs", "convergence_steps"):
+        assert rep.metadata[key] == meta[key], key
+    q = dfa.state_count - 3
+    wc, wl = O.ref_sequential_count(dfa, sym[1000:900_000], state=q)
+    c, last, _ = ctx.scan_range(dh, sh, 1000, 900_000, q)
+    assert c.tolist() == wc.tolist() and last == wl
+    ascii_ = np.frombuffer(b"acgtN", dtype=np.uint8)[sym].tobytes()
+    assert ctx.count_host_ascii(dh, ascii_).tolist() == want.tolist()
+    m = ctx.segment_map(dh, sh, 0, 5000)
+    assert int(m[0]) == int(O.ref_sequential_count(dfa, sym[:5000])[1])
+    half = n // 2
+    counts = np.zeros_like(want)
+    depth = dh.info["sync_depth"]
+    for r, (b, e, h) in enumerate(((0, half, 0), (half, n, 64 * (-(-depth // 64))))):
+        sub = ctx.upload_codes(sym[b - h:e])
+        t = torch.zeros(max(dfa.n_expressions, 1), dtype=torch.int64, device="cuda")
+        ctx.count_shard_async(dh, sub, h, h + (e - b), 0, r, t.data_ptr())
+        ctx.synchronize()
+        counts += t.cpu().numpy()[: dfa.n_expressions]
+    assert counts.tolist() == want.tolist()

@@ -16,7 +16,7 @@ w = workloads.make(3, 1 << 28)
 ctx = _native.context(0)
 sh = ctx.upload_ascii(w.ascii)
 sym = None
-for nlit, length in ((400, 12), (1000, 14), (2000, 14), (2600, 13)):
+for nlit, length in ((400, 12), (1000, 14), (2000, 14), (2600, 13), (6000, 14), (12000, 16)):
     lits = set()
     while len(lits) < nlit:
         lits.add("".join(rng.choice(list("acgt"), size=length)))
