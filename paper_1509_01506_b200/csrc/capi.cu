@@ -64,6 +64,21 @@ int ensure_pinned(ks_ctx* ctx, size_t bytes) {
     return KS_OK;
 }
 
+bool env_flag(const char* name) {
+    const char* v = std::getenv(name);
+    return v && *v && *v != '0';
+}
+
+// Pinned host memory the device can write through the same address (UVA).
+bool host_is_device_visible(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost && at.devicePointer == p;
+}
+
 namespace {
 
 // ------------------------------------------------------------ tiny kernels
@@ -194,6 +209,7 @@ int dispatch(ks_ctx* ctx, const ks_dfa* dfa, const DevTable& T, const ScanPlan& 
         a.tk = T.tkc;
         a.t1 = T.t1z;
         a.t1_pad = int32_t(T.t1z_bytes / 2);
+        a.t1_cols = T.t1z_cols;
         return launch_scan_fast(ctx, a, mode, T.fast_k, launches);
     }
     return launch_scan(ctx, a, mode, T.stride, dfa->tables_in_smem, launches);
@@ -329,9 +345,23 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
     Arena ar;
     int rc = ensure_scratch(ctx, need, &ar);
     if (rc) return rc;
-    // visits | counts | err | exit: one memset before, one D2H after
+    // visits | counts | err | exit: one memset before, one D2H after -- or,
+    // for a plain count on the fast kernel (the last CTA finalizes), the
+    // dfa's persistent block (kept zero by the kernel) and results written
+    // by the kernel straight into pinned host memory
     const size_t res_bytes = size_t(std::max(h.ne, 1)) * 8 + 16;
-    char* blk = static_cast<char*>(ar.take(size_t(h.n_accept) * 8 + res_bytes));
+    const bool fused = !locate && plan.fast && nch > 0;
+    char* scratch_blk = static_cast<char*>(ar.take(size_t(h.n_accept) * 8 + res_bytes));
+    char* blk = fused ? static_cast<char*>(dfa->d_cnt) : scratch_blk;
+    char* direct = nullptr;   // pinned host destination the kernel writes (counts | err | exit)
+    if (fused && !env_flag("KS_NO_DIRECT_RESULTS")) {
+        if (!async_dst) {
+            rc = ensure_pinned(ctx, res_bytes + 64);
+            if (rc) return rc;
+        }
+        char* host = async_dst ? reinterpret_cast<char*>(async_dst) : static_cast<char*>(ctx->pinned);
+        if (host_is_device_visible(host)) direct = host;
+    }
     unsigned long long* visits = reinterpret_cast<unsigned long long*>(blk);
     unsigned long long* counts = reinterpret_cast<unsigned long long*>(blk + size_t(h.n_accept) * 8);
     int32_t* err = reinterpret_cast<int32_t*>(counts + std::max(h.ne, 1));
@@ -356,7 +386,8 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
         mtmp = ar.take(exclusive_scan_monoid_tmp_bytes(nch));
     }
     if (spec) centry = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
-    KS_CUDA(cudaMemsetAsync(blk, 0, size_t(h.n_accept) * 8 + res_bytes, ctx->stream));
+    if (!fused) KS_CUDA(cudaMemsetAsync(blk, 0, size_t(h.n_accept) * 8 + res_bytes, ctx->stream));
+    if (direct && !async_dst) *reinterpret_cast<int32_t*>(direct + size_t(std::max(h.ne, 1)) * 8) = 0;   // err word
 
     ScanArgs a = base_args(dfa, dfa->scan, seq);
     a.begin = begin;
@@ -427,12 +458,15 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
         a.log_cap = cap;
     }
     // plain counts on the fast kernel: its last CTA finalizes (one launch per call)
-    const bool fused = !locate && plan.fast && nch > 0;
     if (fused) {
         a.fin_counts = counts;
         a.fin_exit_src = chunk_exit + (nch - 1);
-        a.fin_exit_dst = exit_slot;
-        a.fin_done = reinterpret_cast<unsigned int*>(err + 1);   // zeroed with the result block
+        a.fin_exit_dst = direct && !async_dst
+                             ? reinterpret_cast<uint16_t*>(direct + size_t(std::max(h.ne, 1)) * 8 + 8)
+                             : exit_slot;
+        a.fin_done = reinterpret_cast<unsigned int*>(err + 1);   // zero between calls
+        a.fin_host = reinterpret_cast<unsigned long long*>(direct);
+        a.n_expr = h.ne;
     }
     rc = dispatch(ctx, dfa, dfa->scan, plan, a, use_log ? kModeLog : locate ? kModeRows : kModeCount, &launches);
     if (rc) return rc;
@@ -445,7 +479,7 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
             KS_CUDA(cudaMemcpyAsync(exit_slot, a.chunk_exit32 + (nch - 1), 4, cudaMemcpyDeviceToDevice, ctx->stream));
     }
     if (async_dst) {
-        if (h.ne > 0)
+        if (h.ne > 0 && !direct)
             KS_CUDA(cudaMemcpyAsync(async_dst, counts, size_t(h.ne) * 8, cudaMemcpyDeviceToHost, ctx->stream));
         ctx->async_launches += launches;
         return KS_OK;
@@ -490,7 +524,7 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
     rc = ensure_pinned(ctx, size_t(std::max(h.ne, 1)) * 8 + 64);
     if (rc) return rc;
     char* pin = static_cast<char*>(ctx->pinned);
-    KS_CUDA(cudaMemcpyAsync(pin, counts, res_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    if (!direct) KS_CUDA(cudaMemcpyAsync(pin, counts, res_bytes, cudaMemcpyDeviceToHost, ctx->stream));
     uint16_t* pin_exit = reinterpret_cast<uint16_t*>(pin + size_t(std::max(h.ne, 1)) * 8 + 8);
     int64_t* host_rows = nullptr;
     if (locate) {
@@ -579,6 +613,7 @@ int upload_table(const CompiledTable& t, DevTable* d, char* blob, size_t* off, b
     d->fast_k = t.fast_k;
     d->hit_rate = t.hit_rate;
     d->t1z_bytes = align16(t.t1z.size() * 2);
+    d->t1z_cols = t.t1z_cols;
     if (t.fast_k) {
         d->tkc = reinterpret_cast<const uint16_t*>(place(t.tkc.data(), t.tkc.size() * 2));
         d->t1z = reinterpret_cast<const uint16_t*>(place(t.t1z.data(), t.t1z.size() * 2));
@@ -821,6 +856,14 @@ int ks_dfa_upload_ex(ks_ctx* ctx, const int32_t* transitions, int32_t n_states, 
         rebase(d->d_pss_off);
         rebase(d->d_pss_inv);
     }
+    const size_t cnt_bytes = size_t(h.n_accept) * 8 + size_t(std::max(h.ne, 1)) * 8 + 16;
+    if (cudaMalloc(&d->d_cnt, cnt_bytes) != cudaSuccess || cudaMemset(d->d_cnt, 0, cnt_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        if (d->d_cnt) cudaFree(d->d_cnt);
+        cudaFree(d->d_blob);
+        delete d;
+        return fail(KS_E_CUDA, "cudaMalloc(dfa result block)");
+    }
     const size_t smem_scan = d->scan.tk_bytes + d->scan.t1_bytes;
     const size_t smem_mono = h.strategy == KS_STRATEGY_MAPSCAN ? d->mono.tk_bytes + d->mono.t1_bytes : 0;
     d->tables_in_smem = !h.wide && std::max(smem_scan, smem_mono) + 1024 <= ctx->smem_optin;
@@ -855,6 +898,7 @@ int ks_dfa_free(ks_dfa* d) {
     if (!d) return KS_OK;
     DeviceGuard guard(d->ctx->device);
     if (d->d_blob) cudaFree(d->d_blob);
+    if (d->d_cnt) cudaFree(d->d_cnt);
     delete d;
     return KS_OK;
 }

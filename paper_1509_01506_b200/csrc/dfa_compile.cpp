@@ -76,8 +76,6 @@ void build_stride_table(CompiledTable* t, size_t budget) {
         const int fw = 1 << (2 * fk);
         const int z = nq;
         t->fast_k = fk;
-        t->t1z.assign(size_t(nq + 1) * 5, uint16_t(z));
-        std::copy(t->t1.begin(), t->t1.end(), t->t1z.begin());
         t->tkc.assign(size_t(1) << 16, uint16_t(z << 1));
         for (int w = 0; w < fw; ++w) {
             for (int s = 0; s < nq; ++s) {
@@ -119,6 +117,14 @@ void build_stride_table(CompiledTable* t, size_t budget) {
     bool resets = true;
     for (int s = 1; s < nq && resets; ++s) resets = t->t1[size_t(s) * 5 + 4] == r;
     t->reset_state = resets ? int(r) : -1;
+    // the fast kernel's 1-base table: 4 columns when OTHER resets every state
+    // (smaller shared footprint, a deeper hit ring), else all 5
+    if (t->fast_k) {
+        t->t1z_cols = resets ? 4 : 5;
+        t->t1z.assign(size_t(nq + 1) * t->t1z_cols, uint16_t(nq));
+        for (int s = 0; s < nq; ++s)
+            for (int c = 0; c < t->t1z_cols; ++c) t->t1z[size_t(s) * t->t1z_cols + c] = t->t1[size_t(s) * 5 + c];
+    }
 }
 
 // Smallest D with |delta(Q, w)| == 1 for all |w| == D, or -1.

@@ -49,7 +49,8 @@ struct CompiledTable {
     int fast_k = 0;                  // 0 = not eligible
     double hit_rate = 0;             // accepting-state visits per base on uniform random input
     std::vector<uint16_t> tkc;       // 65536 entries
-    std::vector<uint16_t> t1z;       // (nq + 1) x 5, row Z -> Z
+    std::vector<uint16_t> t1z;       // (nq + 1) x t1z_cols (4: OTHER resets, not stored)
+    int t1z_cols = 5;
 };
 
 struct HostDfa {
@@ -88,6 +89,7 @@ struct DevTable {
     size_t tk_bytes = 0, t1_bytes = 0;
     const uint16_t* tkc = nullptr;  // fast form (see CompiledTable)
     const uint16_t* t1z = nullptr;
+    int t1z_cols = 5;
     int fast_k = 0;
     size_t t1z_bytes = 0;
     double hit_rate = 0;
@@ -177,6 +179,10 @@ struct ks_dfa {
     int32_t* d_new_of_old = nullptr;
     int32_t* d_old_of_new = nullptr;
     void* d_blob = nullptr;   // single allocation backing the above
+    // persistent result block of the fused count (visits | counts | err |
+    // done | exit, the layout of scan_impl's result block); zero between
+    // calls: the kernel's last CTA cleans it, so a count needs no memset
+    void* d_cnt = nullptr;
     bool tables_in_smem = true;
 };
 

@@ -28,6 +28,8 @@ struct Arena {
 
 int ensure_scratch(ks_ctx* ctx, size_t bytes, Arena* a);
 int ensure_pinned(ks_ctx* ctx, size_t bytes);
+bool env_flag(const char* name);
+bool host_is_device_visible(const void* p);
 
 struct DeviceGuard {
     int prev = -1;

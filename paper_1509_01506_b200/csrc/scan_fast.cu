@@ -134,6 +134,8 @@ struct Ctx {
     int64_t row_base;
     uint32_t n_accept;
     uint32_t ring_thr;  // drain when a lane holds this many ring bytes (depth - chk_steps(K) entries)
+    uint32_t t1_cols;   // 4 or 5
+    uint32_t reset;     // OTHER target when t1_cols == 4
     LogEntry* log;
     unsigned long long* log_n;
     int64_t log_cap;
@@ -177,7 +179,8 @@ __device__ __forceinline__ void record(const Ctx& c, Lane<MODE>& L, int64_t pos,
 }
 
 __device__ __forceinline__ uint32_t step1(const Ctx& c, uint32_t s, uint32_t sym) {
-    return lds16(c.t1 + (s * 5u + sym) * 2u);
+    if (sym == 4u && c.t1_cols == 4u) return c.reset;   // OTHER column not stored
+    return lds16(c.t1 + (s * c.t1_cols + sym) * 2u);
 }
 
 // Re-walk one deferred K-step (ring value = its table byte address).
@@ -326,6 +329,8 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     c.row_base = a.row_base;
     c.n_accept = opaque(uint32_t(a.n_accept));
     c.ring_thr = uint32_t(a.ring_depth - chk_steps(K)) * kRingStride;
+    c.t1_cols = opaque(uint32_t(a.t1_cols));
+    c.reset = uint32_t(a.reset_state);
     c.log = a.log;
     c.log_n = a.log_n;
     c.log_cap = a.log_cap;
@@ -496,12 +501,26 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
             if (is_last) {
                 __threadfence();
                 if (threadIdx.x == 0 && a.fin_exit_src) *a.fin_exit_dst = __ldcg(a.fin_exit_src);
+                // counts accumulate in the (drained) ring's shared memory when they fit
+                const bool in_smem = size_t(a.n_expr) * 8 <= size_t(a.ring_depth) * 4 * blockDim.x;
+                unsigned long long* acc = in_smem ? reinterpret_cast<unsigned long long*>(p_ring) : a.fin_counts;
+                for (int e = threadIdx.x; e < a.n_expr; e += blockDim.x) acc[e] = 0ull;
+                __syncthreads();
                 for (int st = threadIdx.x; st < a.n_accept; st += blockDim.x) {
                     const unsigned long long v = __ldcg(&a.visits[st]);
                     if (!v) continue;
+                    a.visits[st] = 0ull;   // clean for the next call
                     for (int k = __ldg(&a.acc_out_off[st]); k < __ldg(&a.acc_out_off[st + 1]); ++k)
-                        atomicAdd(&a.fin_counts[__ldg(&a.acc_out_ids[k])], v);
+                        atomicAdd(&acc[__ldg(&a.acc_out_ids[k])], v);
                 }
+                if (!in_smem) __threadfence();
+                __syncthreads();
+                for (int e = threadIdx.x; e < a.n_expr; e += blockDim.x) {
+                    const unsigned long long v = in_smem ? acc[e] : __ldcg(&acc[e]);
+                    if (in_smem) a.fin_counts[e] = v;
+                    if (a.fin_host) a.fin_host[e] = v;   // pinned host memory: visible once the kernel completes
+                }
+                if (threadIdx.x == 0) *a.fin_done = 0u;
             }
         }
     }

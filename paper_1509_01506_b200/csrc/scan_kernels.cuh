@@ -61,6 +61,7 @@ struct ScanArgs {
     const uint16_t* tk = nullptr;    // nq x 4^K (global)
     int32_t nq = 0, n_accept = 0, reset_state = -1;
     int32_t tk_pad = 0, t1_pad = 0;  // uint16 entries, multiples of 8
+    int32_t t1_cols = 5;             // fast kernel: columns of t1 (4: OTHER -> reset_state)
     int32_t hist_smem = 0;           // histogram in shared memory
     int32_t ring_depth = 0;          // fast kernel: deferred hits per lane (set by launch_scan_fast)
     // outputs
@@ -75,11 +76,16 @@ struct ScanArgs {
     int64_t row_base = 0;                   // row offset = position + 1 + row_base
     int32_t* error = nullptr;               // set to 1 on an internal invariant failure
     // fast kernel, count mode: the last CTA turns visits into counts (fused
-    // finalize_counts; fin_done must be zero at launch)
+    // finalize_counts).  visits and fin_done must be zero at launch; the last
+    // CTA leaves them zero again (so a persistent block needs no memset),
+    // zeroes fin_counts itself, and copies the counts to fin_host (a device
+    // view of pinned host memory, so no D2H copy follows) when it is set.
     unsigned long long* fin_counts = nullptr;
     const uint16_t* fin_exit_src = nullptr;
     uint16_t* fin_exit_dst = nullptr;
     unsigned int* fin_done = nullptr;
+    unsigned long long* fin_host = nullptr;
+    int32_t n_expr = 0;
     LogEntry* log = nullptr;                // kModeLog
     unsigned long long* log_n = nullptr;    // kModeLog: visits appended (may exceed log_cap)
     int64_t log_cap = 0;
