@@ -215,11 +215,12 @@ int dispatch(ks_ctx* ctx, const ks_dfa* dfa, const DevTable& T, const ScanPlan& 
     return launch_scan(ctx, a, mode, T.stride, dfa->tables_in_smem, launches);
 }
 
-// Map pass + monoid scan over [begin, end): writes per-chunk exclusive
-// prefixes (if excl != null) and the total element into *d_total.
+// Map pass + single-pass monoid scan over [begin, end): the entry state of
+// every chunk into centry (if not null; the range starts in entry_val >= 0
+// or *entry_ptr) and the product of all chunk elements into *d_total.
 int monoid_prefix(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end,
-                  int64_t origin, int64_t L, int64_t nch, uint16_t* elems, uint16_t* excl,
-                  uint16_t* d_total, void* tmp, int* launches) {
+                  int64_t origin, int64_t L, int64_t nch, uint16_t* elems, uint16_t* centry, int32_t entry_val,
+                  const uint16_t* entry_ptr, uint16_t* d_total, int* launches, PhaseTrace* trace) {
     const HostDfa& h = dfa->host;
     ScanArgs m = base_args(dfa, dfa->mono, seq);
     m.begin = begin;
@@ -230,9 +231,14 @@ int monoid_prefix(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t beg
     m.uniform_entry = 0;  // identity element
     m.n_accept = 0;
     m.chunk_exit = elems;
+    if (h.mono_sub) m.map_dirty = dfa->d_prod + size_t(h.mono_other) * h.nm;
     int rc = dispatch(ctx, dfa, dfa->mono, plan_for(ctx, dfa, dfa->mono), m, kModeMap, launches);
     if (rc != KS_OK) return rc;
-    return exclusive_scan_monoid(ctx, elems, nch, dfa->d_prod, h.nm, excl, d_total, tmp, launches);
+    if (trace) trace->mark("map pass");
+    rc = monoid_scan_entries(ctx, elems, nch, dfa->d_prod, h.nm, dfa->d_action, h.nq, entry_val, entry_ptr, centry,
+                             d_total, launches);
+    if (trace) trace->mark("monoid scan");
+    return rc;
 }
 
 // True internal state of the sequence at position pos (state after pos bases).
@@ -295,13 +301,11 @@ int true_state_at(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t pos
         *out = v;
         return KS_OK;
     }
-    int rc = ensure_scratch(ctx, size_t(nch) * 4 + exclusive_scan_monoid_tmp_bytes(nch) + 4096, &ar);
+    int rc = ensure_scratch(ctx, size_t(nch) * 4 + 4096, &ar);
     if (rc) return rc;
     uint16_t* elems = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
-    uint16_t* excl = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
     uint16_t* tot = static_cast<uint16_t*>(ar.take(16));
-    void* tmp = ar.take(exclusive_scan_monoid_tmp_bytes(nch));
-    rc = monoid_prefix(ctx, dfa, seq, 0, pos, origin, L, nch, elems, excl, tot, tmp, launches);
+    rc = monoid_prefix(ctx, dfa, seq, 0, pos, origin, L, nch, elems, nullptr, 0, nullptr, tot, launches);
     if (rc) return rc;
     uint16_t m = 0;
     KS_CUDA(cudaMemcpyAsync(&m, tot, 2, cudaMemcpyDeviceToHost, ctx->stream));
@@ -340,7 +344,7 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
     const bool spec = h.strategy == KS_STRATEGY_SPECULATE;
     size_t need = size_t(h.n_accept) * 8 + size_t(std::max(h.ne, 1)) * 8 + size_t(nch) * 2 + 4096;
     if (locate) need += size_t(nch) * 4 + size_t(nch + 1) * 8 + exclusive_scan_rows_tmp_bytes(nch) + 8 * kAlign;
-    if (mapscan) need += size_t(nch) * 6 + exclusive_scan_monoid_tmp_bytes(nch) + 4 * kAlign;
+    if (mapscan) need += size_t(nch) * 6 + 4 * kAlign;
     if (spec) need += size_t(nch) * 2 + 2 * kAlign;
     Arena ar;
     int rc = ensure_scratch(ctx, need, &ar);
@@ -376,14 +380,11 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
         row_off = static_cast<int64_t*>(ar.take(size_t(nch + 1) * 8));
         rows_tmp = ar.take(exclusive_scan_rows_tmp_bytes(nch));
     }
-    uint16_t *elems = nullptr, *excl = nullptr, *centry = nullptr, *mtot = nullptr;
-    void* mtmp = nullptr;
+    uint16_t *elems = nullptr, *centry = nullptr, *mtot = nullptr;
     if (mapscan) {
         elems = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
-        excl = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
         centry = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
         mtot = static_cast<uint16_t*>(ar.take(16));
-        mtmp = ar.take(exclusive_scan_monoid_tmp_bytes(nch));
     }
     if (spec) centry = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
     if (!fused) KS_CUDA(cudaMemsetAsync(blk, 0, size_t(h.n_accept) * 8 + res_bytes, ctx->stream));
@@ -420,11 +421,13 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
         ++ctx->n_async;
     }
     KS_CUDA(cudaEventRecord(ev_a, ctx->stream));
+    PhaseTrace trace(ctx->stream);
+    trace.mark("start");
     if (mapscan && nch > 0) {
-        rc = monoid_prefix(ctx, dfa, seq, begin, end, origin, L, nch, elems, excl, mtot, mtmp, &launches);
+        rc = monoid_prefix(ctx, dfa, seq, begin, end, origin, L, nch, elems, centry, entry, nullptr, mtot, &launches,
+                           &trace);
         if (rc) return rc;
-        rc = launch_chunk_entry(ctx, excl, nch, dfa->d_action, h.nq, entry, nullptr, centry, &launches);
-        if (rc) return rc;
+        trace.mark("chunk_entry");
         a.chunk_entry = centry;
     }
     if (spec && nch > 0) {
@@ -470,6 +473,7 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
     }
     rc = dispatch(ctx, dfa, dfa->scan, plan, a, use_log ? kModeLog : locate ? kModeRows : kModeCount, &launches);
     if (rc) return rc;
+    trace.mark("scan");
     KS_CUDA(cudaEventRecord(ev_b, ctx->stream));
     if (!fused) {
         rc = launch_finalize_counts(ctx, visits, h.n_accept, dfa->d_acc_out_off, dfa->d_acc_out_ids, counts,
@@ -633,7 +637,7 @@ int choose_lb(const ks_ctx* ctx, int64_t n) {
         const int64_t tile = int64_t(2048) << lb;
         const int64_t tiles = (n + tile - 1) / tile;
         const int64_t per_warp = (tiles + warps - 1) / warps;
-        const double cost = double(per_warp) * double((64 << lb) + 32);
+        const double cost = double(per_warp) * double((64 << lb) + 64);   // ~64 bases of per-unit overhead
         if (cost <= best_cost) {
             best_cost = cost;
             best = lb;
@@ -731,6 +735,7 @@ int ks_close(ks_ctx* ctx) {
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->sbuf) cudaFree(ctx->sbuf);
     if (ctx->spec_buf) cudaFree(ctx->spec_buf);
+    if (ctx->mstat) cudaFree(ctx->mstat);
     if (ctx->log_buf) cudaFree(ctx->log_buf);
     if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
     delete ctx->pool;
@@ -1055,6 +1060,7 @@ int ks_async_wait(ks_ctx* ctx, float* scan_ms_total, int32_t* calls, int32_t* la
         total += ms;
     }
     if (scan_ms_total) *scan_ms_total = total;
+    PhaseTrace::flush();
     if (calls) *calls = ctx->n_async;
     if (launches) *launches = ctx->async_launches;
     ctx->n_async = 0;
@@ -1102,13 +1108,11 @@ int ks_segment_map(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t be
         uint16_t m = 0;
         if (end > begin) {
             Arena ar;
-            int rc = ensure_scratch(ctx, size_t(nch) * 4 + exclusive_scan_monoid_tmp_bytes(nch) + 4096, &ar);
+            int rc = ensure_scratch(ctx, size_t(nch) * 4 + 4096, &ar);
             if (rc) return rc;
             uint16_t* elems = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
-            uint16_t* excl = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
             uint16_t* tot = static_cast<uint16_t*>(ar.take(16));
-            void* tmp = ar.take(exclusive_scan_monoid_tmp_bytes(nch));
-            rc = monoid_prefix(ctx, dfa, seq, begin, end, origin, L, nch, elems, excl, tot, tmp, &launches);
+            rc = monoid_prefix(ctx, dfa, seq, begin, end, origin, L, nch, elems, nullptr, 0, nullptr, tot, &launches);
             if (rc) return rc;
             KS_CUDA(cudaMemcpyAsync(&m, tot, 2, cudaMemcpyDeviceToHost, ctx->stream));
             KS_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1143,15 +1147,13 @@ int ks_segment_map_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
     int64_t origin, L, nch;
     geometry(seq, begin, end, &origin, &L, &nch);
     Arena ar;
-    int rc = ensure_scratch(ctx, size_t(nch) * 4 + exclusive_scan_monoid_tmp_bytes(nch) + 4096, &ar);
+    int rc = ensure_scratch(ctx, size_t(nch) * 4 + 4096, &ar);
     if (rc) return rc;
     uint16_t* elems = static_cast<uint16_t*>(ar.take(size_t(nch) * 2 + 2));
-    uint16_t* excl = static_cast<uint16_t*>(ar.take(size_t(nch) * 2 + 2));
     uint16_t* tot = static_cast<uint16_t*>(ar.take(16));
-    void* tmp = ar.take(exclusive_scan_monoid_tmp_bytes(nch));
     int launches = 0;
     if (nch > 0) {
-        rc = monoid_prefix(ctx, dfa, seq, begin, end, origin, L, nch, elems, excl, tot, tmp, &launches);
+        rc = monoid_prefix(ctx, dfa, seq, begin, end, origin, L, nch, elems, nullptr, 0, nullptr, tot, &launches);
         if (rc) return rc;
     } else {
         KS_CUDA(cudaMemsetAsync(tot, 0, 2, ctx->stream));  // identity element
@@ -1181,7 +1183,7 @@ int ks_count_shard_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
     const bool spec = h.strategy == KS_STRATEGY_SPECULATE;
     Arena ar;
     size_t need = size_t(h.n_accept) * 8 + size_t(nch) * 2 + 64 * kAlign;
-    if (mapscan) need += size_t(nch) * 6 + exclusive_scan_monoid_tmp_bytes(nch);
+    if (mapscan) need += size_t(nch) * 6;
     if (spec) need += size_t(nch) * 2;
     int rc = ensure_scratch(ctx, need, &ar);
     if (rc) return rc;
@@ -1207,13 +1209,9 @@ int ks_count_shard_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
         a.chunk_exit = chunk_exit;
         if (mapscan) {
             uint16_t* elems = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
-            uint16_t* excl = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
             uint16_t* centry = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
             uint16_t* mtot = static_cast<uint16_t*>(ar.take(16));
-            void* mtmp = ar.take(exclusive_scan_monoid_tmp_bytes(nch));
-            rc = monoid_prefix(ctx, dfa, seq, begin, end, origin, L, nch, elems, excl, mtot, mtmp, &launches);
-            if (rc) return rc;
-            rc = launch_chunk_entry(ctx, excl, nch, dfa->d_action, h.nq, 0, entry, centry, &launches);
+            rc = monoid_prefix(ctx, dfa, seq, begin, end, origin, L, nch, elems, centry, 0, entry, mtot, &launches);
             if (rc) return rc;
             a.chunk_entry = centry;
         } else if (spec) {

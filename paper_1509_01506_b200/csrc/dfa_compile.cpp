@@ -16,6 +16,7 @@
 //     is small: chunk maps become monoid element ids, composed by a
 //     product-table lookup in an exclusive device-wide scan.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -170,8 +171,10 @@ int synchronisation_depth(const std::vector<T>& t1, int nq) {
     return -1;
 }
 
-// Closure of the column maps; false if it exceeds the caps.
-bool build_monoid(const CompiledTable& t, int start, HostDfa* h) {
+// Closure of the column maps; false if it exceeds the caps.  With `sub`
+// (OTHER resets every state) the OTHER-free submonoid is closed first, so its
+// elements take the ids [0, nS), and `mono` is built over it alone.
+bool build_monoid(const CompiledTable& t, int start, bool sub, HostDfa* h) {
     const int nq = t.nq;
     const size_t cap_entries = size_t(16) << 20;
     std::vector<uint16_t> maps(nq);
@@ -182,39 +185,51 @@ bool build_monoid(const CompiledTable& t, int start, HostDfa* h) {
         return std::string(reinterpret_cast<const char*>(m), size_t(nq) * 2);
     };
     ids.emplace(key_of(maps.data()), 0);
-    std::vector<int32_t> mt;  // nm x 5
+    std::vector<int32_t> mt(5, -1);  // nm x 5
     std::vector<uint16_t> next(nq);
-    for (size_t m = 0; m < parent.size(); ++m) {
-        for (int c = 0; c < 5; ++c) {
-            const uint16_t* src = &maps[m * nq];
-            for (int q = 0; q < nq; ++q) next[q] = t.t1[size_t(src[q]) * 5 + c];
-            auto key = key_of(next.data());
-            auto it = ids.find(key);
-            int id;
-            if (it == ids.end()) {
-                id = int(parent.size());
-                if (id >= kMaxMonoid || size_t(id + 1) * nq > cap_entries) return false;
-                ids.emplace(std::move(key), id);
-                maps.insert(maps.end(), next.begin(), next.end());
-                parent.push_back(int32_t(m));
-                psym.push_back(c);
-            } else {
-                id = it->second;
+    int n_sub = -1;
+    for (int phase = sub ? 0 : 1; phase < 2; ++phase) {
+        const int nsym = phase == 0 ? 4 : 5;
+        for (size_t m = 0; m < parent.size(); ++m) {
+            for (int c = 0; c < nsym; ++c) {
+                if (mt[m * 5 + c] >= 0) continue;
+                const uint16_t* src = &maps[m * nq];
+                for (int q = 0; q < nq; ++q) next[q] = t.t1[size_t(src[q]) * 5 + c];
+                auto key = key_of(next.data());
+                auto it = ids.find(key);
+                int id;
+                if (it == ids.end()) {
+                    id = int(parent.size());
+                    if (id >= kMaxMonoid || size_t(id + 1) * nq > cap_entries) return false;
+                    ids.emplace(std::move(key), id);
+                    maps.insert(maps.end(), next.begin(), next.end());
+                    parent.push_back(int32_t(m));
+                    psym.push_back(c);
+                    mt.resize(mt.size() + 5, -1);
+                } else {
+                    id = it->second;
+                }
+                mt[m * 5 + c] = id;
             }
-            mt.push_back(id);
         }
+        if (phase == 0) n_sub = int(parent.size());
     }
     const int nm = int(parent.size());
     h->nm = nm;
-    h->mono.nq = nm;
+    h->mono_sub = sub;
+    h->mono_other = mt[4];
+    const int nrow = sub ? n_sub : nm;
+    h->mono.nq = nrow;
     h->mono.n_accept = 0;
-    h->mono.t1.resize(size_t(nm) * 5);
-    for (size_t i = 0; i < mt.size(); ++i) h->mono.t1[i] = uint16_t(mt[i]);
+    h->mono.t1.resize(size_t(nrow) * 5);
+    for (int m = 0; m < nrow; ++m)
+        for (int c = 0; c < 5; ++c)   // submonoid: OTHER is tracked by the kernels, the column is the identity
+            h->mono.t1[size_t(m) * 5 + c] = uint16_t(sub && c == 4 ? 0 : mt[size_t(m) * 5 + c]);
     h->prod.assign(size_t(nm) * nm, 0);
     for (int a = 0; a < nm; ++a) {
         uint16_t* row = &h->prod[size_t(a) * nm];
         row[0] = uint16_t(a);
-        for (int b = 1; b < nm; ++b)  // parents precede children in BFS order
+        for (int b = 1; b < nm; ++b)  // parents precede children in discovery order
             row[b] = uint16_t(mt[size_t(row[parent[b]]) * 5 + psym[b]]);
     }
     h->act0.resize(nm);
@@ -309,7 +324,8 @@ int compile_dfa(const int32_t* trans, int nq, const int32_t* out_off, const int3
         h->strategy = KS_STRATEGY_LOOKBACK;
         return KS_OK;
     }
-    if (force_strategy != KS_STRATEGY_SPECULATE && build_monoid(t, h->start_internal, h)) {
+    if (force_strategy != KS_STRATEGY_SPECULATE &&
+        build_monoid(t, h->start_internal, t.reset_state >= 0 && !(std::getenv("KS_MONO_FULL") && *std::getenv("KS_MONO_FULL") == '1'), h)) {
         build_stride_table(&h->mono, smem_budget > 4096 ? smem_budget - 4096 : 0);
         h->strategy = KS_STRATEGY_MAPSCAN;
         return KS_OK;

@@ -67,6 +67,12 @@ struct HostDfa {
     // MAPSCAN
     int nm = 0;
     CompiledTable mono;                 // transition-monoid automaton (no hits)
+    // mono_sub: when OTHER resets the automaton, `mono` covers only the
+    // OTHER-free submonoid (ids [0, mono.nq), numbered first; its OTHER column
+    // is the identity) and a chunk holding OTHER maps to const(reset) times
+    // the element of what follows its last OTHER: prod[mono_other][e]
+    bool mono_sub = false;
+    int mono_other = -1;                // id of const(reset) = identity . OTHER
     std::vector<uint16_t> prod;         // nm x nm: element(a then b)
     std::vector<uint16_t> act0;         // nm: internal state reached from START
     std::vector<uint16_t> action;       // nm x nq: internal state reached from q
@@ -153,6 +159,11 @@ struct ks_ctx {
     // SPECULATE chunk maps (grow-only, separate from `scratch`)
     void* spec_buf = nullptr;
     size_t spec_bytes = 0;
+    // single-pass monoid scan: per-tile status words (epoch | flag | element),
+    // zeroed once at allocation; every launch uses a fresh epoch
+    unsigned long long* mstat = nullptr;
+    int64_t mstat_cap = 0;
+    uint32_t mepoch = 0;
     // single-pass locate log (grow-only)
     void* log_buf = nullptr;
     size_t log_bytes = 0;

@@ -1,14 +1,18 @@
-// Exclusive device-wide scans (reduce-then-scan, three launches).
+// Exclusive device-wide scans.
 //
 // * rows:   uint32 per-chunk row counts -> int64 exclusive offsets (locate
 //           compaction: every chunk writes its rows at its offset, so the
 //           concatenation is already sorted by (offset, id) -- no sort, unlike
-//           the reference's np.lexsort in engine.py:176);
-// * monoid: per-chunk transition-monoid elements -> exclusive prefix
-//           elements under the (non-commutative) product table.  This is the
-//           composition of chunk "start-state -> end-state" maps that fixes
-//           every chunk's true start state (the reference's left-to-right
-//           chain walk, engine.py:155-163, done as a scan).
+//           the reference's np.lexsort in engine.py:176); reduce-then-scan,
+//           three launches (also the running max of the FASTA line state);
+// * monoid: per-chunk transition-monoid elements -> each chunk's entry state,
+//           the composition of chunk "start-state -> end-state" maps (the
+//           reference's left-to-right chain walk, engine.py:155-163, done as
+//           a scan).  The product is a dependent L2 lookup in the nm x nm
+//           table, so depth is what costs: one single-pass launch with
+//           decoupled look-back (tiles publish their product, then their
+//           inclusive prefix; a tile composes its predecessors' words 32 at a
+//           time) that also applies the prefix to the entry state.
 #include <algorithm>
 
 #include "scan_kernels.cuh"
@@ -52,10 +56,6 @@ __device__ long long load_item<AddOp>(const void* in, int64_t i, int64_t n, cons
 template <>
 __device__ long long load_item<MaxOp>(const void* in, int64_t i, int64_t n, const MaxOp& op) {
     return i < n ? static_cast<const long long*>(in)[i] : op.identity();
-}
-template <>
-__device__ unsigned int load_item<MonoidOp>(const void* in, int64_t i, int64_t n, const MonoidOp& op) {
-    return i < n ? (unsigned int)static_cast<const uint16_t*>(in)[i] : op.identity();
 }
 
 // Block-wide exclusive scan of one value per thread (order = thread order).
@@ -156,13 +156,95 @@ int run_scan(ks_ctx* ctx, const void* in, int64_t n, const Op& op, Out* out, typ
     return KS_OK;
 }
 
+
+// ---------------------------------------------------------------- single pass
+// Status word of a tile: epoch << 32 | flag << 16 | element (flag 1: the
+// tile's own product, 2: inclusive prefix through the tile).
+constexpr unsigned kAgg = 1u, kIncl = 2u;
+
+__device__ __forceinline__ unsigned long long status_word(uint32_t epoch, unsigned flag, unsigned v) {
+    return (static_cast<unsigned long long>(epoch) << 32) | (flag << 16) | (v & 0xFFFFu);
+}
+
+__global__ void __launch_bounds__(kThreads) monoid_entry_scan_kernel(
+    const uint16_t* __restrict__ in, int64_t n, MonoidOp op, const uint16_t* __restrict__ action, int32_t nq,
+    int32_t entry_val, const uint16_t* entry_ptr, uint16_t* __restrict__ centry, uint16_t* d_total,
+    unsigned long long* status, uint32_t epoch) {
+    using T = unsigned int;
+    __shared__ T s_prefix;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t ntiles = (n + kTile - 1) / kTile;
+    const uint32_t q0 = entry_ptr ? uint32_t(*entry_ptr) : uint32_t(entry_val);
+    // tiles in launch order: every tile a CTA waits for belongs to a CTA of
+    // this (co-resident) grid that started it earlier
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t base = t * kTile + int64_t(threadIdx.x) * kItems;
+        T items[kItems];
+        T acc = op.identity();
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {
+            items[i] = base + i < n ? T(in[base + i]) : op.identity();
+            acc = op(acc, items[i]);
+        }
+        T total;
+        const T ex = block_exclusive<MonoidOp>(acc, op, &total);
+        if (warp == 0) {
+            T prefix = op.identity();
+            if (t == 0) {
+                if (lane == 0) atomicExch(&status[0], status_word(epoch, kIncl, total));
+            } else {
+                if (lane == 0) atomicExch(&status[t], status_word(epoch, kAgg, total));
+                // look back over windows of 32 predecessors (lane i: tile j - i)
+                T run = op.identity();
+                for (int64_t j = t - 1;; j -= 32) {
+                    const int64_t k = j - lane;
+                    unsigned flag = kIncl;
+                    T v = op.identity();
+                    if (k >= 0) {
+                        unsigned long long w;
+                        do {
+                            w = atomicAdd(&status[k], 0ull);
+                        } while (uint32_t(w >> 32) != epoch);
+                        flag = unsigned(w >> 16) & 0xFFFFu;
+                        v = T(w & 0xFFFFu);
+                    }
+                    const unsigned incl = __ballot_sync(0xffffffffu, flag == kIncl);
+                    const int stop = incl ? __ffs(incl) - 1 : 32;
+                    T x = lane <= stop ? v : op.identity();
+                    // product in decreasing lane order (older tiles first)
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const T y = __shfl_down_sync(0xffffffffu, x, d);
+                        if (lane + d < 32) x = op(y, x);
+                    }
+                    run = op(__shfl_sync(0xffffffffu, x, 0), run);
+                    if (stop < 32) break;
+                }
+                prefix = run;
+                if (lane == 0) atomicExch(&status[t], status_word(epoch, kIncl, op(prefix, total)));
+            }
+            if (lane == 0) {
+                s_prefix = prefix;
+                if (t == ntiles - 1 && d_total) *d_total = uint16_t(op(prefix, total));
+            }
+        }
+        __syncthreads();
+        if (centry) {
+            T run = op(s_prefix, ex);
+#pragma unroll
+            for (int i = 0; i < kItems; ++i) {
+                if (base + i < n) centry[base + i] = action[size_t(run) * nq + q0];
+                run = op(run, items[i]);
+            }
+        }
+        __syncthreads();   // s_prefix is rewritten by the next tile
+    }
+}
+
 }  // namespace
 
 size_t exclusive_scan_rows_tmp_bytes(int64_t n) {
     return size_t(std::max<int64_t>(1, (n + kTile - 1) / kTile)) * sizeof(long long) + 256;
-}
-size_t exclusive_scan_monoid_tmp_bytes(int64_t n) {
-    return size_t(std::max<int64_t>(1, (n + kTile - 1) / kTile)) * sizeof(unsigned int) + 256;
 }
 
 int exclusive_scan_rows(ks_ctx* ctx, const uint32_t* in, int64_t n, int64_t* out_excl,
@@ -179,20 +261,35 @@ int exclusive_scan_max(ks_ctx* ctx, const int64_t* in, int64_t n, int64_t* out_e
                                       reinterpret_cast<long long*>(d_total), tmp, launches);
 }
 
-// d_total receives the product of all n elements (as uint16 via a uint32 slot).
-int exclusive_scan_monoid(ks_ctx* ctx, const uint16_t* in, int64_t n, const uint16_t* prod,
-                          int32_t nm, uint16_t* out_excl, uint16_t* d_total, void* tmp,
-                          int* launches) {
-    MonoidOp op{prod, nm};
-    // the total goes through a 32-bit slot placed after the tile aggregates
-    const int64_t ntiles = std::max<int64_t>(1, (n + kTile - 1) / kTile);
-    unsigned int* total32 = static_cast<unsigned int*>(tmp) + ntiles;
-    int rc = run_scan<MonoidOp, uint16_t>(ctx, in, n, op, out_excl, total32, tmp, launches);
-    if (rc != KS_OK) return rc;
-    if (d_total) {
-        KS_CUDA(cudaMemcpyAsync(d_total, total32, sizeof(uint16_t), cudaMemcpyDeviceToDevice,
-                                ctx->stream));
+
+}  // namespace ks
+
+namespace ks {
+
+int monoid_scan_entries(ks_ctx* ctx, const uint16_t* in, int64_t n, const uint16_t* prod, int32_t nm,
+                        const uint16_t* action, int32_t nq, int32_t entry_val, const uint16_t* entry_ptr,
+                        uint16_t* centry, uint16_t* d_total, int* launches) {
+    if (n <= 0) return KS_OK;
+    const int64_t ntiles = (n + kTile - 1) / kTile;
+    if (ctx->mstat_cap < ntiles) {
+        KS_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (ctx->mstat) KS_CUDA(cudaFree(ctx->mstat));
+        ctx->mstat = nullptr;
+        ctx->mstat_cap = 0;
+        const int64_t cap = std::max<int64_t>(ntiles, 1024);
+        KS_CUDA(cudaMalloc(&ctx->mstat, size_t(cap) * 8));
+        KS_CUDA(cudaMemset(ctx->mstat, 0, size_t(cap) * 8));
+        ctx->mstat_cap = cap;
     }
+    if (++ctx->mepoch == 0) ctx->mepoch = 1;   // epoch 0 marks never-written words
+    int per_sm = 0;
+    KS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, monoid_entry_scan_kernel, kThreads, 0));
+    const int64_t grid = std::min<int64_t>(ntiles, int64_t(std::max(per_sm, 1)) * ctx->num_sms);
+    monoid_entry_scan_kernel<<<int(grid), kThreads, 0, ctx->stream>>>(in, n, MonoidOp{prod, nm}, action, nq,
+                                                                      entry_val, entry_ptr, centry, d_total,
+                                                                      ctx->mstat, ctx->mepoch);
+    if (launches) ++*launches;
+    KS_CUDA(cudaGetLastError());
     return KS_OK;
 }
 

@@ -4,6 +4,10 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <utility>
+#include <vector>
 
 #include "host_pack.h"
 #include "scan_kernels.cuh"
@@ -57,9 +61,60 @@ ScanPlan plan_for(const ks_ctx* ctx, const ks_dfa* dfa, const DevTable& T);
 void geometry(const ks_seq* seq, int64_t begin, int64_t end, int64_t* origin, int64_t* L, int64_t* nch);
 int dispatch(ks_ctx* ctx, const ks_dfa* dfa, const DevTable& T, const ScanPlan& p, ScanArgs a, int mode,
              int* launches);
+// KS_PHASE_TRACE=1: stream-ordered events between the phases of a scan,
+// printed to stderr once the call completes (diagnostics only).
+// KS_PHASE_TRACE=2: the same, deferred -- no synchronisation per call; the
+// phases of every call are printed by ks_async_wait (async pipelines).
+struct PhaseTrace {
+    using Marks = std::vector<std::pair<const char*, cudaEvent_t>>;
+    cudaStream_t st = nullptr;
+    bool deferred = false;
+    Marks marks;
+    explicit PhaseTrace(cudaStream_t s) {
+        if (env_flag("KS_PHASE_TRACE")) {
+            st = s;
+            const char* v = std::getenv("KS_PHASE_TRACE");
+            deferred = v[0] == '2';
+        }
+    }
+    void mark(const char* name) {
+        if (!st) return;
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return;
+        cudaEventRecord(e, st);
+        marks.emplace_back(name, e);
+    }
+    static std::vector<Marks>& pending() {
+        static std::vector<Marks> p;
+        return p;
+    }
+    static void print(Marks& m) {
+        for (size_t i = 1; i < m.size(); ++i) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, m[i - 1].second, m[i].second);
+            std::fprintf(stderr, "[ks phase] %-14s %9.1f us\n", m[i].first, ms * 1e3f);
+        }
+        for (auto& x : m) cudaEventDestroy(x.second);
+        m.clear();
+    }
+    static void flush() {   // after a synchronisation
+        for (auto& m : pending()) print(m);
+        pending().clear();
+    }
+    ~PhaseTrace() {
+        if (!st || marks.empty()) return;
+        if (deferred) {
+            pending().push_back(std::move(marks));
+            return;
+        }
+        cudaStreamSynchronize(st);
+        print(marks);
+    }
+};
+
 int monoid_prefix(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end,
-                  int64_t origin, int64_t L, int64_t nch, uint16_t* elems, uint16_t* excl, uint16_t* d_total,
-                  void* tmp, int* launches);
+                  int64_t origin, int64_t L, int64_t nch, uint16_t* elems, uint16_t* centry, int32_t entry_val,
+                  const uint16_t* entry_ptr, uint16_t* d_total, int* launches, PhaseTrace* trace = nullptr);
 int spec_entries(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end, int64_t origin,
                  int64_t L, int64_t nch, int32_t entry_val, const uint16_t* entry_ptr, uint16_t* centry,
                  uint16_t* d_exit, int* launches);

@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(1024, 1) scan_kernel(const ScanArgs a) {
         int64_t b = cb >> 6;
         const int64_t bend = (ce + 63) >> 6;
         const int lb = a.seq.lb;
+        bool dirty = false;   // kModeMap over the submonoid: OTHER inside the chunk
         uint4 wb = __ldg(bases4 + blk_slot(b, lb));
         uint64_t wm = __ldg(nmask + blk_slot(b, lb));
         for (; b < bend; ++b) {
@@ -201,6 +202,10 @@ __global__ void __launch_bounds__(1024, 1) scan_kernel(const ScanArgs a) {
             const uint64_t w1 = (uint64_t(wb.w) << 32) | wb.z;
             const bool full = (lo == 0) && (hi == 64);
             const bool alln = wm == ~0ull;
+            if constexpr (MODE == kModeMap) {
+                if (wm && a.map_dirty)
+                    dirty |= (wm & ((hi >= 64 ? ~0ull : ((1ull << hi) - 1ull)) & (~0ull << lo))) != 0ull;
+            }
             const bool fast = full && (wm == 0ull || (alln && a.reset_state >= 0));
             if (__all_sync(__activemask(), fast)) {
                 const uint32_t s2 = fast_block<K, MODE, SM>(s, w0, w1, !alln, p0, a.n_accept, T, sink);
@@ -225,6 +230,9 @@ __global__ void __launch_bounds__(1024, 1) scan_kernel(const ScanArgs a) {
             }
             wb = nb;
             wm = nm;
+        }
+        if constexpr (MODE == kModeMap) {
+            if (dirty) s = __ldg(&a.map_dirty[s]);
         }
         if (a.chunk_exit) a.chunk_exit[c] = uint16_t(s);
         if constexpr (MODE == kModeRows) a.chunk_rows[c] = sink.nrows;
@@ -354,13 +362,6 @@ __global__ void finalize_counts_kernel(const unsigned long long* visits, int32_t
     }
 }
 
-__global__ void chunk_entry_kernel(const uint16_t* excl, int64_t n, const uint16_t* action,
-                                   int32_t nq, int32_t entry, const uint16_t* entry_ptr, uint16_t* out) {
-    const int32_t q = entry_ptr ? int32_t(*entry_ptr) : entry;
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += int64_t(gridDim.x) * blockDim.x)
-        out[i] = action[size_t(excl[i]) * nq + q];
-}
 
 }  // namespace
 
@@ -441,16 +442,5 @@ int launch_scan_wide(ks_ctx* ctx, ScanArgs a, int mode, int* launches) {
     return KS_OK;
 }
 
-int launch_chunk_entry(ks_ctx* ctx, const uint16_t* excl, int64_t n, const uint16_t* action,
-                       int32_t nq, int32_t entry, const uint16_t* entry_ptr, uint16_t* chunk_entry,
-                       int* launches) {
-    if (n <= 0) return KS_OK;
-    const int threads = 256;
-    const int blocks = int(min64((n + threads - 1) / threads, 4096));
-    chunk_entry_kernel<<<blocks, threads, 0, ctx->stream>>>(excl, n, action, nq, entry, entry_ptr, chunk_entry);
-    if (launches) ++*launches;
-    KS_CUDA(cudaGetLastError());
-    return KS_OK;
-}
 
 }  // namespace ks

@@ -414,6 +414,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
         const int kfl = k0 + ((cb & 63) != 0);
         const int kfh = active ? int((ce >> 6) - gfirst) : 0;
         const bool resets = a.reset_state >= 0;
+        bool dirty = false;   // kModeMap over the submonoid: OTHER inside the chunk
         const uint4* pb = bases4 + ubase + (int64_t(k0) << 5);
         const uint64_t* pm = nmask + ubase + (int64_t(k0) << 5);
         uint4 wb = __ldg(pb);
@@ -435,6 +436,13 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
             const bool alln = (mlo & mhi) == ~0u;
             const bool clean = (mlo | mhi) == 0u;
             const bool fast = !has || (k >= kfl && k < kfh && (clean || (alln && resets)));
+            if constexpr (MODE == kModeMap) {
+                if (has && !clean && a.map_dirty) {
+                    const int lo = int(max64(cb - p0, 0)), hi = int(min64(ce - p0, 64));
+                    const uint64_t rm = (hi >= 64 ? ~0ull : ((1ull << hi) - 1ull)) & (~0ull << lo);
+                    dirty |= (wm & rm) != 0ull;
+                }
+            }
             if (__all_sync(am, fast)) {
                 const bool live = has && !alln;
                 const uint32_t s2 = fast_block<K, MODE>(c, L, live ? s : idle, live ? 0x8000u : 0u, wb, p0, am,
@@ -474,6 +482,9 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
         }
         if constexpr (MODE == kModeRows) drain<K, MODE>(c, L, am, rp0, rp, ring_stride);   // rows are per chunk
         if (active) {
+            if constexpr (MODE == kModeMap) {
+                if (dirty) s = __ldg(&a.map_dirty[s]);
+            }
             if (a.chunk_exit) a.chunk_exit[ch] = uint16_t(s);
             if constexpr (MODE == kModeRows || MODE == kModeLog) a.chunk_rows[ch] = L.nrows;
             if constexpr (MODE == kModeEmit) {

@@ -86,6 +86,10 @@ struct ScanArgs {
     unsigned int* fin_done = nullptr;
     unsigned long long* fin_host = nullptr;
     int32_t n_expr = 0;
+    // kModeMap over the OTHER-free submonoid (HostDfa::mono_sub): a chunk
+    // that holds OTHER (the table resets to the identity there) exits with
+    // map_dirty[element since its last OTHER]
+    const uint16_t* map_dirty = nullptr;
     LogEntry* log = nullptr;                // kModeLog
     unsigned long long* log_n = nullptr;    // kModeLog: visits appended (may exceed log_cap)
     int64_t log_cap = 0;
@@ -126,10 +130,13 @@ size_t exclusive_scan_rows_tmp_bytes(int64_t n);
 // exclusive running maximum (identity -1); tmp sized like the rows scan
 int exclusive_scan_max(ks_ctx* ctx, const int64_t* in, int64_t n, int64_t* out_excl, int64_t* d_total,
                        void* tmp, int* launches);
-int exclusive_scan_monoid(ks_ctx* ctx, const uint16_t* in, int64_t n, const uint16_t* prod,
-                          int32_t nm, uint16_t* out_excl, uint16_t* d_total, void* tmp,
-                          int* launches);
-size_t exclusive_scan_monoid_tmp_bytes(int64_t n);
+// Single-pass (decoupled look-back) monoid scan fused with the chunk entry
+// states: centry[i] = action[(in[0] ... in[i-1])][q0] with q0 = entry_val
+// (>= 0) or *entry_ptr; centry may be null.  *d_total = the product of all n
+// elements.  One launch, no temporaries beyond ctx->mstat.
+int monoid_scan_entries(ks_ctx* ctx, const uint16_t* in, int64_t n, const uint16_t* prod, int32_t nm,
+                        const uint16_t* action, int32_t nq, int32_t entry_val, const uint16_t* entry_ptr,
+                        uint16_t* centry, uint16_t* d_total, int* launches);
 
 // Small helper kernels (csrc/scan.cu).
 int launch_finalize_counts(ks_ctx* ctx, const unsigned long long* visits, int32_t n_accept,
@@ -145,8 +152,6 @@ int speculate_entries(ks_ctx* ctx, const SeqView& seq, int64_t begin, int64_t en
                       int64_t nch, const uint16_t* t1, int32_t nq, const uint16_t* pss, const int32_t* pss_off,
                       const int16_t* inv, int32_t pss_max, int32_t entry_val, const uint16_t* entry_ptr,
                       uint16_t* centry, uint16_t* d_exit, void* buf, int64_t seg_chunks, int* launches);
-int launch_chunk_entry(ks_ctx* ctx, const uint16_t* excl, int64_t n, const uint16_t* action,
-                       int32_t nq, int32_t entry, const uint16_t* entry_ptr, uint16_t* chunk_entry,
-                       int* launches);
+
 
 }  // namespace ks

@@ -106,7 +106,7 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
     const bool spec = h.strategy == KS_STRATEGY_SPECULATE;
     Arena ar;
     size_t scratch = size_t(h.n_accept) * 8 + size_t(std::max(h.ne, 1)) * 8 + size_t(nch_max) * 2 + 16 * kAlign;
-    if (mapscan) scratch += size_t(nch_max) * 6 + exclusive_scan_monoid_tmp_bytes(nch_max) + 4 * kAlign;
+    if (mapscan) scratch += size_t(nch_max) * 6 + 4 * kAlign;
     if (spec) scratch += size_t(nch_max) * 2 + 2 * kAlign;
     if (stream_mode == kStreamDevice) scratch += encode_scratch_bytes(piece) + 2 * kAlign;
     if (wire) scratch += size_t(blocks + 1) * 12 + exclusive_scan_rows_tmp_bytes(blocks + 1) + 4 * kAlign;
@@ -125,14 +125,11 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
     void* w_tmp = wire ? ar.take(exclusive_scan_rows_tmp_bytes(blocks + 1)) : nullptr;
     uint32_t* kept = raw_every > 0 ? static_cast<uint32_t*>(ar.take(size_t(blocks + 1) * 4)) : nullptr;
     int* ws_flag = static_cast<int*>(ar.take(16));           // raw pieces of the host-pack stream
-    uint16_t *elems = nullptr, *excl = nullptr, *centry = nullptr, *mtot = nullptr;
-    void* mtmp = nullptr;
+    uint16_t *elems = nullptr, *centry = nullptr, *mtot = nullptr;
     if (mapscan) {
         elems = static_cast<uint16_t*>(ar.take(size_t(nch_max) * 2));
-        excl = static_cast<uint16_t*>(ar.take(size_t(nch_max) * 2));
         centry = static_cast<uint16_t*>(ar.take(size_t(nch_max) * 2));
         mtot = static_cast<uint16_t*>(ar.take(16));
-        mtmp = ar.take(exclusive_scan_monoid_tmp_bytes(nch_max));
     }
     if (spec) centry = static_cast<uint16_t*>(ar.take(size_t(nch_max) * 2));
     rc = ensure_pinned(ctx, size_t(std::max(h.ne, 1)) * 8 + 64);
@@ -297,9 +294,7 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
             a.visits = visits;
             a.chunk_exit = chunk_exit;
             if (mapscan) {
-                rc = monoid_prefix(ctx, dfa, &pseq[b], 0, nsym, o2, L2, nch, elems, excl, mtot, mtmp, &launches);
-                if (rc) return rc;
-                rc = launch_chunk_entry(ctx, excl, nch, dfa->d_action, h.nq, 0, state, centry, &launches);
+                rc = monoid_prefix(ctx, dfa, &pseq[b], 0, nsym, o2, L2, nch, elems, centry, 0, state, mtot, &launches);
                 if (rc) return rc;
                 a.chunk_entry = centry;
             } else if (spec) {

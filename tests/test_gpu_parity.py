@@ -759,3 +759,67 @@ def test_wide_automaton(wide_dfa):
         ctx.synchronize()
         counts += t.cpu().numpy()[: dfa.n_expressions]
     assert counts.tolist() == want.tolist()
+
+
+# ---------------------------------------------------------------- MAPSCAN over the OTHER-free submonoid
+
+def _monoid_dfas():
+    """Non-definite automata with small transition monoids: a shift group
+    (OTHER -> 0), mixed ones resetting to a non-start state (monoids of 156
+    and 3152 maps), and one whose OTHER column is not constant (full-monoid
+    map pass, 582 maps)."""
+    out = [("shift64", workloads.permutation_dfa(64))]
+    outs_all = [[0], [], [1, 1], [], [], [0, 2], [], [], [2], [], [], [1]]
+    mixed = lambda nq, x: [(x + 1) % nq, (x + 3) % nq, x ^ 1 if (x ^ 1) < nq else x, (x // 2) * 2]
+    cycmin = lambda nq, x: [(x + 1) % nq, x, (x + 2) % nq, min(x, 3)]
+    for name, nq, cols, other in (("mixed_reset5", 12, mixed, lambda x: 5),
+                                  ("cycmin_reset5", 8, cycmin, lambda x: 5),
+                                  ("mixed_noreset", 6, mixed, lambda x: x // 3)):
+        trans = np.array([cols(nq, x) + [other(x)] for x in range(nq)], dtype=np.int32)
+        outs = outs_all[:nq]
+        off = np.zeros(nq + 1, dtype=np.int32)
+        off[1:] = np.cumsum([len(o) for o in outs])
+        ids = np.array([e for o in outs for e in o], dtype=np.int32)
+        out.append((name, ks.Dfa(trans, off, ids, ("a", "b", "c"), 3)))
+    return out
+
+
+def _codes_with_n_runs(n, seed):
+    rng = np.random.default_rng(seed)
+    codes = rng.integers(0, 4, n).astype(np.uint8)
+    for _ in range(40):   # N runs of every length class, and lone Ns
+        p = int(rng.integers(0, n))
+        codes[p:p + int(rng.choice([1, 2, 63, 64, 65, 300, 1500]))] = 4
+    codes[rng.random(n) < 0.0005] = 4
+    return codes
+
+
+@pytest.mark.parametrize("mono_full", ["0", "1"])
+@pytest.mark.parametrize("global_tables", ["0", "1"])
+def test_mapscan_submonoid_parity(monkeypatch, mono_full, global_tables):
+    monkeypatch.setenv("KS_MONO_FULL", mono_full)
+    monkeypatch.setenv("KS_FORCE_GLOBAL_TABLES", global_tables)
+    c2 = _native.DeviceContext(0)
+    for name, dfa in _monoid_dfas():
+        dh = c2.dfa(dfa, strategy=_native.STRATEGY_MAPSCAN)
+        assert dh.info["strategy_name"] == "mapscan", name
+        for n, seed in ((1, 1), (777, 2), (200_003, 3)):
+            codes = _codes_with_n_runs(n, seed)
+            want, rows = O.ref_run(dfa, codes, 1, 10, True)[:2]
+            sh = c2.upload_codes(codes)
+            assert c2.count(dh, sh).tolist() == want.tolist(), (name, n)
+            got, grows = c2.locate(dh, sh)
+            assert got.tolist() == want.tolist() and np.array_equal(grows, rows), (name, n)
+            if n > 1000:
+                rng = np.random.default_rng(seed)
+                for _ in range(4):
+                    b, e = sorted(rng.integers(0, n, 2).tolist())
+                    entry = int(rng.integers(0, dfa.state_count))
+                    w2, last = O.ref_sequential_count(dfa, codes, b, e, entry)
+                    g2, ex, _ = c2.scan_range(dh, sh, b, e, entry)
+                    assert g2.tolist() == w2.tolist() and ex == last, (name, b, e)
+                    m = c2.segment_map(dh, sh, b, e)
+                    for q in range(dfa.state_count):
+                        assert m[q] == O.ref_sequential_count(dfa, codes, b, e, q)[1], (name, b, e, q)
+                text = bytes(np.frombuffer(b"ACGTN", dtype=np.uint8)[codes])
+                assert c2.count_host_ascii(dh, text).tolist() == want.tolist(), name
