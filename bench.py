@@ -383,14 +383,14 @@ def run_ours(args) -> None:
     locate = None
     if args.config in (1, 2, 4) and world == 1:
         loc_times = []
-        for i in range(4):
+        for i in range(12):
             torch.cuda.synchronize()
             l0 = time.perf_counter()
             lc, lrows = ctx.locate(dh, sh)
             loc_times.append(time.perf_counter() - l0)
         if not np.array_equal(lc, ref_counts) or lrows.shape[0] != int(ref_counts.sum()):
             raise RuntimeError("locate counts differ")
-        loc_s = statistics.median(loc_times[1:])
+        loc_s = statistics.median(loc_times[2:])
         locate = {"value": n / loc_s / 1e9, "unit": UNIT, "ms_per_step": loc_s * 1e3,
                   "rows_per_gpu": int(lrows.shape[0]),
                   "path": "ks_locate: single-pass visit log + scatter (or rows/emit passes), rows D2H"}

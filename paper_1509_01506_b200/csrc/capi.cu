@@ -494,10 +494,12 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
     if (locate && nch > 0) {
         rc = exclusive_scan_rows(ctx, chunk_rows, nch, row_off, row_off + nch, rows_tmp, &launches);
         if (rc) return rc;
+        trace.mark("row scan");
         KS_CUDA(cudaMemcpyAsync(&total_rows, row_off + nch, 8, cudaMemcpyDeviceToHost, ctx->stream));
         unsigned long long logged = 0;
         if (use_log) KS_CUDA(cudaMemcpyAsync(&logged, log_n, 8, cudaMemcpyDeviceToHost, ctx->stream));
         KS_CUDA(cudaStreamSynchronize(ctx->stream));
+        trace.mark("sync totals");
         if (total_rows > 0 && use_log && logged <= (unsigned long long)a.log_cap) {
             KS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_rows), size_t(total_rows) * 16, ctx->stream));
             rc = launch_log_scatter(ctx, a.log, int64_t(logged), row_off, dfa->d_acc_out_off, dfa->d_acc_out_ids,
@@ -524,9 +526,17 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
         }
     }
 
-    // results
-    rc = ensure_pinned(ctx, size_t(std::max(h.ne, 1)) * 8 + 64);
-    if (rc) return rc;
+    trace.mark("rows");
+    // results; rows below 32 MiB go through the pinned staging buffer (DMA
+    // speed, then one host memcpy), larger ones into the page-locked result
+    const size_t rbytes = locate ? size_t(std::max<int64_t>(total_rows, 0)) * 16 : 0;
+    const bool stage_rows = rbytes > 0 && rbytes < (size_t(32) << 20);
+    const size_t stage_off = (size_t(std::max(h.ne, 1)) * 8 + 64 + 255) & ~size_t(255);
+    rc = ensure_pinned(ctx, stage_rows ? stage_off + rbytes : size_t(std::max(h.ne, 1)) * 8 + 64);
+    if (rc) {
+        if (d_rows) cudaFreeAsync(d_rows, ctx->stream);
+        return rc;
+    }
     char* pin = static_cast<char*>(ctx->pinned);
     if (!direct) KS_CUDA(cudaMemcpyAsync(pin, counts, res_bytes, cudaMemcpyDeviceToHost, ctx->stream));
     uint16_t* pin_exit = reinterpret_cast<uint16_t*>(pin + size_t(std::max(h.ne, 1)) * 8 + 8);
@@ -539,11 +549,11 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
         }
         if (total_rows > 0) {
             // large results: page-lock the destination so the copy runs at DMA speed
-            const size_t rbytes = size_t(total_rows) * 16;
             bool registered = false;
-            if (rbytes >= (size_t(32) << 20))
+            if (!stage_rows)
                 registered = cudaHostRegister(host_rows, rbytes, cudaHostRegisterDefault) == cudaSuccess;
-            cudaError_t ce = cudaMemcpyAsync(host_rows, d_rows, rbytes, cudaMemcpyDeviceToHost, ctx->stream);
+            cudaError_t ce = cudaMemcpyAsync(stage_rows ? static_cast<void*>(pin + stage_off) : host_rows, d_rows,
+                                             rbytes, cudaMemcpyDeviceToHost, ctx->stream);
             if (registered) {
                 if (ce == cudaSuccess) ce = cudaStreamSynchronize(ctx->stream);
                 cudaHostUnregister(host_rows);
@@ -556,6 +566,7 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
         }
         if (d_rows) cudaFreeAsync(d_rows, ctx->stream);
     }
+    trace.mark("results D2H");
     KS_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
     cudaError_t se = cudaStreamSynchronize(ctx->stream);
     if (se != cudaSuccess) {
@@ -568,6 +579,7 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
         return fail(KS_E_CHAIN, "internal invariant failed: chunk row count mismatch");
     }
     std::memcpy(counts_out, pin, size_t(h.ne) * 8);
+    if (stage_rows) std::memcpy(host_rows, pin + stage_off, rbytes);
     if (exit_out) {
         int ex;
         if (nch > 0) ex = h.wide ? int(*reinterpret_cast<uint32_t*>(pin_exit)) : int(*pin_exit);
