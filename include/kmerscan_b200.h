@@ -10,8 +10,9 @@
  * failing call never leaves partial results in caller buffers.
  *
  * Device memory is owned by the context and the dfa/seq handles (freed by
- * ks_*_free).  Handles are immutable after upload; calls on one context are
- * serialised on the context's CUDA stream.
+ * ks_*_free).  Handles are immutable after upload.  Thread safety: calls on
+ * one context (and on its handles) take a per-context lock and run in order on
+ * the context's CUDA stream; separate contexts run concurrently.
  */
 #ifndef KMERSCAN_B200_H
 #define KMERSCAN_B200_H

@@ -769,18 +769,21 @@ int ks_close(ks_ctx* ctx) {
 }
 
 int ks_set_stream(ks_ctx* ctx, void* stream) {
+    CtxLock lock_(ctx);
     if (!ctx) return fail(KS_E_INVALID, "null context");
     ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
     return KS_OK;
 }
 
 int ks_synchronize(ks_ctx* ctx) {
+    CtxLock lock_(ctx);
     if (!ctx) return fail(KS_E_INVALID, "null context");
     KS_CUDA(cudaStreamSynchronize(ctx->stream));
     return KS_OK;
 }
 
 int ks_get_stats(const ks_ctx* ctx, ks_stats* out) {
+    CtxLock lock_(ctx);
     if (!ctx || !out) return fail(KS_E_INVALID, "null argument");
     *out = ctx->stats;
     return KS_OK;
@@ -788,6 +791,7 @@ int ks_get_stats(const ks_ctx* ctx, ks_stats* out) {
 
 int ks_dfa_upload_ex(ks_ctx* ctx, const int32_t* transitions, int32_t n_states, const int32_t* out_offsets,
                      const int32_t* out_ids, int32_t n_expressions, int32_t force_strategy, ks_dfa** out) {
+    CtxLock lock_(ctx);
     if (!ctx || !out) return fail(KS_E_INVALID, "null argument");
     DeviceGuard guard(ctx->device);
     ks_dfa* d = new ks_dfa();
@@ -891,6 +895,7 @@ int ks_dfa_upload_ex(ks_ctx* ctx, const int32_t* transitions, int32_t n_states, 
 
 int ks_dfa_upload(ks_ctx* ctx, const int32_t* transitions, int32_t n_states, const int32_t* out_offsets,
                   const int32_t* out_ids, int32_t n_expressions, ks_dfa** out) {
+    CtxLock lock_(ctx);
     return ks_dfa_upload_ex(ctx, transitions, n_states, out_offsets, out_ids, n_expressions, 0, out);
 }
 
@@ -912,6 +917,7 @@ int ks_dfa_info_get(const ks_dfa* d, ks_dfa_info* out) {
 }
 
 int ks_dfa_free(ks_dfa* d) {
+    CtxLock lock_(d ? d->ctx : nullptr);
     if (!d) return KS_OK;
     DeviceGuard guard(d->ctx->device);
     if (d->d_blob) cudaFree(d->d_blob);
@@ -921,6 +927,7 @@ int ks_dfa_free(ks_dfa* d) {
 }
 
 int ks_seq_upload_codes(ks_ctx* ctx, const uint8_t* codes, int64_t n, ks_seq** out) {
+    CtxLock lock_(ctx);
     if (!ctx || !out || n < 0 || (n > 0 && !codes)) return fail(KS_E_INVALID, "bad argument");
     DeviceGuard guard(ctx->device);
     ks_seq* s = nullptr;
@@ -981,12 +988,14 @@ static int encode_common(ks_ctx* ctx, const uint8_t* d_bytes, int64_t n_bytes, i
 }
 
 int ks_seq_encode_device(ks_ctx* ctx, const uint8_t* d_bytes, int64_t n_bytes, int32_t fasta, ks_seq** out) {
+    CtxLock lock_(ctx);
     if (!ctx || !out || n_bytes < 0 || (n_bytes > 0 && !d_bytes)) return fail(KS_E_INVALID, "bad argument");
     DeviceGuard guard(ctx->device);
     return encode_common(ctx, d_bytes, n_bytes, fasta, out);
 }
 
 int ks_seq_upload_ascii(ks_ctx* ctx, const uint8_t* bytes, int64_t n_bytes, int32_t fasta, ks_seq** out) {
+    CtxLock lock_(ctx);
     if (!ctx || !out || n_bytes < 0 || (n_bytes > 0 && !bytes)) return fail(KS_E_INVALID, "bad argument");
     DeviceGuard guard(ctx->device);
     uint8_t* d_in = nullptr;
@@ -1006,6 +1015,7 @@ int ks_seq_length(const ks_seq* s, int64_t* n) {
 }
 
 int ks_seq_download_codes(ks_ctx* ctx, const ks_seq* s, uint8_t* out) {
+    CtxLock lock_(ctx);
     if (!ctx || !s || (s->n > 0 && !out)) return fail(KS_E_INVALID, "null argument");
     DeviceGuard guard(ctx->device);
     Arena ar;
@@ -1020,6 +1030,7 @@ int ks_seq_download_codes(ks_ctx* ctx, const ks_seq* s, uint8_t* out) {
 }
 
 int ks_seq_download_softmask(ks_ctx* ctx, const ks_seq* s, uint64_t* out, int64_t n_words) {
+    CtxLock lock_(ctx);
     if (!ctx || !s || !out) return fail(KS_E_INVALID, "null argument");
     DeviceGuard guard(ctx->device);
     const int64_t have = (s->n + 63) / 64;
@@ -1038,6 +1049,7 @@ int ks_seq_download_softmask(ks_ctx* ctx, const ks_seq* s, uint64_t* out, int64_
 }
 
 int ks_seq_free(ks_seq* s) {
+    CtxLock lock_(s ? s->ctx : nullptr);
     if (!s) return KS_OK;
     DeviceGuard guard(s->ctx->device);
     cudaStreamSynchronize(s->ctx->stream);
@@ -1046,23 +1058,27 @@ int ks_seq_free(ks_seq* s) {
 }
 
 int ks_count(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t* counts_out) {
+    CtxLock lock_(ctx);
     if (!counts_out) return fail(KS_E_INVALID, "counts_out is null");
     return scan_impl(ctx, dfa, seq, 0, seq ? seq->n : 0, -1, 0, counts_out, nullptr, nullptr, nullptr);
 }
 
 int ks_locate(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t* counts_out, int64_t** rows_out,
               int64_t* n_rows) {
+    CtxLock lock_(ctx);
     if (!counts_out || !rows_out || !n_rows) return fail(KS_E_INVALID, "null output");
     return scan_impl(ctx, dfa, seq, 0, seq ? seq->n : 0, -1, 0, counts_out, nullptr, rows_out, n_rows);
 }
 
 int ks_count_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t* counts_pinned) {
+    CtxLock lock_(ctx);
     if (!counts_pinned) return fail(KS_E_INVALID, "counts_pinned is null");
     int64_t dummy = 0;
     return scan_impl(ctx, dfa, seq, 0, seq ? seq->n : 0, -1, 0, &dummy, nullptr, nullptr, nullptr, counts_pinned);
 }
 
 int ks_async_wait(ks_ctx* ctx, float* scan_ms_total, int32_t* calls, int32_t* launches) {
+    CtxLock lock_(ctx);
     if (!ctx) return fail(KS_E_INVALID, "null context");
     KS_CUDA(cudaStreamSynchronize(ctx->stream));
     float total = 0;
@@ -1083,6 +1099,7 @@ int ks_async_wait(ks_ctx* ctx, float* scan_ms_total, int32_t* calls, int32_t* la
 int ks_scan_range(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end,
                   int32_t entry_state, int64_t row_offset_base, int64_t* counts_out, int32_t* exit_state,
                   int64_t** rows_out, int64_t* n_rows) {
+    CtxLock lock_(ctx);
     if (!counts_out) return fail(KS_E_INVALID, "counts_out is null");
     return scan_impl(ctx, dfa, seq, begin, end, entry_state, row_offset_base, counts_out, exit_state, rows_out,
                      n_rows);
@@ -1090,6 +1107,7 @@ int ks_scan_range(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t beg
 
 int ks_segment_map(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end,
                    int32_t* map_out) {
+    CtxLock lock_(ctx);
     if (!ctx || !dfa || !seq || !map_out) return fail(KS_E_INVALID, "null argument");
     if (begin < 0 || end < begin || end > seq->n) return fail(KS_E_INVALID, "segment out of bounds");
     DeviceGuard guard(ctx->device);
@@ -1137,6 +1155,7 @@ int ks_segment_map(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t be
 
 int ks_segment_map_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end,
                          int32_t* d_map_out) {
+    CtxLock lock_(ctx);
     if (!ctx || !dfa || !seq || !d_map_out) return fail(KS_E_INVALID, "null argument");
     if (begin < 0 || end < begin || end > seq->n) return fail(KS_E_INVALID, "segment out of bounds");
     DeviceGuard guard(ctx->device);
@@ -1178,6 +1197,7 @@ int ks_segment_map_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
 
 int ks_count_shard_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end,
                          const int32_t* d_maps, int32_t rank, unsigned long long* d_counts) {
+    CtxLock lock_(ctx);
     if (!ctx || !dfa || !seq || !d_counts) return fail(KS_E_INVALID, "null argument");
     if (begin < 0 || end < begin || end > seq->n) return fail(KS_E_INVALID, "range out of bounds");
     DeviceGuard guard(ctx->device);
@@ -1253,6 +1273,7 @@ int ks_count_shard_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
 int ks_speculate(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int32_t n_chunks, const int64_t* chunk_begin,
                  const int64_t* chunk_end, const int64_t* pss_off, const int32_t* pss_data, int32_t window,
                  int32_t* conv_out, int64_t* delta_out) {
+    CtxLock lock_(ctx);
     if (!ctx || !dfa || !seq || n_chunks < 0 || window < 0) return fail(KS_E_INVALID, "bad argument");
     if (n_chunks == 0) return KS_OK;
     if (!chunk_begin || !chunk_end || !pss_off || !conv_out) return fail(KS_E_INVALID, "null argument");

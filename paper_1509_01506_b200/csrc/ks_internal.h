@@ -3,6 +3,7 @@
 
 #include <cstdint>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -133,6 +134,7 @@ __device__ __forceinline__ uint32_t seq_sym(const SeqView& q, int64_t p) {
 }  // namespace ks
 
 struct ks_ctx {
+    std::recursive_mutex mu;   // public calls on one context are serialised (CtxLock)
     int device = 0;
     int num_sms = 148;
     size_t smem_optin = 0;
@@ -206,4 +208,12 @@ struct ks_seq {
     void* d_blob = nullptr;
     int64_t n_blocks = 0;   // block slots allocated (whole tiles + one padding tile)
     int32_t lb = 4;         // log2(blocks per unit), see SeqView
+};
+
+// Held for the duration of every public call that uses a context.
+struct CtxLock {
+    std::unique_lock<std::recursive_mutex> lk;
+    explicit CtxLock(const ks_ctx* c) {
+        if (c) lk = std::unique_lock<std::recursive_mutex>(const_cast<ks_ctx*>(c)->mu);
+    }
 };

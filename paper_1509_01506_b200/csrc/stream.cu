@@ -359,6 +359,7 @@ int ks_pack_host_wire(const uint8_t* bytes, int64_t n_bytes, int32_t fasta, uint
 
 int ks_count_host_bytes(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int64_t n_bytes, int32_t fasta,
                         int64_t* counts_out) {
+    CtxLock lock_(ctx);
     if (!ctx || !dfa || !counts_out || n_bytes < 0 || (n_bytes > 0 && !bytes))
         return fail(KS_E_INVALID, "bad argument");
     if (dfa->ctx != ctx) return fail(KS_E_INVALID, "handle belongs to another context");
@@ -399,6 +400,7 @@ int ks_count_host_bytes(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, in
 
 int ks_count_host_ascii(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int64_t n_bytes,
                         int64_t* counts_out) {
+    CtxLock lock_(ctx);
     return ks_count_host_bytes(ctx, dfa, bytes, n_bytes, 0, counts_out);
 }
 
