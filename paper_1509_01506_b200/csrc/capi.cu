@@ -82,6 +82,13 @@ bool host_is_device_visible(const void* p) {
 namespace {
 
 // ------------------------------------------------------------ tiny kernels
+__global__ void copy_rows_kernel(const longlong2* __restrict__ src, const int64_t* __restrict__ n_dev,
+                                 longlong2* __restrict__ dst) {
+    const int64_t n = *n_dev;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        dst[i] = src[i];
+}
+
 template <class T>   // T: uint16_t tables, uint32_t for wide automata
 __global__ void walk_kernel(SeqView seq, int64_t begin, int64_t end, const T* t1, int32_t nq,
                             int32_t uniform_start, uint32_t* out) {
@@ -491,6 +498,80 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
 
     int64_t total_rows = 0;
     int64_t* d_rows = nullptr;
+    // single round trip: rows scattered straight into pinned host staging
+    // (bounded by log capacity x max outputs per state), totals and counts
+    // copied back, one synchronisation; an overflowed log falls through to the
+    // two-pass form below
+    if (locate && nch > 0 && use_log) {
+        const size_t cap_bytes = size_t(a.log_cap) * size_t(std::max(h.max_outcnt, 1)) * 16;
+        bool staged = cap_bytes <= (size_t(256) << 20) && !env_flag("KS_LOCATE_TWO_SYNC");
+        if (staged && ctx->rstage_bytes < cap_bytes) {
+            if (ctx->rstage) KS_CUDA(cudaFreeHost(ctx->rstage));
+            ctx->rstage = nullptr;
+            ctx->rstage_bytes = 0;
+            staged = cudaMallocHost(&ctx->rstage, cap_bytes) == cudaSuccess;
+            if (staged) ctx->rstage_bytes = cap_bytes;
+            else cudaGetLastError();
+        }
+        if (staged && ctx->rdev_bytes < cap_bytes) {
+            if (ctx->rdev) KS_CUDA(cudaFree(ctx->rdev));
+            ctx->rdev = nullptr;
+            ctx->rdev_bytes = 0;
+            staged = cudaMalloc(&ctx->rdev, cap_bytes) == cudaSuccess;
+            if (staged) ctx->rdev_bytes = cap_bytes;
+            else cudaGetLastError();
+        }
+        staged = staged && host_is_device_visible(ctx->rstage);
+        if (staged) {
+            rc = exclusive_scan_rows(ctx, chunk_rows, nch, row_off, row_off + nch, rows_tmp, &launches);
+            if (rc) return rc;
+            rc = launch_log_scatter(ctx, a.log, a.log_cap, log_n, row_off, dfa->d_acc_out_off, dfa->d_acc_out_ids,
+                                    static_cast<int64_t*>(ctx->rdev), &launches);
+            if (rc) return rc;
+            // rows [0, total) -> pinned host memory, coalesced (the total is read on the device)
+            copy_rows_kernel<<<std::max(1, std::min(ctx->num_sms * 4, int((a.log_cap + 255) / 256))), 256, 0,
+                               ctx->stream>>>(static_cast<const longlong2*>(ctx->rdev), row_off + nch,
+                                              static_cast<longlong2*>(ctx->rstage));
+            KS_CUDA(cudaGetLastError());
+            ++launches;
+            trace.mark("rows (staged)");
+            rc = ensure_pinned(ctx, size_t(std::max(h.ne, 1)) * 8 + 64 + 16);
+            if (rc) return rc;
+            char* pin = static_cast<char*>(ctx->pinned);
+            int64_t* tot = reinterpret_cast<int64_t*>(pin + size_t(std::max(h.ne, 1)) * 8 + 32);
+            KS_CUDA(cudaMemcpyAsync(pin, counts, res_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+            KS_CUDA(cudaMemcpyAsync(tot, row_off + nch, 8, cudaMemcpyDeviceToHost, ctx->stream));
+            KS_CUDA(cudaMemcpyAsync(tot + 1, log_n, 8, cudaMemcpyDeviceToHost, ctx->stream));
+            KS_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
+            KS_CUDA(cudaStreamSynchronize(ctx->stream));
+            trace.mark("sync");
+            if (uint64_t(tot[1]) <= uint64_t(a.log_cap)) {
+                total_rows = tot[0];
+                if (*reinterpret_cast<int32_t*>(pin + size_t(std::max(h.ne, 1)) * 8))
+                    return fail(KS_E_CHAIN, "internal invariant failed: chunk row count mismatch");
+                int64_t* host_rows = static_cast<int64_t*>(std::malloc(size_t(std::max<int64_t>(total_rows, 1)) * 16));
+                if (!host_rows) return fail(KS_E_NOMEM, "host allocation of match rows failed");
+                std::memcpy(host_rows, ctx->rstage, size_t(total_rows) * 16);
+                std::memcpy(counts_out, pin, size_t(h.ne) * 8);
+                if (exit_out) {
+                    const uint16_t* pin_exit = reinterpret_cast<const uint16_t*>(pin + size_t(std::max(h.ne, 1)) * 8 + 8);
+                    *exit_out = h.old_of_new[int(*pin_exit)];
+                }
+                *rows_out = host_rows;
+                *n_rows = total_rows;
+                float ms = 0;
+                cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]);
+                ctx->stats.scan_ms = ms;
+                cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[3]);
+                ctx->stats.total_ms = ms;
+                ctx->stats.kernel_launches = launches;
+                ctx->stats.chunks = int32_t(nch);
+                ctx->stats.chunk_len = L;
+                ctx->stats.rows = total_rows;
+                return KS_OK;
+            }
+        }
+    }
     if (locate && nch > 0) {
         rc = exclusive_scan_rows(ctx, chunk_rows, nch, row_off, row_off + nch, rows_tmp, &launches);
         if (rc) return rc;
@@ -502,8 +583,8 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
         trace.mark("sync totals");
         if (total_rows > 0 && use_log && logged <= (unsigned long long)a.log_cap) {
             KS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_rows), size_t(total_rows) * 16, ctx->stream));
-            rc = launch_log_scatter(ctx, a.log, int64_t(logged), row_off, dfa->d_acc_out_off, dfa->d_acc_out_ids,
-                                    d_rows, &launches);
+            rc = launch_log_scatter(ctx, a.log, int64_t(logged), nullptr, row_off, dfa->d_acc_out_off,
+                                    dfa->d_acc_out_ids, d_rows, &launches);
             if (rc) {
                 cudaFreeAsync(d_rows, ctx->stream);
                 return rc;
@@ -748,6 +829,8 @@ int ks_close(ks_ctx* ctx) {
     if (ctx->sbuf) cudaFree(ctx->sbuf);
     if (ctx->spec_buf) cudaFree(ctx->spec_buf);
     if (ctx->mstat) cudaFree(ctx->mstat);
+    if (ctx->rstage) cudaFreeHost(ctx->rstage);
+    if (ctx->rdev) cudaFree(ctx->rdev);
     if (ctx->log_buf) cudaFree(ctx->log_buf);
     if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
     delete ctx->pool;

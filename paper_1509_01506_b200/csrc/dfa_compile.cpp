@@ -273,12 +273,14 @@ int compile_dfa(const int32_t* trans, int nq, const int32_t* out_off, const int3
     h->acc_out_off.assign(1, 0);
     h->acc_out_ids.clear();
     h->acc_outcnt.clear();
+    h->max_outcnt = 0;
     for (int i = 0; i < h->n_accept; ++i) {
         int old = h->old_of_new[i];
         for (int32_t k = out_off[old]; k < out_off[old + 1]; ++k) h->acc_out_ids.push_back(out_ids[k]);
         h->acc_out_off.push_back(int32_t(h->acc_out_ids.size()));
         int cnt = out_off[old + 1] - out_off[old];
         h->acc_outcnt.push_back(uint16_t(std::min(cnt, 65535)));
+        h->max_outcnt = std::max(h->max_outcnt, cnt);
         if (cnt > 65535) return fail(KS_E_UNSUPPORTED, "dfa: more than 65535 outputs on one state");
     }
 

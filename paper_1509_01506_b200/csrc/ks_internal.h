@@ -64,6 +64,7 @@ struct HostDfa {
     std::vector<int32_t> acc_out_off;   // n_accept + 1 (CSR over internal accepting ids)
     std::vector<int32_t> acc_out_ids;
     std::vector<uint16_t> acc_outcnt;   // n_accept
+    int max_outcnt = 0;
     CompiledTable scan;                 // the automaton itself
     // MAPSCAN
     int nm = 0;
@@ -166,6 +167,11 @@ struct ks_ctx {
     unsigned long long* mstat = nullptr;
     int64_t mstat_cap = 0;
     uint32_t mepoch = 0;
+    // pinned host staging the locate scatter writes rows into (grow-only)
+    void* rstage = nullptr;
+    size_t rstage_bytes = 0;
+    void* rdev = nullptr;      // device rows of the same capacity (scatter target)
+    size_t rdev_bytes = 0;
     // single-pass locate log (grow-only)
     void* log_buf = nullptr;
     size_t log_bytes = 0;

@@ -551,9 +551,13 @@ FastFn pick_mode(int mode) {
     return nullptr;
 }
 
-__global__ void log_scatter_kernel(const LogEntry* __restrict__ log, int64_t n, const int64_t* __restrict__ row_off,
-                                   const int32_t* __restrict__ off, const int32_t* __restrict__ ids,
-                                   int64_t* __restrict__ rows) {
+__global__ void log_scatter_kernel(const LogEntry* __restrict__ log, int64_t n, const unsigned long long* n_dev,
+                                   const int64_t* __restrict__ row_off, const int32_t* __restrict__ off,
+                                   const int32_t* __restrict__ ids, int64_t* __restrict__ rows) {
+    if (n_dev) {   // entries logged on the device; none when the log overflowed (n = capacity)
+        const unsigned long long v = *n_dev;
+        n = v <= (unsigned long long)n ? int64_t(v) : 0;
+    }
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
         const LogEntry e = log[i];
         const int64_t base = row_off[e.chunk] + e.local;
@@ -597,12 +601,13 @@ size_t fast_smem_bytes(int mode, int32_t t1_pad, int32_t hist_words, int threads
 
 int fast_threads() { return kFastThreads; }
 
-int launch_log_scatter(ks_ctx* ctx, const LogEntry* log, int64_t n, const int64_t* row_off,
-                       const int32_t* acc_out_off, const int32_t* acc_out_ids, int64_t* rows, int* launches) {
+int launch_log_scatter(ks_ctx* ctx, const LogEntry* log, int64_t n, const unsigned long long* n_dev,
+                       const int64_t* row_off, const int32_t* acc_out_off, const int32_t* acc_out_ids, int64_t* rows,
+                       int* launches) {
     if (n <= 0) return KS_OK;
     const int threads = 256;
     const int blocks = int(max64(1, min64((n + threads - 1) / threads, int64_t(ctx->num_sms) * 8)));
-    log_scatter_kernel<<<blocks, threads, 0, ctx->stream>>>(log, n, row_off, acc_out_off, acc_out_ids, rows);
+    log_scatter_kernel<<<blocks, threads, 0, ctx->stream>>>(log, n, n_dev, row_off, acc_out_off, acc_out_ids, rows);
     if (launches) ++*launches;
     KS_CUDA(cudaGetLastError());
     return KS_OK;

@@ -120,8 +120,11 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches);
 size_t fast_smem_bytes(int mode, int32_t t1_pad, int32_t hist_words, int threads);
 int fast_threads();
 // rows of the logged visits: rows[row_off[chunk] + local + k] = (pos1, id_k)
-int launch_log_scatter(ks_ctx* ctx, const LogEntry* log, int64_t n, const int64_t* row_off,
-                       const int32_t* acc_out_off, const int32_t* acc_out_ids, int64_t* rows, int* launches);
+// Rows of the visit log at their chunk offsets.  With n_dev the count is read
+// on the device (n is then the log capacity; an overflowed log writes nothing).
+int launch_log_scatter(ks_ctx* ctx, const LogEntry* log, int64_t n, const unsigned long long* n_dev,
+                       const int64_t* row_off, const int32_t* acc_out_off, const int32_t* acc_out_ids, int64_t* rows,
+                       int* launches);
 
 // Prefix scans (csrc/prefix_scan.cu).
 int exclusive_scan_rows(ks_ctx* ctx, const uint32_t* in, int64_t n, int64_t* out_excl,

@@ -823,3 +823,45 @@ def test_mapscan_submonoid_parity(monkeypatch, mono_full, global_tables):
                         assert m[q] == O.ref_sequential_count(dfa, codes, b, e, q)[1], (name, b, e, q)
                 text = bytes(np.frombuffer(b"ACGTN", dtype=np.uint8)[codes])
                 assert c2.count_host_ascii(dh, text).tolist() == want.tolist(), name
+
+
+def test_concurrent_calls_on_one_context():
+    """The C ABI serialises calls on one context: threads that call ks_count /
+    ks_locate directly (no Python-side lock; ctypes releases the GIL) all get
+    the reference's results."""
+    import ctypes as C
+    import threading
+
+    w = workloads.make(2, 300_001)
+    codes = ks.encode_bytes(w.ascii.tobytes())
+    want, rows = O.ref_run(w.dfa, codes, 1, 10, True)[:2]
+    c2 = _native.DeviceContext(0)
+    dh = c2.dfa(w.dfa)
+    sh = c2.upload_codes(codes)
+    lib = _native.library()
+    errors = []
+
+    def worker(k):
+        try:
+            for i in range(12):
+                counts = np.zeros(max(w.dfa.n_expressions, 1), dtype=np.int64)
+                if (i + k) % 3:
+                    rc = lib.ks_count(c2.handle, dh.handle, sh.handle, _native._ptr(counts, C.c_int64))
+                    assert rc == 0 and counts.tolist() == want.tolist()
+                else:
+                    rp, nr = C.POINTER(C.c_int64)(), C.c_int64()
+                    rc = lib.ks_locate(c2.handle, dh.handle, sh.handle, _native._ptr(counts, C.c_int64),
+                                       C.byref(rp), C.byref(nr))
+                    assert rc == 0 and counts.tolist() == want.tolist() and nr.value == rows.shape[0]
+                    got = np.ctypeslib.as_array(rp, shape=(nr.value * 2,)).reshape(-1, 2).copy()
+                    lib.ks_free(rp)
+                    assert np.array_equal(got, rows)
+        except Exception as exc:   # surfaced below
+            errors.append(repr(exc))
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors[:3]

@@ -25,6 +25,14 @@ for cfg in [int(c) for c in (sys.argv[1:] or ["2"])]:
     print(f"C{cfg} locate wall {np.median(ts) * 1e3:.3f} ms, total_ms {st['total_ms']:.3f}, scan_ms {st['scan_ms']:.3f}, rows {rows.shape[0]}", flush=True)
     t0 = time.perf_counter(); ctx.count(dh, sh); t1 = time.perf_counter()
     print(f"C{cfg} count wall {(t1 - t0) * 1e3:.3f} ms", flush=True)
+    ts = []
+    for _ in range(5):
+        t0 = time.perf_counter(); ctx.count(dh, sh); ts.append(time.perf_counter() - t0)
+    st = ctx.stats()
+    print(f"C{cfg} count wall x5 {[round(t * 1e3, 3) for t in ts]} ms, total_ms {st['total_ms']:.3f}, scan_ms {st['scan_ms']:.3f}", flush=True)
     os.environ["KS_PHASE_TRACE"] = "1"
+    print("locate phases:", flush=True)
     ctx.locate(dh, sh)
+    print("count phases:", flush=True)
+    ctx.count(dh, sh)
     os.environ["KS_PHASE_TRACE"] = "0"
