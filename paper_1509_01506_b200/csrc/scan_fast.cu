@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     unsigned char* p_t1 = f_smem + TK_BYTES;
     unsigned char* p_ring = p_t1 + size_t(a.t1_pad) * 2;
     unsigned int* s_hist = reinterpret_cast<unsigned int*>(
-        p_ring + (RING ? size_t(a.ring_depth) * 4 * blockDim.x : 0));
+        p_ring + (RING ? size_t(a.ring_depth) * 4 * kFastThreads : 0));
     // stage the tables with bulk copies (TMA engine, UBLKCP) completing on an
     // mbarrier, while the threads clear the histogram
     __shared__ __align__(8) unsigned long long tables_ready;
@@ -645,9 +645,26 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
     }
     const int64_t u0 = a.origin / a.chunk_len;
     const int64_t tiles = ((u0 + a.nchunks - 1) >> 5) - (u0 >> 5) + 1;
-    const int64_t need = (tiles * 32 + kFastThreads - 1) / kFastThreads;
+    // one tile (32 units) per warp at a time: when the tiles do not divide
+    // into whole rounds over 148 x 32 warps, fewer warps per CTA can (e.g.
+    // 4096 tiles: 28 warps x 148 = 4144 slots, one round, instead of 128
+    // CTAs with 20 SMs idle); the shared-memory layout stays the 1024-thread one
+    int warps = kFastThreads / 32;
+    if (tiles >= int64_t(ctx->num_sms) * 24) {
+        double best = -1.0;
+        for (int w = kFastThreads / 32; w >= 24; --w) {
+            const int64_t slots = int64_t(ctx->num_sms) * w;
+            const int64_t rounds = (tiles + slots - 1) / slots;
+            const double eff = double(tiles) / double(rounds * slots);
+            if (eff > best + 0.02) {   // fewer warps only when clearly better balanced
+                best = eff;
+                warps = w;
+            }
+        }
+    }
+    const int64_t need = (tiles + warps - 1) / warps;
     const int blocks = int(max64(1, min64(need, int64_t(ctx->num_sms))));
-    fn<<<blocks, kFastThreads, smem, ctx->stream>>>(a);
+    fn<<<blocks, warps * 32, smem, ctx->stream>>>(a);
     if (launches) ++*launches;
     KS_CUDA(cudaGetLastError());
     return KS_OK;
