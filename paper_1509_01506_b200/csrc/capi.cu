@@ -719,18 +719,19 @@ int upload_table(const CompiledTable& t, DevTable* d, char* blob, size_t* off, b
 }
 
 // Blocks per unit (2^lb): the fast scan gives each warp one tile (32 units)
-// at a time, so pick the unit size that minimises (tiles per warp, rounded
-// up) x (unit length + lookback), i.e. wave quantisation vs entry overhead.
+// at a time, so pick the unit size that minimises (rounds of tiles over the
+// SMs' warps, with the CTA size fast_warps_per_cta picks) x (unit length +
+// per-unit overhead), i.e. wave quantisation vs entry overhead.
 int choose_lb(const ks_ctx* ctx, int64_t n) {
     if (const char* e = std::getenv("KS_TILE_LB"); e && *e) return std::min(6, std::max(0, std::atoi(e)));
-    const int64_t warps = int64_t(ctx->num_sms) * 32;
     int best = 2;
     double best_cost = 1e300;
-    for (int lb = 2; lb <= 5; ++lb) {
+    for (int lb = 2; lb <= 6; ++lb) {
         const int64_t tile = int64_t(2048) << lb;
-        const int64_t tiles = (n + tile - 1) / tile;
-        const int64_t per_warp = (tiles + warps - 1) / warps;
-        const double cost = double(per_warp) * double((64 << lb) + 64);   // ~64 bases of per-unit overhead
+        const int64_t tiles = std::max<int64_t>(1, (n + tile - 1) / tile);
+        const int64_t slots = int64_t(ctx->num_sms) * fast_warps_per_cta(tiles, ctx->num_sms);
+        const int64_t rounds = (tiles + slots - 1) / slots;
+        const double cost = double(rounds) * double((64 << lb) + 128);   // ~128 bases of per-unit overhead
         if (cost <= best_cost) {
             best_cost = cost;
             best = lb;

@@ -601,6 +601,23 @@ size_t fast_smem_bytes(int mode, int32_t t1_pad, int32_t hist_words, int threads
 
 int fast_threads() { return kFastThreads; }
 
+int fast_warps_per_cta(int64_t tiles, int num_sms) {
+    int warps = kFastThreads / 32;
+    if (tiles >= int64_t(num_sms) * 24) {
+        double best = -1.0;
+        for (int w = kFastThreads / 32; w >= 24; --w) {
+            const int64_t slots = int64_t(num_sms) * w;
+            const int64_t rounds = (tiles + slots - 1) / slots;
+            const double eff = double(tiles) / double(rounds * slots);
+            if (eff > best + 0.02) {   // fewer warps only when clearly better balanced
+                best = eff;
+                warps = w;
+            }
+        }
+    }
+    return warps;
+}
+
 int launch_log_scatter(ks_ctx* ctx, const LogEntry* log, int64_t n, const unsigned long long* n_dev,
                        const int64_t* row_off, const int32_t* acc_out_off, const int32_t* acc_out_ids, int64_t* rows,
                        int* launches) {
@@ -649,19 +666,7 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
     // into whole rounds over 148 x 32 warps, fewer warps per CTA can (e.g.
     // 4096 tiles: 28 warps x 148 = 4144 slots, one round, instead of 128
     // CTAs with 20 SMs idle); the shared-memory layout stays the 1024-thread one
-    int warps = kFastThreads / 32;
-    if (tiles >= int64_t(ctx->num_sms) * 24) {
-        double best = -1.0;
-        for (int w = kFastThreads / 32; w >= 24; --w) {
-            const int64_t slots = int64_t(ctx->num_sms) * w;
-            const int64_t rounds = (tiles + slots - 1) / slots;
-            const double eff = double(tiles) / double(rounds * slots);
-            if (eff > best + 0.02) {   // fewer warps only when clearly better balanced
-                best = eff;
-                warps = w;
-            }
-        }
-    }
+    const int warps = fast_warps_per_cta(tiles, ctx->num_sms);
     const int64_t need = (tiles + warps - 1) / warps;
     const int blocks = int(max64(1, min64(need, int64_t(ctx->num_sms))));
     fn<<<blocks, warps * 32, smem, ctx->stream>>>(a);

@@ -118,6 +118,9 @@ void chunk_geometry(int64_t begin, int64_t end, int64_t threads, int64_t* origin
 // Fast shared-memory kernel for tables with a fast form (csrc/scan_fast.cu).
 int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches);
 size_t fast_smem_bytes(int mode, int32_t t1_pad, int32_t hist_words, int threads);
+// Warps per CTA of the fast scan for `tiles` tiles of 32 units: 32, or fewer
+// when that makes the tiles fill whole rounds over all SMs.
+int fast_warps_per_cta(int64_t tiles, int num_sms);
 int fast_threads();
 // rows of the logged visits: rows[row_off[chunk] + local + k] = (pos1, id_k)
 // Rows of the visit log at their chunk offsets.  With n_dev the count is read
