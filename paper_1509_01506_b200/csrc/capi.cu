@@ -242,8 +242,10 @@ int monoid_prefix(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t beg
     int rc = dispatch(ctx, dfa, dfa->mono, plan_for(ctx, dfa, dfa->mono), m, kModeMap, launches);
     if (rc != KS_OK) return rc;
     if (trace) trace->mark("map pass");
+    const size_t window = size_t(reinterpret_cast<const char*>(dfa->d_action + size_t(h.nm) * h.nq) -
+                                 reinterpret_cast<const char*>(dfa->d_prod));
     rc = monoid_scan_entries(ctx, elems, nch, dfa->d_prod, h.nm, dfa->d_action, h.nq, entry_val, entry_ptr, centry,
-                             d_total, launches);
+                             d_total, window, launches);
     if (trace) trace->mark("monoid scan");
     return rc;
 }
@@ -802,6 +804,7 @@ int ks_open(int device, ks_ctx** out) {
         return fail(KS_E_UNSUPPORTED, "kmerscan_b200 requires an sm_100 (Blackwell) device");
     }
     c->num_sms = prop.multiProcessorCount;
+    c->l2_persist_max = size_t(prop.persistingL2CacheMaxSize);
     c->smem_optin = prop.sharedMemPerBlockOptin;
     e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {

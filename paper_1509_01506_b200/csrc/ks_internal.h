@@ -167,6 +167,8 @@ struct ks_ctx {
     unsigned long long* mstat = nullptr;
     int64_t mstat_cap = 0;
     uint32_t mepoch = 0;
+    size_t l2_persist = 0;      // persisting-L2 set-aside requested so far (monoid tables)
+    size_t l2_persist_max = 0;  // the device's limit
     // pinned host staging the locate scatter writes rows into (grow-only)
     void* rstage = nullptr;
     size_t rstage_bytes = 0;

@@ -14,6 +14,7 @@
 //           inclusive prefix; a tile composes its predecessors' words 32 at a
 //           time) that also applies the prefix to the entry state.
 #include <algorithm>
+#include <cstdlib>
 
 #include "scan_kernels.cuh"
 
@@ -268,7 +269,7 @@ namespace ks {
 
 int monoid_scan_entries(ks_ctx* ctx, const uint16_t* in, int64_t n, const uint16_t* prod, int32_t nm,
                         const uint16_t* action, int32_t nq, int32_t entry_val, const uint16_t* entry_ptr,
-                        uint16_t* centry, uint16_t* d_total, int* launches) {
+                        uint16_t* centry, uint16_t* d_total, size_t window_bytes, int* launches) {
     if (n <= 0) return KS_OK;
     const int64_t ntiles = (n + kTile - 1) / kTile;
     if (ctx->mstat_cap < ntiles) {
@@ -285,9 +286,29 @@ int monoid_scan_entries(ks_ctx* ctx, const uint16_t* in, int64_t n, const uint16
     int per_sm = 0;
     KS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, monoid_entry_scan_kernel, kThreads, 0));
     const int64_t grid = std::min<int64_t>(ntiles, int64_t(std::max(per_sm, 1)) * ctx->num_sms);
-    monoid_entry_scan_kernel<<<int(grid), kThreads, 0, ctx->stream>>>(in, n, MonoidOp{prod, nm}, action, nq,
-                                                                      entry_val, entry_ptr, centry, d_total,
-                                                                      ctx->mstat, ctx->mepoch);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    if (window_bytes && ctx->l2_persist_max && !std::getenv("KS_NO_L2_PERSIST")) {
+        const size_t want = std::min(ctx->l2_persist_max, std::max(ctx->l2_persist, window_bytes));
+        if (want > ctx->l2_persist && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess)
+            ctx->l2_persist = want;
+        cudaGetLastError();
+        if (ctx->l2_persist) {
+            attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+            attr[0].val.accessPolicyWindow.base_ptr = const_cast<uint16_t*>(prod);
+            attr[0].val.accessPolicyWindow.num_bytes = window_bytes;
+            attr[0].val.accessPolicyWindow.hitRatio = float(std::min(1.0, double(ctx->l2_persist) / double(window_bytes)));
+            attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+            attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+        }
+    }
+    KS_CUDA(cudaLaunchKernelEx(&cfg, monoid_entry_scan_kernel, in, n, MonoidOp{prod, nm}, action, nq, entry_val,
+                               entry_ptr, centry, d_total, ctx->mstat, ctx->mepoch));
     if (launches) ++*launches;
     KS_CUDA(cudaGetLastError());
     return KS_OK;

@@ -140,9 +140,12 @@ int exclusive_scan_max(ks_ctx* ctx, const int64_t* in, int64_t n, int64_t* out_e
 // states: centry[i] = action[(in[0] ... in[i-1])][q0] with q0 = entry_val
 // (>= 0) or *entry_ptr; centry may be null.  *d_total = the product of all n
 // elements.  One launch, no temporaries beyond ctx->mstat.
+// The product and action tables (window_bytes from prod on) are kept in the
+// persisting part of L2, so the dependent lookups stay L2 hits while the
+// sequence streams through (and across calls).
 int monoid_scan_entries(ks_ctx* ctx, const uint16_t* in, int64_t n, const uint16_t* prod, int32_t nm,
                         const uint16_t* action, int32_t nq, int32_t entry_val, const uint16_t* entry_ptr,
-                        uint16_t* centry, uint16_t* d_total, int* launches);
+                        uint16_t* centry, uint16_t* d_total, size_t window_bytes, int* launches);
 
 // Small helper kernels (csrc/scan.cu).
 int launch_finalize_counts(ks_ctx* ctx, const unsigned long long* visits, int32_t n_accept,
