@@ -8,13 +8,14 @@ steps ii-iv) over one batch of synthetic input.  Workload at N=1: config C3
 (1 GiB, 256 class patterns, |Q| ~ 3.3k, count only) -- the config the
 BASELINE target (>= 60% of HBM roofline at 1 GPU) is stated on.  For N > 1
 (torchrun, one rank per GPU) every rank scans its own 1 GiB shard of an
-N GiB sequence (weak scaling): boundary maps are all-gathered and the counts
-all-reduced over NCCL each step.
+N GiB sequence (weak scaling): definite automata (C3) load the previous
+shard's tail once (halo) and all-reduce the counts over NCCL each step; other
+automata all-gather their boundary maps first.
 
 Printed JSON (rank 0): value = bases/s over all ranks in GB/s (1 B/base);
 ``roofline`` for the dominant scan kernel against the measured HBM copy
 bandwidth; ``e2e`` = the same metric through the C ABI from pinned host
-ASCII (H2D + device encode + scan + D2H of the counts, every step);
+ASCII (host pack + H2D + scan + counts back to the host, every step);
 ``cpu_baseline`` = the reference algorithm (oracle/ref_scan.c, a C port of
 kmerscan.run) on this host's cores over a bounded sample.
 """
@@ -260,7 +261,7 @@ def run_ours(args) -> None:
         sh_halo = ctx.upload_ascii(np.concatenate([prev, wl.ascii]))
 
     def step() -> None:
-        if world == 1:  # enqueue only: scan + count + D2H of the counts, no host sync
+        if world == 1:  # enqueue only: one scan kernel that writes the counts into pinned host memory
             ctx.count_async(dh, sh, out_np)
             return
         if halo_mode:   # scan from the halo's lookback -> all-reduce of the counts
@@ -356,8 +357,8 @@ def run_ours(args) -> None:
     ctx.count(dh, sh)  # one synchronous call for the geometry stats
     stats = ctx.stats()
 
-    # e2e through the C ABI from pinned host ASCII: pipelined H2D + device
-    # encode + scan + D2H of the counts (ks_count_host_ascii), every step
+    # e2e through the C ABI from pinned host ASCII: pipelined host pack + H2D
+    # + scan + counts back to the host (ks_count_host_ascii), every step
     e2e_times = []
     host_np = ascii_host.numpy()
     for i in range(max(args.e2e_steps, 1) + 1):
