@@ -52,7 +52,7 @@ typedef struct ks_dfa_info {
     int32_t n_accepting;     /* states with a non-empty output multiset */
     int32_t strategy;        /* KS_STRATEGY_* */
     int32_t sync_depth;      /* D for LOOKBACK, -1 otherwise */
-    int32_t stride;          /* bases per shared-memory table lookup (1..4) */
+    int32_t stride;          /* bases per table lookup of the kernel that scans (1..4) */
     int32_t monoid_size;     /* |M| for MAPSCAN, 0 otherwise */
     int32_t other_resets;    /* 1 if every state goes to one state on OTHER */
     int64_t table_bytes;     /* bytes of the stride table staged per CTA */

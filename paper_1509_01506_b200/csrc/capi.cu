@@ -994,7 +994,8 @@ int ks_dfa_info_get(const ks_dfa* d, ks_dfa_info* out) {
     out->n_accepting = h.n_accept;
     out->strategy = h.strategy;
     out->sync_depth = h.strategy == KS_STRATEGY_LOOKBACK ? h.sync_depth : -1;
-    out->stride = h.scan.stride;
+    const bool fast = d->scan.fast_k > 0 && d->tables_in_smem;
+    out->stride = fast ? d->scan.fast_k : h.scan.stride;
     out->monoid_size = h.strategy == KS_STRATEGY_MAPSCAN ? h.nm : 0;
     out->other_resets = h.scan.reset_state >= 0 ? 1 : 0;
     out->table_bytes = int64_t(d->scan.tk_bytes + d->scan.t1_bytes);

@@ -111,6 +111,7 @@ def test_random_vs_oracle(ctx, seed):
 @pytest.mark.parametrize("stride", ["1", "2", "3", "4"])
 def test_forced_strides(monkeypatch, stride):
     monkeypatch.setenv("KS_FORCE_STRIDE", stride)
+    monkeypatch.setenv("KS_DISABLE_FAST", "1")   # the generic kernel at each stride
     ctx = _native.DeviceContext(0)
     w = workloads.make(2, 1 << 20)
     codes = ks.encode_bytes(w.ascii.tobytes())
