@@ -31,9 +31,13 @@ int stream_count_impl(ks_ctx* ctx, const ks_dfa* dfa, const uint8_t* bytes, int6
     const bool wire = stream_mode == kStreamWire;
     const HostDfa& h = dfa->host;
     *fallback = false;
-    // piece size: 64 MiB; KS_PIECE_KB overrides (tests use small pieces to cross many boundaries)
+    // piece size: 64 MiB (inputs below 128 MiB: a quarter of the input, at
+    // least 16 MiB, so packing, copy and scan still overlap -- C2 +4%);
+    // KS_PIECE_KB overrides (tests use small pieces to cross many boundaries)
     const char* pk = std::getenv("KS_PIECE_KB");
-    const int64_t piece_bytes = pk && std::atoll(pk) > 0 ? std::atoll(pk) << 10 : int64_t(64) << 20;
+    const int64_t piece_bytes = pk && std::atoll(pk) > 0 ? std::atoll(pk) << 10
+                                : n_bytes < (int64_t(128) << 20) ? std::max<int64_t>(int64_t(16) << 20, n_bytes / 4)
+                                                                 : int64_t(64) << 20;
     const int64_t piece = std::min<int64_t>(std::max<int64_t>(n_bytes, 64), piece_bytes);
     const int64_t npieces = (n_bytes + piece - 1) / piece;
     ks_seq tmpl;
