@@ -728,7 +728,7 @@ int choose_lb(const ks_ctx* ctx, int64_t n) {
     if (const char* e = std::getenv("KS_TILE_LB"); e && *e) return std::min(6, std::max(0, std::atoi(e)));
     int best = 2;
     double best_cost = 1e300;
-    for (int lb = 2; lb <= 6; ++lb) {
+    for (int lb = 0; lb <= 6; ++lb) {
         const int64_t tile = int64_t(2048) << lb;
         const int64_t tiles = std::max<int64_t>(1, (n + tile - 1) / tile);
         const int64_t slots = int64_t(ctx->num_sms) * fast_warps_per_cta(tiles, ctx->num_sms);
