@@ -37,7 +37,10 @@ constexpr int kRing = 8;      // minimum ring depth (deferred hits per lane)
 constexpr int kRingMax = 32;  // the ring takes what shared memory is left, up to this
 // steps between ring-fill checks: every 4th step at K = 2 (high hit rates),
 // every 8th otherwise (the vote is pure overhead when hits are rare)
-__host__ __device__ constexpr int chk_steps(int k) { return k == 2 ? 4 : 8; }
+#ifndef KS_CHK2   // build-time tuning knob (make EXTRA=-DKS_CHK2=n)
+#define KS_CHK2 4
+#endif
+__host__ __device__ constexpr int chk_steps(int k) { return k == 2 ? KS_CHK2 : 8; }
 constexpr int kFastThreads = 1024;
 constexpr uint32_t kRingStride = 4u * kFastThreads;  // bytes between ring slots
 
