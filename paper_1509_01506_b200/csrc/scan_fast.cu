@@ -215,13 +215,51 @@ __device__ __forceinline__ void resolve(const Ctx& c, Lane<MODE>& L, uint32_t a)
     }
 }
 
+// Predicated (branch-free) shared-memory helpers for the count drain.
+__device__ __forceinline__ uint32_t lds32_if(uint32_t p, uint32_t addr) {
+    uint32_t v = 0;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q ld.shared.u32 %0, [%2];\n\t}"
+                 : "+r"(v) : "r"(p), "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t lds16_if(uint32_t p, uint32_t addr) {
+    unsigned short v = 0;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q ld.shared.u16 %0, [%2];\n\t}"
+                 : "+h"(v) : "r"(p), "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_if(uint32_t p, uint32_t addr) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q red.shared.add.u32 [%1], 1;\n\t}"
+                 :: "r"(p), "r"(addr) : "memory");
+}
+
+#ifndef KS_PRED_DRAIN
+#define KS_PRED_DRAIN 1
+#endif
+// Count-mode drain of 2-base ring entries without divergent branches: every
+// lane runs every row, the loads and the histogram adds are predicated.
+__device__ __forceinline__ void drain_count2(const Ctx& c, uint32_t rp0, uint32_t cnt, uint32_t kmax) {
+    for (uint32_t k = 0; k < kmax; ++k) {
+        const uint32_t v = lds32_if(k < cnt, rp0 + k * kRingStride);
+        const uint32_t e = v >> 17;
+        const uint32_t h1 = e & 0x2000u, h2 = e & 0x4000u;
+        const uint32_t s1 = lds16_if(h1, c.t1 + (((v >> 1) & 0xFFFu) * c.t1_cols + ((v >> 13) & 3u)) * 2u);
+        red_if(h1, c.hist + 4u * s1);
+        red_if(h2, c.hist + 4u * ((e >> 1) & 0xFFFu));
+    }
+}
+
 template <int K, int MODE>
 __device__ __forceinline__ void drain(const Ctx& c, Lane<MODE>& L, unsigned am, uint32_t rp0,
                                       uint32_t& rp, uint32_t ring_stride) {
     const uint32_t cnt = (rp - rp0) / kRingStride;
     const uint32_t kmax = __reduce_max_sync(am, cnt);  // warp-uniform trip count
-    for (uint32_t k = 0; k < kmax; ++k)
-        if (k < cnt) resolve<K, MODE>(c, L, lds32(rp0 + k * ring_stride));
+    if constexpr (K == 2 && MODE == kModeCount && KS_PRED_DRAIN) {
+        drain_count2(c, rp0, cnt, kmax);
+    } else {
+        for (uint32_t k = 0; k < kmax; ++k)
+            if (k < cnt) resolve<K, MODE>(c, L, lds32(rp0 + k * ring_stride));
+    }
     rp = rp0;
 }
 
@@ -229,6 +267,10 @@ __device__ __forceinline__ void drain(const Ctx& c, Lane<MODE>& L, unsigned am, 
 // loop (one copy of the resolve code instead of one per site).
 template <int K, int MODE>
 __device__ __noinline__ uint32_t drain_out(const Ctx c, uint32_t rp0, uint32_t cnt) {
+    if constexpr (K == 2 && MODE == kModeCount && KS_PRED_DRAIN) {
+        drain_count2(c, rp0, cnt, __reduce_max_sync(0xffffffffu, cnt));
+        return 0u;
+    }
     Lane<MODE> L;
     const uint32_t kmax = __reduce_max_sync(0xffffffffu, cnt);
     for (uint32_t k = 0; k < kmax; ++k)
