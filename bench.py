@@ -83,7 +83,7 @@ class ClockSampler:
         "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4,
     }
 
-    def __init__(self, gpu: int, period_s: float = 0.002):
+    def __init__(self, gpu: int, period_s: float = 0.001):
         self.gpu = gpu
         self.period = period_s
         self.samples: list[tuple[int, int, int]] = []
@@ -127,7 +127,7 @@ class ClockSampler:
         reasons = sorted({name for _, _, rs in self.samples for name, bit in self.REASONS.items() if rs & bit})
         return {"sm_mhz": statistics.median(s for s, _, _ in self.samples),
                 "sm_max_mhz": max(m for _, m, _ in self.samples), "reasons": reasons,
-                "samples": len(self.samples), "source": "NVML, 2 ms poll during the timed steps"}
+                "samples": len(self.samples), "source": "NVML, 1 ms poll during the timed steps"}
 
 
 def cpu_baseline(wl, sample_bases: int, min_seconds: float = 10.0, max_reps: int = 20) -> dict:
@@ -450,7 +450,7 @@ def run_ours(args) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--bases", type=int, default=None, help="override bases per GPU")
