@@ -162,6 +162,11 @@ int run_scan(ks_ctx* ctx, const void* in, int64_t n, const Op& op, Out* out, typ
 // Status word of a tile: epoch << 32 | flag << 16 | element (flag 1: the
 // tile's own product, 2: inclusive prefix through the tile).
 constexpr unsigned kAgg = 1u, kIncl = 2u;
+#ifndef KS_MITEMS   // build-time knob: elements per thread of the monoid scan
+#define KS_MITEMS 2
+#endif
+constexpr int kMItems = KS_MITEMS;
+constexpr int kMTile = kThreads * kMItems;
 
 __device__ __forceinline__ unsigned long long status_word(uint32_t epoch, unsigned flag, unsigned v) {
     return (static_cast<unsigned long long>(epoch) << 32) | (flag << 16) | (v & 0xFFFFu);
@@ -174,16 +179,16 @@ __global__ void __launch_bounds__(kThreads) monoid_entry_scan_kernel(
     using T = unsigned int;
     __shared__ T s_prefix;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t ntiles = (n + kTile - 1) / kTile;
+    const int64_t ntiles = (n + kMTile - 1) / kMTile;
     const uint32_t q0 = entry_ptr ? uint32_t(*entry_ptr) : uint32_t(entry_val);
     // tiles in launch order: every tile a CTA waits for belongs to a CTA of
     // this (co-resident) grid that started it earlier
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int64_t base = t * kTile + int64_t(threadIdx.x) * kItems;
-        T items[kItems];
+        const int64_t base = t * kMTile + int64_t(threadIdx.x) * kMItems;
+        T items[kMItems];
         T acc = op.identity();
 #pragma unroll
-        for (int i = 0; i < kItems; ++i) {
+        for (int i = 0; i < kMItems; ++i) {
             items[i] = base + i < n ? T(in[base + i]) : op.identity();
             acc = op(acc, items[i]);
         }
@@ -233,7 +238,7 @@ __global__ void __launch_bounds__(kThreads) monoid_entry_scan_kernel(
         if (centry) {
             T run = op(s_prefix, ex);
 #pragma unroll
-            for (int i = 0; i < kItems; ++i) {
+            for (int i = 0; i < kMItems; ++i) {
                 if (base + i < n) centry[base + i] = action[size_t(run) * nq + q0];
                 run = op(run, items[i]);
             }
@@ -271,7 +276,7 @@ int monoid_scan_entries(ks_ctx* ctx, const uint16_t* in, int64_t n, const uint16
                         const uint16_t* action, int32_t nq, int32_t entry_val, const uint16_t* entry_ptr,
                         uint16_t* centry, uint16_t* d_total, size_t window_bytes, int* launches) {
     if (n <= 0) return KS_OK;
-    const int64_t ntiles = (n + kTile - 1) / kTile;
+    const int64_t ntiles = (n + kMTile - 1) / kMTile;
     if (ctx->mstat_cap < ntiles) {
         KS_CUDA(cudaStreamSynchronize(ctx->stream));
         if (ctx->mstat) KS_CUDA(cudaFree(ctx->mstat));
