@@ -11,7 +11,7 @@
 //   * the 1-base table (|Q|+1) x 5 (row-major, OTHER column included) for
 //     re-walks, OTHER blocks and the lookback;
 //   * a per-lane ring of deferred hits, as deep as the shared memory left
-//     allows (C3: 13): a flagged step only stores its table address (K = 2:
+//     allows (C3: 15): a flagged step only stores its table address (K = 2:
 //     address | entry << 17) with a predicated STS, no divergence; every
 //     chk_steps(K) steps the warp votes whether some lane's ring is nearly
 //     full and only then calls the out-of-line drain, which resolves every
