@@ -8,8 +8,9 @@
 //     next K bases overwrite, so the next lookup address is a single LOP3
 //     bit-select of the previous entry and the funnel-shifted input word:
 //     per K bases the critical path is SHF -> LOP3 -> LDS.
-//   * the 1-base table (|Q|+1) x 5 (row-major, OTHER column included) for
-//     re-walks, OTHER blocks and the lookback;
+//   * the 1-base table (|Q|+1) x 5, row-major (x 4 when OTHER resets every
+//     state: the column is not stored) for re-walks, OTHER blocks and the
+//     lookback;
 //   * a per-lane ring of deferred hits, as deep as the shared memory left
 //     allows (C3: 15): a flagged step only stores its table address (K = 2:
 //     address | entry << 17) with a predicated STS, no divergence; every
