@@ -217,6 +217,10 @@ int dispatch(ks_ctx* ctx, const ks_dfa* dfa, const DevTable& T, const ScanPlan& 
         a.t1 = T.t1z;
         a.t1_pad = int32_t(T.t1z_bytes / 2);
         a.t1_cols = T.t1z_cols;
+        // rare hits (expected < 5% of warp-blocks): scan blocks without hit
+        // bookkeeping, re-run the few that hit (KS_LEAN=0/1 overrides)
+        a.lean = T.hit_rate * 64.0 * 32.0 < 0.05 ? 1 : 0;
+        if (const char* e = std::getenv("KS_LEAN"); e && *e) a.lean = std::atoi(e) != 0;
         return launch_scan_fast(ctx, a, mode, T.fast_k, launches);
     }
     return launch_scan(ctx, a, mode, T.stride, dfa->tables_in_smem, launches);

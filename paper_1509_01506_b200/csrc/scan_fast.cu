@@ -279,6 +279,33 @@ __device__ __noinline__ uint32_t drain_out(const Ctx c, uint32_t rp0, uint32_t c
     return L.nrows;
 }
 
+// A block without hit bookkeeping: the state after it, and in `hm` the OR of
+// the entries (bit 15: some state on the way accepts).
+template <int K>
+__device__ __forceinline__ uint32_t fast_block_lean(const Ctx& c, uint32_t s, const uint4& xb, uint32_t& hm) {
+    constexpr int NL = 64 / K;
+    constexpr int LC = 17 - 2 * K;
+    constexpr uint32_t FM = ((1u << (2 * K)) - 1u) << LC;
+    uint32_t e = s << 1, acc = 0;
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+        uint32_t a = bitsel<FM>(field<K>(xb, j), e);
+        if constexpr (swizzled(K)) a ^= field_at<K, 1>(xb, j) & 0x3Eu;
+        e = lds16(c.tk + a);
+        acc |= e;
+    }
+    s = (e >> 1) & ((1u << (LC - 1)) - 1u);
+    const uint64_t w0 = (uint64_t(xb.y) << 32) | xb.x;
+    const uint64_t w1 = (uint64_t(xb.w) << 32) | xb.z;
+#pragma unroll
+    for (int r = NL * K; r < 64; ++r) {
+        s = step1(c, s, uint32_t(r < 32 ? w0 >> (2 * r) : w1 >> (2 * (r - 32))) & 3u);
+        acc |= s < c.n_accept ? 0x8000u : 0u;
+    }
+    hm = acc;
+    return s;
+}
+
 // One full, OTHER-free 64-base block.  Live lanes (lm = 0x8000) record
 // hits; the others (lm = 0: no work for this block) ride along from any
 // state without recording, so the warp never diverges.
@@ -330,7 +357,7 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
 
 extern __shared__ __align__(128) unsigned char f_smem[];
 
-template <int K, int MODE>
+template <int K, int MODE, bool LEAN = false>
 __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     constexpr bool RING = MODE == kModeCount || MODE == kModeRows;
     constexpr bool HIST = RING || MODE == kModeLog;
@@ -491,8 +518,33 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
             }
             if (__all_sync(am, fast)) {
                 const bool live = has && !alln;
-                const uint32_t s2 = fast_block<K, MODE>(c, L, live ? s : idle, live ? 0x8000u : 0u, wb, p0, am,
-                                                        rp0, rp, ring_stride);
+                uint32_t s2;
+                // rare-hit automata (a compile-time variant: one path per kernel
+                // keeps the registers of the other untouched)
+                if constexpr (LEAN && MODE != kModeMap) {
+                    uint32_t hm;
+                    s2 = fast_block_lean<K>(c, live ? s : idle, wb, hm);
+                    if constexpr (MODE == kModeLog) {
+                        // rare: the lanes that hit re-walk the block base by base
+                        // (a compact loop: the unrolled recording block would not
+                        // fit the log mode into 64 registers)
+                        if (live && (hm & 0x8000u)) {
+                            const uint64_t b0 = (uint64_t(wb.y) << 32) | wb.x, b1 = (uint64_t(wb.w) << 32) | wb.z;
+                            uint32_t x = s;
+#pragma unroll 1
+                            for (int q = 0; q < 64; ++q) {
+                                x = step1(c, x, uint32_t(q < 32 ? b0 >> (2 * q) : b1 >> (2 * (q - 32))) & 3u);
+                                if (x < c.n_accept) record<MODE>(c, L, p0 + q, x);
+                            }
+                        }
+                    } else if (__any_sync(am, live && (hm & 0x8000u))) {   // rare: re-run the block recording
+                        s2 = fast_block<K, MODE>(c, L, live ? s : idle, live ? 0x8000u : 0u, wb, p0, am, rp0, rp,
+                                                 ring_stride);
+                    }
+                } else {
+                    s2 = fast_block<K, MODE>(c, L, live ? s : idle, live ? 0x8000u : 0u, wb, p0, am, rp0, rp,
+                                             ring_stride);
+                }
                 if (live) {
                     s = s2;
                 } else if (has) {
@@ -586,13 +638,13 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
 using FastFn = void (*)(const ScanArgs);
 
 template <int K>
-FastFn pick_mode(int mode) {
+FastFn pick_mode(int mode, bool lean) {
     switch (mode) {
-        case kModeCount: return scan_fast_kernel<K, kModeCount>;
-        case kModeRows: return scan_fast_kernel<K, kModeRows>;
-        case kModeEmit: return scan_fast_kernel<K, kModeEmit>;
+        case kModeCount: return lean ? scan_fast_kernel<K, kModeCount, true> : scan_fast_kernel<K, kModeCount, false>;
+        case kModeRows: return lean ? scan_fast_kernel<K, kModeRows, true> : scan_fast_kernel<K, kModeRows, false>;
+        case kModeEmit: return lean ? scan_fast_kernel<K, kModeEmit, true> : scan_fast_kernel<K, kModeEmit, false>;
         case kModeMap: return scan_fast_kernel<K, kModeMap>;
-        case kModeLog: return scan_fast_kernel<K, kModeLog>;
+        case kModeLog: return lean ? scan_fast_kernel<K, kModeLog, true> : scan_fast_kernel<K, kModeLog, false>;
     }
     return nullptr;
 }
@@ -617,11 +669,11 @@ __global__ void log_scatter_kernel(const LogEntry* __restrict__ log, int64_t n, 
     }
 }
 
-FastFn pick(int mode, int k) {
+FastFn pick(int mode, int k, bool lean) {
     switch (k) {
-        case 2: return pick_mode<2>(mode);
-        case 3: return pick_mode<3>(mode);
-        case 4: return pick_mode<4>(mode);
+        case 2: return pick_mode<2>(mode, lean);
+        case 3: return pick_mode<3>(mode, lean);
+        case 4: return pick_mode<4>(mode, lean);
     }
     return nullptr;
 }
@@ -681,7 +733,7 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
     const bool ring = mode == kModeCount || mode == kModeRows;
     const bool hist = ring || mode == kModeLog;
     a.hist_smem = hist ? 1 : 0;
-    FastFn fn = pick(mode, k);
+    FastFn fn = pick(mode, k, a.lean != 0);
     if (!fn) return fail(KS_E_INVALID, "fast scan: bad mode/stride");
     size_t smem = fast_fixed_bytes(a.t1_pad, hist ? a.n_accept : 0);
     if (ring) {

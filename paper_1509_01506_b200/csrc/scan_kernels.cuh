@@ -62,6 +62,8 @@ struct ScanArgs {
     int32_t nq = 0, n_accept = 0, reset_state = -1;
     int32_t tk_pad = 0, t1_pad = 0;  // uint16 entries, multiples of 8
     int32_t t1_cols = 5;             // fast kernel: columns of t1 (4: OTHER -> reset_state)
+    int32_t lean = 0;                // fast kernel: hits so rare that blocks run without recording
+                                     // and a warp re-runs a block only when one of its lanes hit
     int32_t hist_smem = 0;           // histogram in shared memory
     int32_t ring_depth = 0;          // fast kernel: deferred hits per lane (set by launch_scan_fast)
     // outputs

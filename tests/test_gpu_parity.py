@@ -866,3 +866,29 @@ def test_concurrent_calls_on_one_context():
     for t in threads:
         t.join()
     assert not errors, errors[:3]
+
+
+@pytest.mark.parametrize("lean", ["0", "1"])
+@pytest.mark.parametrize("config", [1, 2, 3, 4])
+def test_lean_blocks_forced(monkeypatch, config, lean):
+    """Blocks scanned without hit bookkeeping and re-run when a lane hit
+    (the default for rare-hit automata such as C4's) forced on and off for
+    every config automaton: counts, rows, ranges, streamed input."""
+    monkeypatch.setenv("KS_LEAN", lean)
+    w = workloads.make(config, 300_007)
+    codes = ks.encode_bytes(w.ascii.tobytes())
+    want, rows = O.ref_run(w.dfa, codes, 1, 10, True)[:2]
+    c2 = _native.DeviceContext(0)
+    dh = c2.dfa(w.dfa)
+    sh = c2.upload_codes(codes)
+    assert c2.count(dh, sh).tolist() == want.tolist()
+    got, grows = c2.locate(dh, sh)
+    assert got.tolist() == want.tolist() and np.array_equal(grows, rows)
+    assert c2.count_host_ascii(dh, w.ascii.tobytes()).tolist() == want.tolist()
+    rng = np.random.default_rng(config)
+    for _ in range(4):
+        b, e = sorted(rng.integers(0, codes.size, 2).tolist())
+        entry = int(rng.integers(0, w.dfa.state_count))
+        w2, last = O.ref_sequential_count(w.dfa, codes, b, e, entry)
+        g2, ex, _ = c2.scan_range(dh, sh, b, e, entry)
+        assert g2.tolist() == w2.tolist() and ex == last
