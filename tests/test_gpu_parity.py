@@ -633,14 +633,18 @@ def test_speculate_streamed_and_sharded(monkeypatch):
     assert total.tolist() == want.tolist()
 
 
+@pytest.mark.parametrize("lean", ["", "1"])
 @pytest.mark.parametrize("n", [200_000, 6_000_000])
-def test_locate_log_and_overflow_fallback(n):
+def test_locate_log_and_overflow_fallback(monkeypatch, n, lean):
     """Single-pass locate logs every accepting visit; a hit-dense scan whose
     visits overflow the log (C3's automaton on 6 M bases: > 64 Ki visits)
-    takes the two-pass path.  Both give the reference's sorted rows."""
+    takes the two-pass path.  Both give the reference's sorted rows (also
+    with lean blocks forced: their re-runs in the rows and emit passes)."""
+    if lean:
+        monkeypatch.setenv("KS_LEAN", lean)
     w = workloads.make(3, n)
     sym = ks.encode_bytes(w.ascii.tobytes())
-    ctx = _native.context(0)
+    ctx = _native.DeviceContext(0)
     dh = ctx.dfa(w.dfa)
     counts, rows = ctx.locate(dh, ctx.upload_codes(sym))
     ref_counts, _, ref_rows = O.ref_scan_rows(w.dfa, sym, 0, n, w.dfa.start)
