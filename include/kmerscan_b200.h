@@ -132,10 +132,13 @@ KS_API int ks_count(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t* 
 KS_API int ks_locate(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t* counts_out,
               int64_t** rows_out, int64_t* n_rows);
 
-/* Asynchronous ks_count on the device-resident sequence: enqueues the scan,
- * the count reduction and the copy of the int64 counts into `counts_pinned`
- * (page-locked host memory) without waiting.  ks_async_wait synchronises and
- * reports the summed scan-kernel time of the calls since the last wait. */
+/* Asynchronous ks_count on the device-resident sequence: enqueues the scan
+ * (whose last CTA reduces the counts and writes them into `counts_pinned`,
+ * page-locked host memory; a copy follows when that memory is not device-
+ * visible) without waiting.  ks_async_wait synchronises and reports the calls
+ * and kernel launches since the last wait; the summed scan-kernel time only
+ * with KS_ASYNC_EVENTS=1 (per-call events, else 0: events between
+ * back-to-back scans cost time and block their early launch). */
 KS_API int ks_count_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t* counts_pinned);
 KS_API int ks_async_wait(ks_ctx* ctx, float* scan_ms_total, int32_t* calls, int32_t* launches);
 

@@ -234,6 +234,9 @@ __device__ __forceinline__ void red_if(uint32_t p, uint32_t addr) {
                  :: "r"(p), "r"(addr) : "memory");
 }
 
+#ifndef KS_PDL   // build-time knob: programmatic dependent launch of the fast scan
+#define KS_PDL 1
+#endif
 #ifndef KS_PRED_DRAIN
 #define KS_PRED_DRAIN 1
 #endif
@@ -388,6 +391,14 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     }
     if constexpr (HIST)
         for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x) s_hist[i] = 0u;
+    if constexpr (KS_PDL) {
+        // launched with programmatic stream serialisation: let the next
+        // kernel of the stream start its own prologue as our CTAs retire, and
+        // wait for the previous one only now -- nothing above reads memory a
+        // preceding kernel writes (the tables come from a synchronous upload)
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
     mbar_wait_parity0(mbar);
     __syncthreads();
 
@@ -767,7 +778,21 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
     const int warps = fast_warps_per_cta(tiles, ctx->num_sms);
     const int64_t need = (tiles + warps - 1) / warps;
     const int blocks = int(max64(1, min64(need, int64_t(ctx->num_sms))));
-    fn<<<blocks, warps * 32, smem, ctx->stream>>>(a);
+    if constexpr (KS_PDL) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(unsigned(blocks));
+        cfg.blockDim = dim3(unsigned(warps * 32));
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        KS_CUDA(cudaLaunchKernelEx(&cfg, fn, a));
+    } else {
+        fn<<<blocks, warps * 32, smem, ctx->stream>>>(a);
+    }
     if (launches) ++*launches;
     KS_CUDA(cudaGetLastError());
     return KS_OK;
