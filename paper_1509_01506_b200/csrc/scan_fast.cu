@@ -719,6 +719,8 @@ size_t fast_smem_bytes(int mode, int32_t t1_pad, int32_t hist_words, int threads
 int fast_threads() { return kFastThreads; }
 
 int fast_warps_per_cta(int64_t tiles, int num_sms) {
+    if (const char* e = std::getenv("KS_FAST_WARPS"); e && *e)   // tuning knob (16..32)
+        return std::min(kFastThreads / 32, std::max(16, std::atoi(e)));
     int warps = kFastThreads / 32;
     if (tiles >= int64_t(num_sms) * 24) {
         double best = -1.0;
