@@ -112,6 +112,10 @@ struct PhaseTrace {
     }
 };
 
+// Walk [begin, end) from every state (uniform_start < 0, nlanes = |Q|) or
+// from one state; internal ids into out (uint32).
+int launch_walk(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end, int32_t nlanes,
+                int32_t uniform_start, uint32_t* out);
 int monoid_prefix(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end,
                   int64_t origin, int64_t L, int64_t nch, uint16_t* elems, uint16_t* centry, int32_t entry_val,
                   const uint16_t* entry_ptr, uint16_t* d_total, int* launches, PhaseTrace* trace = nullptr);
