@@ -235,3 +235,24 @@ def test_cli_matches_reference_transcript_gpu(case, capsys, monkeypatch):
     code, out, err = _run_case(case, capsys, monkeypatch)
     assert code == 0 and err == ""
     assert _untimed(case["argv"], out) == _untimed(case["argv"], case["stdout"])
+
+
+def test_bench_reference_arm_contract():
+    """`bench.py --impl reference` (the reference algorithm's C port on the host
+    cores) prints one JSON line with the contract's keys -- runs on CPU."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    repo = Path(__file__).resolve().parents[1]
+    out = subprocess.run([sys.executable, str(repo / "bench.py"), "--impl", "reference", "--config", "1",
+                          "--steps", "1", "--warmup", "1", "--cpu-sample", str(1 << 18)],
+                         capture_output=True, text=True, timeout=600, cwd=repo)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["unit"] == "GB/s" and line["value"] > 0
+    for key in ("metric", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "config"):
+        assert key in line
+    assert {"value", "unit", "cores", "kind", "sample"} <= set(line["cpu_baseline"])
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
