@@ -720,6 +720,7 @@ int ks_close(ks_ctx* ctx) {
     if (ctx->sbuf) cudaFree(ctx->sbuf);
     if (ctx->spec_buf) cudaFree(ctx->spec_buf);
     if (ctx->mstat) cudaFree(ctx->mstat);
+    if (ctx->rowstat) cudaFree(ctx->rowstat);
     if (ctx->rstage) cudaFreeHost(ctx->rstage);
     if (ctx->rdev) cudaFree(ctx->rdev);
     if (ctx->log_buf) cudaFree(ctx->log_buf);

@@ -167,6 +167,11 @@ struct ks_ctx {
     unsigned long long* mstat = nullptr;
     int64_t mstat_cap = 0;
     uint32_t mepoch = 0;
+    // single-pass row-offset scan: per-tile flags (epoch | flag) and the
+    // tiles' sums / inclusive prefixes, zeroed once at allocation
+    void* rowstat = nullptr;
+    int64_t rowstat_cap = 0;
+    uint32_t rowepoch = 0;
     size_t l2_persist = 0;      // persisting-L2 set-aside requested so far (monoid tables)
     size_t l2_persist_max = 0;  // the device's limit
     // pinned host staging the locate scatter writes rows into (grow-only)

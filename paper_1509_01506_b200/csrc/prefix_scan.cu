@@ -247,6 +247,92 @@ __global__ void __launch_bounds__(kThreads) monoid_entry_scan_kernel(
     }
 }
 
+
+// Single-pass exclusive sum of uint32 counts into int64 offsets (decoupled
+// look-back; replaces three launches on the locate and compaction paths).
+// Tile t publishes its sum (flag 1) and then its inclusive prefix (flag 2);
+// the flag word carries the call's epoch, values sit in separate arrays
+// written before the flag.
+__global__ void __launch_bounds__(kThreads) rows_scan_kernel(const uint32_t* __restrict__ in, int64_t n,
+                                                              long long* __restrict__ out, long long* total,
+                                                              unsigned long long* flag, long long* agg,
+                                                              long long* inc, uint32_t epoch) {
+    using T = long long;
+    AddOp op;
+    __shared__ T s_prefix;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t ntiles = (n + kTile - 1) / kTile;
+    const unsigned long long e2 = (unsigned long long)epoch << 2;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t base = t * kTile + int64_t(threadIdx.x) * kItems;
+        T items[kItems];
+        T acc = 0;
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {
+            items[i] = base + i < n ? T(in[base + i]) : 0;
+            acc += items[i];
+        }
+        T tot;
+        const T ex = block_exclusive<AddOp>(acc, op, &tot);
+        if (warp == 0) {
+            T prefix = 0;
+            if (t == 0) {
+                if (lane == 0) {
+                    inc[0] = tot;
+                    __threadfence();
+                    atomicExch(&flag[0], e2 | 2ull);
+                }
+            } else {
+                if (lane == 0) {
+                    agg[t] = tot;
+                    __threadfence();
+                    atomicExch(&flag[t], e2 | 1ull);
+                }
+                T run = 0;
+                for (int64_t j = t - 1;; j -= 32) {
+                    const int64_t k = j - lane;
+                    unsigned f = 2;
+                    T v = 0;
+                    if (k >= 0) {
+                        unsigned long long w;
+                        do {
+                            w = atomicAdd(&flag[k], 0ull);
+                        } while ((w >> 2) != (unsigned long long)epoch);
+                        f = unsigned(w & 3ull);
+                        __threadfence();
+                        v = f == 2 ? __ldcg(&inc[k]) : __ldcg(&agg[k]);
+                    }
+                    const unsigned incl = __ballot_sync(0xffffffffu, f == 2);
+                    const int stop = incl ? __ffs(incl) - 1 : 32;
+                    T x = lane <= stop ? v : 0;
+#pragma unroll
+                    for (int d = 16; d > 0; d >>= 1) x += __shfl_down_sync(0xffffffffu, x, d);
+                    run += __shfl_sync(0xffffffffu, x, 0);
+                    if (stop < 32) break;
+                }
+                prefix = run;
+                if (lane == 0) {
+                    inc[t] = prefix + tot;
+                    __threadfence();
+                    atomicExch(&flag[t], e2 | 2ull);
+                }
+            }
+            if (lane == 0) {
+                s_prefix = prefix;
+                if (t == ntiles - 1 && total) *total = prefix + tot;
+            }
+        }
+        __syncthreads();
+        T run = s_prefix + ex;
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {
+            if (base + i < n) out[base + i] = run;
+            run += items[i];
+        }
+        __syncthreads();
+    }
+}
+
 }  // namespace
 
 size_t exclusive_scan_rows_tmp_bytes(int64_t n) {
@@ -255,9 +341,35 @@ size_t exclusive_scan_rows_tmp_bytes(int64_t n) {
 
 int exclusive_scan_rows(ks_ctx* ctx, const uint32_t* in, int64_t n, int64_t* out_excl,
                         int64_t* d_total, void* tmp, int* launches) {
-    AddOp op;
-    return run_scan<AddOp, long long>(ctx, in, n, op, reinterpret_cast<long long*>(out_excl),
-                                      reinterpret_cast<long long*>(d_total), tmp, launches);
+    (void)tmp;
+    if (n <= 0) {
+        if (d_total) KS_CUDA(cudaMemsetAsync(d_total, 0, 8, ctx->stream));
+        return KS_OK;
+    }
+    const int64_t ntiles = (n + kTile - 1) / kTile;
+    if (ctx->rowstat_cap < ntiles) {
+        KS_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (ctx->rowstat) KS_CUDA(cudaFree(ctx->rowstat));
+        ctx->rowstat = nullptr;
+        ctx->rowstat_cap = 0;
+        const int64_t cap = std::max<int64_t>(ntiles, 1024);
+        KS_CUDA(cudaMalloc(&ctx->rowstat, size_t(cap) * 24));
+        KS_CUDA(cudaMemset(ctx->rowstat, 0, size_t(cap) * 24));
+        ctx->rowstat_cap = cap;
+    }
+    if (++ctx->rowepoch == 0) ctx->rowepoch = 1;
+    unsigned long long* flag = static_cast<unsigned long long*>(ctx->rowstat);
+    long long* agg = reinterpret_cast<long long*>(flag + ctx->rowstat_cap);
+    long long* inc = agg + ctx->rowstat_cap;
+    int per_sm = 0;
+    KS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rows_scan_kernel, kThreads, 0));
+    const int64_t grid = std::min<int64_t>(ntiles, int64_t(std::max(per_sm, 1)) * ctx->num_sms);
+    rows_scan_kernel<<<int(grid), kThreads, 0, ctx->stream>>>(in, n, reinterpret_cast<long long*>(out_excl),
+                                                               reinterpret_cast<long long*>(d_total), flag, agg,
+                                                               inc, ctx->rowepoch);
+    if (launches) ++*launches;
+    KS_CUDA(cudaGetLastError());
+    return KS_OK;
 }
 
 int exclusive_scan_max(ks_ctx* ctx, const int64_t* in, int64_t n, int64_t* out_excl, int64_t* d_total,
