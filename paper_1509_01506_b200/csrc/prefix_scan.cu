@@ -3,8 +3,11 @@
 // * rows:   uint32 per-chunk row counts -> int64 exclusive offsets (locate
 //           compaction: every chunk writes its rows at its offset, so the
 //           concatenation is already sorted by (offset, id) -- no sort, unlike
-//           the reference's np.lexsort in engine.py:176); reduce-then-scan,
-//           three launches (also the running max of the FASTA line state);
+//           the reference's np.lexsort in engine.py:176), and the kept-symbol
+//           positions of the device compaction: one single-pass launch
+//           (decoupled look-back, rows_scan_kernel);
+// * max:    the FASTA line state's running maximum (reduce-then-scan, three
+//           launches);
 // * monoid: per-chunk transition-monoid elements -> each chunk's entry state,
 //           the composition of chunk "start-state -> end-state" maps (the
 //           reference's left-to-right chain walk, engine.py:155-163, done as
