@@ -6,8 +6,7 @@
 //           the reference's np.lexsort in engine.py:176), and the kept-symbol
 //           positions of the device compaction: one single-pass launch
 //           (decoupled look-back, rows_scan_kernel);
-// * max:    the FASTA line state's running maximum (reduce-then-scan, three
-//           launches);
+// * max:    the FASTA line state's running maximum (the same single pass);
 // * monoid: per-chunk transition-monoid elements -> each chunk's entry state,
 //           the composition of chunk "start-state -> end-state" maps (the
 //           reference's left-to-right chain walk, engine.py:155-163, done as
@@ -50,18 +49,6 @@ struct MonoidOp {
     }
 };
 
-template <class Op>
-__device__ typename Op::T load_item(const void* in, int64_t i, int64_t n, const Op& op);
-
-template <>
-__device__ long long load_item<AddOp>(const void* in, int64_t i, int64_t n, const AddOp& op) {
-    return i < n ? (long long)static_cast<const uint32_t*>(in)[i] : op.identity();
-}
-template <>
-__device__ long long load_item<MaxOp>(const void* in, int64_t i, int64_t n, const MaxOp& op) {
-    return i < n ? static_cast<const long long*>(in)[i] : op.identity();
-}
-
 // Block-wide exclusive scan of one value per thread (order = thread order).
 template <class Op>
 __device__ typename Op::T block_exclusive(typename Op::T v, const Op& op, typename Op::T* total) {
@@ -95,70 +82,6 @@ __device__ typename Op::T block_exclusive(typename Op::T v, const Op& op, typena
     return r;
 }
 
-template <class Op>
-__global__ void __launch_bounds__(kThreads) tile_reduce(const void* in, int64_t n, Op op,
-                                                        typename Op::T* agg) {
-    using T = typename Op::T;
-    const int64_t base = int64_t(blockIdx.x) * kTile + int64_t(threadIdx.x) * kItems;
-    T acc = op.identity();
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) acc = op(acc, load_item<Op>(in, base + i, n, op));
-    T total;
-    block_exclusive<Op>(acc, op, &total);
-    if (threadIdx.x == 0) agg[blockIdx.x] = total;
-}
-
-// One block: exclusive scan of the tile aggregates in place, total to *d_total.
-template <class Op>
-__global__ void __launch_bounds__(kThreads) agg_scan(typename Op::T* agg, int64_t ntiles, Op op,
-                                                     typename Op::T* d_total) {
-    using T = typename Op::T;
-    T carry = op.identity();
-    for (int64_t b0 = 0; b0 < ntiles; b0 += kThreads) {
-        const int64_t i = b0 + threadIdx.x;
-        T v = i < ntiles ? agg[i] : op.identity();
-        T total;
-        T ex = block_exclusive<Op>(v, op, &total);
-        if (i < ntiles) agg[i] = op(carry, ex);
-        carry = op(carry, total);
-    }
-    if (threadIdx.x == 0 && d_total) *d_total = carry;
-}
-
-template <class Op, class Out>
-__global__ void __launch_bounds__(kThreads) tile_scan(const void* in, int64_t n, Op op,
-                                                      const typename Op::T* agg_excl, Out* out) {
-    using T = typename Op::T;
-    const int64_t base = int64_t(blockIdx.x) * kTile + int64_t(threadIdx.x) * kItems;
-    T items[kItems];
-    T acc = op.identity();
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-        items[i] = load_item<Op>(in, base + i, n, op);
-        acc = op(acc, items[i]);
-    }
-    T ex = block_exclusive<Op>(acc, op, nullptr);
-    T run = op(agg_excl[blockIdx.x], ex);
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-        if (base + i < n) out[base + i] = Out(run);
-        run = op(run, items[i]);
-    }
-}
-
-template <class Op, class Out>
-int run_scan(ks_ctx* ctx, const void* in, int64_t n, const Op& op, Out* out, typename Op::T* d_total,
-             void* tmp, int* launches) {
-    using T = typename Op::T;
-    const int64_t ntiles = std::max<int64_t>(1, (n + kTile - 1) / kTile);
-    T* agg = static_cast<T*>(tmp);
-    tile_reduce<Op><<<int(ntiles), kThreads, 0, ctx->stream>>>(in, n, op, agg);
-    agg_scan<Op><<<1, kThreads, 0, ctx->stream>>>(agg, ntiles, op, d_total);
-    if (n > 0) tile_scan<Op, Out><<<int(ntiles), kThreads, 0, ctx->stream>>>(in, n, op, agg, out);
-    if (launches) *launches += n > 0 ? 3 : 2;
-    KS_CUDA(cudaGetLastError());
-    return KS_OK;
-}
 
 
 // ---------------------------------------------------------------- single pass
@@ -256,12 +179,13 @@ __global__ void __launch_bounds__(kThreads) monoid_entry_scan_kernel(
 // Tile t publishes its sum (flag 1) and then its inclusive prefix (flag 2);
 // the flag word carries the call's epoch, values sit in separate arrays
 // written before the flag.
-__global__ void __launch_bounds__(kThreads) rows_scan_kernel(const uint32_t* __restrict__ in, int64_t n,
+template <class Op, class In>   // Op: commutative (sum, max) over long long
+__global__ void __launch_bounds__(kThreads) rows_scan_kernel(const In* __restrict__ in, int64_t n,
                                                               long long* __restrict__ out, long long* total,
                                                               unsigned long long* flag, long long* agg,
                                                               long long* inc, uint32_t epoch) {
     using T = long long;
-    AddOp op;
+    Op op;
     __shared__ T s_prefix;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t ntiles = (n + kTile - 1) / kTile;
@@ -269,16 +193,16 @@ __global__ void __launch_bounds__(kThreads) rows_scan_kernel(const uint32_t* __r
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int64_t base = t * kTile + int64_t(threadIdx.x) * kItems;
         T items[kItems];
-        T acc = 0;
+        T acc = op.identity();
 #pragma unroll
         for (int i = 0; i < kItems; ++i) {
-            items[i] = base + i < n ? T(in[base + i]) : 0;
-            acc += items[i];
+            items[i] = base + i < n ? T(in[base + i]) : op.identity();
+            acc = op(acc, items[i]);
         }
         T tot;
-        const T ex = block_exclusive<AddOp>(acc, op, &tot);
+        const T ex = block_exclusive<Op>(acc, op, &tot);
         if (warp == 0) {
-            T prefix = 0;
+            T prefix = op.identity();
             if (t == 0) {
                 if (lane == 0) {
                     inc[0] = tot;
@@ -291,11 +215,11 @@ __global__ void __launch_bounds__(kThreads) rows_scan_kernel(const uint32_t* __r
                     __threadfence();
                     atomicExch(&flag[t], e2 | 1ull);
                 }
-                T run = 0;
+                T run = op.identity();
                 for (int64_t j = t - 1;; j -= 32) {
                     const int64_t k = j - lane;
                     unsigned f = 2;
-                    T v = 0;
+                    T v = op.identity();
                     if (k >= 0) {
                         unsigned long long w;
                         do {
@@ -307,30 +231,30 @@ __global__ void __launch_bounds__(kThreads) rows_scan_kernel(const uint32_t* __r
                     }
                     const unsigned incl = __ballot_sync(0xffffffffu, f == 2);
                     const int stop = incl ? __ffs(incl) - 1 : 32;
-                    T x = lane <= stop ? v : 0;
+                    T x = lane <= stop ? v : op.identity();
 #pragma unroll
-                    for (int d = 16; d > 0; d >>= 1) x += __shfl_down_sync(0xffffffffu, x, d);
-                    run += __shfl_sync(0xffffffffu, x, 0);
+                    for (int d = 16; d > 0; d >>= 1) x = op(x, __shfl_down_sync(0xffffffffu, x, d));
+                    run = op(run, __shfl_sync(0xffffffffu, x, 0));
                     if (stop < 32) break;
                 }
                 prefix = run;
                 if (lane == 0) {
-                    inc[t] = prefix + tot;
+                    inc[t] = op(prefix, tot);
                     __threadfence();
                     atomicExch(&flag[t], e2 | 2ull);
                 }
             }
             if (lane == 0) {
                 s_prefix = prefix;
-                if (t == ntiles - 1 && total) *total = prefix + tot;
+                if (t == ntiles - 1 && total) *total = op(prefix, tot);
             }
         }
         __syncthreads();
-        T run = s_prefix + ex;
+        T run = op(s_prefix, ex);
 #pragma unroll
         for (int i = 0; i < kItems; ++i) {
             if (base + i < n) out[base + i] = run;
-            run += items[i];
+            run = op(run, items[i]);
         }
         __syncthreads();
     }
@@ -342,11 +266,15 @@ size_t exclusive_scan_rows_tmp_bytes(int64_t n) {
     return size_t(std::max<int64_t>(1, (n + kTile - 1) / kTile)) * sizeof(long long) + 256;
 }
 
-int exclusive_scan_rows(ks_ctx* ctx, const uint32_t* in, int64_t n, int64_t* out_excl,
-                        int64_t* d_total, void* tmp, int* launches) {
-    (void)tmp;
+template <class Op, class In>
+int single_pass_scan(ks_ctx* ctx, const In* in, int64_t n, int64_t* out_excl, int64_t* d_total, int* launches) {
+    Op op;
     if (n <= 0) {
-        if (d_total) KS_CUDA(cudaMemsetAsync(d_total, 0, 8, ctx->stream));
+        if (d_total) {
+            const long long id = op.identity();
+            KS_CUDA(cudaMemcpyAsync(d_total, &id, 8, cudaMemcpyHostToDevice, ctx->stream));
+            KS_CUDA(cudaStreamSynchronize(ctx->stream));   // `id` lives on this stack frame
+        }
         return KS_OK;
     }
     const int64_t ntiles = (n + kTile - 1) / kTile;
@@ -365,21 +293,26 @@ int exclusive_scan_rows(ks_ctx* ctx, const uint32_t* in, int64_t n, int64_t* out
     long long* agg = reinterpret_cast<long long*>(flag + ctx->rowstat_cap);
     long long* inc = agg + ctx->rowstat_cap;
     int per_sm = 0;
-    KS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rows_scan_kernel, kThreads, 0));
+    KS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rows_scan_kernel<Op, In>, kThreads, 0));
     const int64_t grid = std::min<int64_t>(ntiles, int64_t(std::max(per_sm, 1)) * ctx->num_sms);
-    rows_scan_kernel<<<int(grid), kThreads, 0, ctx->stream>>>(in, n, reinterpret_cast<long long*>(out_excl),
-                                                               reinterpret_cast<long long*>(d_total), flag, agg,
-                                                               inc, ctx->rowepoch);
+    rows_scan_kernel<Op, In><<<int(grid), kThreads, 0, ctx->stream>>>(
+        in, n, reinterpret_cast<long long*>(out_excl), reinterpret_cast<long long*>(d_total), flag, agg, inc,
+        ctx->rowepoch);
     if (launches) ++*launches;
     KS_CUDA(cudaGetLastError());
     return KS_OK;
 }
 
+int exclusive_scan_rows(ks_ctx* ctx, const uint32_t* in, int64_t n, int64_t* out_excl,
+                        int64_t* d_total, void* tmp, int* launches) {
+    (void)tmp;
+    return single_pass_scan<AddOp, uint32_t>(ctx, in, n, out_excl, d_total, launches);
+}
+
 int exclusive_scan_max(ks_ctx* ctx, const int64_t* in, int64_t n, int64_t* out_excl, int64_t* d_total,
                        void* tmp, int* launches) {
-    MaxOp op;
-    return run_scan<MaxOp, long long>(ctx, in, n, op, reinterpret_cast<long long*>(out_excl),
-                                      reinterpret_cast<long long*>(d_total), tmp, launches);
+    (void)tmp;
+    return single_pass_scan<MaxOp, int64_t>(ctx, in, n, out_excl, d_total, launches);
 }
 
 
