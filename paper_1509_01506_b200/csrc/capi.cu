@@ -715,6 +715,8 @@ int ks_close(ks_ctx* ctx) {
     if (!ctx) return KS_OK;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);   // before freeing what it reads
+    if (ctx->l2_persist) cudaCtxResetPersistingL2Cache();
     if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->sbuf) cudaFree(ctx->sbuf);
@@ -724,7 +726,6 @@ int ks_close(ks_ctx* ctx) {
     if (ctx->rstage) cudaFreeHost(ctx->rstage);
     if (ctx->rdev) cudaFree(ctx->rdev);
     if (ctx->log_buf) cudaFree(ctx->log_buf);
-    if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
     delete ctx->pool;
     if (ctx->hstage) cudaFreeHost(ctx->hstage);
     for (auto& ev : ctx->hev)
