@@ -896,3 +896,25 @@ def test_lean_blocks_forced(monkeypatch, config, lean):
         w2, last = O.ref_sequential_count(w.dfa, codes, b, e, entry)
         g2, ex, _ = c2.scan_range(dh, sh, b, e, entry)
         assert g2.tolist() == w2.tolist() and ex == last
+
+
+def test_async_back_to_back_mixed():
+    """Back-to-back ks_count_async calls (no host sync, no events between the
+    kernels, programmatic dependent launch) alternating automata, sequences
+    and result buffers: every call's counts are the oracle's."""
+    ctx = _native.DeviceContext(0)
+    work = []
+    for cfg, n in ((2, 200_003), (4, 300_001), (5, 150_007), (3, 250_009)):
+        w = workloads.make(cfg, n)
+        codes = ks.encode_bytes(w.ascii.tobytes())
+        work.append((ctx.dfa(w.dfa), ctx.upload_codes(codes), O.ref_sequential_count(w.dfa, codes)[0]))
+    outs = []
+    for rep in range(3):
+        for dh, sh, want in work:
+            buf = torch.zeros(max(dh.n_expressions, 1), dtype=torch.int64).pin_memory()
+            ctx.count_async(dh, sh, buf.numpy())
+            outs.append((buf, want))
+    waited = ctx.async_wait()
+    assert waited["kernel_launches"] >= len(outs)
+    for buf, want in outs:
+        assert buf.numpy()[: want.size].tolist() == want.tolist()
