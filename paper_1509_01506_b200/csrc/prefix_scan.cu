@@ -320,6 +320,22 @@ int exclusive_scan_max(ks_ctx* ctx, const int64_t* in, int64_t n, int64_t* out_e
 
 namespace ks {
 
+bool l2_persist_attr(ks_ctx* ctx, const void* base, size_t bytes, cudaLaunchAttribute* attr) {
+    if (!bytes || !ctx->l2_persist_max || std::getenv("KS_NO_L2_PERSIST")) return false;
+    const size_t want = std::min(ctx->l2_persist_max, std::max(ctx->l2_persist, bytes));
+    if (want > ctx->l2_persist && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess)
+        ctx->l2_persist = want;
+    cudaGetLastError();
+    if (!ctx->l2_persist) return false;
+    attr->id = cudaLaunchAttributeAccessPolicyWindow;
+    attr->val.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+    attr->val.accessPolicyWindow.num_bytes = bytes;
+    attr->val.accessPolicyWindow.hitRatio = float(std::min(1.0, double(ctx->l2_persist) / double(bytes)));
+    attr->val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr->val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    return true;
+}
+
 int monoid_scan_entries(ks_ctx* ctx, const uint16_t* in, int64_t n, const uint16_t* prod, int32_t nm,
                         const uint16_t* action, int32_t nq, int32_t entry_val, const uint16_t* entry_ptr,
                         uint16_t* centry, uint16_t* d_total, size_t window_bytes, int* launches) {
@@ -344,21 +360,9 @@ int monoid_scan_entries(ks_ctx* ctx, const uint16_t* in, int64_t n, const uint16
     cfg.blockDim = dim3(kThreads);
     cfg.stream = ctx->stream;
     cudaLaunchAttribute attr[1];
-    if (window_bytes && ctx->l2_persist_max && !std::getenv("KS_NO_L2_PERSIST")) {
-        const size_t want = std::min(ctx->l2_persist_max, std::max(ctx->l2_persist, window_bytes));
-        if (want > ctx->l2_persist && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess)
-            ctx->l2_persist = want;
-        cudaGetLastError();
-        if (ctx->l2_persist) {
-            attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-            attr[0].val.accessPolicyWindow.base_ptr = const_cast<uint16_t*>(prod);
-            attr[0].val.accessPolicyWindow.num_bytes = window_bytes;
-            attr[0].val.accessPolicyWindow.hitRatio = float(std::min(1.0, double(ctx->l2_persist) / double(window_bytes)));
-            attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-            attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-            cfg.attrs = attr;
-            cfg.numAttrs = 1;
-        }
+    if (l2_persist_attr(ctx, prod, window_bytes, &attr[0])) {
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
     }
     KS_CUDA(cudaLaunchKernelEx(&cfg, monoid_entry_scan_kernel, in, n, MonoidOp{prod, nm}, action, nq, entry_val,
                                entry_ptr, centry, d_total, ctx->mstat, ctx->mepoch));

@@ -794,11 +794,16 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
         cfg.blockDim = dim3(unsigned(warps * 32));
         cfg.dynamicSmemBytes = smem;
         cfg.stream = ctx->stream;
-        cudaLaunchAttribute attr[1];
+        cudaLaunchAttribute attr[2];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
+        // the staged tables (stride table, then the 1-base table) in persisting L2
+        const size_t tbytes = size_t(reinterpret_cast<const char*>(a.t1) - reinterpret_cast<const char*>(a.tk)) +
+                              size_t(a.t1_pad) * 2;
+        if (a.t1 > a.tk && tbytes <= (size_t(1) << 20) && l2_persist_attr(ctx, a.tk, tbytes, &attr[1]))
+            cfg.numAttrs = 2;
         KS_CUDA(cudaLaunchKernelEx(&cfg, fn, a));
     } else {
         fn<<<blocks, warps * 32, smem, ctx->stream>>>(a);

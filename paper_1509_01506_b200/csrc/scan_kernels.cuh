@@ -99,6 +99,12 @@ struct ScanArgs {
 
 inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
+// Launch attribute keeping [base, base + bytes) in the persisting part of L2
+// (constant automaton tables: they survive the sequence streaming through L2
+// and the calls in between).  Grows the device's set-aside as needed; false
+// (attribute not filled) when unavailable or KS_NO_L2_PERSIST is set.
+bool l2_persist_attr(ks_ctx* ctx, const void* base, size_t bytes, cudaLaunchAttribute* attr);
+
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
 
