@@ -6,18 +6,28 @@
 One step = one pass of the hot path (scan + compose + count, SURVEY §8d
 steps ii-iv) over one batch of synthetic input.  Workload at N=1: config C3
 (1 GiB, 256 class patterns, |Q| ~ 3.3k, count only) -- the config the
-BASELINE target (>= 60% of HBM roofline at 1 GPU) is stated on.  For N > 1
-(torchrun, one rank per GPU) every rank scans its own 1 GiB shard of an
-N GiB sequence (weak scaling): definite automata (C3) load the previous
-shard's tail once (halo) and all-reduce the counts over NCCL each step; other
-automata all-gather their boundary maps first.
+BASELINE target (>= 60% of HBM roofline at 1 GPU) is stated on.
+
+``--gpus N`` with N > 1 and no torchrun environment re-launches this script
+under ``torch.distributed.run`` with N ranks (one per GPU); under torchrun the
+world size must equal ``--gpus``.  At N > 1 the main line is weak scaling
+(every rank scans its own 1 GiB shard of an N GiB sequence: halo load once,
+then scan + NCCL all-reduce per step) and a ``strong`` object carries the
+north star's split of ONE sequence: C4 (3.2e9 bases, generated once and
+shared through /dev/shm) cut into N contiguous shards, each with the true
+previous shard's tail as halo, scan + all-reduce per step, speed-up against
+the whole C4 on one GPU timed in the same run, counts and rank-ordered rows
+checked against the 1-GPU result and the oracle.
 
 Printed JSON (rank 0): value = bases/s over all ranks in GB/s (1 B/base);
 ``roofline`` for the dominant scan kernel against the measured HBM copy
 bandwidth; ``e2e`` = the same metric through the C ABI from pinned host
 ASCII (host pack + H2D + scan + counts back to the host, every step);
-``cpu_baseline`` = the reference algorithm (oracle/ref_scan.c, a C port of
-kmerscan.run) on this host's cores over a bounded sample.
+``parity`` = the step's counts against the oracle (oracle/ref_scan.c, the C
+restatement of kmerscan.run) on the same full-size input, after the timed
+region; ``others`` = the other BASELINE configs (C1, C2, C4, C5) measured the
+same way, each with its own parity check; ``cpu_baseline`` = the reference
+algorithm (the same C port) on this host's cores over the whole C3 sequence.
 """
 
 from __future__ import annotations
@@ -25,7 +35,9 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import time
 from pathlib import Path
@@ -37,9 +49,10 @@ sys.path.insert(0, str(REPO))
 
 METRIC = "bases scanned/s (GB/s) at 1/2/4/8 B200, % of HBM roofline; counts bit-exact"
 UNIT = "GB/s"
-
+ORACLE_NAME = "oracle/ref_scan.c (C restatement of kmerscan.run, engine.py:207-237 + _kernels.py:18-113)"
 
 L2_FLUSH_BYTES = 256 << 20   # twice the B200's 126 MB L2
+LOCATE_CONFIGS = (1, 2, 4)
 
 
 def log(*a):
@@ -73,9 +86,29 @@ def profile_traffic(config: int) -> float | None:
     return None
 
 
+def host_codes(ascii_: np.ndarray) -> np.ndarray:
+    """Symbol codes of whitespace-free ASCII (ks.encode_bytes, threaded in
+    64 MiB pieces): the oracle's input."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_1509_01506_b200.alphabet import BYTE_CODES, DROP
+
+    out = np.empty(ascii_.size, dtype=np.uint8)
+    step = 64 << 20
+
+    def piece(lo):
+        np.take(BYTE_CODES, ascii_[lo:lo + step], out=out[lo:lo + step])
+
+    with ThreadPoolExecutor(os.cpu_count() or 4) as ex:
+        list(ex.map(piece, range(0, ascii_.size, step)))
+    if np.any(out == DROP):
+        raise ValueError("host_codes: input holds whitespace")
+    return out
+
+
 class ClockSampler:
     """SM clocks and throttle reasons sampled during the timed region: NVML
-    polled from a thread every ~2 ms (nvidia-smi's 100 ms floor would miss a
+    polled from a thread every ~1 ms (nvidia-smi's 100 ms floor would miss a
     timed region of a few ms).  Native calls release the GIL."""
 
     REASONS = {  # NVML clocks-event reason bits
@@ -130,24 +163,37 @@ class ClockSampler:
                 "samples": len(self.samples), "source": "NVML, 1 ms poll during the timed steps"}
 
 
-def cpu_baseline(wl, sample_bases: int, min_seconds: float = 10.0, max_reps: int = 20) -> dict:
-    """The reference algorithm (C port, pthreads, one chunk per core) on a
-    bounded prefix sample, timed like kmerscan.bench (1 warmup, median)."""
+def oracle_counts(dfa, codes: np.ndarray, workers: int, locate: bool = False):
+    """The checker: the oracle's run() on the same input (after the timed region)."""
     from oracle import oracle as O
-    import paper_1509_01506_b200 as ks
+
+    t0 = time.perf_counter()
+    counts, rows, _ = O.ref_run(dfa, codes, workers, 10, locate)
+    return counts, rows, time.perf_counter() - t0
+
+
+def oracle_workers(config: int) -> int:
+    # C1: the config's 4 chunks; C5: one worker (with more, every chunk
+    # speculates all 1024 states -- |Q|x the work, SURVEY §8d)
+    return 4 if config == 1 else 1 if config == 5 else (os.cpu_count() or 1)
+
+
+def cpu_baseline(wl, codes: np.ndarray, min_seconds: float = 10.0, max_reps: int = 20) -> dict:
+    """The reference algorithm (C port, pthreads, one chunk per core) over the
+    whole workload sequence, timed like kmerscan.bench (1 warmup, median)."""
+    from oracle import oracle as O
 
     cores = os.cpu_count() or 1
-    sample = ks.encode_bytes(wl.ascii[:sample_bases].tobytes())
-    O.ref_run(wl.dfa, sample, cores, 10, False)  # warmup
+    O.ref_run(wl.dfa, codes, cores, 10, False)  # warmup
     times = []
     t_start = time.perf_counter()
     while len(times) < max_reps and (time.perf_counter() - t_start < min_seconds or len(times) < 3):
         t0 = time.perf_counter()
-        O.ref_run(wl.dfa, sample, cores, 10, False)
+        O.ref_run(wl.dfa, codes, cores, 10, False)
         times.append(time.perf_counter() - t0)
     med = statistics.median(times)
-    return {"value": sample.size / med / 1e9, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"first {sample.size} bases of the C{wl.config} sequence, kmerscan.run "
+    return {"value": codes.size / med / 1e9, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"the whole C{wl.config} sequence ({codes.size} bases), kmerscan.run "
                       f"(workers={cores}, window=10, count) restated in C (oracle/ref_scan.c); "
                       f"median of {len(times)} reps after 1 warmup",
             "median_s": med}
@@ -160,19 +206,36 @@ def dist_env():
     return world, rank, local
 
 
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args) -> None:
+    """--gpus N > 1 outside torchrun: run this script under torch.distributed.run
+    with N local ranks (rendezvous on 127.0.0.1) and exit with its code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", str(Path(__file__).resolve())]
+    cmd += sys.argv[1:]
+    log(f"self-launch: {' '.join(cmd)}")
+    sys.exit(subprocess.call(cmd))
+
+
 def run_reference(args) -> None:
+    """The reference's CPU implementation of the path (the C port of
+    kmerscan.run, all host threads) on OUR arm's workload: the whole config
+    sequence every step."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
     from paper_1509_01506_b200 import workloads
-
-    sample = args.cpu_sample
-    wl = workloads.make(args.config, min(sample, workloads.FULL_SIZES[args.config]))
     from oracle import oracle as O
-    import paper_1509_01506_b200 as ks
 
+    n = workloads.FULL_SIZES[args.config] if args.bases is None else args.bases
+    wl = workloads.make(args.config, n)
     cores = os.cpu_count() or 1
-    codes = ks.encode_bytes(wl.ascii.tobytes())
+    codes = host_codes(wl.ascii)
     for _ in range(args.warmup):
         O.ref_run(wl.dfa, codes, cores, 10, False)
     times = []
@@ -187,14 +250,230 @@ def run_reference(args) -> None:
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic",
-        "config": {"workload": f"C{args.config}: {wl.description}", "n_bases_sample": int(codes.size),
-                   "parallelism": f"{cores} host threads"},
+        "config": {"workload": f"C{args.config}: {wl.description}", "n_bases_per_gpu": int(codes.size),
+                   "parallelism": f"{cores} host threads", "same_config_as_ours": args.bases is None},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"first {codes.size} bases of C{args.config} per step; kmerscan.run "
+                         "sample": f"the whole C{args.config} sequence ({codes.size} bases) per step; kmerscan.run "
                                    f"(workers={cores}, window=10, count) restated in C (oracle/ref_scan.c)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def time_steps(ctx, step, stream, steps: int, flush, local: int, sync_each=None):
+    """Time `steps` back-to-back steps with CUDA events on the library's
+    stream (inputs that fit in L2: a flush before each step, steps timed one
+    by one).  Returns (ms total, clocks summary, launches)."""
+    import torch
+
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(steps if flush is not None else 0)]
+    if sync_each is not None:
+        sync_each()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for i in range(steps):
+            if flush is not None:
+                flush.zero_()
+                step_ev[i][0].record(stream)
+            step()
+            if flush is not None:
+                step_ev[i][1].record(stream)
+        ev1.record(stream)
+        waited = ctx.async_wait()
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) if flush is None else sum(a.elapsed_time(b) for a, b in step_ev)
+    return ms, clocks.summary(), waited["kernel_launches"]
+
+
+def kernel_ms(ctx, dh, sh, flush, reps: int = 5, scan=None) -> float:
+    """Median CUDA-event time of the scan kernel over `reps` synchronous calls
+    (each after the same L2 flush as the timed steps)."""
+    import torch
+
+    ts = []
+    for _ in range(reps):
+        if flush is not None:
+            flush.zero_()
+        torch.cuda.synchronize()
+        (scan or (lambda: ctx.count(dh, sh)))()
+        ts.append(ctx.stats()["scan_ms"])
+    return statistics.median(ts)
+
+
+def measure_config(ctx, stream, local: int, config: int, steps: int, warmup: int, flush_buf) -> dict:
+    """One other BASELINE config on one GPU: device-resident count steps,
+    kernel roofline, clocks, and counts (plus rows for the locate configs)
+    against the oracle on the same full-size input."""
+    from paper_1509_01506_b200 import workloads
+
+    t0 = time.perf_counter()
+    wl = workloads.make(config)
+    n = wl.n
+    dh = ctx.dfa(wl.dfa)
+    sh = ctx.upload_ascii(wl.ascii)
+    ne = max(wl.dfa.n_expressions, 1)
+    import torch
+
+    out_pin = torch.zeros(ne, dtype=torch.int64).pin_memory()
+    out_np = out_pin.numpy()
+    flush = flush_buf if n * 3 // 8 < L2_FLUSH_BYTES else None
+
+    def step():
+        ctx.count_async(dh, sh, out_np)
+
+    for _ in range(warmup):
+        step()
+    ctx.async_wait()
+    got = out_np[:wl.dfa.n_expressions].copy()
+    ms, clocks, launches = time_steps(ctx, step, stream, steps, flush, local)
+    if not np.array_equal(out_np[:wl.dfa.n_expressions], got):
+        raise RuntimeError(f"C{config}: counts changed between steps")
+    kms = kernel_ms(ctx, dh, sh, flush)
+    ms_step = ms / steps
+    peak = measured_peaks()["hbm_gbs"]
+    achieved = n / (kms / 1e3) / 1e9
+    res = {"workload": f"C{config}: {wl.description}", "n_bases": n, "dfa_states": wl.dfa.state_count,
+           "strategy": dh.info["strategy_name"], "stride_bases": dh.info["stride"],
+           "value": n / (ms_step / 1e3) / 1e9, "unit": UNIT, "ms_per_step": ms_step, "steps": steps,
+           "kernel_ms": kms, "frac": achieved / peak, "clocks": clocks, "gpu_launches": launches,
+           "l2": "flushed between steps" if flush is not None else "input larger than L2"}
+    if config == 5:   # lookup-bound: 2 passes of n/3 K=3 lookups (SURVEY §8d roofline exception)
+        res["frac_note"] = "C5 is bound by shared-memory lookups (never-converging automaton), not HBM"
+    # parity: counts (and rows) against the oracle on the same input
+    codes = host_codes(wl.ascii)
+    locate = config in LOCATE_CONFIGS
+    want, want_rows, o_s = oracle_counts(wl.dfa, codes, oracle_workers(config), locate)
+    par = {"oracle": ORACLE_NAME, "n_bases": n, "workers": oracle_workers(config),
+           "counts_equal": bool(np.array_equal(got, want)), "total_matches": int(want.sum()),
+           "oracle_s": round(o_s, 3)}
+    if locate:
+        lc, rows = ctx.locate(dh, sh)
+        par["rows_equal"] = bool(np.array_equal(rows, want_rows) and np.array_equal(lc, want))
+        par["rows"] = int(rows.shape[0])
+        if rows.shape[0]:
+            par["max_offset"] = int(rows[-1, 0])
+    res["parity"] = par
+    log(f"C{config}: {res['value']:.0f} GB/s, kernel {kms:.4f} ms, parity {par} "
+        f"({time.perf_counter() - t0:.1f}s)")
+    return res
+
+
+def strong_leg(args, ctx, stream, world: int, rank: int, local: int, dev) -> dict | None:
+    """The north star's split of ONE sequence: C4 (3.2e9 bases) in `world`
+    contiguous shards, each with the true previous shard's tail as halo;
+    scan + NCCL all-reduce per step.  Rank 0 also times the whole C4 on its
+    GPU alone (the 1-GPU reference point) and checks counts and rank-ordered
+    rows against that run and the oracle."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1509_01506_b200 import workloads
+    from paper_1509_01506_b200.distributed import shard_bounds
+
+    t0 = time.perf_counter()
+    n = workloads.FULL_SIZES[4] if args.strong_bases is None else args.strong_bases
+    shm = Path("/dev/shm") / f"ks_bench_c4_{os.environ.get('MASTER_PORT', 'x')}_{n}.u8"
+    if rank == 0:
+        wl = workloads.make(4, n)
+        ascii_ = wl.ascii
+        if world > 1:
+            tmp = shm.with_suffix(".tmp")
+            ascii_.tofile(tmp)
+            tmp.rename(shm)
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        ascii_ = np.memmap(shm, dtype=np.uint8, mode="r", shape=(n,))
+        wl = workloads.make(4, 64)          # same pattern stream -> the same automaton
+    log(f"[rank {rank}] strong leg: C4 n={n} ready in {time.perf_counter() - t0:.1f}s")
+
+    dh = ctx.dfa(wl.dfa)
+    ne = wl.dfa.n_expressions
+    lo, hi = shard_bounds(n, world)[rank]
+    H = -(-max(int(dh.info["sync_depth"]), 1) // 64) * 64
+    hl = min(H, lo)
+    sh = ctx.upload_ascii(np.ascontiguousarray(ascii_[lo - hl:hi]))
+    counts_dev = torch.zeros(ne, dtype=torch.int64, device=dev)
+    cdev = dev if args.dist_backend == "nccl" else torch.device("cpu")
+
+    def step():
+        ctx.count_shard_async(dh, sh, hl, hl + hi - lo, 0, rank, counts_dev.data_ptr())
+        if world > 1:
+            if args.dist_backend == "nccl":
+                dist.all_reduce(counts_dev)
+            else:
+                c = counts_dev.cpu()
+                dist.all_reduce(c)
+
+    for _ in range(args.warmup):
+        step()
+    ctx.async_wait()
+    torch.cuda.synchronize()
+    ms, clocks, launches = time_steps(ctx, step, stream, args.steps, None, local,
+                                      sync_each=(dist.barrier if world > 1 else None))
+    t = torch.tensor([ms], dtype=torch.float64, device=cdev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_n = float(t[0]) / args.steps
+    # counts of this step + rows of this shard (global offsets, rank order)
+    if world > 1 and args.dist_backend == "nccl":
+        counts = counts_dev.cpu().numpy()
+    else:
+        counts_dev.zero_()
+        ctx.count_shard_async(dh, sh, hl, hl + hi - lo, 0, rank, counts_dev.data_ptr())
+        ctx.async_wait()
+        c = counts_dev.cpu()
+        if world > 1:
+            dist.all_reduce(c)
+        counts = c.numpy()
+    rows = ctx.scan_range(dh, sh, hl, hl + hi - lo, -1, lo - hl, True)[2]
+    gathered = [None] * world
+    if world > 1:
+        dist.all_gather_object(gathered, rows)
+    else:
+        gathered = [rows]
+    out = None
+    if rank == 0:
+        rows_all = np.concatenate(gathered) if gathered else np.empty((0, 2), np.int64)
+        # the 1-GPU reference point: the whole C4 on this GPU
+        full = ctx.upload_ascii(np.ascontiguousarray(ascii_))
+        one = torch.zeros(max(ne, 1), dtype=torch.int64).pin_memory()
+        one_np = one.numpy()
+
+        def step1():
+            ctx.count_async(dh, full, one_np)
+
+        for _ in range(args.warmup):
+            step1()
+        ctx.async_wait()
+        ms1, _, _ = time_steps(ctx, step1, stream, args.steps, None, local)
+        ms1 /= args.steps
+        c1, rows1 = ctx.locate(dh, full)
+        codes = host_codes(np.asarray(ascii_))
+        want, want_rows, o_s = oracle_counts(wl.dfa, codes, oracle_workers(4), True)
+        out = {"config": "C4", "n_bases": n, "n_gpus": world, "ms_per_step": ms_n,
+               "value": n / (ms_n / 1e3) / 1e9, "unit": UNIT,
+               "one_gpu_ms_per_step": ms1, "speedup_vs_1": ms1 / ms_n,
+               "step": ("scan of each rank's contiguous shard from its halo's lookback (ks_count_shard_async) "
+                        "+ NCCL all-reduce of the int64 counts; events per rank, max over ranks"),
+               "halo_bases": H, "clocks_rank0": clocks, "gpu_launches_rank0": launches,
+               "parity": {"oracle": ORACLE_NAME, "counts_equal_oracle": bool(np.array_equal(counts, want)),
+                          "counts_equal_1gpu": bool(np.array_equal(counts, c1[:ne])),
+                          "rows_equal_oracle": bool(np.array_equal(rows_all, want_rows)),
+                          "rows_equal_1gpu": bool(np.array_equal(rows_all, rows1)),
+                          "rows": int(rows_all.shape[0]), "oracle_s": round(o_s, 3)}}
+        full.free()
+        log(f"strong: {out}")
+    if world > 1:
+        dist.barrier()
+        if rank == 0:
+            shm.unlink(missing_ok=True)
+    sh.free()
+    return out
 
 
 def run_ours(args) -> None:
@@ -251,14 +530,14 @@ def run_ours(args) -> None:
     # bases (a halo >= the synchronisation depth, exchanged once at load
     # time), so a step needs no boundary-map exchange -- scan + one all-reduce
     halo_mode = world > 1 and dh.info["strategy_name"] == "lookback"
-    sh_halo, halo_len = None, 0
+    sh_halo, halo_len, prev_tail = None, 0, np.empty(0, dtype=np.uint8)
     if halo_mode:
         H = -(-max(int(dh.info["sync_depth"]), 1) // 64) * 64
         tails = [torch.empty(H, dtype=torch.uint8, device=cdev) for _ in range(world)]
         dist.all_gather(tails, torch.from_numpy(wl.ascii[-H:].copy()).to(cdev))
-        prev = tails[rank - 1].cpu().numpy() if rank > 0 else np.empty(0, dtype=np.uint8)
-        halo_len = int(prev.size)
-        sh_halo = ctx.upload_ascii(np.concatenate([prev, wl.ascii]))
+        prev_tail = tails[rank - 1].cpu().numpy() if rank > 0 else np.empty(0, dtype=np.uint8)
+        halo_len = int(prev_tail.size)
+        sh_halo = ctx.upload_ascii(np.concatenate([prev_tail, wl.ascii]))
 
     def step() -> None:
         if world == 1:  # enqueue only: one scan kernel that writes the counts into pinned host memory
@@ -312,54 +591,24 @@ def run_ours(args) -> None:
             raise RuntimeError("NCCL path counts differ from the host-composed exchange")
     launches[0] = 0
     scan_ms_sum[0] = 0.0
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
     # inputs that fit in L2 (packed 0.375 B/base): write a buffer twice the L2
     # size between steps and time each step on its own (events on the stream)
     packed_bytes = n * 3 // 8
-    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev) if packed_bytes < L2_FLUSH_BYTES else None
-    step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(args.steps if flush is not None else 0)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
-        ev0.record(stream)
-        for i in range(args.steps):
-            if flush is not None:
-                flush.zero_()
-                step_ev[i][0].record(stream)
-            step()
-            if flush is not None:
-                step_ev[i][1].record(stream)
-        ev1.record(stream)
-        waited = ctx.async_wait()
-        torch.cuda.synchronize()
+    flush_buf = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    flush = flush_buf if packed_bytes < L2_FLUSH_BYTES else None
+    ms, clocks, waited_launches = time_steps(ctx, step, stream, args.steps, flush, local,
+                                             sync_each=(dist.barrier if world > 1 else None))
     if world == 1 or args.dist_backend == "nccl" or halo_mode:
-        launches[0] = waited["kernel_launches"]
-        if world == 1 and waited["scan_ms_total"] > 0:   # KS_ASYNC_EVENTS=1: per-call events
-            scan_ms_sum[0] = waited["scan_ms_total"]
-        else:
-            # the timed async calls carry no events (they would sit between the
-            # back-to-back kernels): the kernel time is the median of 5
-            # synchronous calls' CUDA-event scan times, each after the same L2
-            # flush as the timed steps
-            ts = []
-            for _ in range(5):
-                if flush is not None:
-                    flush.zero_()
-                torch.cuda.synchronize()
-                if world == 1:
-                    ctx.count(dh, sh)
-                else:
-                    ctx.scan_range(dh, sh, 0, n, -1)
-                ts.append(ctx.stats()["scan_ms"])
-            scan_ms_sum[0] = statistics.median(ts) * args.steps
+        launches[0] = waited_launches
+        # the timed async calls carry no events (they would sit between the
+        # back-to-back kernels): the kernel time is the median of 5
+        # synchronous calls' CUDA-event scan times
+        scan = (lambda: ctx.count(dh, sh)) if world == 1 else (lambda: ctx.scan_range(dh, sh, 0, n, -1))
+        scan_ms_sum[0] = kernel_ms(ctx, dh, sh, flush, scan=scan) * args.steps
     if not np.array_equal(out_np[:ne], ref_counts):
         raise RuntimeError("counts changed between steps")
     if world > 1:
         dist.barrier()
-    ms = ev0.elapsed_time(ev1) if flush is None else sum(a.elapsed_time(b) for a, b in step_ev)
     t = torch.tensor([ms, scan_ms_sum[0]], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -395,7 +644,7 @@ def run_ours(args) -> None:
     # (count + sorted (offset, id) rows landed in host memory) on the resident
     # sequence, 1 GPU
     locate = None
-    if args.config in (1, 2, 4) and world == 1:
+    if args.config in LOCATE_CONFIGS and world == 1:
         loc_times = []
         for i in range(12):
             torch.cuda.synchronize()
@@ -409,9 +658,45 @@ def run_ours(args) -> None:
                   "rows_per_gpu": int(lrows.shape[0]),
                   "path": "ks_locate: single-pass visit log + scatter (or rows/emit passes), rows D2H"}
 
+    # parity gate: the step's global counts against the oracle on the same
+    # full-size input (each rank checks its shard -- halo scanned first, its
+    # counts subtracted -- and the shard results are summed)
+    codes = None
+    parity = None
+    if not args.no_parity:
+        p0 = time.perf_counter()
+        codes = host_codes(wl.ascii)
+        workers = oracle_workers(args.config) if world == 1 else max(1, (os.cpu_count() or 1) // world)
+        if halo_mode and rank > 0:
+            both = np.concatenate([host_codes(prev_tail), codes])
+            want = oracle_counts(wl.dfa, both, workers)[0] - oracle_counts(wl.dfa, both[:halo_len], 1)[0]
+        else:
+            want = oracle_counts(wl.dfa, codes, workers)[0]
+        if world > 1:
+            tw = torch.from_numpy(want.astype(np.int64)).to(cdev)
+            dist.all_reduce(tw)
+            want = tw.cpu().numpy()
+        parity = {"oracle": ORACLE_NAME, "n_bases": int(world * n), "workers_per_rank": workers,
+                  "counts_equal": bool(np.array_equal(ref_counts, want)), "total_matches": int(want.sum()),
+                  "checked": "counts of the timed step" + (" (all ranks, summed)" if world > 1 else ""),
+                  "oracle_s": round(time.perf_counter() - p0, 2)}
+        log(f"[rank {rank}] parity: {parity}")
+
+    strong = None
+    if world > 1 or args.strong:
+        strong = strong_leg(args, ctx, stream, world, rank, local, dev)
+
+    others = None
+    if world == 1 and not args.no_others:
+        others = {}
+        for c in (1, 2, 4, 5):
+            if c != args.config:
+                others[f"C{c}"] = measure_config(ctx, stream, local, c, args.others_steps, args.warmup, flush_buf)
+
     if rank == 0:
         peaks = measured_peaks()
         achieved = n / (scan_ms / 1e3) / 1e9
+        traffic = profile_traffic(args.config)
         info = dh.info
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -436,9 +721,12 @@ def run_ours(args) -> None:
             },
             "roofline": {
                 "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], "traffic": profile_traffic(args.config),
-                "kernel": "scan_kernel (count mode)", "algorithmic_bytes_per_launch": n,
+                "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                "kernel": "scan_fast_kernel (count mode)", "algorithmic_bytes_per_launch": n,
                 "kernel_ms": scan_ms, "peak_source": peaks["source"],
+                "dram_frac": (traffic / (scan_ms / 1e3) / 1e9 / peaks["hbm_gbs"]) if traffic else None,
+                "limiter": ("shared-memory data pipe (L1TEX): random 2-byte table gathers + hit bookkeeping; "
+                            "the packed input moves 0.375 B/base (dram_frac), the metric counts 1 B/base"),
             },
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": e2e_stats["h2d_bytes"],
                     "d2h_bytes_per_step": e2e_stats["d2h_bytes"], "seconds_per_step": e2e_s,
@@ -450,16 +738,30 @@ def run_ours(args) -> None:
                     "host_threads": host_threads()},
             "gpu_launches": launches[0],
             **({"locate": locate} if locate else {}),
-            "clocks": clocks.summary(),
+            "clocks": clocks,
+            "parity": parity,
+            **({"strong": strong} if strong else {}),
+            **({"others": others} if others is not None else {}),
         }
         # the CPU baseline is timed at N = 1 only (its rank would idle the others)
         line["cpu_baseline"] = None
         if world == 1 and not args.no_cpu_baseline:
             try:
-                line["cpu_baseline"] = cpu_baseline(wl, args.cpu_sample)
+                line["cpu_baseline"] = cpu_baseline(wl, codes if codes is not None else host_codes(wl.ascii))
             except Exception as exc:   # the reported baseline must not sink the measurement
                 line["cpu_baseline"] = {"error": f"{type(exc).__name__}: {exc}"}
         print(json.dumps(line), flush=True)
+        bad = []
+        if parity is not None and not parity["counts_equal"]:
+            bad.append("C%d counts" % args.config)
+        for name, o in (others or {}).items():
+            if not (o["parity"]["counts_equal"] and o["parity"].get("rows_equal", True)):
+                bad.append(name)
+        if strong and not all(v for k, v in strong["parity"].items() if k.endswith(("_oracle", "_1gpu"))):
+            bad.append("strong C4")
+        if bad:
+            log(f"PARITY FAILURE: {bad}")
+            sys.exit(3)
     if world > 1:
         dist.destroy_process_group()
 
@@ -475,14 +777,24 @@ def main() -> None:
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--strategy", default="auto", choices=["auto", "lookback", "mapscan", "speculate"],
                     help="force a scan strategy (exploration; the contract line uses auto)")
-    ap.add_argument("--cpu-sample", type=int, default=256 << 20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle check (exploration only)")
+    ap.add_argument("--no-others", action="store_true", help="skip the C1/C2/C4/C5 lines at N=1")
+    ap.add_argument("--others-steps", type=int, default=20)
+    ap.add_argument("--strong", action="store_true", help="also run the C4 strong-scaling leg at N=1")
+    ap.add_argument("--strong-bases", type=int, default=None, help="override the strong leg's C4 length")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only for dry runs of the multi-rank path")
     args = ap.parse_args()
     if args.warmup < 3:
         log("note: raising --warmup to the contract minimum of 3")
         args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "0") or 0)
+    if args.gpus > 1 and world == 0:
+        self_launch(args)
+    if max(world, 1) != args.gpus:
+        log(f"error: --gpus {args.gpus} but the launcher's WORLD_SIZE is {max(world, 1)}")
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args)
     else:

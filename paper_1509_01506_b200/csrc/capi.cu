@@ -399,6 +399,7 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
         ev_b = ctx->aev[2 * ctx->n_async + 1];
         ++ctx->n_async;
     }
+    if (async_dst) ++ctx->async_calls;
     if (timed) KS_CUDA(cudaEventRecord(ev_a, ctx->stream));
     PhaseTrace trace(ctx->stream);
     trace.mark("start");
@@ -700,6 +701,7 @@ int ks_open(int device, ks_ctx** out) {
     }
     c->stream = c->own_stream;
     for (auto& ev : c->ev) cudaEventCreate(&ev);
+    l2_persist_acquire(device);
     // keep freed stream-ordered allocations (match rows, upload staging) in
     // the pool instead of returning them to the driver at every sync
     cudaMemPool_t pool = nullptr;
@@ -715,8 +717,9 @@ int ks_close(ks_ctx* ctx) {
     if (!ctx) return KS_OK;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    cudaStreamSynchronize(ctx->own_stream);
     if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);   // before freeing what it reads
-    if (ctx->l2_persist) cudaCtxResetPersistingL2Cache();
+    l2_persist_release(ctx);
     if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->sbuf) cudaFree(ctx->sbuf);
@@ -747,7 +750,16 @@ int ks_close(ks_ctx* ctx) {
 int ks_set_stream(ks_ctx* ctx, void* stream) {
     CtxLock lock_(ctx);
     if (!ctx) return fail(KS_E_INVALID, "null context");
-    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    cudaStream_t next = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    if (next != ctx->stream) {
+        // the context's scratch, result blocks and look-back status words
+        // assume one stream: order everything queued on the old stream before
+        // any work the new one receives
+        DeviceGuard guard(ctx->device);
+        KS_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+        KS_CUDA(cudaStreamWaitEvent(next, ctx->ev[0], 0));
+        ctx->stream = next;
+    }
     return KS_OK;
 }
 
@@ -797,9 +809,10 @@ int ks_async_wait(ks_ctx* ctx, float* scan_ms_total, int32_t* calls, int32_t* la
     }
     if (scan_ms_total) *scan_ms_total = total;
     PhaseTrace::flush();
-    if (calls) *calls = ctx->n_async;
+    if (calls) *calls = ctx->async_calls;
     if (launches) *launches = ctx->async_launches;
     ctx->n_async = 0;
+    ctx->async_calls = 0;
     ctx->async_launches = 0;
     return KS_OK;
 }

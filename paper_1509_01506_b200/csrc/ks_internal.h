@@ -184,7 +184,8 @@ struct ks_ctx {
     size_t log_bytes = 0;
     // ks_count_async: one event pair per call until ks_async_wait
     std::vector<cudaEvent_t> aev;
-    int n_async = 0;
+    int n_async = 0;            // per-call event pairs in use (KS_ASYNC_EVENTS=1)
+    int async_calls = 0;        // async enqueues since the last ks_async_wait
     int async_launches = 0;
 };
 

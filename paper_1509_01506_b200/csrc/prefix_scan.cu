@@ -15,6 +15,7 @@
 //           decoupled look-back (tiles publish their product, then their
 //           inclusive prefix; a tile composes its predecessors' words 32 at a
 //           time) that also applies the prefix to the entry state.
+#include <mutex>
 #include <algorithm>
 #include <cstdlib>
 
@@ -285,7 +286,7 @@ int single_pass_scan(ks_ctx* ctx, const In* in, int64_t n, int64_t* out_excl, in
         ctx->rowstat_cap = 0;
         const int64_t cap = std::max<int64_t>(ntiles, 1024);
         KS_CUDA(cudaMalloc(&ctx->rowstat, size_t(cap) * 24));
-        KS_CUDA(cudaMemset(ctx->rowstat, 0, size_t(cap) * 24));
+        KS_CUDA(cudaMemsetAsync(ctx->rowstat, 0, size_t(cap) * 24, ctx->stream));   // stream-ordered before the scan
         ctx->rowstat_cap = cap;
     }
     if (++ctx->rowepoch == 0) ctx->rowepoch = 1;
@@ -320,12 +321,56 @@ int exclusive_scan_max(ks_ctx* ctx, const int64_t* in, int64_t n, int64_t* out_e
 
 namespace ks {
 
+// The persisting-L2 set-aside is a device-wide limit: it is only ever raised
+// here (read first, never lowered under another context's window), and the
+// value found before the first raise is restored when the last context of the
+// device closes (l2_persist_release, called by ks_close).
+namespace {
+std::mutex g_l2_mu;
+struct L2Dev {
+    int refs = 0;
+    size_t orig = 0;
+    bool saved = false;
+};
+L2Dev g_l2[64];
+}  // namespace
+
+void l2_persist_acquire(int device) {
+    std::lock_guard<std::mutex> g(g_l2_mu);
+    if (device >= 0 && device < 64) ++g_l2[device].refs;
+}
+
+void l2_persist_release(ks_ctx* ctx) {
+    std::lock_guard<std::mutex> g(g_l2_mu);
+    const int dev = ctx->device;
+    if (dev < 0 || dev >= 64) return;
+    L2Dev& d = g_l2[dev];
+    if (--d.refs > 0 || !d.saved) return;
+    cudaCtxResetPersistingL2Cache();
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, d.orig);
+    cudaGetLastError();
+    d.saved = false;
+}
+
 bool l2_persist_attr(ks_ctx* ctx, const void* base, size_t bytes, cudaLaunchAttribute* attr) {
     if (!bytes || !ctx->l2_persist_max || std::getenv("KS_NO_L2_PERSIST")) return false;
-    const size_t want = std::min(ctx->l2_persist_max, std::max(ctx->l2_persist, bytes));
-    if (want > ctx->l2_persist && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess)
-        ctx->l2_persist = want;
-    cudaGetLastError();
+    {
+        std::lock_guard<std::mutex> g(g_l2_mu);
+        size_t cur = 0;
+        if (cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) == cudaSuccess) {
+            L2Dev* d = ctx->device >= 0 && ctx->device < 64 ? &g_l2[ctx->device] : nullptr;
+            const size_t want = std::min(ctx->l2_persist_max, std::max(cur, bytes));
+            if (want > cur && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess) {
+                if (d && !d->saved) {
+                    d->orig = cur;
+                    d->saved = true;
+                }
+                cur = want;
+            }
+            ctx->l2_persist = cur;
+        }
+        cudaGetLastError();
+    }
     if (!ctx->l2_persist) return false;
     attr->id = cudaLaunchAttributeAccessPolicyWindow;
     attr->val.accessPolicyWindow.base_ptr = const_cast<void*>(base);
@@ -348,7 +393,7 @@ int monoid_scan_entries(ks_ctx* ctx, const uint16_t* in, int64_t n, const uint16
         ctx->mstat_cap = 0;
         const int64_t cap = std::max<int64_t>(ntiles, 1024);
         KS_CUDA(cudaMalloc(&ctx->mstat, size_t(cap) * 8));
-        KS_CUDA(cudaMemset(ctx->mstat, 0, size_t(cap) * 8));
+        KS_CUDA(cudaMemsetAsync(ctx->mstat, 0, size_t(cap) * 8, ctx->stream));   // stream-ordered before the scan
         ctx->mstat_cap = cap;
     }
     if (++ctx->mepoch == 0) ctx->mepoch = 1;   // epoch 0 marks never-written words

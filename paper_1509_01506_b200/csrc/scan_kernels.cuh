@@ -104,6 +104,8 @@ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 // and the calls in between).  Grows the device's set-aside as needed; false
 // (attribute not filled) when unavailable or KS_NO_L2_PERSIST is set.
 bool l2_persist_attr(ks_ctx* ctx, const void* base, size_t bytes, cudaLaunchAttribute* attr);
+void l2_persist_acquire(int device);     // ks_open: one more context on the device
+void l2_persist_release(ks_ctx* ctx);    // ks_close: the last one restores the set-aside
 
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }

@@ -135,6 +135,8 @@ int ks_segment_map_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
                 view_of(seq), uniform ? end - h.sync_depth : begin, end, dfa->scan.t1, h.nq,
                 uniform ? h.start_internal : -1, dfa->d_new_of_old, dfa->d_old_of_new, d_map_out);
         KS_CUDA(cudaGetLastError());
+        ctx->async_launches += 1;
+        ++ctx->async_calls;
         return KS_OK;
     }
     int64_t origin, L, nch;
@@ -154,6 +156,8 @@ int ks_segment_map_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
     action_map_kernel<<<blocks, threads, 0, ctx->stream>>>(tot, dfa->d_action, h.nq, dfa->d_new_of_old,
                                                            dfa->d_old_of_new, d_map_out);
     KS_CUDA(cudaGetLastError());
+    ctx->async_launches += launches + 1;
+    ++ctx->async_calls;
     return KS_OK;
 }
 
@@ -229,6 +233,7 @@ int ks_count_shard_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
                                 nullptr, nullptr, &launches);
     if (rc) return rc;
     ctx->async_launches += launches + 2;
+    ++ctx->async_calls;
     return KS_OK;
 }
 

@@ -154,7 +154,11 @@ int ks_dfa_upload_ex(ks_ctx* ctx, const int32_t* transitions, int32_t n_states, 
         delete d;
         return cuda_fail(e, "cudaMalloc(dfa)");
     }
-    e = cudaMemcpy(d->d_blob, host.data(), bytes, cudaMemcpyHostToDevice);
+    // on the context's (non-blocking) stream and waited for: a pageable
+    // cudaMemcpy may return before its DMA lands, and nothing would order the
+    // legacy stream against the kernels that read these tables
+    e = cudaMemcpyAsync(d->d_blob, host.data(), bytes, cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) {
         cudaFree(d->d_blob);
         delete d;
@@ -191,7 +195,9 @@ int ks_dfa_upload_ex(ks_ctx* ctx, const int32_t* transitions, int32_t n_states, 
         rebase(d->d_pss_inv);
     }
     const size_t cnt_bytes = size_t(h.n_accept) * 8 + size_t(std::max(h.ne, 1)) * 8 + 16;
-    if (cudaMalloc(&d->d_cnt, cnt_bytes) != cudaSuccess || cudaMemset(d->d_cnt, 0, cnt_bytes) != cudaSuccess) {
+    if (cudaMalloc(&d->d_cnt, cnt_bytes) != cudaSuccess ||
+        cudaMemsetAsync(d->d_cnt, 0, cnt_bytes, ctx->stream) != cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
         cudaGetLastError();
         if (d->d_cnt) cudaFree(d->d_cnt);
         cudaFree(d->d_blob);

@@ -20,6 +20,7 @@ C5  256 MiB uniform ACGT; hand-built 1024-state "G count mod 1024" DFA.
 from __future__ import annotations
 
 import itertools
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -60,6 +61,20 @@ def _iid_codes(rng, n: int, gc: float | None) -> np.ndarray:
     for lo in range(0, n, _BLOCK):
         hi = min(n, lo + _BLOCK)
         out[lo:hi] = lut[rng.integers(0, 65536, hi - lo, dtype=np.uint16)]
+    return out
+
+
+def _to_ascii(codes: np.ndarray) -> np.ndarray:
+    """codes 0..3 -> b"ACGT" (threaded gather in 64 MiB pieces)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    out = np.empty(codes.size, dtype=np.uint8)
+
+    def piece(lo):
+        np.take(ASCII_UPPER, codes[lo:lo + _BLOCK], out=out[lo:lo + _BLOCK])
+
+    with ThreadPoolExecutor(min(16, os.cpu_count() or 1)) as ex:
+        list(ex.map(piece, range(0, codes.size, _BLOCK)))
     return out
 
 
@@ -145,21 +160,30 @@ def _markov3(rng, n: int) -> np.ndarray:
     try:  # compiled loop when numba is present (it is in this image)
         from numba import njit
 
-        @njit(cache=False)
+        @njit(cache=False, nogil=True)
         def walk(u, cdf, out, ctx):
+            # b = first index with r < cdf[ctx, b] (cdf rows are increasing),
+            # counted branch-free
             for i in range(u.shape[0]):
                 r = u[i]
-                b = 0
-                while b < 3 and r >= cdf[ctx, b]:
-                    b += 1
+                b = (r >= cdf[ctx, 0]) + (r >= cdf[ctx, 1]) + (r >= cdf[ctx, 2])
                 out[i] = b
                 ctx = ((ctx << 2) | b) & 63
             return ctx
 
+        from concurrent.futures import ThreadPoolExecutor
+
+        # the next block's uniforms are drawn (numpy releases the GIL) while
+        # the compiled walk consumes this one; the stream is consumed in order
         ctx = 0
-        for lo in range(0, n, _BLOCK):
-            hi = min(n, lo + _BLOCK)
-            ctx = walk(rng.random(hi - lo), cdf, out[lo:hi], ctx)
+        blocks = [(lo, min(n, lo + _BLOCK)) for lo in range(0, n, _BLOCK)]
+        with ThreadPoolExecutor(1) as ex:
+            nxt = ex.submit(rng.random, blocks[0][1] - blocks[0][0]) if blocks else None
+            for i, (lo, hi) in enumerate(blocks):
+                u = nxt.result()
+                if i + 1 < len(blocks):
+                    nxt = ex.submit(rng.random, blocks[i + 1][1] - blocks[i + 1][0])
+                ctx = walk(u, cdf, out[lo:hi], ctx)
     except ImportError:  # pragma: no cover
         ctx = 0
         u = rng.random(n)
@@ -202,7 +226,7 @@ def make(k: int, n: int | None = None, shard: int = 0) -> Workload:
         desc = "256 MiB uniform ACGT, 1024-state permutation DFA"
     else:
         raise ValueError("config must be 1..5")
-    ascii_ = ASCII_UPPER[codes]
+    ascii_ = _to_ascii(codes)
     del codes
     if k == 2:
         _apply_spans(ascii_, _runs(srng, n, 0.05, 300), lambda b: b | 0x20)

@@ -247,7 +247,7 @@ def test_bench_reference_arm_contract():
 
     repo = Path(__file__).resolve().parents[1]
     out = subprocess.run([sys.executable, str(repo / "bench.py"), "--impl", "reference", "--config", "1",
-                          "--steps", "1", "--warmup", "1", "--cpu-sample", str(1 << 18)],
+                          "--steps", "1", "--warmup", "1", "--bases", str(1 << 18)],
                          capture_output=True, text=True, timeout=600, cwd=repo)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
@@ -256,3 +256,36 @@ def test_bench_reference_arm_contract():
         assert key in line
     assert {"value", "unit", "cores", "kind", "sample"} <= set(line["cpu_baseline"])
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+
+
+def test_bench_gpus_self_launch_on_cpu():
+    """`bench.py --gpus 2` outside torchrun re-launches itself with two ranks
+    (torch.distributed.run, rendezvous on 127.0.0.1); the reference arm's
+    rank 0 prints n_gpus 2 and the other rank exits 0 -- runs on CPU."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    repo = Path(__file__).resolve().parents[1]
+    env = {k: v for k, v in __import__("os").environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, str(repo / "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--config", "1", "--steps", "1", "--warmup", "3", "--bases", str(1 << 16)],
+                         capture_output=True, text=True, timeout=600, cwd=repo, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(x) for x in out.stdout.strip().splitlines() if x.startswith("{")]
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["impl"] == "reference"
+
+
+def test_bench_world_size_mismatch_fails():
+    """Under a launcher whose world size differs from --gpus, bench.py refuses."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    repo = Path(__file__).resolve().parents[1]
+    env = dict(__import__("os").environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, str(repo / "bench.py"), "--impl", "reference", "--gpus", "4",
+                          "--config", "1", "--steps", "1", "--bases", "4096"],
+                         capture_output=True, text=True, timeout=300, cwd=repo, env=env)
+    assert out.returncode == 2 and "WORLD_SIZE" in out.stderr
