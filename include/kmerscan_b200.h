@@ -227,6 +227,55 @@ KS_API int ks_speculate(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int32
                  const int64_t* pss_off, const int32_t* pss_data, int32_t window,
                  int32_t* conv_out, int64_t* delta_out);
 
+/* Exhaustive reconciliation sweep (reference _kernels.py:116-179,
+ * oracle.py:94-116): every base word of `length` (4^length words) x every
+ * border class b (candidates pss_data[pss_off[b] .. pss_off[b+1]), entry 0 =
+ * the full run) runs the chunk kernel's speculation with `window`, and each
+ * converged speculative run is checked against a full scan from its own
+ * start state -- one device thread per (word, border).  Tables are the
+ * reference Dfa arrays (original ids).  result_out[4] = speculative runs,
+ * converged runs, count mismatches, final-state mismatches.  length <= 13,
+ * n_expressions <= 16 (else KS_E_UNSUPPORTED). */
+KS_API int ks_reconciliation_sweep(ks_ctx* ctx, const int32_t* transitions, int32_t n_states,
+                                   const int32_t* out_offsets, const int32_t* out_ids, int32_t n_expressions,
+                                   const int32_t* pss_data, const int32_t* pss_off, int32_t n_borders,
+                                   int32_t length, int32_t window, int64_t* result_out);
+
+/* ---- multi-device (one process, several GPUs) -------------------------- */
+/* One sequence sharded over devices dev_ids[0..n_dev) -- the reference's
+ * run() spreading one call over all its workers (engine.py:207-237,
+ * ingest.py:78-94 partition) with the workers being GPUs.  Distinct devices
+ * exchange over NCCL (ncclCommInitAll; libnccl.so.2 loaded at run time:
+ * all-gather of boundary maps, all-reduce of the counts); a device id may
+ * repeat (tests on one GPU), or KS_MULTI_NCCL=0 be set, and the exchanges
+ * then run as stream-ordered peer copies.  Results equal ks_count/ks_locate
+ * of the whole sequence on one device. */
+typedef struct ks_mctx ks_mctx;
+typedef struct ks_mdfa ks_mdfa;
+typedef struct ks_mseq ks_mseq;
+KS_API int ks_open_multi(int32_t n_dev, const int32_t* dev_ids, ks_mctx** out);
+KS_API int ks_close_multi(ks_mctx* m);
+KS_API int ks_multi_info(const ks_mctx* m, int32_t* n_dev, int32_t* uses_nccl);
+/* The automaton on every device (same arguments as ks_dfa_upload). */
+KS_API int ks_mdfa_upload(ks_mctx* m, const int32_t* transitions, int32_t n_states,
+                          const int32_t* out_offsets, const int32_t* out_ids, int32_t n_expressions,
+                          ks_mdfa** out);
+KS_API int ks_mdfa_free(ks_mdfa* d);
+/* Codes 0..4: contiguous slices on 64-symbol boundaries, each slice with the
+ * previous slice's last 2048 symbols in front (definite automata then need
+ * no boundary-map exchange). */
+KS_API int ks_mseq_upload_codes(ks_mctx* m, const uint8_t* codes, int64_t n, ks_mseq** out);
+/* Raw / FASTA bytes cut into n_dev pieces (FASTA: at line starts), each
+ * encoded on its device; slice offsets are the kept-symbol prefix sums. */
+KS_API int ks_mseq_upload_ascii(ks_mctx* m, const uint8_t* bytes, int64_t n_bytes, int32_t fasta,
+                                ks_mseq** out);
+KS_API int ks_mseq_length(const ks_mseq* s, int64_t* n);
+KS_API int ks_mseq_free(ks_mseq* s);
+KS_API int ks_mcount(ks_mctx* m, const ks_mdfa* d, const ks_mseq* s, int64_t* counts_out);
+/* Rows as ks_locate (library-allocated, ks_free), global offsets. */
+KS_API int ks_mlocate(ks_mctx* m, const ks_mdfa* d, const ks_mseq* s, int64_t* counts_out,
+                      int64_t** rows_out, int64_t* n_rows);
+
 KS_API void ks_free(void* p);
 
 #ifdef __cplusplus

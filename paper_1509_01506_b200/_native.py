@@ -62,6 +62,9 @@ EXPORTED = (
     "ks_count_host_ascii", "ks_count_async", "ks_async_wait", "ks_segment_map_async",
     "ks_count_shard_async", "ks_pack_host_ascii", "ks_count_host_bytes", "ks_pack_host_wire",
     "ks_scan_range", "ks_segment_map", "ks_speculate", "ks_free",
+    "ks_open_multi", "ks_close_multi", "ks_multi_info", "ks_mdfa_upload", "ks_mdfa_free",
+    "ks_mseq_upload_codes", "ks_mseq_upload_ascii", "ks_mseq_length", "ks_mseq_free", "ks_mcount",
+    "ks_mlocate", "ks_reconciliation_sweep",
 )
 
 _lib = None
@@ -110,6 +113,19 @@ def _declare(lib) -> None:
         "ks_speculate": (C.c_int, [_P, _P, _P, C.c_int32, _i64p, _i64p, _i64p, _i32p, C.c_int32,
                                    _i32p, _i64p]),
         "ks_free": (None, [_P]),
+        "ks_open_multi": (C.c_int, [C.c_int32, _i32p, C.POINTER(_P)]),
+        "ks_close_multi": (C.c_int, [_P]),
+        "ks_multi_info": (C.c_int, [_P, _i32p, _i32p]),
+        "ks_mdfa_upload": (C.c_int, [_P, _i32p, C.c_int32, _i32p, _i32p, C.c_int32, C.POINTER(_P)]),
+        "ks_mdfa_free": (C.c_int, [_P]),
+        "ks_mseq_upload_codes": (C.c_int, [_P, _u8p, C.c_int64, C.POINTER(_P)]),
+        "ks_mseq_upload_ascii": (C.c_int, [_P, _u8p, C.c_int64, C.c_int32, C.POINTER(_P)]),
+        "ks_mseq_length": (C.c_int, [_P, _i64p]),
+        "ks_mseq_free": (C.c_int, [_P]),
+        "ks_mcount": (C.c_int, [_P, _P, _P, _i64p]),
+        "ks_mlocate": (C.c_int, [_P, _P, _P, _i64p, C.POINTER(_i64p), _i64p]),
+        "ks_reconciliation_sweep": (C.c_int, [_P, _i32p, C.c_int32, _i32p, _i32p, C.c_int32, _i32p, _i32p,
+                                              C.c_int32, C.c_int32, C.c_int32, _i64p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -396,6 +412,24 @@ class DeviceContext:
             delta = delta[:total, : dfa.n_expressions]
         return conv, delta
 
+    def reconciliation_sweep(self, dfa, pss_sets, length: int, window: int) -> np.ndarray:
+        """ks_reconciliation_sweep: int64[4] = speculative runs, converged
+        runs, count mismatches, final-state mismatches."""
+        trans = np.ascontiguousarray(np.asarray(dfa.transitions, dtype=np.int32))
+        off = np.ascontiguousarray(np.asarray(dfa.out_offsets, dtype=np.int32))
+        ids = np.ascontiguousarray(np.asarray(dfa.out_ids, dtype=np.int32))
+        ids = ids if ids.size else np.zeros(1, dtype=np.int32)
+        data = np.ascontiguousarray(np.concatenate([np.asarray(p, dtype=np.int32) for p in pss_sets]))
+        poff = np.zeros(len(pss_sets) + 1, dtype=np.int32)
+        poff[1:] = np.cumsum([len(p) for p in pss_sets])
+        out = np.zeros(4, dtype=np.int64)
+        with self.lock:
+            _check(library().ks_reconciliation_sweep(
+                self.handle, _ptr(trans, C.c_int32), int(trans.shape[0]), _ptr(off, C.c_int32),
+                _ptr(ids, C.c_int32), int(dfa.n_expressions), _ptr(data, C.c_int32), _ptr(poff, C.c_int32),
+                len(pss_sets), int(length), int(window), _ptr(out, C.c_int64)))
+        return out
+
     def stats(self) -> dict:
         st = Stats()
         _check(library().ks_get_stats(self.handle, C.byref(st)))
@@ -448,6 +482,120 @@ def pack_host_wire(data, fasta: bool) -> tuple[np.ndarray, np.ndarray, int]:
     _check(library().ks_pack_host_wire(_ptr(buf, C.c_uint8), int(arr.size), int(bool(fasta)), bases.ctypes.data,
                                        special.ctypes.data, C.byref(kept)))
     return bases, special, int(kept.value)
+
+
+def _free_with(fn_name: str, h) -> None:
+    try:
+        getattr(library(), fn_name)(h)
+    except Exception:  # interpreter shutdown
+        pass
+
+
+class MultiContext:
+    """One sequence over several devices of this process (ks_mctx): slices
+    per device, NCCL between distinct devices (peer copies when a device id
+    repeats).  Same results as DeviceContext.count/locate on one device."""
+
+    def __init__(self, devices):
+        devs = [int(d) for d in devices]
+        if not devs or min(devs) < 0:
+            raise ValueError("devices must be a non-empty list of device ids")
+        arr = np.asarray(devs, dtype=np.int32)
+        h = _P()
+        _check(library().ks_open_multi(len(devs), _ptr(arr, C.c_int32), C.byref(h)))
+        self.devices = tuple(devs)
+        self.handle = h
+        self.lock = threading.RLock()
+        n, nc = C.c_int32(), C.c_int32()
+        _check(library().ks_multi_info(h, C.byref(n), C.byref(nc)))
+        self.uses_nccl = bool(nc.value)
+        self._dfas: dict[int, tuple] = {}
+        self._finalizer = weakref.finalize(self, _free_with, "ks_close_multi", h)
+
+    def close(self) -> None:
+        self._finalizer()
+
+    def dfa(self, dfa):
+        key = id(dfa)
+        hit = self._dfas.get(key)
+        if hit is not None and hit[0]() is dfa:
+            return hit[1]
+        trans = np.ascontiguousarray(np.asarray(dfa.transitions, dtype=np.int32))
+        off = np.ascontiguousarray(np.asarray(dfa.out_offsets, dtype=np.int32))
+        ids = np.ascontiguousarray(np.asarray(dfa.out_ids, dtype=np.int32))
+        ids = ids if ids.size else np.zeros(1, dtype=np.int32)
+        h = _P()
+        with self.lock:
+            _check(library().ks_mdfa_upload(self.handle, _ptr(trans, C.c_int32), int(trans.shape[0]),
+                                            _ptr(off, C.c_int32), _ptr(ids, C.c_int32), int(dfa.n_expressions),
+                                            C.byref(h)))
+        handle = _MultiHandle(h, "ks_mdfa_free", n_expressions=int(dfa.n_expressions), owner=self)
+        try:
+            self._dfas[key] = (weakref.ref(dfa, lambda _r, k=key, d=self._dfas: d.pop(k, None)), handle)
+        except TypeError:
+            pass
+        return handle
+
+    def _seq(self, fn: str, *args):
+        h = _P()
+        with self.lock:
+            _check(getattr(library(), fn)(self.handle, *args, C.byref(h)))
+        n = C.c_int64()
+        _check(library().ks_mseq_length(h, C.byref(n)))
+        return _MultiHandle(h, "ks_mseq_free", length=int(n.value), owner=self)
+
+    def upload_codes(self, codes: np.ndarray):
+        arr = np.ascontiguousarray(np.asarray(codes, dtype=np.uint8))
+        buf = arr if arr.size else np.zeros(1, dtype=np.uint8)
+        return self._seq("ks_mseq_upload_codes", _ptr(buf, C.c_uint8), int(arr.size))
+
+    def upload_ascii(self, data, fasta: bool = False):
+        arr = np.frombuffer(data, dtype=np.uint8) if isinstance(data, (bytes, bytearray, memoryview)) \
+            else np.ascontiguousarray(np.asarray(data, dtype=np.uint8))
+        buf = arr if arr.size else np.zeros(1, dtype=np.uint8)
+        return self._seq("ks_mseq_upload_ascii", _ptr(buf, C.c_uint8), int(arr.size), int(bool(fasta)))
+
+    def count(self, dfa, seq) -> np.ndarray:
+        counts = np.zeros(max(dfa.n_expressions, 1), dtype=np.int64)
+        with self.lock:
+            _check(library().ks_mcount(self.handle, dfa.handle, seq.handle, _ptr(counts, C.c_int64)))
+        return counts[: dfa.n_expressions]
+
+    def locate(self, dfa, seq) -> tuple[np.ndarray, np.ndarray]:
+        counts = np.zeros(max(dfa.n_expressions, 1), dtype=np.int64)
+        rows_p = _i64p()
+        n = C.c_int64()
+        with self.lock:
+            _check(library().ks_mlocate(self.handle, dfa.handle, seq.handle, _ptr(counts, C.c_int64),
+                                        C.byref(rows_p), C.byref(n)))
+        return counts[: dfa.n_expressions], _take_rows(rows_p, int(n.value))
+
+
+class _MultiHandle:
+    """ks_mdfa / ks_mseq handle (freed with its context kept alive)."""
+
+    def __init__(self, handle, free_fn: str, owner, **attrs):
+        self.handle = handle
+        self.owner = owner
+        self.__dict__.update(attrs)
+        self._finalizer = weakref.finalize(self, _free_with, free_fn, handle)
+
+    def free(self) -> None:
+        self._finalizer()
+
+
+_multi: dict[tuple, MultiContext] = {}
+
+
+def multi_context(devices) -> MultiContext:
+    """Process-wide multi-device context for a tuple of device ids."""
+    key = tuple(int(d) for d in devices)
+    with _ctx_lock:
+        m = _multi.get(key)
+        if m is None:
+            m = MultiContext(key)
+            _multi[key] = m
+        return m
 
 
 def context(device: int = 0) -> DeviceContext:

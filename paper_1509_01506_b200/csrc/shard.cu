@@ -173,7 +173,7 @@ int ks_count_shard_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
     const bool halo = rank > 0 && !d_maps;
     if (h.wide && rank > 0 && !halo)
         return fail(KS_E_UNSUPPORTED, "wide automata shard in halo mode only (no map exchange)");
-    if (halo && (h.strategy != KS_STRATEGY_LOOKBACK || begin < h.sync_depth))
+    if (halo && end > begin && (h.strategy != KS_STRATEGY_LOOKBACK || begin < h.sync_depth))
         return fail(KS_E_INVALID, "shard without maps needs a definite automaton and a halo of sync_depth bases");
     int64_t origin, L, nch;
     geometry(seq, begin, end, &origin, &L, &nch);
@@ -185,18 +185,25 @@ int ks_count_shard_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
     if (spec) need += size_t(nch) * 2;
     int rc = ensure_scratch(ctx, need, &ar);
     if (rc) return rc;
-    unsigned long long* visits = static_cast<unsigned long long*>(ar.take(size_t(h.n_accept) * 8));
+    const ScanPlan plan = plan_for(ctx, dfa, dfa->scan);
+    // the fast kernel's last CTA finalizes the counts straight into d_counts
+    // (it zeroes them first) from the dfa's persistent visit block, which it
+    // leaves zeroed: a halo-mode shard count is then one launch
+    const bool fused = plan.fast && nch > 0;
+    unsigned long long* visits = fused ? static_cast<unsigned long long*>(dfa->d_cnt)
+                                       : static_cast<unsigned long long*>(ar.take(size_t(h.n_accept) * 8));
     uint16_t* entry = static_cast<uint16_t*>(ar.take(16));
     uint16_t* chunk_exit = static_cast<uint16_t*>(ar.take(size_t(nch) * 2 + 2));
     int launches = 0;
-    if (h.n_accept > 0) KS_CUDA(cudaMemsetAsync(visits, 0, size_t(h.n_accept) * 8, ctx->stream));
-    KS_CUDA(cudaMemsetAsync(d_counts, 0, size_t(std::max(h.ne, 1)) * 8, ctx->stream));
+    if (!fused) {
+        if (h.n_accept > 0) KS_CUDA(cudaMemsetAsync(visits, 0, size_t(h.n_accept) * 8, ctx->stream));
+        KS_CUDA(cudaMemsetAsync(d_counts, 0, size_t(std::max(h.ne, 1)) * 8, ctx->stream));
+    }
     if (!halo) {
         compose_entry_kernel<<<1, 1, 0, ctx->stream>>>(d_maps, h.nq, rank, 0, dfa->d_new_of_old, entry);
         KS_CUDA(cudaGetLastError());
     }
     if (nch > 0) {
-        const ScanPlan plan = plan_for(ctx, dfa, dfa->scan);
         ScanArgs a = base_args(dfa, dfa->scan, seq);
         a.begin = begin;
         a.end = end;
@@ -224,15 +231,26 @@ int ks_count_shard_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
             a.base_state_ptr = halo ? nullptr : entry;
             a.any_state = h.start_internal;
         }
-        KS_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
+        if (fused) {
+            char* blk = static_cast<char*>(dfa->d_cnt);
+            int32_t* err = reinterpret_cast<int32_t*>(blk + size_t(h.n_accept) * 8 + size_t(std::max(h.ne, 1)) * 8);
+            a.fin_counts = d_counts;
+            a.fin_exit_src = chunk_exit + (nch - 1);
+            a.fin_exit_dst = reinterpret_cast<uint16_t*>(err + 2);
+            a.fin_done = reinterpret_cast<unsigned int*>(err + 1);   // zero between calls
+            a.fin_host = nullptr;
+            a.n_expr = h.ne;
+        }
         rc = dispatch(ctx, dfa, dfa->scan, plan, a, kModeCount, &launches);
         if (rc) return rc;
-        KS_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
     }
-    rc = launch_finalize_counts(ctx, visits, h.n_accept, dfa->d_acc_out_off, dfa->d_acc_out_ids, d_counts,
-                                nullptr, nullptr, &launches);
-    if (rc) return rc;
-    ctx->async_launches += launches + 2;
+    if (!fused) {
+        rc = launch_finalize_counts(ctx, visits, h.n_accept, dfa->d_acc_out_off, dfa->d_acc_out_ids, d_counts,
+                                    nullptr, nullptr, &launches);
+        if (rc) return rc;
+        launches += 2;   // the memsets
+    }
+    ctx->async_launches += launches;
     ++ctx->async_calls;
     return KS_OK;
 }

@@ -41,12 +41,16 @@ __all__ = [
 @dataclass(frozen=True)
 class EngineConfig:
     """``workers``/``window``/``mode`` as in the reference (`engine.py:38-50`);
-    ``device`` selects the CUDA device of this process."""
+    ``device`` selects the CUDA device of this process; ``devices`` (a tuple
+    of device ids) shards the sequence over several GPUs of this process --
+    the reference's workers spread over devices (ks_open_multi: NCCL between
+    distinct devices)."""
 
     workers: int = 1
     window: int = DEFAULT_WINDOW
     mode: str = "count"  # "count" or "locate"
     device: int = 0
+    devices: tuple[int, ...] | None = None
 
     def __post_init__(self):
         if self.workers < 1:
@@ -57,6 +61,10 @@ class EngineConfig:
             raise ValueError(f"unknown mode {self.mode!r}")
         if self.device < 0:
             raise ValueError("device must be >= 0")
+        if self.devices is not None:
+            if len(self.devices) == 0 or min(int(d) for d in self.devices) < 0:
+                raise ValueError("devices must be a non-empty tuple of device ids >= 0")
+            object.__setattr__(self, "devices", tuple(int(d) for d in self.devices))
 
 
 @dataclass(frozen=True)
@@ -131,10 +139,57 @@ def _speculation_metadata(ctx, dh, sh, dfa, seq, plan: ChunkPlan, cfg: EngineCon
     }
 
 
+def _speculation_metadata_windows(ctx, dfa, seq, plan: ChunkPlan, cfg: EngineConfig) -> dict:
+    """The same metadata when the sequence lives sharded over several devices:
+    the speculative runs only read the first min(window, chunk length)
+    symbols of each chunk, so those windows are uploaded to one device."""
+    sym = np.asarray(seq.symbols)
+    parts, bounds, pos = [], [(0, 0)], 0
+    for i in range(1, plan.worker_count):
+        b, e = plan.bounds[i]
+        w = sym[b:b + min(cfg.window, e - b)]
+        parts.append(w)
+        bounds.append((pos, pos + w.size))
+        pos += w.size
+    if plan.worker_count == 1:
+        return _speculation_metadata(ctx, None, None, dfa, seq, plan, cfg)
+    sh = ctx.upload_codes(np.concatenate(parts) if pos else np.zeros(0, np.uint8))
+    compact = ChunkPlan(plan.worker_count, tuple(bounds), plan.boundary_symbols)
+    meta = _speculation_metadata(ctx, ctx.dfa(dfa), sh, dfa, seq, compact, cfg)
+    meta["input_length"] = plan.bounds[-1][1]
+    return meta
+
+
+def _run_multi(dfa: Dfa, seq: Sequence, cfg: EngineConfig, plan: ChunkPlan, t0: float) -> MatchReport:
+    m = _native.multi_context(cfg.devices)
+    dh = m.dfa(dfa)
+    key = ("multi",) + cfg.devices
+    cache = getattr(seq, "_device", None)
+    sh = cache.get(key) if isinstance(cache, dict) else None
+    if sh is None:
+        sh = m.upload_codes(seq.symbols)
+        if isinstance(cache, dict):
+            cache[key] = sh
+    if cfg.mode == "locate":
+        counts, locations = m.locate(dh, sh)
+    else:
+        counts, locations = m.count(dh, sh), None
+    total = int(counts.sum())
+    if locations is not None and locations.shape[0] != total:
+        raise ReductionChainError(f"{locations.shape[0]} rows for {total} matches")
+    dstats = {"devices": list(cfg.devices), "nccl": m.uses_nccl}
+    metadata = _speculation_metadata_windows(_native.context(cfg.devices[0]), dfa, seq, plan, cfg)
+    metadata["input_name"] = getattr(seq, "source_name", "")
+    metadata["elapsed_seconds"] = time.perf_counter() - t0
+    return MatchReport(counts, total, locations, metadata, dstats)
+
+
 def run(dfa: Dfa, seq: Sequence, cfg: EngineConfig = EngineConfig()) -> MatchReport:
     """Scan the whole sequence on the GPU and report counts (and rows)."""
     t0 = time.perf_counter()
     plan = plan_chunks(seq, cfg.workers)
+    if cfg.devices is not None:
+        return _run_multi(dfa, seq, cfg, plan, t0)
     ctx = _ctx(cfg)
     dh = ctx.dfa(dfa)
     sh = ctx.seq(seq)

@@ -67,11 +67,17 @@ def exhaustive_reconciliation_check(dfa: Dfa, length: int, window: int) -> dict:
     from . import _native
 
     ctx = _native.context(0)
+    pss_sets = [possible_starting_states(dfa, b, 0) for b in range(N_SYMBOLS)]
+    if length <= 13 and dfa.n_expressions <= 16 and dfa.state_count <= 1024:
+        # one device thread per (word, border): ks_reconciliation_sweep
+        r = ctx.reconciliation_sweep(dfa, pss_sets, length, window)
+        return {"length": length, "speculative_runs": int(r[0]), "converged_runs": int(r[1]),
+                "count_mismatches": int(r[2]), "final_state_mismatches": int(r[3])}
+    # larger automata: words laid end to end, ks_speculate + ks_scan_range per word
     dh = ctx.dfa(dfa)
     words = np.array(list(itertools.product(range(4), repeat=length)), dtype=np.uint8).reshape(-1)
     n_words = 4 ** length
     sh = ctx.upload_codes(words)
-    pss_sets = [possible_starting_states(dfa, b, 0) for b in range(N_SYMBOLS)]
     runs = converged = bad_counts = bad_state = 0
     for pss in pss_sets:
         begins = np.arange(n_words, dtype=np.int64) * length

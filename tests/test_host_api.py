@@ -266,3 +266,11 @@ class TestEngineHost:
         assert rep.per_expression_counts.tolist() == [2, 0, 0, 0]
         assert rep.locations.tolist() == [[3, 0], [6, 0]]
         assert rep.metadata["convergence_steps"] == {0: 1}
+
+
+def test_engine_config_devices_validation():
+    with pytest.raises(ValueError):
+        ks.EngineConfig(devices=())
+    with pytest.raises(ValueError):
+        ks.EngineConfig(devices=(0, -1))
+    assert ks.EngineConfig(devices=[1, 0]).devices == (1, 0)
