@@ -134,6 +134,9 @@ ScanArgs base_args(const ks_dfa* dfa, const DevTable& T, const ks_seq* seq) {
     a.seq = view_of(seq);
     a.t1 = T.t1;
     a.t1w = T.t1w;
+    a.ht = T.ht;
+    a.hot_lo = T.hot_lo;
+    a.hot_n = T.hot_n;
     a.tk = T.tk;
     a.nq = T.nq;
     a.n_accept = T.n_accept;
@@ -729,6 +732,7 @@ int ks_close(ks_ctx* ctx) {
     if (ctx->rstage) cudaFreeHost(ctx->rstage);
     if (ctx->rdev) cudaFree(ctx->rdev);
     if (ctx->log_buf) cudaFree(ctx->log_buf);
+    if (ctx->wctr) cudaFree(ctx->wctr);
     delete ctx->pool;
     if (ctx->hstage) cudaFreeHost(ctx->hstage);
     for (auto& ev : ctx->hev)

@@ -16,6 +16,7 @@
 //     is small: chunk maps become monoid element ids, composed by a
 //     product-table lookup in an exclusive device-wide scan.
 #include <algorithm>
+#include <cstdint>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
@@ -262,11 +263,54 @@ int compile_dfa(const int32_t* trans, int nq, const int32_t* out_off, const int3
     h->ne = ne;
     h->new_of_old.assign(nq, 0);
     h->old_of_new.clear();
-    for (int s = 0; s < nq; ++s)
-        if (out_off[s + 1] > out_off[s]) h->old_of_new.push_back(s);
-    h->n_accept = int(h->old_of_new.size());
-    for (int s = 0; s < nq; ++s)
-        if (out_off[s + 1] == out_off[s]) h->old_of_new.push_back(s);
+    int hot_lo = 0, hot_n = 0;
+    if (nq > kMaxStates) {
+        // wide automata: accepting states still first ([0, A): the hit test),
+        // and the hot set -- the states nearest START (BFS depth, then id:
+        // a scan of AC-like automata spends almost every step there) -- one
+        // contiguous range: [cold accepting | hot accepting | hot other | cold other]
+        std::vector<int32_t> depth(nq, -1), q;
+        q.reserve(nq);
+        depth[0] = 0;
+        q.push_back(0);
+        for (size_t i = 0; i < q.size(); ++i)
+            for (int c = 0; c < 5; ++c) {
+                const int32_t x = trans[size_t(q[i]) * 5 + c];
+                if (depth[x] < 0) {
+                    depth[x] = depth[q[i]] + 1;
+                    q.push_back(x);
+                }
+            }
+        std::vector<int32_t> by(nq);
+        std::iota(by.begin(), by.end(), 0);
+        auto key = [&](int32_t x) { return depth[x] < 0 ? INT32_MAX : depth[x]; };
+        std::stable_sort(by.begin(), by.end(), [&](int32_t x, int32_t y) { return key(x) < key(y); });
+        const int A = int(std::count_if(by.begin(), by.end(), [&](int32_t x) { return out_off[x + 1] > out_off[x]; }));
+        const size_t hist = std::min<size_t>(size_t(A) * 4, 64 * 1024);
+        const size_t room = smem_budget > hist + 4096 ? smem_budget - hist - 4096 : 0;
+        hot_n = int(std::min<size_t>({size_t(nq), size_t(32766), room / 8}));
+        if (const char* e = std::getenv("KS_WIDE_HOT_STATES"); e && *e)   // test knob: a smaller hot set
+            hot_n = std::max(0, std::min(hot_n, std::atoi(e)));
+        std::vector<char> hot(nq, 0);
+        for (int i = 0; i < hot_n; ++i) hot[by[i]] = 1;
+        auto acc = [&](int32_t x) { return out_off[x + 1] > out_off[x]; };
+        for (int32_t x = nq - 1; x >= 0; --x)   // cold accepting, deepest first
+            if (acc(by[x]) && !hot[by[x]]) h->old_of_new.push_back(by[x]);
+        hot_lo = int(h->old_of_new.size());
+        for (int32_t x = 0; x < nq; ++x)
+            if (acc(by[x]) && hot[by[x]]) h->old_of_new.push_back(by[x]);
+        h->n_accept = int(h->old_of_new.size());
+        for (int32_t x = 0; x < nq; ++x)
+            if (!acc(by[x]) && hot[by[x]]) h->old_of_new.push_back(by[x]);
+        for (int32_t x = 0; x < nq; ++x)
+            if (!acc(by[x]) && !hot[by[x]]) h->old_of_new.push_back(by[x]);
+    } else {
+        for (int s = 0; s < nq; ++s)
+            if (out_off[s + 1] > out_off[s]) h->old_of_new.push_back(s);
+        h->n_accept = int(h->old_of_new.size());
+        for (int s = 0; s < nq; ++s)
+            if (out_off[s + 1] == out_off[s]) h->old_of_new.push_back(s);
+    }
     for (int i = 0; i < nq; ++i) h->new_of_old[h->old_of_new[i]] = i;
     h->start_internal = h->new_of_old[0];
 
@@ -302,6 +346,16 @@ int compile_dfa(const int32_t* trans, int nq, const int32_t* out_off, const int3
         bool resets = true;
         for (int s = 1; s < nq && resets; ++s) resets = t.t1w[size_t(s) * 5 + 4] == r;
         t.reset_state = resets ? int(r) : -1;
+        if (resets && hot_n > 0) {   // hot table (4 columns: OTHER resets, not stored)
+            t.hot_lo = hot_lo;
+            t.hot_n = hot_n;
+            t.ht.assign(size_t(hot_n) * 4, 0xFFFFu);
+            for (int i = 0; i < hot_n; ++i)
+                for (int c = 0; c < 4; ++c) {
+                    const uint32_t x = t.t1w[size_t(hot_lo + i) * 5 + c];
+                    if (x - uint32_t(hot_lo) < uint32_t(hot_n)) t.ht[size_t(i) * 4 + c] = uint16_t(x - hot_lo);
+                }
+        }
         h->sync_depth = synchronisation_depth(t.t1w, nq);
         if (h->sync_depth < 0)
             return fail(KS_E_UNSUPPORTED, "dfa: automata above 32767 states must be definite "

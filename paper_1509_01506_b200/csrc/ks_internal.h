@@ -52,6 +52,12 @@ struct CompiledTable {
     std::vector<uint16_t> tkc;       // 65536 entries
     std::vector<uint16_t> t1z;       // (nq + 1) x t1z_cols (4: OTHER resets, not stored)
     int t1z_cols = 5;
+    // wide automata (> kMaxStates): the hot states [hot_lo, hot_lo + hot_n)
+    // (the shallowest, where a scan spends nearly all its steps) get a
+    // 4-column shared-memory table of hot indices, 0xFFFF = the next state is
+    // cold (read the 32-bit 1-base table from L2)
+    std::vector<uint16_t> ht;
+    int hot_lo = 0, hot_n = 0;
 };
 
 struct HostDfa {
@@ -101,6 +107,8 @@ struct DevTable {
     int fast_k = 0;
     size_t t1z_bytes = 0;
     double hit_rate = 0;
+    const uint16_t* ht = nullptr;   // wide automata: hot table (CompiledTable::ht)
+    int hot_lo = 0, hot_n = 0;
 };
 
 // Packed sequence layout ("lane-tiled").  The sequence is cut into units of
@@ -181,6 +189,7 @@ struct ks_ctx {
     size_t rdev_bytes = 0;
     // single-pass locate log (grow-only)
     void* log_buf = nullptr;
+    unsigned int* wctr = nullptr;   // task counter of the wide count kernel
     size_t log_bytes = 0;
     // ks_count_async: one event pair per call until ks_async_wait
     std::vector<cudaEvent_t> aev;

@@ -1,4 +1,5 @@
 // Chunked DFA scan kernels and their launchers (see scan_kernels.cuh).
+#include <cstdlib>
 #include <algorithm>
 
 #include "scan_kernels.cuh"
@@ -296,6 +297,235 @@ __global__ void __launch_bounds__(256) scan_wide_kernel(const ScanArgs a) {
     }
 }
 
+// Wide automata with a hot table (CompiledTable::ht): states in
+// [hot_lo, hot_lo + hot_n) step through the shared-memory table (2-byte hot
+// indices), every other transition -- from a cold state, or into one (0xFFFF)
+// -- reads the 32-bit 1-base table through L1/L2.  One thread per unit chunk
+// (a warp's 32 chunks are one tile: each block load is one coalesced 512 B
+// read), whole 64-base blocks stepped from registers, hits into the
+// shared-memory visit histogram when it fits (global atomics otherwise).
+__device__ __forceinline__ uint32_t wide_hot_step(const uint16_t* ht, const uint32_t* __restrict__ t1w, uint32_t s,
+                                                  uint32_t sym, uint32_t lo, uint32_t H) {
+    const uint32_t hs = s - lo;
+    if (hs < H) {
+        const uint32_t e = ht[hs * 4u + sym];
+        if (e != 0xFFFFu) return e + lo;
+    }
+    return __ldg(&t1w[size_t(s) * 5 + sym]);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(1024, 1) scan_wide_hot_kernel(const ScanArgs a) {
+    extern __shared__ __align__(16) unsigned char wh_smem[];
+    uint16_t* ht = reinterpret_cast<uint16_t*>(wh_smem);
+    const size_t ht_bytes = (size_t(a.hot_n) * 8 + 15) & ~size_t(15);
+    unsigned int* shist = reinterpret_cast<unsigned int*>(wh_smem + ht_bytes);
+    const bool hist_smem = (MODE == kModeCount || MODE == kModeRows) && a.hist_smem;
+    for (size_t i = threadIdx.x; i < ht_bytes / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(ht)[i] = __ldg(reinterpret_cast<const uint4*>(a.ht) + i);
+    if (hist_smem)
+        for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x) shist[i] = 0u;
+    __syncthreads();
+    const uint32_t A = uint32_t(a.n_accept), lo = uint32_t(a.hot_lo), H = uint32_t(a.hot_n);
+    const uint32_t reset = uint32_t(a.reset_state);
+    const uint4* bases4 = reinterpret_cast<const uint4*>(a.seq.bases);
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < a.nchunks; c += stride) {
+        const int64_t cb = max64(a.begin, a.origin + c * a.chunk_len);
+        const int64_t ce = min64(a.end, a.origin + (c + 1) * a.chunk_len);
+        const int64_t lb = max64(a.base_pos, cb - a.lookback);
+        uint32_t s = uint32_t(lb == a.base_pos ? a.base_state : a.any_state);
+        for (int64_t p = lb; p < cb; ++p) {
+            const uint32_t y = seq_sym(a.seq, p);
+            s = y == 4u ? reset : wide_hot_step(ht, a.t1w, s, y, lo, H);
+        }
+        Sink<MODE> sink;
+        sink.shist = hist_smem ? shist : nullptr;
+        sink.visits = a.visits;
+        sink.outcnt = a.acc_outcnt;
+        sink.off = a.acc_out_off;
+        sink.ids = a.acc_out_ids;
+        sink.rows = a.rows;
+        sink.row_base = a.row_base;
+        sink.nrows = 0;
+        sink.cur = (MODE == kModeEmit) ? a.chunk_row_off[c] : 0;
+        for (int64_t g = cb >> 6; g <= (ce - 1) >> 6 && cb < ce; ++g) {
+            const int64_t slot = blk_slot(g, a.seq.lb);
+            const uint4 xb = __ldg(bases4 + slot);
+            const uint64_t xm = __ldg(a.seq.nmask + slot);
+            const int64_t p0 = g << 6;
+            const int q0 = int(max64(cb - p0, 0)), q1 = int(min64(ce - p0, 64));
+            if (q0 == 0 && q1 == 64 && xm == 0ull) {   // a whole OTHER-free block
+#pragma unroll
+                for (int q = 0; q < 64; ++q) {
+                    const uint32_t w = q < 16 ? xb.x : q < 32 ? xb.y : q < 48 ? xb.z : xb.w;
+                    s = wide_hot_step(ht, a.t1w, s, (w >> (2 * (q & 15))) & 3u, lo, H);
+                    if constexpr (MODE != kModeMap) {
+                        if (s < A) sink.hit(p0 + q, s);
+                    }
+                }
+            } else {
+                for (int q = q0; q < q1; ++q) {
+                    const uint32_t w = q < 16 ? xb.x : q < 32 ? xb.y : q < 48 ? xb.z : xb.w;
+                    const uint32_t y = ((xm >> q) & 1ull) ? 4u : (w >> (2 * (q & 15))) & 3u;
+                    s = y == 4u ? reset : wide_hot_step(ht, a.t1w, s, y, lo, H);
+                    if constexpr (MODE != kModeMap) {
+                        if (s < A) sink.hit(p0 + q, s);
+                    }
+                }
+            }
+        }
+        if (a.chunk_exit32) a.chunk_exit32[c] = s;
+        if constexpr (MODE == kModeRows) a.chunk_rows[c] = sink.nrows;
+        if constexpr (MODE == kModeEmit) {
+            if (sink.cur != a.chunk_row_off[c + 1]) atomicExch(a.error, 1);
+        }
+    }
+    if (hist_smem) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x)
+            if (shist[i]) atomicAdd(&a.visits[i], (unsigned long long)shist[i]);
+    }
+}
+
+// Count mode, lean steps and dynamic work: warps take tasks of 32 runs of
+// U blocks (one run per lane) from a counter, so warps the scheduler favours
+// take more and none idles at the end (a static split left 28% of warp time
+// at the final barrier).  A run enters by its own lookback (the automaton is
+// definite).  A step from a hot state is one shared lookup in the hot table
+// -- whose row hot_n is all 0xFFFF, the target of cold states, so there is
+// no predicate -- and the warp takes the L2 path only when some lane's next
+// state is cold (a warp-uniform branch).  Hits are predicated reductions
+// into the shared (HSM) or global visit histogram.  Blocks with OTHER or cut
+// by the span edge take the per-symbol path.
+template <bool HSM>
+__device__ __forceinline__ void red_hit(bool p, uint32_t saddr, unsigned long long* g) {
+    if constexpr (HSM) {
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q red.shared.add.u32 [%1], 1;\n\t}"
+                     :: "r"(uint32_t(p)), "r"(saddr) : "memory");
+    } else {
+        if (p) atomicAdd(g, 1ull);
+    }
+}
+
+__device__ __forceinline__ uint32_t lds16u(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+template <bool HSM>
+__global__ void __launch_bounds__(1024, 1) scan_wide_hot_ilp_kernel(const ScanArgs a) {
+    extern __shared__ __align__(16) unsigned char wh_smem[];
+    uint16_t* ht = reinterpret_cast<uint16_t*>(wh_smem);
+    const uint32_t H = uint32_t(a.hot_n);
+    const size_t ht_bytes = (size_t(H + 1) * 8 + 15) & ~size_t(15);   // + the all-cold row H
+    unsigned int* shist = reinterpret_cast<unsigned int*>(wh_smem + ht_bytes);
+    for (size_t i = threadIdx.x; i < size_t(H) * 8 / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(ht)[i] = __ldg(reinterpret_cast<const uint4*>(a.ht) + i);
+    for (size_t i = size_t(H) * 4 + threadIdx.x; i < ht_bytes / 2; i += blockDim.x) ht[i] = 0xFFFFu;
+    if (HSM)
+        for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x) shist[i] = 0u;
+    __syncthreads();
+    const uint32_t A = uint32_t(a.n_accept), lo = uint32_t(a.hot_lo);
+    const uint32_t reset = uint32_t(a.reset_state);
+    const uint32_t ht_s = uint32_t(__cvta_generic_to_shared(ht));
+    const uint32_t hist_s = uint32_t(__cvta_generic_to_shared(shist));
+    const uint4* bases4 = reinterpret_cast<const uint4*>(a.seq.bases);
+    const uint32_t* t1w = a.t1w;
+    const int lane = threadIdx.x & 31;
+    const int64_t B0 = a.begin >> 6, nB = ((a.end - 1) >> 6) - B0 + 1;
+    const int64_t U = a.run_blocks;
+    const int64_t ntasks = (nB + U * 32 - 1) / (U * 32);
+    auto step = [&](uint32_t x, uint32_t y) -> uint32_t {   // one symbol 0..3 (per-symbol paths)
+        const uint32_t e = lds16u(ht_s + min(x - lo, H) * 8u + y * 2u);
+        return e != 0xFFFFu ? e + lo : __ldg(&t1w[size_t(x) * 5 + y]);
+    };
+    for (;;) {
+        unsigned int task = 0;
+        if (lane == 0) task = atomicAdd(a.work_ctr, 1u);
+        task = __shfl_sync(0xffffffffu, task, 0);
+        if (int64_t(task) >= ntasks) break;
+        const int64_t r = int64_t(task) * 32 + lane;
+        const int64_t b0 = min64(B0 + r * U, B0 + nB), b1 = min64(B0 + (r + 1) * U, B0 + nB);
+        const int64_t rb = max64(a.begin, b0 << 6), re = min64(a.end, b1 << 6);
+        const int nb = int(b1 - b0);
+        const int nmax = __reduce_max_sync(0xffffffffu, nb);
+        uint32_t Aj = nb > 0 ? A : 0u;   // idle lanes ride along without hits
+        uint32_t s = lo;
+        if (nb > 0) {   // lookback
+            const int64_t lbp = max64(a.base_pos, rb - a.lookback);
+            s = uint32_t(lbp == a.base_pos ? a.base_state : a.any_state);
+            if ((rb & 63) == 0 && rb - lbp <= 64 && rb > lbp) {
+                // the tail of the previous block, from registers (one load)
+                const int64_t slot = blk_slot((rb >> 6) - 1, a.seq.lb);
+                const uint4 pb = __ldg(bases4 + slot);
+                const uint64_t pm = __ldg(a.seq.nmask + slot);
+                for (int q = int(64 - (rb - lbp)); q < 64; ++q) {
+                    const uint32_t w = q < 16 ? pb.x : q < 32 ? pb.y : q < 48 ? pb.z : pb.w;
+                    const uint32_t y = ((pm >> q) & 1ull) ? 4u : (w >> (2 * (q & 15))) & 3u;
+                    s = y == 4u ? reset : step(s, y);
+                }
+            } else {
+                for (int64_t p = lbp; p < rb; ++p) {
+                    const uint32_t y = seq_sym(a.seq, p);
+                    s = y == 4u ? reset : step(s, y);
+                }
+            }
+        }
+        uint32_t ex = s;
+        for (int k = 0; k < nmax; ++k) {
+            uint4 xb = make_uint4(0, 0, 0, 0);
+            uint64_t xm = 0;
+            bool fast = true;
+            const int64_t gb = b0 + k;
+            if (k < nb) {
+                const int64_t slot = blk_slot(gb, a.seq.lb);
+                xm = __ldg(a.seq.nmask + slot);
+                xb = __ldg(bases4 + slot);
+                fast = xm == 0ull && (gb << 6) >= rb && (gb << 6) + 64 <= re;
+            } else {
+                if (k == nb) ex = s;
+                Aj = 0u;
+            }
+            if (__all_sync(0xffffffffu, fast)) {
+#pragma unroll 1
+                for (int wi = 0; wi < 4; ++wi) {
+                    const uint32_t w = wi == 0 ? xb.x : wi == 1 ? xb.y : wi == 2 ? xb.z : xb.w;
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        const uint32_t y2 = (q == 0 ? (w << 1) : (w >> (2 * q - 1))) & 6u;   // symbol * 2
+                        uint32_t e = lds16u(ht_s + min(s - lo, H) * 8u + y2);
+                        const bool cold = e == 0xFFFFu;
+                        if (__any_sync(0xffffffffu, cold)) {
+                            const uint32_t g2 = cold ? __ldg(&t1w[size_t(s) * 5 + (y2 >> 1)]) : 0u;
+                            e = cold ? g2 - lo : e;
+                        }
+                        s = e + lo;
+                        red_hit<HSM>(s < Aj, hist_s + s * 4u, a.visits + s);
+                    }
+                }
+            } else if (k < nb) {
+                const int64_t p0 = gb << 6;
+                const int q0 = int(max64(rb - p0, 0)), q1 = int(min64(re - p0, 64));
+                for (int q = q0; q < q1; ++q) {
+                    const uint32_t w = q < 16 ? xb.x : q < 32 ? xb.y : q < 48 ? xb.z : xb.w;
+                    const uint32_t y = ((xm >> q) & 1ull) ? 4u : (w >> (2 * (q & 15))) & 3u;
+                    s = y == 4u ? reset : step(s, y);
+                    red_hit<HSM>(s < Aj, hist_s + s * 4u, a.visits + s);
+                }
+            }
+        }
+        if (nb == nmax) ex = s;
+        if (a.chunk_exit32 && a.nchunks > 0 && nb > 0 && re == a.end) a.chunk_exit32[a.nchunks - 1] = ex;
+    }
+    if (HSM) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x)
+            if (shist[i]) atomicAdd(&a.visits[i], (unsigned long long)shist[i]);
+    }
+}
+
 using ScanFn = void (*)(const ScanArgs);
 
 template <int K, bool SM>
@@ -420,6 +650,47 @@ int launch_finalize_counts(ks_ctx* ctx, const unsigned long long* visits, int32_
 
 int launch_scan_wide(ks_ctx* ctx, ScanArgs a, int mode, int* launches) {
     if (a.end <= a.begin || a.nchunks <= 0) return KS_OK;
+    const char* hot_env = std::getenv("KS_WIDE_HOT");
+    if (a.ht && a.hot_n > 0 && a.reset_state >= 0 && !(hot_env && *hot_env == '0')) {
+        // count mode: the dynamic-task kernel (KS_WIDE_TASKS=0: one chunk per thread)
+        const char* tk_env = std::getenv("KS_WIDE_TASKS");
+        const bool tasks = mode == kModeCount && !(tk_env && *tk_env == '0');
+        const size_t ht_need = (size_t(a.hot_n + 1) * 8 + 15) & ~size_t(15);
+        const bool hsm = ht_need + size_t(a.n_accept) * 4 + 1024 <= ctx->smem_optin;
+        ScanFn fn = tasks ? (hsm ? scan_wide_hot_ilp_kernel<true> : scan_wide_hot_ilp_kernel<false>)
+                  : mode == kModeCount ? scan_wide_hot_kernel<kModeCount>
+                  : mode == kModeRows  ? scan_wide_hot_kernel<kModeRows>
+                  : mode == kModeEmit  ? scan_wide_hot_kernel<kModeEmit>
+                                       : nullptr;
+        if (!fn) return fail(KS_E_UNSUPPORTED, "wide automata: mode not supported");
+        size_t smem = tasks ? ht_need : align16(size_t(a.hot_n) * 8);
+        a.hist_smem = 0;
+        if ((mode == kModeCount || mode == kModeRows) && smem + size_t(a.n_accept) * 4 + 1024 <= ctx->smem_optin) {
+            a.hist_smem = 1;
+            smem += size_t(a.n_accept) * 4;
+        }
+        KS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(smem)));
+        const int threads = 1024;
+        int blocks = int(max64(1, min64((a.nchunks + threads - 1) / threads, int64_t(ctx->num_sms))));
+        if (tasks) {
+            // runs of U blocks, tasks of 32 runs handed out by a counter:
+            // about 6 tasks per warp (U in [2, 16]; 256 MiB: U = 3)
+            const int64_t nB = ((a.end - 1) >> 6) - (a.begin >> 6) + 1;
+            const int64_t warps = int64_t(ctx->num_sms) * (threads / 32);
+            a.run_blocks = int32_t(std::max<int64_t>(2, std::min<int64_t>(16, nB / (32 * 6 * warps))));
+            if (const char* e = std::getenv("KS_WIDE_RUN_BLOCKS"); e && *e) a.run_blocks = std::max(1, std::atoi(e));
+            if (!ctx->wctr) KS_CUDA(cudaMalloc(&ctx->wctr, 256));
+            KS_CUDA(cudaMemsetAsync(ctx->wctr, 0, 4, ctx->stream));
+            a.work_ctr = ctx->wctr;
+            const int64_t ntasks = (nB + int64_t(a.run_blocks) * 32 - 1) / (int64_t(a.run_blocks) * 32);
+            blocks = int(max64(1, min64(int64_t(ctx->num_sms), (ntasks + 31) / 32)));
+        }
+        fn<<<blocks, threads, smem, ctx->stream>>>(a);
+        if (launches) ++*launches;
+        KS_CUDA(cudaGetLastError());
+        return KS_OK;
+    }
     ScanFn fn = mode == kModeCount ? scan_wide_kernel<kModeCount>
               : mode == kModeRows  ? scan_wide_kernel<kModeRows>
               : mode == kModeEmit  ? scan_wide_kernel<kModeEmit>

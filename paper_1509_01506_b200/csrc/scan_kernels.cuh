@@ -58,6 +58,8 @@ struct ScanArgs {
     const uint16_t* t1 = nullptr;    // nq x 5 (global)
     const uint32_t* t1w = nullptr;   // nq x 5, 32-bit ids (wide automata, scan_wide_kernel)
     uint32_t* chunk_exit32 = nullptr;   // wide automata: per chunk exit state (optional)
+    const uint16_t* ht = nullptr;    // wide automata: hot table (hot_n x 4, hot indices, 0xFFFF = cold)
+    int32_t hot_lo = 0, hot_n = 0;
     const uint16_t* tk = nullptr;    // nq x 4^K (global)
     int32_t nq = 0, n_accept = 0, reset_state = -1;
     int32_t tk_pad = 0, t1_pad = 0;  // uint16 entries, multiples of 8
@@ -95,6 +97,8 @@ struct ScanArgs {
     LogEntry* log = nullptr;                // kModeLog
     unsigned long long* log_n = nullptr;    // kModeLog: visits appended (may exceed log_cap)
     int64_t log_cap = 0;
+    unsigned int* work_ctr = nullptr;       // wide count kernel: task counter (zeroed per launch)
+    int32_t run_blocks = 0;                 // wide count kernel: blocks per run
 };
 
 inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }

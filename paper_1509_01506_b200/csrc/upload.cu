@@ -30,6 +30,9 @@ int upload_table(const CompiledTable& t, DevTable* d, char* blob, size_t* off, b
     d->tk = reinterpret_cast<const uint16_t*>(place(t.tk.data(), t.tk.size() * 2));
     d->t1 = reinterpret_cast<const uint16_t*>(place(t.t1.data(), t.t1.size() * 2));
     if (!t.t1w.empty()) d->t1w = reinterpret_cast<const uint32_t*>(place(t.t1w.data(), t.t1w.size() * 4));
+    if (!t.ht.empty()) d->ht = reinterpret_cast<const uint16_t*>(place(t.ht.data(), t.ht.size() * 2));
+    d->hot_lo = t.hot_lo;
+    d->hot_n = t.ht.empty() ? 0 : t.hot_n;
     d->fast_k = t.fast_k;
     d->hit_rate = t.hit_rate;
     d->t1z_bytes = align16(t.t1z.size() * 2);
@@ -173,6 +176,7 @@ int ks_dfa_upload_ex(ks_ctx* ctx, const int32_t* transitions, int32_t n_states, 
     rebase(d->scan.tk);
     rebase(d->scan.t1);
     rebase(d->scan.t1w);
+    rebase(d->scan.ht);
     rebase(d->scan.tkc);
     rebase(d->scan.t1z);
     rebase(d->d_acc_out_off);

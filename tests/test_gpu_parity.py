@@ -719,13 +719,23 @@ def wide_dfa():
     return dfa, sorted(lits)
 
 
-def test_wide_automaton(wide_dfa):
+@pytest.mark.parametrize("hot", ["default", "64", "chunks", "off"])
+def test_wide_automaton(wide_dfa, hot, monkeypatch):
     """Automata above the 16-bit state range: 32-bit ids, LOOKBACK, the wide
-    scan kernel -- counts, sorted rows, ranges, run() with metadata, the
-    streamed call (which falls back to one upload) and the halo shard."""
+    scan kernels (hot table in shared memory + cold transitions from L2; a
+    64-state hot set; the L2-only kernel) -- counts, sorted rows, ranges,
+    run() with metadata, the streamed call (which falls back to one upload)
+    and the halo shard."""
     import torch
 
+    if hot == "off":
+        monkeypatch.setenv("KS_WIDE_HOT", "0")
+    elif hot == "chunks":
+        monkeypatch.setenv("KS_WIDE_TASKS", "0")
+    elif hot != "default":
+        monkeypatch.setenv("KS_WIDE_HOT_STATES", hot)
     dfa, lits = wide_dfa
+    dfa = ks.Dfa(dfa.transitions, dfa.out_offsets, dfa.out_ids, dfa.labels, dfa.n_expressions)  # fresh upload
     rng = np.random.default_rng(9)
     n = 1 << 20
     sym = rng.integers(0, 4, n).astype(np.uint8)
@@ -734,7 +744,7 @@ def test_wide_automaton(wide_dfa):
         p = int(rng.integers(0, n - len(lit)))
         sym[p:p + len(lit)] = ["acgt".index(c) for c in lit]
     sym[rng.integers(0, n, 40)] = 4
-    ctx = _native.context(0)
+    ctx = _native.DeviceContext(0)
     dh = ctx.dfa(dfa)
     assert dh.info["strategy_name"] == "lookback"
     want, rows, meta = O.ref_run(dfa, sym, 6, 10, True)
@@ -918,3 +928,18 @@ def test_async_back_to_back_mixed():
     assert waited["kernel_launches"] >= len(outs)
     for buf, want in outs:
         assert buf.numpy()[: want.size].tolist() == want.tolist()
+
+
+def test_kernels_scan_from_dropin(toy_dfa):
+    """paper_1509_01506_b200._kernels.scan_from: the reference's raw-array
+    kernel signature (_kernels.py:18-29) on the device, counts added in place."""
+    from paper_1509_01506_b200 import _kernels
+
+    rng = np.random.default_rng(3)
+    sym = rng.integers(0, 5, 5000).astype(np.uint8)
+    for start, end, state in ((0, 5000, 0), (17, 4000, 3), (100, 100, 2), (4999, 5000, 1)):
+        counts = np.full(toy_dfa.n_expressions, 7, dtype=np.int64)
+        last = _kernels.scan_from(toy_dfa.transitions, toy_dfa.out_offsets, toy_dfa.out_ids, sym, start, end,
+                                  state, counts)
+        want, wl = O.ref_sequential_count(toy_dfa, sym, start, end, state)
+        assert counts.tolist() == (want + 7).tolist() and last == wl

@@ -16,7 +16,10 @@ w = workloads.make(3, 1 << 28)
 ctx = _native.context(0)
 sh = ctx.upload_ascii(w.ascii)
 sym = None
-for nlit, length in ((400, 12), (1000, 14), (2000, 14), (2600, 13), (6000, 14), (12000, 16)):
+sizes = [(400, 12), (1000, 14), (2000, 14), (2600, 13), (6000, 14), (12000, 16)]
+if len(sys.argv) > 1 and sys.argv[1] == "wide":   # automata above 32767 states
+    sizes = [(4000, 14), (8000, 16), (5000, 24), (12000, 20)]
+for nlit, length in sizes:
     lits = set()
     while len(lits) < nlit:
         lits.add("".join(rng.choice(list("acgt"), size=length)))
