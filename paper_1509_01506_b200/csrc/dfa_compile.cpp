@@ -264,7 +264,20 @@ int compile_dfa(const int32_t* trans, int nq, const int32_t* out_off, const int3
     h->new_of_old.assign(nq, 0);
     h->old_of_new.clear();
     int hot_lo = 0, hot_n = 0;
-    if (nq > kMaxStates) {
+    // the wide form (32-bit ids, hot table in shared memory + cold
+    // transitions from L2) above the 16-bit range, and for definite automata
+    // whose 1-base table does not fit shared memory (~22K-32K states: the
+    // 16-bit kernel would read it through L1/L2 on every step)
+    bool wide = nq > kMaxStates;
+    if (!wide && nq > 16384 && (force_strategy == 0 || force_strategy == KS_STRATEGY_LOOKBACK)) {
+        size_t acc_n = 0;
+        for (int s = 0; s < nq; ++s) acc_n += out_off[s + 1] > out_off[s];
+        if (size_t(nq) * 10 + acc_n * 4 + 4096 > smem_budget) {
+            const std::vector<uint32_t> t(trans, trans + size_t(nq) * 5);
+            wide = synchronisation_depth(t, nq) >= 0;
+        }
+    }
+    if (wide) {
         // wide automata: accepting states still first ([0, A): the hit test),
         // and the hot set -- the states nearest START (BFS depth, then id:
         // a scan of AC-like automata spends almost every step there) -- one
@@ -331,9 +344,9 @@ int compile_dfa(const int32_t* trans, int nq, const int32_t* out_off, const int3
     CompiledTable& t = h->scan;
     t.nq = nq;
     t.n_accept = h->n_accept;
-    if (nq > kMaxStates) {
+    if (wide) {
         // wide automata: 32-bit ids, definite only (every build_dfa automaton
-        // is), scanned one base at a time from the 1-base table in L1/L2
+        // is), scanned one base at a time from the hot table / L2
         if (force_strategy != 0 && force_strategy != KS_STRATEGY_LOOKBACK)
             return fail(KS_E_UNSUPPORTED, "dfa: automata above 32767 states scan with the LOOKBACK strategy only");
         h->wide = true;

@@ -321,8 +321,8 @@ __global__ void __launch_bounds__(1024, 1) scan_wide_hot_kernel(const ScanArgs a
     const size_t ht_bytes = (size_t(a.hot_n) * 8 + 15) & ~size_t(15);
     unsigned int* shist = reinterpret_cast<unsigned int*>(wh_smem + ht_bytes);
     const bool hist_smem = (MODE == kModeCount || MODE == kModeRows) && a.hist_smem;
-    for (size_t i = threadIdx.x; i < ht_bytes / 16; i += blockDim.x)
-        reinterpret_cast<uint4*>(ht)[i] = __ldg(reinterpret_cast<const uint4*>(a.ht) + i);
+    for (size_t i = threadIdx.x; i < size_t(a.hot_n); i += blockDim.x)   // 8-byte rows
+        reinterpret_cast<uint2*>(ht)[i] = __ldg(reinterpret_cast<const uint2*>(a.ht) + i);
     if (hist_smem)
         for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x) shist[i] = 0u;
     __syncthreads();
@@ -421,8 +421,8 @@ __global__ void __launch_bounds__(1024, 1) scan_wide_hot_ilp_kernel(const ScanAr
     const uint32_t H = uint32_t(a.hot_n);
     const size_t ht_bytes = (size_t(H + 1) * 8 + 15) & ~size_t(15);   // + the all-cold row H
     unsigned int* shist = reinterpret_cast<unsigned int*>(wh_smem + ht_bytes);
-    for (size_t i = threadIdx.x; i < size_t(H) * 8 / 16; i += blockDim.x)
-        reinterpret_cast<uint4*>(ht)[i] = __ldg(reinterpret_cast<const uint4*>(a.ht) + i);
+    for (size_t i = threadIdx.x; i < size_t(H); i += blockDim.x)   // 8-byte rows (H may be odd)
+        reinterpret_cast<uint2*>(ht)[i] = __ldg(reinterpret_cast<const uint2*>(a.ht) + i);
     for (size_t i = size_t(H) * 4 + threadIdx.x; i < ht_bytes / 2; i += blockDim.x) ht[i] = 0xFFFFu;
     if (HSM)
         for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x) shist[i] = 0u;

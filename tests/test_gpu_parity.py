@@ -943,3 +943,35 @@ def test_kernels_scan_from_dropin(toy_dfa):
                                   state, counts)
         want, wl = O.ref_sequential_count(toy_dfa, sym, start, end, state)
         assert counts.tolist() == (want + 7).tolist() and last == wl
+
+
+def test_mid_automaton_takes_the_wide_path():
+    """A definite automaton of ~27K states: its 16-bit 1-base table does not
+    fit shared memory, so it is compiled to the wide form (hot table in
+    shared memory, cold transitions from L2) -- counts, rows and ranges
+    against the oracle."""
+    rng = np.random.default_rng(11)
+    lits = set()
+    while len(lits) < 3000:
+        lits.add("".join(rng.choice(list("acgt"), size=14)))
+    lits = sorted(lits)
+    dfa = dfa_of("\n".join(lits))
+    assert 16384 < dfa.state_count <= 32767
+    n = 1 << 20
+    sym = rng.integers(0, 4, n).astype(np.uint8)
+    for k in range(300):
+        lit = lits[int(rng.integers(0, len(lits)))]
+        p = int(rng.integers(0, n - len(lit)))
+        sym[p:p + len(lit)] = ["acgt".index(c) for c in lit]
+    sym[rng.integers(0, n, 50)] = 4
+    ctx = _native.DeviceContext(0)
+    dh = ctx.dfa(dfa)
+    assert dh.info["strategy_name"] == "lookback" and dh.info["tables_in_smem"] == 0
+    want, rows, _ = O.ref_run(dfa, sym, 4, 10, True)
+    sh = ctx.upload_codes(sym)
+    assert ctx.count(dh, sh).tolist() == want.tolist() and want.sum() >= 300
+    got, grows = ctx.locate(dh, sh)
+    assert got.tolist() == want.tolist() and np.array_equal(grows, rows)
+    wc, wl = O.ref_sequential_count(dfa, sym[777:600_001], state=5)
+    c, last, _ = ctx.scan_range(dh, sh, 777, 600_001, 5)
+    assert c.tolist() == wc.tolist() and last == wl

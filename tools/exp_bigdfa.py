@@ -17,6 +17,8 @@ ctx = _native.context(0)
 sh = ctx.upload_ascii(w.ascii)
 sym = None
 sizes = [(400, 12), (1000, 14), (2000, 14), (2600, 13), (6000, 14), (12000, 16)]
+if len(sys.argv) > 1 and sys.argv[1] == "mid":    # 16-bit automata whose table exceeds shared memory
+    sizes = [(2800, 14), (3200, 14), (3600, 14), (3900, 14)]
 if len(sys.argv) > 1 and sys.argv[1] == "wide":   # automata above 32767 states
     sizes = [(4000, 14), (8000, 16), (5000, 24), (12000, 20)]
 for nlit, length in sizes:

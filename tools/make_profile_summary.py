@@ -12,7 +12,7 @@ from pathlib import Path
 
 REPO = Path(__file__).resolve().parents[1]
 OUT = REPO / "gpurun_out"
-ALG = {"3": 1 << 30, "4": 3_200_000_000, "5": 1 << 28}
+ALG = {"3": 1 << 30, "4": 3_200_000_000, "5": 1 << 28, "2": 1 << 26, "wide": 1 << 28}
 
 
 def launch_list(path):
@@ -83,12 +83,12 @@ def config_summary(c, d):
 if __name__ == "__main__":
     tag, rnd = sys.argv[1], int(sys.argv[2])
     out = {"round": rnd,
-           "command": "python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 [--config C]",
+           "command": "python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 --no-parity --no-others [--config C]; wide: python tools/exp_wide_one.py 4000 14",
            "note": "ncu per-launch times are cold-cache and serialised (--clock-control none); "
                    "bench.py's roofline uses CUDA-event times of the same kernel",
            "launch_list": launch_list(OUT / f"launches_{tag}.csv"), "configs": {}}
-    for c in ("3", "4", "5"):
-        p = OUT / f"raw_{tag}_c{c}.csv"
+    for c in ("3", "4", "5", "2", "wide"):
+        p = OUT / (f"raw_{tag}_{c}.csv" if c == "wide" else f"raw_{tag}_c{c}.csv")
         if p.exists():
             out["configs"][c] = config_summary(c, raw(p))
     dst = REPO / "profiles" / f"ncu_summary_r{rnd:02d}.json"
