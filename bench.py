@@ -374,19 +374,32 @@ def strong_leg(args, ctx, stream, world: int, rank: int, local: int, dev) -> dic
     from paper_1509_01506_b200 import workloads
     from paper_1509_01506_b200.distributed import shard_bounds
 
+    import shutil
+
     t0 = time.perf_counter()
     n = workloads.FULL_SIZES[4] if args.strong_bases is None else args.strong_bases
     shm = Path("/dev/shm") / f"ks_bench_c4_{os.environ.get('MASTER_PORT', 'x')}_{n}.u8"
-    if rank == 0:
+    # generated once and shared through /dev/shm when it has room; otherwise
+    # every rank draws the same seeded sequence itself
+    try:
+        shared = world > 1 and shutil.disk_usage("/dev/shm").free > n + (1 << 30)
+    except OSError:
+        shared = False
+    if world > 1:
+        flag = torch.tensor([1 if shared else 0], dtype=torch.int32, device=dev if args.dist_backend == "nccl"
+                            else torch.device("cpu"))
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)   # every rank takes the same branch
+        shared = bool(flag.item())
+    if rank == 0 or not shared:
         wl = workloads.make(4, n)
         ascii_ = wl.ascii
-        if world > 1:
+        if rank == 0 and shared:
             tmp = shm.with_suffix(".tmp")
             ascii_.tofile(tmp)
             tmp.rename(shm)
     if world > 1:
         dist.barrier()
-    if rank != 0:
+    if rank != 0 and shared:
         ascii_ = np.memmap(shm, dtype=np.uint8, mode="r", shape=(n,))
         wl = workloads.make(4, 64)          # same pattern stream -> the same automaton
     log(f"[rank {rank}] strong leg: C4 n={n} ready in {time.perf_counter() - t0:.1f}s")
@@ -470,7 +483,7 @@ def strong_leg(args, ctx, stream, world: int, rank: int, local: int, dev) -> dic
         log(f"strong: {out}")
     if world > 1:
         dist.barrier()
-        if rank == 0:
+        if rank == 0 and shared:
             shm.unlink(missing_ok=True)
     sh.free()
     return out
