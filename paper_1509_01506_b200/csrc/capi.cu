@@ -451,6 +451,7 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
                              ? reinterpret_cast<uint16_t*>(direct + size_t(std::max(h.ne, 1)) * 8 + 8)
                              : exit_slot;
         a.fin_done = reinterpret_cast<unsigned int*>(err + 1);   // zero between calls
+        a.tile_ctr = reinterpret_cast<unsigned int*>(err + 3);   // zero between calls (fast kernel)
         a.fin_host = reinterpret_cast<unsigned long long*>(direct);
         a.n_expr = h.ne;
     }

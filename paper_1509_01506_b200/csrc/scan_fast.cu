@@ -35,6 +35,7 @@
 // The lane/chunk/entry-state logic is the one of scan.cu (lookback, uniform
 // or per-chunk entry states).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "scan_kernels.cuh"
@@ -133,6 +134,22 @@ __device__ __forceinline__ uint32_t field_at(const uint4& x, int j) {
     const uint32_t hi = q == 0 ? x.y : q == 1 ? x.z : q == 2 ? x.w : 0u;
     if (r == 0) return lo;
     return __funnelshift_r(lo, hi, r);
+}
+
+// KS_KTIME=1 (diagnostic): per-phase device timestamps of the fast scan,
+// min/max over CTAs (globaltimer ns), printed by launch_scan_fast.
+__device__ unsigned long long g_ktime[10];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void kt_mark(int on, int slot, bool is_min, bool per_warp = false) {
+    if (on && (per_warp ? (threadIdx.x & 31) == 0 : threadIdx.x == 0)) {
+        const unsigned long long t = gtimer();
+        if (is_min) atomicMin(&g_ktime[slot], t);
+        else atomicMax(&g_ktime[slot], t);
+    }
 }
 
 struct Ctx {
@@ -382,6 +399,8 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     // mbarrier, while the threads clear the histogram
     __shared__ __align__(8) unsigned long long tables_ready;
     const uint32_t mbar = smem_addr(&tables_ready);
+    kt_mark(a.ktime, 0, true);
+    kt_mark(a.ktime, 1, false);
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -409,6 +428,8 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     }
     mbar_wait_parity0(mbar);
     __syncthreads();
+    kt_mark(a.ktime, 2, true);
+    kt_mark(a.ktime, 3, false);
 
     Ctx c;
     c.tk = smem_addr(f_smem);
@@ -442,12 +463,47 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     const int64_t t1 = (u0 + a.nchunks - 1) >> 5;
     const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
     constexpr unsigned am = 0xffffffffu;
-    for (int64_t t = t0 + ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); t <= t1; t += nwarps) {
+    // Work items.  Static: warp w takes tiles t0 + w, t0 + w + nwarps, ...
+    // Dynamic (count mode with a tile counter): items are whole tiles, then
+    // the last split_tiles tiles cut into split_parts block ranges (lane
+    // chunks entered by lookback mid-unit, so the tail is a fraction of a
+    // tile); items below static_items go round-robin, the rest come from
+    // the counter (fetched one item ahead) -- faster SMs take more of the
+    // last rounds.
+    const bool dyn = MODE == kModeCount && a.tile_ctr != nullptr;
+    const int64_t ntiles = t1 - t0 + 1;
+    const int64_t whole = dyn ? ntiles - a.split_tiles : ntiles;
+    const int64_t n_items = dyn ? whole + int64_t(a.split_tiles) * a.split_parts : ntiles;
+    const int ublocks = int(a.chunk_len >> 6);
+    const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    int64_t item = wid;
+    for (; item < n_items;) {
+        int64_t next = item + nwarps;
+        if (dyn && next >= a.static_items) {
+            unsigned int g = 0;
+            if (lane == 0) g = atomicAdd(a.tile_ctr, 1u);
+            next = a.static_items + int64_t(__shfl_sync(am, g, 0));
+        }
+        int64_t t;
+        int pl = 0, ph = ublocks;   // blocks [pl, ph) of each lane's unit
+        if (item < whole) {
+            t = t0 + item;
+        } else {
+            const int64_t j = item - whole;
+            t = t0 + whole + j / a.split_parts;
+            const int q = int(j % a.split_parts);
+            pl = q * ublocks / a.split_parts;
+            ph = (q + 1) * ublocks / a.split_parts;
+        }
         const int64_t u = (t << 5) + lane;
         const int64_t ch = u - u0;
-        const bool active = ch >= 0 && ch < a.nchunks;
-        const int64_t cb = active ? max64(a.begin, u * a.chunk_len) : 0;
-        const int64_t ce = active ? min64(a.end, (u + 1) * a.chunk_len) : 0;
+        const int64_t cend = min64(a.end, (u + 1) * a.chunk_len);   // the chunk's end
+        const int64_t cb0 = max64(a.begin, u * a.chunk_len + (int64_t(pl) << 6));
+        const int64_t ce0 = ph == ublocks ? cend : min64(cend, u * a.chunk_len + (int64_t(ph) << 6));
+        const bool active = ch >= 0 && ch < a.nchunks && cb0 < ce0;
+        const int64_t cb = active ? cb0 : 0;
+        const int64_t ce = active ? ce0 : 0;
+        item = next;
 
         uint32_t s = idle;
         if (!active) {
@@ -602,7 +658,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
             if constexpr (MODE == kModeMap) {
                 if (dirty) s = __ldg(&a.map_dirty[s]);
             }
-            if (a.chunk_exit) a.chunk_exit[ch] = uint16_t(s);
+            if (a.chunk_exit && ce == cend) a.chunk_exit[ch] = uint16_t(s);
             if constexpr (MODE == kModeRows || MODE == kModeLog) a.chunk_rows[ch] = L.nrows;
             if constexpr (MODE == kModeEmit) {
                 if (L.cur != a.chunk_row_off[ch + 1]) atomicExch(a.error, 1);
@@ -610,6 +666,8 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
         }
     }
 
+    kt_mark(a.ktime, 4, true, true);
+    kt_mark(a.ktime, 5, false, true);
     if constexpr (MODE == kModeCount) {   // the ring's leftovers
         Lane<MODE> L;
         drain<K, MODE>(c, L, am, rp0, rp, ring_stride);
@@ -619,6 +677,9 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
         for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x)
             if (s_hist[i]) atomicAdd(&a.visits[i], (unsigned long long)s_hist[i]);
     }
+    __syncthreads();
+    kt_mark(a.ktime, 6, true);
+    kt_mark(a.ktime, 7, false);
     if constexpr (MODE == kModeCount) {
         if (a.fin_counts) {   // fused finalize: the last CTA to finish converts visits to counts
             __shared__ unsigned int is_last;
@@ -648,7 +709,11 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                     if (in_smem) a.fin_counts[e] = v;
                     if (a.fin_host) a.fin_host[e] = v;   // pinned host memory: visible once the kernel completes
                 }
-                if (threadIdx.x == 0) *a.fin_done = 0u;
+                if (threadIdx.x == 0) {
+                    *a.fin_done = 0u;
+                    if (a.tile_ctr) *a.tile_ctr = 0u;   // every item has been taken
+                }
+                kt_mark(a.ktime, 8, false);
             }
         }
     }
@@ -786,6 +851,34 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
     // 4096 tiles: 28 warps x 148 = 4144 slots, one round, instead of 128
     // CTAs with 20 SMs idle); the shared-memory layout stays the 1024-thread one
     const int warps = fast_warps_per_cta(tiles, ctx->num_sms);
+    // dynamic work items (count mode, fused finalize: its last CTA resets the
+    // counter); the last round of tiles is cut into block ranges when lane
+    // chunks are entered by lookback (per-chunk or uniform entry states hold
+    // only at chunk starts)
+    // (three or more rounds of tiles: below that the counter's first fetches
+    // come in one burst with nothing to hide them, C1/C2 lose 5-20%)
+    const int64_t nw = int64_t(warps) * std::max<int64_t>(1, std::min<int64_t>((tiles + warps - 1) / warps,
+                                                                               ctx->num_sms));
+    if (mode == kModeCount && a.fin_counts && a.tile_ctr && tiles > 2 * nw &&
+        !(std::getenv("KS_STATIC_TILES") && *std::getenv("KS_STATIC_TILES") == '1')) {
+        const int ub = int(a.chunk_len >> 6);
+        const bool entered_by_lookback = !a.chunk_entry && a.uniform_entry < 0;
+        int parts = entered_by_lookback ? std::min(ub, 2) : 1;
+        if (const char* e = std::getenv("KS_SPLIT_PARTS"); e && *e && entered_by_lookback)
+            parts = std::max(1, std::min(ub, std::atoi(e)));
+        a.split_parts = parts;
+        a.split_tiles = parts > 1 ? int32_t(std::min<int64_t>(tiles, nw)) : 0;
+        // round-robin for all but the last two rounds of items
+        const int64_t items = tiles - a.split_tiles + int64_t(a.split_tiles) * parts;
+        a.static_items = std::max<int64_t>(nw, (items / nw - 2) * nw);
+    } else {
+        a.tile_ctr = nullptr;
+    }
+    if (const char* e = std::getenv("KS_KTIME"); e && *e == '1') {
+        unsigned long long h[10] = {~0ull, 0, ~0ull, 0, ~0ull, 0, ~0ull, 0, 0, 0};
+        KS_CUDA(cudaMemcpyToSymbolAsync(g_ktime, h, sizeof(h), 0, cudaMemcpyHostToDevice, ctx->stream));
+        a.ktime = 1;
+    }
     const int64_t need = (tiles + warps - 1) / warps;
     const int blocks = int(max64(1, min64(need, int64_t(ctx->num_sms))));
     if constexpr (KS_PDL) {
@@ -810,6 +903,16 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
     }
     if (launches) ++*launches;
     KS_CUDA(cudaGetLastError());
+    if (a.ktime) {
+        unsigned long long h[10];
+        KS_CUDA(cudaStreamSynchronize(ctx->stream));
+        KS_CUDA(cudaMemcpyFromSymbol(h, g_ktime, sizeof(h)));
+        auto us = [&](int i) { return h[i] ? (double(h[i]) - double(h[0])) * 1e-3 : -1.0; };
+        std::fprintf(stderr,
+                     "[ks ktime] grid %d x %d: CTA start 0..%.2f | tables ready %.2f..%.2f | warp scan end "
+                     "%.2f..%.2f | CTA flushed %.2f..%.2f | finalized %.2f us\n",
+                     blocks, warps * 32, us(1), us(2), us(3), us(4), us(5), us(6), us(7), us(8));
+    }
     return KS_OK;
 }
 

@@ -99,6 +99,12 @@ struct ScanArgs {
     int64_t log_cap = 0;
     unsigned int* work_ctr = nullptr;       // wide count kernel: task counter (zeroed per launch)
     int32_t run_blocks = 0;                 // wide count kernel: blocks per run
+    // fast kernel, count mode: dynamic work items (tile counter zero at
+    // launch, reset by the finalizing CTA; only with fin_counts)
+    unsigned int* tile_ctr = nullptr;
+    int32_t split_tiles = 0, split_parts = 1;
+    int64_t static_items = 0;               // items below this go round-robin
+    int32_t ktime = 0;                      // fast kernel: per-phase timestamps (KS_KTIME=1, diagnostic)
 };
 
 inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }

@@ -975,3 +975,35 @@ def test_mid_automaton_takes_the_wide_path():
     wc, wl = O.ref_sequential_count(dfa, sym[777:600_001], state=5)
     c, last, _ = ctx.scan_range(dh, sh, 777, 600_001, 5)
     assert c.tolist() == wc.tolist() and last == wl
+
+
+@pytest.mark.parametrize("config", [3, 4])
+def test_dynamic_tiles_and_split_tails(monkeypatch, config):
+    """Count-mode work items beyond two rounds come from a device counter and
+    the last round is cut into block ranges entered by lookback mid-chunk
+    (scan_fast.cu): every split (1, 2, 4 parts) and the static round-robin
+    give the oracle's counts, whole sequence and unaligned ranges from an
+    explicit entry state."""
+    monkeypatch.setenv("KS_TILE_LB", "2")   # 256-base units: > 2 rounds of tiles at this size
+    w = workloads.make(config, 100_000_037)
+    codes = ks.encode_bytes(w.ascii.tobytes())
+    want = O.ref_run(w.dfa, codes, 16, 10, False)[0]
+    rng = np.random.default_rng(config)
+    ranges = []
+    for _ in range(3):
+        b, e = sorted(rng.integers(0, codes.size, 2).tolist())
+        entry = int(rng.integers(0, w.dfa.state_count))
+        ranges.append((b, e, entry, *O.ref_sequential_count(w.dfa, codes, b, e, entry)))
+    c2 = _native.DeviceContext(0)
+    dh = c2.dfa(w.dfa)
+    sh = c2.upload_codes(codes)
+    for env in ({"KS_STATIC_TILES": "1"}, {"KS_SPLIT_PARTS": "1"}, {"KS_SPLIT_PARTS": "2"},
+                {"KS_SPLIT_PARTS": "4"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        assert c2.count(dh, sh).tolist() == want.tolist(), env
+        for b, e, entry, w2, last in ranges:
+            g2, ex, _ = c2.scan_range(dh, sh, b, e, entry)
+            assert g2.tolist() == w2.tolist() and ex == last, (env, b, e)
+        for k in env:
+            monkeypatch.delenv(k)
