@@ -36,6 +36,7 @@
 // or per-chunk entry states).
 #include <algorithm>
 #include <cstdio>
+#include <vector>
 #include <cstdlib>
 
 #include "scan_kernels.cuh"
@@ -139,6 +140,7 @@ __device__ __forceinline__ uint32_t field_at(const uint4& x, int j) {
 // KS_KTIME=1 (diagnostic): per-phase device timestamps of the fast scan,
 // min/max over CTAs (globaltimer ns), printed by launch_scan_fast.
 __device__ unsigned long long g_ktime[10];
+__device__ unsigned long long g_kcta[1024];   // KS_KTIME=2: per CTA: smid << 48 | (flush time - kernel-wide min start) ns
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -680,6 +682,11 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     __syncthreads();
     kt_mark(a.ktime, 6, true);
     kt_mark(a.ktime, 7, false);
+    if (a.ktime == 2 && threadIdx.x == 0 && blockIdx.x < 1024) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_kcta[blockIdx.x] = (static_cast<unsigned long long>(smid) << 48) | (gtimer() & 0xFFFFFFFFFFFFull);
+    }
     if constexpr (MODE == kModeCount) {
         if (a.fin_counts) {   // fused finalize: the last CTA to finish converts visits to counts
             __shared__ unsigned int is_last;
@@ -874,10 +881,10 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
     } else {
         a.tile_ctr = nullptr;
     }
-    if (const char* e = std::getenv("KS_KTIME"); e && *e == '1') {
+    if (const char* e = std::getenv("KS_KTIME"); e && (*e == '1' || *e == '2')) {
         unsigned long long h[10] = {~0ull, 0, ~0ull, 0, ~0ull, 0, ~0ull, 0, 0, 0};
         KS_CUDA(cudaMemcpyToSymbolAsync(g_ktime, h, sizeof(h), 0, cudaMemcpyHostToDevice, ctx->stream));
-        a.ktime = 1;
+        a.ktime = *e - '0';
     }
     const int64_t need = (tiles + warps - 1) / warps;
     const int blocks = int(max64(1, min64(need, int64_t(ctx->num_sms))));
@@ -912,6 +919,15 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
                      "[ks ktime] grid %d x %d: CTA start 0..%.2f | tables ready %.2f..%.2f | warp scan end "
                      "%.2f..%.2f | CTA flushed %.2f..%.2f | finalized %.2f us\n",
                      blocks, warps * 32, us(1), us(2), us(3), us(4), us(5), us(6), us(7), us(8));
+        if (a.ktime == 2) {
+            std::vector<unsigned long long> c(size_t(std::min(blocks, 1024)));
+            KS_CUDA(cudaMemcpyFromSymbol(c.data(), g_kcta, c.size() * 8));
+            std::fprintf(stderr, "[ks ktime cta] smid:us");
+            for (size_t i = 0; i < c.size(); ++i)
+                std::fprintf(stderr, " %u:%.1f", unsigned(c[i] >> 48),
+                             (double(c[i] & 0xFFFFFFFFFFFFull) - double(h[0] & 0xFFFFFFFFFFFFull)) * 1e-3);
+            std::fprintf(stderr, "\n");
+        }
     }
     return KS_OK;
 }
