@@ -260,7 +260,7 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
-def time_steps(ctx, step, stream, steps: int, flush, local: int, sync_each=None):
+def time_steps(ctx, step, stream, steps: int, flush, local: int, sync_each=None, finish=None):
     """Time `steps` back-to-back steps with CUDA events on the library's
     stream (inputs that fit in L2: a flush before each step, steps timed one
     by one).  Returns (ms total, clocks summary, launches)."""
@@ -282,11 +282,60 @@ def time_steps(ctx, step, stream, steps: int, flush, local: int, sync_each=None)
             step()
             if flush is not None:
                 step_ev[i][1].record(stream)
+        if finish is not None:
+            finish()   # e.g. the stream waits for the last in-flight collectives
         ev1.record(stream)
         waited = ctx.async_wait()
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) if flush is None else sum(a.elapsed_time(b) for a, b in step_ev)
     return ms, clocks.summary(), waited["kernel_launches"]
+
+
+class PipelinedAllReduce:
+    """The per-step NCCL all-reduce of a step's counts overlapped with the next
+    step's scan: two count buffers; step i's all-reduce runs asynchronously on
+    NCCL's stream while step i + 1 scans into the other buffer (the scan grid
+    leaves RESERVED_SMS SMs free for NCCL's kernel -- a scan CTA fills its SM).
+    Before a buffer is reused the stream waits for its all-reduce and copies
+    that step's reduced counts to pinned host memory; finish() drains both."""
+
+    RESERVED_SMS = 2
+
+    def __init__(self, ne: int, dev, out_pin):
+        import torch
+
+        self.bufs = [torch.zeros(max(ne, 1), dtype=torch.int64, device=dev) for _ in range(2)]
+        self.work = [None, None]
+        self.order = []
+        self.out_pin = out_pin
+
+    def acquire(self):
+        import torch  # noqa: F401
+
+        b = len(self.order) % 2
+        if self.work[b] is not None:
+            self._retire(b)
+        return self.bufs[b]
+
+    def launch(self, buf) -> None:
+        import torch.distributed as dist
+
+        b = 0 if buf is self.bufs[0] else 1
+        self.work[b] = dist.all_reduce(buf, async_op=True)
+        self.order.append(b)
+
+    def _retire(self, b: int) -> None:
+        self.work[b].wait()          # the current stream waits for the collective
+        self.out_pin.copy_(self.bufs[b], non_blocking=True)
+        self.work[b] = None
+
+    def finish(self) -> None:
+        for b in self.order[-2:]:    # older step first: out_pin ends with the last step
+            if self.work[b] is not None:
+                self._retire(b)
+
+    def last(self):
+        return self.bufs[self.order[-1]] if self.order else self.bufs[0]
 
 
 def kernel_ms(ctx, dh, sh, flush, reps: int = 5, scan=None) -> float:
@@ -412,29 +461,40 @@ def strong_leg(args, ctx, stream, world: int, rank: int, local: int, dev) -> dic
     sh = ctx.upload_ascii(np.ascontiguousarray(ascii_[lo - hl:hi]))
     counts_dev = torch.zeros(ne, dtype=torch.int64, device=dev)
     cdev = dev if args.dist_backend == "nccl" else torch.device("cpu")
+    pipe = None
+    if world > 1 and args.dist_backend == "nccl":
+        pipe = PipelinedAllReduce(ne, dev, torch.zeros(max(ne, 1), dtype=torch.int64).pin_memory())
 
     def step():
+        if pipe is not None:   # scan into one buffer while the other's all-reduce runs
+            buf = pipe.acquire()
+            ctx.count_shard_async(dh, sh, hl, hl + hi - lo, 0, rank, buf.data_ptr())
+            pipe.launch(buf)
+            return
         ctx.count_shard_async(dh, sh, hl, hl + hi - lo, 0, rank, counts_dev.data_ptr())
         if world > 1:
-            if args.dist_backend == "nccl":
-                dist.all_reduce(counts_dev)
-            else:
-                c = counts_dev.cpu()
-                dist.all_reduce(c)
+            c = counts_dev.cpu()
+            dist.all_reduce(c)
 
     for _ in range(args.warmup):
         step()
+    if pipe is not None:
+        pipe.finish()
     ctx.async_wait()
     torch.cuda.synchronize()
     ms, clocks, launches = time_steps(ctx, step, stream, args.steps, None, local,
-                                      sync_each=(dist.barrier if world > 1 else None))
+                                      sync_each=(dist.barrier if world > 1 else None),
+                                      finish=(pipe.finish if pipe is not None else None))
     t = torch.tensor([ms], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_n = float(t[0]) / args.steps
     # counts of this step + rows of this shard (global offsets, rank order)
-    if world > 1 and args.dist_backend == "nccl":
-        counts = counts_dev.cpu().numpy()
+    if pipe is not None:
+        torch.cuda.synchronize()
+        counts = pipe.last().cpu().numpy()[:ne]
+        if not np.array_equal(counts, pipe.out_pin.numpy()[:ne]):
+            raise RuntimeError("strong leg: pinned result differs from the last reduced counts")
     else:
         counts_dev.zero_()
         ctx.count_shard_async(dh, sh, hl, hl + hi - lo, 0, rank, counts_dev.data_ptr())
@@ -452,7 +512,9 @@ def strong_leg(args, ctx, stream, world: int, rank: int, local: int, dev) -> dic
     out = None
     if rank == 0:
         rows_all = np.concatenate(gathered) if gathered else np.empty((0, 2), np.int64)
-        # the 1-GPU reference point: the whole C4 on this GPU
+        # the 1-GPU reference point: the whole C4 on this GPU, all SMs
+        if pipe is not None:
+            ctx.set_reserved_sms(0)
         full = ctx.upload_ascii(np.ascontiguousarray(ascii_))
         one = torch.zeros(max(ne, 1), dtype=torch.int64).pin_memory()
         one_np = one.numpy()
@@ -472,7 +534,10 @@ def strong_leg(args, ctx, stream, world: int, rank: int, local: int, dev) -> dic
                "value": n / (ms_n / 1e3) / 1e9, "unit": UNIT,
                "one_gpu_ms_per_step": ms1, "speedup_vs_1": ms1 / ms_n,
                "step": ("scan of each rank's contiguous shard from its halo's lookback (ks_count_shard_async) "
-                        "+ NCCL all-reduce of the int64 counts; events per rank, max over ranks"),
+                        "+ NCCL all-reduce of the int64 counts"
+                        + (", overlapped with the next step's scan (two count buffers; the scan grid leaves "
+                           f"{PipelinedAllReduce.RESERVED_SMS} SMs to NCCL)" if pipe is not None else "")
+                        + "; events per rank, max over ranks"),
                "halo_bases": H, "clocks_rank0": clocks, "gpu_launches_rank0": launches,
                "parity": {"oracle": ORACLE_NAME, "counts_equal_oracle": bool(np.array_equal(counts, want)),
                           "counts_equal_1gpu": bool(np.array_equal(counts, c1[:ne])),
@@ -480,6 +545,8 @@ def strong_leg(args, ctx, stream, world: int, rank: int, local: int, dev) -> dic
                           "rows_equal_1gpu": bool(np.array_equal(rows_all, rows1)),
                           "rows": int(rows_all.shape[0]), "oracle_s": round(o_s, 3)}}
         full.free()
+        if pipe is not None:
+            ctx.set_reserved_sms(PipelinedAllReduce.RESERVED_SMS)
         log(f"strong: {out}")
     if world > 1:
         dist.barrier()
@@ -523,6 +590,9 @@ def run_ours(args) -> None:
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
+    if world > 1 and args.dist_backend == "nccl":
+        # the per-step all-reduce overlaps the next scan on SMs the scan leaves free
+        ctx.set_reserved_sms(PipelinedAllReduce.RESERVED_SMS)
     dh = ctx.dfa(wl.dfa, strategy={"auto": 0, "lookback": 1, "mapscan": 2, "speculate": 3}[args.strategy])
     ascii_host = torch.from_numpy(wl.ascii).pin_memory()
     sh = ctx.upload_ascii(ascii_host.numpy())        # resident packed sequence
@@ -552,16 +622,19 @@ def run_ours(args) -> None:
         halo_len = int(prev_tail.size)
         sh_halo = ctx.upload_ascii(np.concatenate([prev_tail, wl.ascii]))
 
+    pipe_main = (PipelinedAllReduce(ne, dev, out_pin) if halo_mode and args.dist_backend == "nccl" else None)
+
     def step() -> None:
         if world == 1:  # enqueue only: one scan kernel that writes the counts into pinned host memory
             ctx.count_async(dh, sh, out_np)
             return
         if halo_mode:   # scan from the halo's lookback -> all-reduce of the counts
-            ctx.count_shard_async(dh, sh_halo, halo_len, halo_len + n, 0, rank, counts_dev.data_ptr())
-            if args.dist_backend == "nccl":
-                dist.all_reduce(counts_dev)
-                out_pin.copy_(counts_dev, non_blocking=True)
+            if pipe_main is not None:   # overlapped with the next step's scan
+                buf = pipe_main.acquire()
+                ctx.count_shard_async(dh, sh_halo, halo_len, halo_len + n, 0, rank, buf.data_ptr())
+                pipe_main.launch(buf)
             else:   # gloo dry run: the reduction on host tensors
+                ctx.count_shard_async(dh, sh_halo, halo_len, halo_len + n, 0, rank, counts_dev.data_ptr())
                 c = counts_dev.cpu()
                 dist.all_reduce(c)
                 out_np[:] = c.numpy()
@@ -595,7 +668,10 @@ def run_ours(args) -> None:
     scan_ms_sum = [0.0]
     for _ in range(args.warmup):
         step()
+    if pipe_main is not None:
+        pipe_main.finish()
     ctx.async_wait()
+    torch.cuda.synchronize()
     ref_counts = out_np[:ne].copy()
     if world > 1 and (args.dist_backend == "nccl" or halo_mode):
         # the device-side step (halo or device-composed maps) must equal the
@@ -610,7 +686,8 @@ def run_ours(args) -> None:
     flush_buf = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     flush = flush_buf if packed_bytes < L2_FLUSH_BYTES else None
     ms, clocks, waited_launches = time_steps(ctx, step, stream, args.steps, flush, local,
-                                             sync_each=(dist.barrier if world > 1 else None))
+                                             sync_each=(dist.barrier if world > 1 else None),
+                                             finish=(pipe_main.finish if pipe_main is not None else None))
     if world == 1 or args.dist_backend == "nccl" or halo_mode:
         launches[0] = waited_launches
         # the timed async calls carry no events (they would sit between the

@@ -79,6 +79,11 @@ KS_API int ks_close(ks_ctx* ctx);
 /* Use an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);
  * NULL restores the context's own stream. */
 KS_API int ks_set_stream(ks_ctx* ctx, void* cuda_stream);
+/* Size the scan grids for (SM count - n_sms) SMs, leaving n_sms free for
+ * kernels on other streams (an NCCL collective overlapping the next scan: a
+ * scan CTA fills its SM's shared memory and registers).  0 restores the
+ * default; KS_RESERVE_SMS sets the initial value at ks_open. */
+KS_API int ks_set_reserved_sms(ks_ctx* ctx, int32_t n_sms);
 KS_API int ks_synchronize(ks_ctx* ctx);
 KS_API int ks_get_stats(const ks_ctx* ctx, ks_stats* out);
 KS_API const char* ks_last_error(void);

@@ -55,7 +55,7 @@ class Stats(C.Structure):
 
 
 EXPORTED = (
-    "ks_open", "ks_close", "ks_set_stream", "ks_synchronize", "ks_get_stats", "ks_last_error",
+    "ks_open", "ks_close", "ks_set_stream", "ks_set_reserved_sms", "ks_synchronize", "ks_get_stats", "ks_last_error",
     "ks_version", "ks_dfa_upload", "ks_dfa_upload_ex", "ks_dfa_info_get", "ks_dfa_free",
     "ks_seq_upload_codes", "ks_seq_upload_ascii", "ks_seq_encode_device", "ks_seq_length",
     "ks_seq_download_codes", "ks_seq_download_softmask", "ks_seq_free", "ks_count", "ks_locate",
@@ -81,6 +81,7 @@ def _declare(lib) -> None:
         "ks_open": (C.c_int, [C.c_int, C.POINTER(_P)]),
         "ks_close": (C.c_int, [_P]),
         "ks_set_stream": (C.c_int, [_P, _P]),
+        "ks_set_reserved_sms": (C.c_int, [_P, C.c_int32]),
         "ks_synchronize": (C.c_int, [_P]),
         "ks_get_stats": (C.c_int, [_P, C.POINTER(Stats)]),
         "ks_last_error": (C.c_char_p, []),
@@ -313,6 +314,10 @@ class DeviceContext:
     # ------------------------------------------------------------------ scans
     def set_stream(self, stream_ptr: int | None) -> None:
         _check(library().ks_set_stream(self.handle, _P(stream_ptr or 0)))
+
+    def set_reserved_sms(self, n_sms: int) -> None:
+        """Leave n_sms SMs free of scan CTAs (for kernels on other streams)."""
+        _check(library().ks_set_reserved_sms(self.handle, int(n_sms)))
 
     def synchronize(self) -> None:
         _check(library().ks_synchronize(self.handle))

@@ -695,7 +695,10 @@ int ks_open(int device, ks_ctx** out) {
         delete c;
         return fail(KS_E_UNSUPPORTED, "kmerscan_b200 requires an sm_100 (Blackwell) device");
     }
-    c->num_sms = prop.multiProcessorCount;
+    c->sms_total = prop.multiProcessorCount;
+    c->num_sms = c->sms_total;
+    if (const char* r = std::getenv("KS_RESERVE_SMS"); r && *r)
+        c->num_sms = std::max(1, c->sms_total - std::max(0, std::atoi(r)));
     c->l2_persist_max = size_t(prop.persistingL2CacheMaxSize);
     c->smem_optin = prop.sharedMemPerBlockOptin;
     e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
@@ -765,6 +768,14 @@ int ks_set_stream(ks_ctx* ctx, void* stream) {
         KS_CUDA(cudaStreamWaitEvent(next, ctx->ev[0], 0));
         ctx->stream = next;
     }
+    return KS_OK;
+}
+
+int ks_set_reserved_sms(ks_ctx* ctx, int32_t n_sms) {
+    CtxLock lock_(ctx);
+    if (!ctx) return fail(KS_E_INVALID, "null context");
+    if (n_sms < 0 || n_sms >= ctx->sms_total) return fail(KS_E_INVALID, "reserved SMs out of range");
+    ctx->num_sms = ctx->sms_total - n_sms;
     return KS_OK;
 }
 

@@ -145,7 +145,8 @@ __device__ __forceinline__ uint32_t seq_sym(const SeqView& q, int64_t p) {
 struct ks_ctx {
     std::recursive_mutex mu;   // public calls on one context are serialised (CtxLock)
     int device = 0;
-    int num_sms = 148;
+    int num_sms = 148;          // SMs the grids are sized for (sms_total - reserved)
+    int sms_total = 148;
     size_t smem_optin = 0;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;

@@ -1007,3 +1007,52 @@ def test_dynamic_tiles_and_split_tails(monkeypatch, config):
             assert g2.tolist() == w2.tolist() and ex == last, (env, b, e)
         for k in env:
             monkeypatch.delenv(k)
+
+
+def test_pipelined_allreduce_single_rank_nccl():
+    """bench.py's overlapped per-step all-reduce (PipelinedAllReduce: two count
+    buffers, async NCCL collective, the stream waits before a buffer is
+    reused) on a one-rank NCCL group with the scan grid leaving SMs free
+    (ks_set_reserved_sms): every step's counts reach the pinned buffer."""
+    import socket
+
+    import torch.distributed as dist
+
+    import bench as B
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dev = torch.device("cuda", 0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1, device_id=dev)
+    prev = torch.cuda.current_stream()
+    try:
+        c2 = _native.DeviceContext(0)
+        stream = torch.cuda.Stream(dev)
+        torch.cuda.set_stream(stream)
+        c2.set_stream(stream.cuda_stream)
+        with pytest.raises(ValueError):
+            c2.set_reserved_sms(10_000)
+        c2.set_reserved_sms(B.PipelinedAllReduce.RESERVED_SMS)
+        w = workloads.make(3, 3_000_017)
+        codes = ks.encode_bytes(w.ascii.tobytes())
+        want = O.ref_sequential_count(w.dfa, codes)[0]
+        dh = c2.dfa(w.dfa)
+        sh = c2.upload_codes(codes)
+        ne = w.dfa.n_expressions
+        pin = torch.zeros(max(ne, 1), dtype=torch.int64).pin_memory()
+        pipe = B.PipelinedAllReduce(ne, dev, pin)
+        for _ in range(7):
+            buf = pipe.acquire()
+            c2.count_shard_async(dh, sh, 0, codes.size, 0, 0, buf.data_ptr())
+            pipe.launch(buf)
+        pipe.finish()
+        c2.async_wait()
+        torch.cuda.synchronize()
+        assert pin.numpy()[:ne].tolist() == want.tolist()
+        assert pipe.last().cpu().numpy()[:ne].tolist() == want.tolist()
+        c2.set_reserved_sms(0)
+        assert c2.count(dh, sh).tolist() == want.tolist()
+    finally:
+        torch.cuda.set_stream(prev)
+        dist.destroy_process_group()
