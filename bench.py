@@ -296,8 +296,9 @@ class PipelinedAllReduce:
     step's scan: two count buffers; step i's all-reduce runs asynchronously on
     NCCL's stream while step i + 1 scans into the other buffer (the scan grid
     leaves RESERVED_SMS SMs free for NCCL's kernel -- a scan CTA fills its SM).
-    Before a buffer is reused the stream waits for its all-reduce and copies
-    that step's reduced counts to pinned host memory; finish() drains both."""
+    Before a buffer is reused the stream waits for its all-reduce (an event
+    wait, no copy on the scan stream); finish() drains both and copies the
+    last step's reduced counts to pinned host memory."""
 
     RESERVED_SMS = 2
 
@@ -326,13 +327,14 @@ class PipelinedAllReduce:
 
     def _retire(self, b: int) -> None:
         self.work[b].wait()          # the current stream waits for the collective
-        self.out_pin.copy_(self.bufs[b], non_blocking=True)
         self.work[b] = None
 
     def finish(self) -> None:
-        for b in self.order[-2:]:    # older step first: out_pin ends with the last step
+        for b in self.order[-2:]:
             if self.work[b] is not None:
                 self._retire(b)
+        if self.order:
+            self.out_pin.copy_(self.last(), non_blocking=True)
 
     def last(self):
         return self.bufs[self.order[-1]] if self.order else self.bufs[0]
