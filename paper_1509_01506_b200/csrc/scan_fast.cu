@@ -420,13 +420,21 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     }
     if constexpr (HIST)
         for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x) s_hist[i] = 0u;
+    // Launched with programmatic stream serialisation: let the next kernel of
+    // the stream start as our CTAs retire, and wait for the previous one only
+    // before touching memory it may still use -- nothing above reads memory a
+    // preceding kernel writes (the tables come from a synchronous upload).
+    // A fused count whose chunks are entered by lookback from constants reads
+    // only the sequence and the tables while it scans, so it defers the wait
+    // to the first write of state shared between calls (chunk exits, the
+    // work counter, the visit flush): its CTAs scan while the previous
+    // call's last CTA still finalizes and its other CTAs drain.
+    const bool late_wait = KS_PDL && MODE == kModeCount && a.fin_counts && !a.chunk_entry && !a.base_state_ptr &&
+                           a.uniform_entry < 0 && !a.early_wait;
+    bool waited = !late_wait;
     if constexpr (KS_PDL) {
-        // launched with programmatic stream serialisation: let the next
-        // kernel of the stream start its own prologue as our CTAs retire, and
-        // wait for the previous one only now -- nothing above reads memory a
-        // preceding kernel writes (the tables come from a synchronous upload)
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-        asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (!late_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
     }
     mbar_wait_parity0(mbar);
     __syncthreads();
@@ -483,6 +491,10 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
         int64_t next = item + nwarps;
         if (dyn && next >= a.static_items) {
             unsigned int g = 0;
+            if (!waited) {
+                asm volatile("griddepcontrol.wait;" ::: "memory");
+                waited = true;
+            }
             if (lane == 0) g = atomicAdd(a.tile_ctr, 1u);
             next = a.static_items + int64_t(__shfl_sync(am, g, 0));
         }
@@ -660,6 +672,10 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
             if constexpr (MODE == kModeMap) {
                 if (dirty) s = __ldg(&a.map_dirty[s]);
             }
+            if (!waited) {
+                asm volatile("griddepcontrol.wait;" ::: "memory");
+                waited = true;
+            }
             if (a.chunk_exit && ce == cend) a.chunk_exit[ch] = uint16_t(s);
             if constexpr (MODE == kModeRows || MODE == kModeLog) a.chunk_rows[ch] = L.nrows;
             if constexpr (MODE == kModeEmit) {
@@ -674,6 +690,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
         Lane<MODE> L;
         drain<K, MODE>(c, L, am, rp0, rp, ring_stride);
     }
+    if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
     if constexpr (HIST) {
         __syncthreads();
         for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x)
@@ -858,6 +875,7 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
     // 4096 tiles: 28 warps x 148 = 4144 slots, one round, instead of 128
     // CTAs with 20 SMs idle); the shared-memory layout stays the 1024-thread one
     const int warps = fast_warps_per_cta(tiles, ctx->num_sms);
+    if (const char* e = std::getenv("KS_EARLY_WAIT"); e && *e == '1') a.early_wait = 1;
     // dynamic work items (count mode, fused finalize: its last CTA resets the
     // counter); the last round of tiles is cut into block ranges when lane
     // chunks are entered by lookback (per-chunk or uniform entry states hold

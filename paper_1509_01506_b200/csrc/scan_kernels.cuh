@@ -104,6 +104,7 @@ struct ScanArgs {
     unsigned int* tile_ctr = nullptr;
     int32_t split_tiles = 0, split_parts = 1;
     int64_t static_items = 0;               // items below this go round-robin
+    int32_t early_wait = 0;                 // fast kernel: wait for the preceding kernel up front (KS_EARLY_WAIT=1)
     int32_t ktime = 0;                      // fast kernel: per-phase timestamps (KS_KTIME=1, diagnostic)
 };
 
