@@ -429,8 +429,10 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     // to the first write of state shared between calls (chunk exits, the
     // work counter, the visit flush): its CTAs scan while the previous
     // call's last CTA still finalizes and its other CTAs drain.
-    const bool late_wait = KS_PDL && MODE == kModeCount && a.fin_counts && !a.chunk_entry && !a.base_state_ptr &&
-                           a.uniform_entry < 0 && !a.early_wait;
+    // (the map pass of MAPSCAN likewise: every chunk starts from the identity)
+    const bool late_wait = KS_PDL && !a.early_wait && !a.chunk_entry && !a.base_state_ptr &&
+                           ((MODE == kModeCount && a.fin_counts && a.uniform_entry < 0) ||
+                            (MODE == kModeMap && a.uniform_entry >= 0));
     bool waited = !late_wait;
     if constexpr (KS_PDL) {
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
