@@ -10,6 +10,7 @@ import os
 import statistics
 
 import numpy as np
+import torch
 import sys
 from pathlib import Path
 
@@ -24,6 +25,7 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--n", type=int, default=0)
     ap.add_argument("--reps", type=int, default=7)
+    ap.add_argument("--flush", action="store_true", help="write 256 MiB before every timed call (L2 flush)")
     ap.add_argument("variants", nargs="*", default=["base"])
     args = ap.parse_args()
     w = workloads.make(args.config, args.n or None)
@@ -31,6 +33,7 @@ def main():
     dh = _native.DfaHandle(ctx, w.dfa)
     sh = ctx.upload_ascii(w.ascii.tobytes())
     want = None
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if args.flush else None
     for rnd in range(2):
         for v in args.variants:
             env = dict(kv.split("=", 1) for kv in v.split(",") if "=" in kv)
@@ -43,6 +46,9 @@ def main():
                 ok = bool((counts == want).all())
                 ms = []
                 for _ in range(args.reps):
+                    if flush is not None:
+                        flush.zero_()
+                        torch.cuda.synchronize()
                     ctx.count(dh, sh)
                     ms.append(ctx.stats()["scan_ms"])
                 med = statistics.median(ms)
