@@ -714,6 +714,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
             if (threadIdx.x == 0) is_last = atomicAdd(a.fin_done, 1u) == gridDim.x - 1;
             __syncthreads();
             if (is_last) {
+                kt_mark(a.ktime, 9, false);
                 __threadfence();
                 if (threadIdx.x == 0 && a.fin_exit_src) *a.fin_exit_dst = __ldcg(a.fin_exit_src);
                 // counts accumulate in the (drained) ring's shared memory when they fit
@@ -937,8 +938,8 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
         auto us = [&](int i) { return h[i] ? (double(h[i]) - double(h[0])) * 1e-3 : -1.0; };
         std::fprintf(stderr,
                      "[ks ktime] grid %d x %d: CTA start 0..%.2f | tables ready %.2f..%.2f | warp scan end "
-                     "%.2f..%.2f | CTA flushed %.2f..%.2f | finalized %.2f us\n",
-                     blocks, warps * 32, us(1), us(2), us(3), us(4), us(5), us(6), us(7), us(8));
+                     "%.2f..%.2f | CTA flushed %.2f..%.2f | last CTA found %.2f | finalized %.2f us\n",
+                     blocks, warps * 32, us(1), us(2), us(3), us(4), us(5), us(6), us(7), us(9), us(8));
         if (a.ktime == 2) {
             std::vector<unsigned long long> c(size_t(std::min(blocks, 1024)));
             KS_CUDA(cudaMemcpyFromSymbol(c.data(), g_kcta, c.size() * 8));
