@@ -138,17 +138,15 @@ __global__ void __launch_bounds__(1024, 1) scan_kernel(const ScanArgs a) {
     uint16_t* s_t1 = s_tk + (SM ? a.tk_pad : 0);
     unsigned int* s_hist = reinterpret_cast<unsigned int*>(s_t1 + (SM ? a.t1_pad : 0));
 
-    if constexpr (SM) {
-        const uint4* src = reinterpret_cast<const uint4*>(a.tk);
-        uint4* dst = reinterpret_cast<uint4*>(s_tk);
-        for (int i = threadIdx.x; i < a.tk_pad / 8; i += blockDim.x) dst[i] = __ldg(src + i);
-        src = reinterpret_cast<const uint4*>(a.t1);
-        dst = reinterpret_cast<uint4*>(s_t1);
-        for (int i = threadIdx.x; i < a.t1_pad / 8; i += blockDim.x) dst[i] = __ldg(src + i);
-    }
+    __shared__ __align__(8) unsigned long long staged;
+    BulkStage st;
+    if constexpr (SM)   // both tables by bulk copies (TMA engine) while the threads clear the histogram
+        st.begin(&staged, smem_u32(s_tk), a.tk, uint32_t(a.tk_pad) * 2u, smem_u32(s_t1), a.t1,
+                 uint32_t(a.t1_pad) * 2u);
     const bool hist_smem = (MODE == kModeCount || MODE == kModeRows) && a.hist_smem;
     if (hist_smem)
         for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x) s_hist[i] = 0u;
+    if constexpr (SM) st.wait();
     __syncthreads();
 
     Tables<SM> T;
@@ -321,10 +319,13 @@ __global__ void __launch_bounds__(1024, 1) scan_wide_hot_kernel(const ScanArgs a
     const size_t ht_bytes = (size_t(a.hot_n) * 8 + 15) & ~size_t(15);
     unsigned int* shist = reinterpret_cast<unsigned int*>(wh_smem + ht_bytes);
     const bool hist_smem = (MODE == kModeCount || MODE == kModeRows) && a.hist_smem;
-    for (size_t i = threadIdx.x; i < size_t(a.hot_n); i += blockDim.x)   // 8-byte rows
-        reinterpret_cast<uint2*>(ht)[i] = __ldg(reinterpret_cast<const uint2*>(a.ht) + i);
+    // the hot table (8-byte rows, padded to 16 bytes in the blob) by bulk copies
+    __shared__ __align__(8) unsigned long long staged;
+    BulkStage st;
+    st.begin(&staged, smem_u32(ht), a.ht, uint32_t(ht_bytes));
     if (hist_smem)
         for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x) shist[i] = 0u;
+    st.wait();
     __syncthreads();
     const uint32_t A = uint32_t(a.n_accept), lo = uint32_t(a.hot_lo), H = uint32_t(a.hot_n);
     const uint32_t reset = uint32_t(a.reset_state);
@@ -421,11 +422,15 @@ __global__ void __launch_bounds__(1024, 1) scan_wide_hot_ilp_kernel(const ScanAr
     const uint32_t H = uint32_t(a.hot_n);
     const size_t ht_bytes = (size_t(H + 1) * 8 + 15) & ~size_t(15);   // + the all-cold row H
     unsigned int* shist = reinterpret_cast<unsigned int*>(wh_smem + ht_bytes);
-    for (size_t i = threadIdx.x; i < size_t(H); i += blockDim.x)   // 8-byte rows (H may be odd)
-        reinterpret_cast<uint2*>(ht)[i] = __ldg(reinterpret_cast<const uint2*>(a.ht) + i);
-    for (size_t i = size_t(H) * 4 + threadIdx.x; i < ht_bytes / 2; i += blockDim.x) ht[i] = 0xFFFFu;
+    // the H hot rows by bulk copies (8-byte rows; an odd H copies 8 bytes of
+    // the blob's padding too), then the all-cold sentinel row over them
+    __shared__ __align__(8) unsigned long long staged;
+    BulkStage st;
+    st.begin(&staged, smem_u32(ht), a.ht, uint32_t((size_t(H) * 8 + 15) & ~size_t(15)));
     if (HSM)
         for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x) shist[i] = 0u;
+    st.wait();
+    for (size_t i = size_t(H) * 4 + threadIdx.x; i < ht_bytes / 2; i += blockDim.x) ht[i] = 0xFFFFu;
     __syncthreads();
     const uint32_t A = uint32_t(a.n_accept), lo = uint32_t(a.hot_lo);
     const uint32_t reset = uint32_t(a.reset_state);

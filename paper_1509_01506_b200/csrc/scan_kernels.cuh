@@ -110,6 +110,50 @@ struct ScanArgs {
 
 inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
+#ifdef __CUDACC__
+// ---- table staging with bulk copies (the TMA engine: UBLKCP + SYNCS) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+// global -> shared bulk copy; completion counted in bytes on the mbarrier
+__device__ __forceinline__ void bulk_copy_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void mbarrier_wait0(uint32_t mbar) {
+    asm volatile(
+        "{\n\t.reg .pred done;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], 0;\n\t"
+        "@!done bra WAIT_%=;\n\t}"
+        ::"r"(mbar) : "memory");
+}
+// Stage up to two global regions (16-byte aligned, sizes multiples of 16)
+// into shared memory: one thread arms the CTA's mbarrier and issues 32 KiB
+// bulk copies while the other threads go on (histogram clears etc.); call
+// stage_wait before reading the staged bytes.  Every thread calls both.
+struct BulkStage {
+    uint32_t mbar;
+    __device__ __forceinline__ void begin(unsigned long long* bar, uint32_t d0, const void* s0, uint32_t n0,
+                                          uint32_t d1 = 0, const void* s1 = nullptr, uint32_t n1 = 0) {
+        mbar = smem_u32(bar);
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(n0 + n1)
+                         : "memory");
+            constexpr uint32_t kPart = 32768;
+            for (uint32_t o = 0; o < n0; o += kPart)
+                bulk_copy_g2s(d0 + o, static_cast<const char*>(s0) + o, n0 - o < kPart ? n0 - o : kPart, mbar);
+            for (uint32_t o = 0; o < n1; o += kPart)
+                bulk_copy_g2s(d1 + o, static_cast<const char*>(s1) + o, n1 - o < kPart ? n1 - o : kPart, mbar);
+        }
+    }
+    __device__ __forceinline__ void wait() const { mbarrier_wait0(mbar); }
+};
+#endif
+
 // Launch attribute keeping [base, base + bytes) in the persisting part of L2
 // (constant automaton tables: they survive the sequence streaming through L2
 // and the calls in between).  Grows the device's set-aside as needed; false
