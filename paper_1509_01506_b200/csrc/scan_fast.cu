@@ -88,20 +88,6 @@ __device__ __forceinline__ uint32_t opaque(uint32_t x) {
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return uint32_t(__cvta_generic_to_shared(p));
 }
-// Bulk (non-tensor TMA) copy global -> shared, completion counted in bytes on mbar.
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_parity0(uint32_t mbar) {
-    asm volatile(
-        "{\n\t.reg .pred done;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], 0;\n\t"
-        "@!done bra WAIT_%=;\n\t}"
-        ::"r"(mbar) : "memory");
-}
-
 // K input bases of step j shifted so they start at bit LC; bits outside
 // [LC, LC + 2K) are garbage (removed by the bit-select).  x0..x3 are the
 // block's 128 bits; compile-time j makes this one SHF (funnel) or nothing.
@@ -414,9 +400,9 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                      ::"r"(mbar), "r"(uint32_t(TK_BYTES) + t1_bytes) : "memory");
         constexpr uint32_t kPart = 32768;   // bytes per bulk copy
         for (uint32_t o = 0; o < uint32_t(TK_BYTES); o += kPart)
-            bulk_g2s(smem_addr(f_smem) + o, reinterpret_cast<const char*>(a.tk) + o, kPart, mbar);
+            bulk_copy_g2s(smem_addr(f_smem) + o, reinterpret_cast<const char*>(a.tk) + o, kPart, mbar);
         for (uint32_t o = 0; o < t1_bytes; o += kPart)
-            bulk_g2s(smem_addr(p_t1) + o, reinterpret_cast<const char*>(a.t1) + o, min(kPart, t1_bytes - o), mbar);
+            bulk_copy_g2s(smem_addr(p_t1) + o, reinterpret_cast<const char*>(a.t1) + o, min(kPart, t1_bytes - o), mbar);
     }
     if constexpr (HIST)
         for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x) s_hist[i] = 0u;
@@ -438,7 +424,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         if (!late_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
     }
-    mbar_wait_parity0(mbar);
+    mbarrier_wait0(mbar);
     __syncthreads();
     kt_mark(a.ktime, 2, true);
     kt_mark(a.ktime, 3, false);
