@@ -451,7 +451,7 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
                              ? reinterpret_cast<uint16_t*>(direct + size_t(std::max(h.ne, 1)) * 8 + 8)
                              : exit_slot;
         a.fin_done = reinterpret_cast<unsigned int*>(err + 1);   // zero between calls
-        a.tile_ctr = reinterpret_cast<unsigned int*>(err + 3);   // zero between calls (fast kernel)
+        a.dyn_items = 1;   // fused: the finalizing CTA resets the dynamic-item counters
         a.fin_host = reinterpret_cast<unsigned long long*>(direct);
         a.n_expr = h.ne;
     }
@@ -737,6 +737,7 @@ int ks_close(ks_ctx* ctx) {
     if (ctx->rdev) cudaFree(ctx->rdev);
     if (ctx->log_buf) cudaFree(ctx->log_buf);
     if (ctx->wctr) cudaFree(ctx->wctr);
+    if (ctx->tctr) cudaFree(ctx->tctr);
     delete ctx->pool;
     if (ctx->hstage) cudaFreeHost(ctx->hstage);
     for (auto& ev : ctx->hev)

@@ -191,6 +191,7 @@ struct ks_ctx {
     // single-pass locate log (grow-only)
     void* log_buf = nullptr;
     unsigned int* wctr = nullptr;   // task counter of the wide count kernel
+    unsigned int* tctr = nullptr;   // dynamic-item counters of the fast count kernel (32 x 128 B)
     size_t log_bytes = 0;
     // ks_count_async: one event pair per call until ks_async_wait
     std::vector<cudaEvent_t> aev;

@@ -53,6 +53,7 @@ constexpr int kRingMax = 32;  // the ring takes what shared memory is left, up t
 #endif
 __host__ __device__ constexpr int chk_steps(int k) { return k == 2 ? KS_CHK2 : 8; }
 constexpr int kFastThreads = 1024;
+constexpr int kTileCtrs = 32;   // dynamic-item counters of the count kernel, 128 B apart (ks_ctx::tctr)
 constexpr uint32_t kRingStride = 4u * kFastThreads;  // bytes between ring slots
 
 __device__ __forceinline__ uint32_t lds16(uint32_t addr) {
@@ -474,18 +475,20 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     const int64_t n_items = dyn ? whole + int64_t(a.split_tiles) * a.split_parts : ntiles;
     const int ublocks = int(a.chunk_len >> 6);
     const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    unsigned int* const my_ctr = dyn ? a.tile_ctr + size_t(wid % kTileCtrs) * 32u : nullptr;
     int64_t item = wid;
     for (; item < n_items;) {
         int64_t next = item + nwarps;
-        if (dyn && next >= a.static_items) {
-            unsigned int g = 0;
-            if (!waited) {
-                asm volatile("griddepcontrol.wait;" ::: "memory");
-                waited = true;
-            }
-            if (lane == 0) g = atomicAdd(a.tile_ctr, 1u);
-            next = a.static_items + int64_t(__shfl_sync(am, g, 0));
-        }
+        // dynamic items come from kTileCtrs counters 128 B apart (warp w asks
+        // counter w % kTileCtrs, which hands out every kTileCtrs-th item): a
+        // single counter serialised thousands of warps' first requests.  The
+        // request goes out at the start of an item and is read at its end
+        // once the preceding kernel is known to be done (the counters are
+        // reset by its finalizing CTA); the first one waits for that at the end.
+        const bool fetch = dyn && next >= a.static_items;
+        const bool ask_now = fetch && waited;
+        unsigned int g = 0;
+        if (ask_now && lane == 0) g = atomicAdd(my_ctr, 1u);
         int64_t t;
         int pl = 0, ph = ublocks;   // blocks [pl, ph) of each lane's unit
         if (item < whole) {
@@ -505,7 +508,6 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
         const bool active = ch >= 0 && ch < a.nchunks && cb0 < ce0;
         const int64_t cb = active ? cb0 : 0;
         const int64_t ce = active ? ce0 : 0;
-        item = next;
 
         uint32_t s = idle;
         if (!active) {
@@ -670,6 +672,18 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                 if (L.cur != a.chunk_row_off[ch + 1]) atomicExch(a.error, 1);
             }
         }
+        if (fetch) {
+            if (!ask_now) {
+                if (!waited) {
+                    asm volatile("griddepcontrol.wait;" ::: "memory");
+                    waited = true;
+                }
+                if (lane == 0) g = atomicAdd(my_ctr, 1u);
+            }
+            item = a.static_items + int64_t(wid % kTileCtrs) + int64_t(kTileCtrs) * __shfl_sync(am, g, 0);
+        } else {
+            item = next;
+        }
     }
 
     kt_mark(a.ktime, 4, true, true);
@@ -722,10 +736,8 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                     if (in_smem) a.fin_counts[e] = v;
                     if (a.fin_host) a.fin_host[e] = v;   // pinned host memory: visible once the kernel completes
                 }
-                if (threadIdx.x == 0) {
-                    *a.fin_done = 0u;
-                    if (a.tile_ctr) *a.tile_ctr = 0u;   // every item has been taken
-                }
+                if (threadIdx.x == 0) *a.fin_done = 0u;
+                if (a.tile_ctr && threadIdx.x < kTileCtrs) a.tile_ctr[threadIdx.x * 32u] = 0u;   // all items taken
                 kt_mark(a.ktime, 8, false);
             }
         }
@@ -873,8 +885,14 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
     // come in one burst with nothing to hide them, C1/C2 lose 5-20%)
     const int64_t nw = int64_t(warps) * std::max<int64_t>(1, std::min<int64_t>((tiles + warps - 1) / warps,
                                                                                ctx->num_sms));
-    if (mode == kModeCount && a.fin_counts && a.tile_ctr && tiles > 2 * nw &&
+    a.tile_ctr = nullptr;
+    if (mode == kModeCount && a.fin_counts && a.dyn_items && tiles > 2 * nw &&
         !(std::getenv("KS_STATIC_TILES") && *std::getenv("KS_STATIC_TILES") == '1')) {
+        if (!ctx->tctr) {   // zero once; every fused count's finalizing CTA leaves them zero
+            KS_CUDA(cudaMalloc(&ctx->tctr, size_t(kTileCtrs) * 128));
+            KS_CUDA(cudaMemsetAsync(ctx->tctr, 0, size_t(kTileCtrs) * 128, ctx->stream));
+        }
+        a.tile_ctr = ctx->tctr;
         const int ub = int(a.chunk_len >> 6);
         const bool entered_by_lookback = !a.chunk_entry && a.uniform_entry < 0;
         int parts = entered_by_lookback ? std::min(ub, 2) : 1;
@@ -885,8 +903,6 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
         // round-robin for all but the last two rounds of items
         const int64_t items = tiles - a.split_tiles + int64_t(a.split_tiles) * parts;
         a.static_items = std::max<int64_t>(nw, (items / nw - 2) * nw);
-    } else {
-        a.tile_ctr = nullptr;
     }
     if (const char* e = std::getenv("KS_KTIME"); e && (*e == '1' || *e == '2')) {
         unsigned long long h[10] = {~0ull, 0, ~0ull, 0, ~0ull, 0, ~0ull, 0, 0, 0};

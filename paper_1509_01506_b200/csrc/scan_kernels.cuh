@@ -99,8 +99,10 @@ struct ScanArgs {
     int64_t log_cap = 0;
     unsigned int* work_ctr = nullptr;       // wide count kernel: task counter (zeroed per launch)
     int32_t run_blocks = 0;                 // wide count kernel: blocks per run
-    // fast kernel, count mode: dynamic work items (tile counter zero at
-    // launch, reset by the finalizing CTA; only with fin_counts)
+    // fast kernel, count mode: dynamic work items (dyn_items: the caller's
+    // fused finalize allows them; tile_ctr = the context's counters, zero at
+    // launch and reset by the finalizing CTA)
+    int32_t dyn_items = 0;
     unsigned int* tile_ctr = nullptr;
     int32_t split_tiles = 0, split_parts = 1;
     int64_t static_items = 0;               // items below this go round-robin

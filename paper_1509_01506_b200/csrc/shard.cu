@@ -238,7 +238,7 @@ int ks_count_shard_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
             a.fin_exit_src = chunk_exit + (nch - 1);
             a.fin_exit_dst = reinterpret_cast<uint16_t*>(err + 2);
             a.fin_done = reinterpret_cast<unsigned int*>(err + 1);   // zero between calls
-            a.tile_ctr = reinterpret_cast<unsigned int*>(err + 3);   // zero between calls (fast kernel)
+            a.dyn_items = 1;   // fused: the finalizing CTA resets the dynamic-item counters
             a.fin_host = nullptr;
             a.n_expr = h.ne;
         }

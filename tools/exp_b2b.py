@@ -20,7 +20,7 @@ stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 variants = sys.argv[2:] or ["base"]
 for cfg in cfgs:
-    w = workloads.make(cfg)
+    w = workloads.make(cfg, int(os.environ["N"]) if os.environ.get("N") else None)
     ctx = _native.context(0)
     ctx.set_stream(stream.cuda_stream)   # events and scans on one stream
     dh = ctx.dfa(w.dfa)
