@@ -881,12 +881,14 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
     // counter); the last round of tiles is cut into block ranges when lane
     // chunks are entered by lookback (per-chunk or uniform entry states hold
     // only at chunk starts)
-    // (three or more rounds of tiles: below that the counter's first fetches
-    // come in one burst with nothing to hide them, C1/C2 lose 5-20%)
+    // (seven or more rounds of tiles: with fewer, the extra items' restarts
+    // and lookbacks cost more than the balance gains -- isolated C4 shards of
+    // 400 M / 800 M bases (3 / 6 rounds) ran 7-9% slower dynamic, C1/C2 (one
+    // round) 5-20%; C3 (7 rounds) and C4 (10) gain 1.5-4%)
     const int64_t nw = int64_t(warps) * std::max<int64_t>(1, std::min<int64_t>((tiles + warps - 1) / warps,
                                                                                ctx->num_sms));
     a.tile_ctr = nullptr;
-    if (mode == kModeCount && a.fin_counts && a.dyn_items && tiles > 2 * nw &&
+    if (mode == kModeCount && a.fin_counts && a.dyn_items && tiles > 6 * nw &&
         !(std::getenv("KS_STATIC_TILES") && *std::getenv("KS_STATIC_TILES") == '1')) {
         if (!ctx->tctr) {   // zero once; every fused count's finalizing CTA leaves them zero
             KS_CUDA(cudaMalloc(&ctx->tctr, size_t(kTileCtrs) * 128));

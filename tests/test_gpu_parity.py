@@ -981,11 +981,11 @@ def test_mid_automaton_takes_the_wide_path():
 def test_dynamic_tiles_and_split_tails(monkeypatch, config):
     """Count-mode work items beyond two rounds come from a device counter and
     the last round is cut into block ranges entered by lookback mid-chunk
-    (scan_fast.cu): every split (1, 2, 4 parts) and the static round-robin
+    (scan_fast.cu): every split (1, 2 parts) and the static round-robin
     give the oracle's counts, whole sequence and unaligned ranges from an
     explicit entry state."""
-    monkeypatch.setenv("KS_TILE_LB", "2")   # 256-base units: > 2 rounds of tiles at this size
-    w = workloads.make(config, 100_000_037)
+    monkeypatch.setenv("KS_TILE_LB", "1")   # 128-base units: > 6 rounds of tiles at this size
+    w = workloads.make(config, 150_000_037)
     codes = ks.encode_bytes(w.ascii.tobytes())
     want = O.ref_run(w.dfa, codes, 16, 10, False)[0]
     rng = np.random.default_rng(config)
@@ -997,8 +997,7 @@ def test_dynamic_tiles_and_split_tails(monkeypatch, config):
     c2 = _native.DeviceContext(0)
     dh = c2.dfa(w.dfa)
     sh = c2.upload_codes(codes)
-    for env in ({"KS_STATIC_TILES": "1"}, {"KS_SPLIT_PARTS": "1"}, {"KS_SPLIT_PARTS": "2"},
-                {"KS_SPLIT_PARTS": "4"}):
+    for env in ({"KS_STATIC_TILES": "1"}, {"KS_SPLIT_PARTS": "1"}, {"KS_SPLIT_PARTS": "2"}):
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         assert c2.count(dh, sh).tolist() == want.tolist(), env
