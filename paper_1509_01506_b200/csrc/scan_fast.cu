@@ -460,7 +460,9 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     const int64_t u0 = a.origin / a.chunk_len;
     const int64_t t0 = u0 >> 5;
     const int64_t t1 = (u0 + a.nchunks - 1) >> 5;
-    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    // item bookkeeping in 32 bits (tiles of >= 2048 bases: < 2^31 items for
+    // any sequence this library addresses) -- the 64-register budget is tight
+    const int nwarps = int((gridDim.x * blockDim.x) >> 5);
     constexpr unsigned am = 0xffffffffu;
     // Work items.  Static: warp w takes tiles t0 + w, t0 + w + nwarps, ...
     // Dynamic (count mode with a tile counter): items are whole tiles, then
@@ -470,22 +472,23 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     // the counter (fetched one item ahead) -- faster SMs take more of the
     // last rounds.
     const bool dyn = MODE == kModeCount && a.tile_ctr != nullptr;
-    const int64_t ntiles = t1 - t0 + 1;
-    const int64_t whole = dyn ? ntiles - a.split_tiles : ntiles;
-    const int64_t n_items = dyn ? whole + int64_t(a.split_tiles) * a.split_parts : ntiles;
+    const int ntiles = int(t1 - t0 + 1);
+    const int whole = dyn ? ntiles - a.split_tiles : ntiles;
+    const int n_items = dyn ? whole + a.split_tiles * a.split_parts : ntiles;
+    const int static_items = int(a.static_items);
     const int ublocks = int(a.chunk_len >> 6);
-    const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    unsigned int* const my_ctr = dyn ? a.tile_ctr + size_t(wid % kTileCtrs) * 32u : nullptr;
-    int64_t item = wid;
+    const int wid = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    unsigned int* const my_ctr = dyn ? a.tile_ctr + (wid % kTileCtrs) * 32u : nullptr;
+    int item = wid;
     for (; item < n_items;) {
-        int64_t next = item + nwarps;
+        int next = item + nwarps;
         // dynamic items come from kTileCtrs counters 128 B apart (warp w asks
         // counter w % kTileCtrs, which hands out every kTileCtrs-th item): a
         // single counter serialised thousands of warps' first requests.  The
         // request goes out at the start of an item and is read at its end
         // once the preceding kernel is known to be done (the counters are
         // reset by its finalizing CTA); the first one waits for that at the end.
-        const bool fetch = dyn && next >= a.static_items;
+        const bool fetch = dyn && next >= static_items;
         const bool ask_now = fetch && waited;
         unsigned int g = 0;
         if (ask_now && lane == 0) g = atomicAdd(my_ctr, 1u);
@@ -494,9 +497,9 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
         if (item < whole) {
             t = t0 + item;
         } else {
-            const int64_t j = item - whole;
+            const int j = item - whole;
             t = t0 + whole + j / a.split_parts;
-            const int q = int(j % a.split_parts);
+            const int q = j % a.split_parts;
             pl = q * ublocks / a.split_parts;
             ph = (q + 1) * ublocks / a.split_parts;
         }
@@ -680,7 +683,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                 }
                 if (lane == 0) g = atomicAdd(my_ctr, 1u);
             }
-            item = a.static_items + int64_t(wid % kTileCtrs) + int64_t(kTileCtrs) * __shfl_sync(am, g, 0);
+            item = static_items + wid % kTileCtrs + kTileCtrs * int(__shfl_sync(am, g, 0));
         } else {
             item = next;
         }
