@@ -292,52 +292,60 @@ def time_steps(ctx, step, stream, steps: int, flush, local: int, sync_each=None,
 
 
 class PipelinedAllReduce:
-    """The per-step NCCL all-reduce of a step's counts overlapped with the next
-    step's scan: two count buffers; step i's all-reduce runs asynchronously on
-    NCCL's stream while step i + 1 scans into the other buffer (the scan grid
-    leaves RESERVED_SMS SMs free for NCCL's kernel -- a scan CTA fills its SM).
-    Before a buffer is reused the stream waits for its all-reduce (an event
-    wait, no copy on the scan stream); finish() drains both and copies the
-    last step's reduced counts to pinned host memory."""
+    """The per-step NCCL all-reduce of a step's counts, overlapped with the next
+    steps' scans without touching the scan stream: the scan kernel's
+    finalizing CTA raises a device flag once the counts are final
+    (ks_count_shard_async_signal), a side stream waits on that flag
+    (ks_stream_wait_value32) and runs the all-reduce, so the scan stream holds
+    nothing but back-to-back scan kernels (their programmatic overlap is kept;
+    an event recorded between them would break it) and the scan grid leaves
+    RESERVED_SMS SMs to NCCL's kernel (a scan CTA fills its SM).  Every step
+    writes its own count buffer; finish() makes the scan stream wait for the
+    collectives and copies the last step's reduced counts to pinned memory."""
 
     RESERVED_SMS = 2
+    NBUF = 256
 
     def __init__(self, ne: int, dev, out_pin):
         import torch
 
-        self.bufs = [torch.zeros(max(ne, 1), dtype=torch.int64, device=dev) for _ in range(2)]
-        self.work = [None, None]
-        self.order = []
+        self.side = torch.cuda.Stream(dev)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.bufs = torch.zeros((self.NBUF, max(ne, 1)), dtype=torch.int64, device=dev)
+        self.seq = 0          # flag value of the latest step (monotone)
+        self.k = 0            # buffers used since the last finish()
+        self.works = []
+        self.last_buf = None
         self.out_pin = out_pin
 
-    def acquire(self):
-        import torch  # noqa: F401
-
-        b = len(self.order) % 2
-        if self.work[b] is not None:
-            self._retire(b)
-        return self.bufs[b]
-
-    def launch(self, buf) -> None:
+    def step(self, scan) -> None:
+        """scan(counts_ptr, flag_ptr, value) enqueues the signalled count."""
+        import torch
         import torch.distributed as dist
 
-        b = 0 if buf is self.bufs[0] else 1
-        self.work[b] = dist.all_reduce(buf, async_op=True)
-        self.order.append(b)
+        from paper_1509_01506_b200 import _native
 
-    def _retire(self, b: int) -> None:
-        self.work[b].wait()          # the current stream waits for the collective
-        self.work[b] = None
+        if self.k == self.NBUF:
+            self.finish()
+        buf = self.bufs[self.k]
+        self.k += 1
+        self.seq += 1
+        scan(buf.data_ptr(), self.flag.data_ptr(), self.seq)
+        with torch.cuda.stream(self.side):
+            _native.DeviceContext.stream_wait_value32(self.side.cuda_stream, self.flag.data_ptr(), self.seq)
+            self.works.append(dist.all_reduce(buf, async_op=True))
+        self.last_buf = buf
 
     def finish(self) -> None:
-        for b in self.order[-2:]:
-            if self.work[b] is not None:
-                self._retire(b)
-        if self.order:
-            self.out_pin.copy_(self.last(), non_blocking=True)
+        for w in self.works:
+            w.wait()          # the current (scan) stream waits for the collective
+        self.works = []
+        if self.last_buf is not None:
+            self.out_pin.copy_(self.last_buf, non_blocking=True)
+        self.k = 0
 
     def last(self):
-        return self.bufs[self.order[-1]] if self.order else self.bufs[0]
+        return self.last_buf if self.last_buf is not None else self.bufs[0]
 
 
 def kernel_ms(ctx, dh, sh, flush, reps: int = 5, scan=None) -> float:
@@ -468,10 +476,8 @@ def strong_leg(args, ctx, stream, world: int, rank: int, local: int, dev) -> dic
         pipe = PipelinedAllReduce(ne, dev, torch.zeros(max(ne, 1), dtype=torch.int64).pin_memory())
 
     def step():
-        if pipe is not None:   # scan into one buffer while the other's all-reduce runs
-            buf = pipe.acquire()
-            ctx.count_shard_async(dh, sh, hl, hl + hi - lo, 0, rank, buf.data_ptr())
-            pipe.launch(buf)
+        if pipe is not None:   # the all-reduce runs beside the next scans
+            pipe.step(lambda cp, fp, v: ctx.count_shard_async_signal(dh, sh, hl, hl + hi - lo, 0, rank, cp, fp, v))
             return
         ctx.count_shard_async(dh, sh, hl, hl + hi - lo, 0, rank, counts_dev.data_ptr())
         if world > 1:
@@ -537,8 +543,9 @@ def strong_leg(args, ctx, stream, world: int, rank: int, local: int, dev) -> dic
                "one_gpu_ms_per_step": ms1, "speedup_vs_1": ms1 / ms_n,
                "step": ("scan of each rank's contiguous shard from its halo's lookback (ks_count_shard_async) "
                         "+ NCCL all-reduce of the int64 counts"
-                        + (", overlapped with the next step's scan (two count buffers; the scan grid leaves "
-                           f"{PipelinedAllReduce.RESERVED_SMS} SMs to NCCL)" if pipe is not None else "")
+                        + (", on a side stream gated by a device flag the scan kernel raises, overlapped with the "
+                           f"next scans (the scan grid leaves {PipelinedAllReduce.RESERVED_SMS} SMs to NCCL)"
+                           if pipe is not None else "")
                         + "; events per rank, max over ranks"),
                "halo_bases": H, "clocks_rank0": clocks, "gpu_launches_rank0": launches,
                "parity": {"oracle": ORACLE_NAME, "counts_equal_oracle": bool(np.array_equal(counts, want)),
@@ -631,10 +638,9 @@ def run_ours(args) -> None:
             ctx.count_async(dh, sh, out_np)
             return
         if halo_mode:   # scan from the halo's lookback -> all-reduce of the counts
-            if pipe_main is not None:   # overlapped with the next step's scan
-                buf = pipe_main.acquire()
-                ctx.count_shard_async(dh, sh_halo, halo_len, halo_len + n, 0, rank, buf.data_ptr())
-                pipe_main.launch(buf)
+            if pipe_main is not None:   # the all-reduce runs beside the next scans
+                pipe_main.step(lambda cp, fp, v: ctx.count_shard_async_signal(dh, sh_halo, halo_len, halo_len + n,
+                                                                              0, rank, cp, fp, v))
             else:   # gloo dry run: the reduction on host tensors
                 ctx.count_shard_async(dh, sh_halo, halo_len, halo_len + n, 0, rank, counts_dev.data_ptr())
                 c = counts_dev.cpu()

@@ -217,6 +217,18 @@ KS_API int ks_segment_map_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* se
 KS_API int ks_count_shard_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin,
                                 int64_t end, const int32_t* d_maps, int32_t rank,
                                 unsigned long long* d_counts);
+/* The same, and once the counts are final the device writes signal_value to
+ * *d_signal (uint32, device memory; raised by the scan kernel's finalizing
+ * CTA, so the context's stream carries no extra operation between
+ * back-to-back scans).  Another stream can then start the all-reduce of
+ * d_counts after ks_stream_wait_value32(stream, d_signal, signal_value)
+ * without the scan stream recording an event -- back-to-back scans keep
+ * their programmatic overlap while the collectives run beside them. */
+KS_API int ks_count_shard_async_signal(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin,
+                                       int64_t end, const int32_t* d_maps, int32_t rank,
+                                       unsigned long long* d_counts, uint32_t* d_signal, uint32_t signal_value);
+/* Make `cuda_stream` wait until *d_addr >= value (cuStreamWaitValue32, GEQ). */
+KS_API int ks_stream_wait_value32(void* cuda_stream, const uint32_t* d_addr, uint32_t value);
 
 /* Speculative-start convergence (match_chunk_kernel's speculative runs,
  * _kernels.py:91-112): for chunk k, candidate start states

@@ -60,7 +60,7 @@ EXPORTED = (
     "ks_seq_upload_codes", "ks_seq_upload_ascii", "ks_seq_encode_device", "ks_seq_length",
     "ks_seq_download_codes", "ks_seq_download_softmask", "ks_seq_free", "ks_count", "ks_locate",
     "ks_count_host_ascii", "ks_count_async", "ks_async_wait", "ks_segment_map_async",
-    "ks_count_shard_async", "ks_pack_host_ascii", "ks_count_host_bytes", "ks_pack_host_wire",
+    "ks_count_shard_async", "ks_count_shard_async_signal", "ks_stream_wait_value32", "ks_pack_host_ascii", "ks_count_host_bytes", "ks_pack_host_wire",
     "ks_scan_range", "ks_segment_map", "ks_speculate", "ks_free",
     "ks_open_multi", "ks_close_multi", "ks_multi_info", "ks_mdfa_upload", "ks_mdfa_free",
     "ks_mseq_upload_codes", "ks_mseq_upload_ascii", "ks_mseq_length", "ks_mseq_free", "ks_mcount",
@@ -107,6 +107,9 @@ def _declare(lib) -> None:
         "ks_pack_host_wire": (C.c_int, [_u8p, C.c_int64, C.c_int32, _P, _P, _i64p]),
         "ks_segment_map_async": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, _P]),
         "ks_count_shard_async": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, _P, C.c_int32, _P]),
+        "ks_count_shard_async_signal": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, _P, C.c_int32, _P, _P,
+                                                  C.c_uint32]),
+        "ks_stream_wait_value32": (C.c_int, [_P, _P, C.c_uint32]),
         "ks_async_wait": (C.c_int, [_P, C.POINTER(C.c_float), _i32p, _i32p]),
         "ks_scan_range": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, C.c_int32, C.c_int64, _i64p,
                                     _i32p, C.POINTER(_i64p), _i64p]),
@@ -348,6 +351,19 @@ class DeviceContext:
         (uint64) into device memory."""
         _check(library().ks_count_shard_async(self.handle, dfa.handle, seq.handle, int(begin), int(end),
                                               _P(d_maps), int(rank), _P(d_counts)))
+
+    def count_shard_async_signal(self, dfa: DfaHandle, seq: SeqHandle, begin: int, end: int, d_maps: int,
+                                 rank: int, d_counts: int, d_signal: int, value: int) -> None:
+        """count_shard_async, then the device sets *d_signal = value once the
+        counts are final (for a collective on another stream)."""
+        _check(library().ks_count_shard_async_signal(self.handle, dfa.handle, seq.handle, int(begin), int(end),
+                                                     _P(d_maps), int(rank), _P(d_counts), _P(d_signal),
+                                                     int(value) & 0xFFFFFFFF))
+
+    @staticmethod
+    def stream_wait_value32(stream_ptr: int, d_addr: int, value: int) -> None:
+        """The CUDA stream waits until the uint32 at d_addr is >= value."""
+        _check(library().ks_stream_wait_value32(_P(stream_ptr), _P(d_addr), int(value) & 0xFFFFFFFF))
 
     def async_wait(self) -> dict:
         ms, calls, launches = C.c_float(), C.c_int32(), C.c_int32()

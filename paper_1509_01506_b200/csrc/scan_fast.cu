@@ -741,6 +741,14 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                 }
                 if (threadIdx.x == 0) *a.fin_done = 0u;
                 if (a.tile_ctr && threadIdx.x < kTileCtrs) a.tile_ctr[threadIdx.x * 32u] = 0u;   // all items taken
+                if (a.fin_signal) {   // the counts are final: release them to a stream waiting on the flag
+                    __syncthreads();
+                    if (threadIdx.x == 0) {
+                        __threadfence_system();
+                        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.fin_signal), "r"(a.fin_signal_value)
+                                     : "memory");
+                    }
+                }
                 kt_mark(a.ktime, 8, false);
             }
         }

@@ -90,6 +90,8 @@ struct ScanArgs {
     unsigned int* fin_done = nullptr;
     unsigned long long* fin_host = nullptr;
     int32_t n_expr = 0;
+    unsigned int* fin_signal = nullptr;     // optional: set to fin_signal_value once the counts are final
+    unsigned int fin_signal_value = 0;
     // kModeMap over the OTHER-free submonoid (HostDfa::mono_sub): a chunk
     // that holds OTHER (the table resets to the identity there) exits with
     // map_dirty[element since its last OTHER]

@@ -60,7 +60,32 @@ __global__ void compose_entry_kernel(const int32_t* maps, int32_t nq, int32_t ra
     *entry_internal = uint16_t(new_of_old[s]);
 }
 
+
+// cuStreamWaitValue32 / cuStreamWriteValue32 through the runtime's driver
+// entry points (no -lcuda link).
+using StreamValueFn = int (*)(cudaStream_t, unsigned long long, unsigned int, unsigned int);
+StreamValueFn stream_value_fn(const char* name) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return reinterpret_cast<StreamValueFn>(fn);
+}
+int stream_write_value(cudaStream_t st, unsigned int* addr, unsigned int value) {
+    static const StreamValueFn fn = stream_value_fn("cuStreamWriteValue32");
+    if (!fn) return fail(KS_E_UNSUPPORTED, "cuStreamWriteValue32 unavailable");
+    if (fn(st, reinterpret_cast<unsigned long long>(addr), value, 0u) != 0)
+        return fail(KS_E_CUDA, "cuStreamWriteValue32 failed");
+    return KS_OK;
+}
+
 }  // namespace
+
+int count_shard_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end,
+                     const int32_t* d_maps, int32_t rank, unsigned long long* d_counts, unsigned int* d_signal,
+                     unsigned int signal_value);
 }  // namespace ks
 
 using namespace ks;
@@ -161,8 +186,33 @@ int ks_segment_map_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
     return KS_OK;
 }
 
+
 int ks_count_shard_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end,
                          const int32_t* d_maps, int32_t rank, unsigned long long* d_counts) {
+    return count_shard_impl(ctx, dfa, seq, begin, end, d_maps, rank, d_counts, nullptr, 0u);
+}
+
+int ks_count_shard_async_signal(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end,
+                                const int32_t* d_maps, int32_t rank, unsigned long long* d_counts,
+                                uint32_t* d_signal, uint32_t signal_value) {
+    if (!d_signal) return fail(KS_E_INVALID, "null signal");
+    return count_shard_impl(ctx, dfa, seq, begin, end, d_maps, rank, d_counts, d_signal, signal_value);
+}
+
+int ks_stream_wait_value32(void* stream, const uint32_t* d_addr, uint32_t value) {
+    static const StreamValueFn fn = stream_value_fn("cuStreamWaitValue32");
+    if (!d_addr) return fail(KS_E_INVALID, "null address");
+    if (!fn) return fail(KS_E_UNSUPPORTED, "cuStreamWaitValue32 unavailable");
+    if (fn(static_cast<cudaStream_t>(stream), reinterpret_cast<unsigned long long>(d_addr), value, 0u /* GEQ */) != 0)
+        return fail(KS_E_CUDA, "cuStreamWaitValue32 failed");
+    return KS_OK;
+}
+
+}  // extern "C"
+
+int ks::count_shard_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, int64_t end,
+                         const int32_t* d_maps, int32_t rank, unsigned long long* d_counts, unsigned int* d_signal,
+                         unsigned int signal_value) {
     CtxLock lock_(ctx);
     if (!ctx || !dfa || !seq || !d_counts) return fail(KS_E_INVALID, "null argument");
     if (begin < 0 || end < begin || end > seq->n) return fail(KS_E_INVALID, "range out of bounds");
@@ -241,6 +291,8 @@ int ks_count_shard_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
             a.dyn_items = 1;   // fused: the finalizing CTA resets the dynamic-item counters
             a.fin_host = nullptr;
             a.n_expr = h.ne;
+            a.fin_signal = d_signal;   // the finalizing CTA raises the flag after the counts
+            a.fin_signal_value = signal_value;
         }
         rc = dispatch(ctx, dfa, dfa->scan, plan, a, kModeCount, &launches);
         if (rc) return rc;
@@ -250,11 +302,17 @@ int ks_count_shard_async(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
                                     nullptr, nullptr, &launches);
         if (rc) return rc;
         launches += 2;   // the memsets
+        if (d_signal) {   // no fused kernel raised it: a stream write after the finalize
+            rc = stream_write_value(ctx->stream, d_signal, signal_value);
+            if (rc) return rc;
+        }
     }
     ctx->async_launches += launches;
     ++ctx->async_calls;
     return KS_OK;
 }
+
+extern "C" {
 
 int ks_speculate(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int32_t n_chunks, const int64_t* chunk_begin,
                  const int64_t* chunk_end, const int64_t* pss_off, const int32_t* pss_data, int32_t window,

@@ -1009,10 +1009,11 @@ def test_dynamic_tiles_and_split_tails(monkeypatch, config):
 
 
 def test_pipelined_allreduce_single_rank_nccl():
-    """bench.py's overlapped per-step all-reduce (PipelinedAllReduce: two count
-    buffers, async NCCL collective, the stream waits before a buffer is
-    reused) on a one-rank NCCL group with the scan grid leaving SMs free
-    (ks_set_reserved_sms): every step's counts reach the pinned buffer."""
+    """bench.py's overlapped per-step all-reduce (PipelinedAllReduce: the scan
+    kernel raises a device flag, a side stream waits on it with
+    ks_stream_wait_value32 and runs the NCCL collective) on a one-rank NCCL
+    group with the scan grid leaving SMs free (ks_set_reserved_sms): every
+    step's counts reach their buffer and the last one the pinned buffer."""
     import socket
 
     import torch.distributed as dist
@@ -1042,16 +1043,48 @@ def test_pipelined_allreduce_single_rank_nccl():
         pin = torch.zeros(max(ne, 1), dtype=torch.int64).pin_memory()
         pipe = B.PipelinedAllReduce(ne, dev, pin)
         for _ in range(7):
-            buf = pipe.acquire()
-            c2.count_shard_async(dh, sh, 0, codes.size, 0, 0, buf.data_ptr())
-            pipe.launch(buf)
+            pipe.step(lambda cp, fp, v: c2.count_shard_async_signal(dh, sh, 0, codes.size, 0, 0, cp, fp, v))
         pipe.finish()
         c2.async_wait()
         torch.cuda.synchronize()
         assert pin.numpy()[:ne].tolist() == want.tolist()
         assert pipe.last().cpu().numpy()[:ne].tolist() == want.tolist()
+        assert int(pipe.flag.item()) == pipe.seq == 7
+        # every step's buffer holds that step's (identical) counts
+        assert all(pipe.bufs[k].cpu().numpy()[:ne].tolist() == want.tolist() for k in range(7))
         c2.set_reserved_sms(0)
         assert c2.count(dh, sh).tolist() == want.tolist()
     finally:
         torch.cuda.set_stream(prev)
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("generic", [False, True])
+def test_count_shard_signal_raises_flag(monkeypatch, generic):
+    """ks_count_shard_async_signal: the fused kernel's finalizing CTA (or, on
+    the multi-launch generic path, a stream write after the finalize) sets
+    the flag once the counts are final; a side stream gated by
+    ks_stream_wait_value32 reads the final counts."""
+    if generic:
+        monkeypatch.setenv("KS_DISABLE_FAST", "1")
+    w = workloads.make(2, 2_000_003)
+    codes = ks.encode_bytes(w.ascii.tobytes())
+    want = O.ref_sequential_count(w.dfa, codes)[0]
+    c2 = _native.DeviceContext(0)
+    dh = c2.dfa(w.dfa)
+    sh = c2.upload_codes(codes)
+    ne = w.dfa.n_expressions
+    dev = torch.device("cuda", 0)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    counts = torch.zeros(max(ne, 1), dtype=torch.int64, device=dev)
+    side = torch.cuda.Stream(dev)
+    got = torch.zeros_like(counts)
+    for v in (3, 4):
+        c2.count_shard_async_signal(dh, sh, 0, codes.size, 0, 0, counts.data_ptr(), flag.data_ptr(), v)
+        with torch.cuda.stream(side):
+            _native.DeviceContext.stream_wait_value32(side.cuda_stream, flag.data_ptr(), v)
+            got.copy_(counts)
+        side.synchronize()
+        assert got.cpu().numpy()[:ne].tolist() == want.tolist()
+        assert int(flag.item()) == v
+    c2.async_wait()
