@@ -249,7 +249,10 @@ int ks::count_shard_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
         if (h.n_accept > 0) KS_CUDA(cudaMemsetAsync(visits, 0, size_t(h.n_accept) * 8, ctx->stream));
         KS_CUDA(cudaMemsetAsync(d_counts, 0, size_t(std::max(h.ne, 1)) * 8, ctx->stream));
     }
-    if (!halo) {
+    // rank 0 enters in START: a constant, so no compose launch and (LOOKBACK)
+    // a scan whose wait for the preceding kernel is deferred
+    const bool const_entry = !halo && rank == 0;
+    if (!halo && !const_entry) {
         compose_entry_kernel<<<1, 1, 0, ctx->stream>>>(d_maps, h.nq, rank, 0, dfa->d_new_of_old, entry);
         KS_CUDA(cudaGetLastError());
     }
@@ -266,19 +269,21 @@ int ks::count_shard_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int6
             uint16_t* elems = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
             uint16_t* centry = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
             uint16_t* mtot = static_cast<uint16_t*>(ar.take(16));
-            rc = monoid_prefix(ctx, dfa, seq, begin, end, origin, L, nch, elems, centry, 0, entry, mtot, &launches);
+            rc = monoid_prefix(ctx, dfa, seq, begin, end, origin, L, nch, elems, centry,
+                               const_entry ? h.start_internal : 0, const_entry ? nullptr : entry, mtot, &launches);
             if (rc) return rc;
             a.chunk_entry = centry;
         } else if (spec) {
             uint16_t* centry = static_cast<uint16_t*>(ar.take(size_t(nch) * 2));
-            rc = spec_entries(ctx, dfa, seq, begin, end, origin, L, nch, -1, entry, centry, nullptr, &launches);
+            rc = spec_entries(ctx, dfa, seq, begin, end, origin, L, nch, const_entry ? h.start_internal : -1,
+                              const_entry ? nullptr : entry, centry, nullptr, &launches);
             if (rc) return rc;
             a.chunk_entry = centry;
         } else {
             a.lookback = h.sync_depth;
             a.base_pos = halo ? 0 : begin;   // halo: every chunk, the first included, looks back
             a.base_state = h.start_internal;
-            a.base_state_ptr = halo ? nullptr : entry;
+            a.base_state_ptr = (halo || const_entry) ? nullptr : entry;
             a.any_state = h.start_internal;
         }
         if (fused) {
