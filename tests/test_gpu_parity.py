@@ -1088,3 +1088,37 @@ def test_count_shard_signal_raises_flag(monkeypatch, generic):
         assert got.cpu().numpy()[:ne].tolist() == want.tolist()
         assert int(flag.item()) == v
     c2.async_wait()
+
+
+def test_back_to_back_dynamic_and_deferred_wait(monkeypatch):
+    """Back-to-back async counts (deferred griddepcontrol.wait: each scan
+    starts while the previous call drains) alternating automata, sequences
+    and the static / dynamic item paths (> 6 rounds of tiles at 64-base
+    units), interleaved with signalled shard counts and a MAPSCAN call: every
+    call's counts are the oracle's."""
+    monkeypatch.setenv("KS_TILE_LB", "0")
+    ctx = _native.DeviceContext(0)
+    work = []
+    for cfg, n in ((3, 60_000_013), (4, 60_000_011), (2, 3_000_017), (5, 1_000_003)):
+        w = workloads.make(cfg, n)
+        codes = ks.encode_bytes(w.ascii.tobytes())
+        want = O.ref_run(w.dfa, codes, 16 if cfg != 5 else 1, 10, False)[0]
+        work.append((ctx.dfa(w.dfa), ctx.upload_codes(codes), want, codes.size))
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    outs = []
+    v = 0
+    for rep in range(3):
+        for dh, sh, want, n in work:
+            buf = torch.zeros(max(dh.n_expressions, 1), dtype=torch.int64).pin_memory()
+            ctx.count_async(dh, sh, buf.numpy())
+            outs.append((buf, want))
+            if dh.info["strategy_name"] == "lookback":
+                v += 1
+                dbuf = torch.zeros(max(dh.n_expressions, 1), dtype=torch.int64, device="cuda")
+                ctx.count_shard_async_signal(dh, sh, 0, n, 0, 0, dbuf.data_ptr(), flag.data_ptr(), v)
+                outs.append((dbuf, want))
+    ctx.async_wait()
+    torch.cuda.synchronize()
+    assert int(flag.item()) == v
+    for buf, want in outs:
+        assert buf.cpu().numpy()[: want.size].tolist() == want.tolist()
