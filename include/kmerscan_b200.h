@@ -181,6 +181,10 @@ KS_API int ks_pack_host_ascii(const uint8_t* bytes, int64_t n_bytes, int32_t lb,
  * bases[2g..2g+1] 2-bit codes, special[g] a mask of non-base positions --
  * code 01 = dropped (whitespace, header line, past the end), code 00 =
  * OTHER.  *kept = retained symbols. */
+/* The host side of the packed codes upload (ks_seq_upload_codes of >= 8 Mi
+ * symbols) on its own: codes 0..4 -> the tile-slot layout of
+ * ks_pack_host_ascii (no GPU needed); KS_E_INVALID for a code above 4. */
+KS_API int ks_pack_host_codes(const uint8_t* codes, int64_t n, int32_t lb, uint64_t* bases, uint64_t* nmask);
 KS_API int ks_pack_host_wire(const uint8_t* bytes, int64_t n_bytes, int32_t fasta, uint64_t* bases,
                              uint64_t* special, int64_t* kept);
 

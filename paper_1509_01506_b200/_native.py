@@ -60,7 +60,7 @@ EXPORTED = (
     "ks_seq_upload_codes", "ks_seq_upload_ascii", "ks_seq_encode_device", "ks_seq_length",
     "ks_seq_download_codes", "ks_seq_download_softmask", "ks_seq_free", "ks_count", "ks_locate",
     "ks_count_host_ascii", "ks_count_async", "ks_async_wait", "ks_segment_map_async",
-    "ks_count_shard_async", "ks_count_shard_async_signal", "ks_stream_wait_value32", "ks_pack_host_ascii", "ks_count_host_bytes", "ks_pack_host_wire",
+    "ks_count_shard_async", "ks_count_shard_async_signal", "ks_stream_wait_value32", "ks_pack_host_ascii", "ks_pack_host_codes", "ks_count_host_bytes", "ks_pack_host_wire",
     "ks_scan_range", "ks_segment_map", "ks_speculate", "ks_free",
     "ks_open_multi", "ks_close_multi", "ks_multi_info", "ks_mdfa_upload", "ks_mdfa_free",
     "ks_mseq_upload_codes", "ks_mseq_upload_ascii", "ks_mseq_length", "ks_mseq_free", "ks_mcount",
@@ -105,6 +105,7 @@ def _declare(lib) -> None:
         "ks_count_async": (C.c_int, [_P, _P, _P, _i64p]),
         "ks_pack_host_ascii": (C.c_int, [_u8p, C.c_int64, C.c_int32, _P, _P, _i32p]),
         "ks_pack_host_wire": (C.c_int, [_u8p, C.c_int64, C.c_int32, _P, _P, _i64p]),
+        "ks_pack_host_codes": (C.c_int, [_u8p, C.c_int64, C.c_int32, _P, _P]),
         "ks_segment_map_async": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, _P]),
         "ks_count_shard_async": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, _P, C.c_int32, _P]),
         "ks_count_shard_async_signal": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, _P, C.c_int32, _P, _P,
@@ -489,6 +490,20 @@ def pack_host_ascii(data, lb: int) -> tuple[np.ndarray, np.ndarray, int]:
     _check(library().ks_pack_host_ascii(_ptr(buf, C.c_uint8), int(arr.size), int(lb), bases.ctypes.data,
                                         nmask.ctypes.data, C.byref(flags)))
     return bases, nmask, int(flags.value)
+
+
+def pack_host_codes(codes, lb: int) -> tuple[np.ndarray, np.ndarray]:
+    """The codes upload's host packer on its own (no GPU needed): symbol codes
+    0..4 -> (bases uint64[2*slots], nmask uint64[slots]) in tile-slot order."""
+    arr = np.ascontiguousarray(np.asarray(codes, dtype=np.uint8))
+    tile = 32 << lb
+    slots = max(-(-((arr.size + 63) // 64) // tile) * tile, 1)
+    bases = np.zeros(2 * slots, dtype=np.uint64)
+    nmask = np.zeros(slots, dtype=np.uint64)
+    buf = arr if arr.size else np.zeros(1, dtype=np.uint8)
+    _check(library().ks_pack_host_codes(_ptr(buf, C.c_uint8), int(arr.size), int(lb), bases.ctypes.data,
+                                        nmask.ctypes.data))
+    return bases, nmask
 
 
 def pack_host_wire(data, fasta: bool) -> tuple[np.ndarray, np.ndarray, int]:

@@ -185,6 +185,76 @@ bool has_avx512bw() {
 
 }  // namespace
 
+namespace {
+
+inline bool pack_codes_block_scalar(const uint8_t* p, int lim, uint64_t* w, uint64_t* nm) {
+    uint64_t w0 = 0, w1 = 0, n = 0;
+    bool ok = true;
+    for (int i = 0; i < lim; ++i) {
+        const uint8_t c = p[i];
+        ok &= c <= 4;
+        const uint64_t code = c & 3u;
+        if (i < 32) w0 |= code << (2 * i);
+        else w1 |= code << (2 * (i - 32));
+        n |= uint64_t(c == 4) << i;
+    }
+    w[0] = w0;
+    w[1] = w1;
+    *nm = n;
+    return ok;
+}
+
+// 64 codes -> 16 B of bases (code & 3; OTHER = 4 packs as 0) + the OTHER mask;
+// the same madd packing as the ASCII path after its classification.
+__attribute__((target("avx512f,avx512bw"))) bool pack_codes_avx512(const uint8_t* in, int64_t b0, int64_t b1,
+                                                                    int lb, uint64_t* bases, uint64_t* nmask,
+                                                                    int64_t sbase) {
+    const __m512i k3 = _mm512_set1_epi8(3), k4 = _mm512_set1_epi8(4);
+    const __m512i m16 = _mm512_set1_epi16(0x0401), m32 = _mm512_set1_epi32(0x00100001);
+    const int64_t umask = (int64_t(1) << lb) - 1;
+    __mmask64 bad = 0;
+    int64_t s = blk_slot(b0, lb) - sbase;
+    static const int pf = std::getenv("KS_PACK_PREFETCH") ? std::atoi(std::getenv("KS_PACK_PREFETCH")) : 8192;
+    for (int64_t b = b0; b < b1; ++b) {
+        if (pf) _mm_prefetch(reinterpret_cast<const char*>(in + (b << 6) + pf), _MM_HINT_T0);
+        const __m512i x = _mm512_loadu_si512(in + (b << 6));
+        bad |= _mm512_cmpgt_epu8_mask(x, k4);
+        const __mmask64 other = _mm512_cmpeq_epi8_mask(x, k4);
+        const __m512i code = _mm512_and_si512(x, k3);
+        const __m512i p32 = _mm512_madd_epi16(_mm512_maddubs_epi16(code, m16), m32);
+        _mm_storeu_si128(reinterpret_cast<__m128i*>(bases + 2 * s), _mm512_cvtepi32_epi8(p32));
+        nmask[s] = uint64_t(other);
+        s = ((b + 1) & umask) ? s + 32 : blk_slot(b + 1, lb) - sbase;
+    }
+    return bad == 0;
+}
+
+}  // namespace
+
+bool pack_codes_blocks(const uint8_t* codes, int64_t n, int64_t b0, int64_t b1, int lb, uint64_t* bases,
+                       uint64_t* nmask, int64_t sbase) {
+    bool ok = true;
+    const int64_t full = std::min(b1, n >> 6);
+    int64_t b = b0;
+    if (b < full) {
+        if (has_avx512bw()) {
+            ok = pack_codes_avx512(codes, b, full, lb, bases, nmask, sbase);
+        } else {
+            for (int64_t k = b; k < full; ++k) {
+                const int64_t s = blk_slot(k, lb) - sbase;
+                ok &= pack_codes_block_scalar(codes + (k << 6), 64, bases + 2 * s, nmask + s);
+            }
+        }
+        b = full;
+    }
+    for (; b < b1; ++b) {
+        const int64_t s = blk_slot(b, lb) - sbase;
+        const int lim = int(std::max<int64_t>(0, std::min<int64_t>(64, n - (b << 6))));
+        ok &= pack_codes_block_scalar(codes + (b << 6), lim, bases + 2 * s, nmask + s);
+    }
+    return ok;
+}
+
 PackFlags pack_ascii_blocks(const uint8_t* in, int64_t n_bytes, int64_t b0, int64_t b1, int lb,
                             uint64_t* bases, uint64_t* nmask, int64_t sbase) {
     PackFlags f;

@@ -54,6 +54,12 @@ struct PackFlags {
 PackFlags pack_ascii_blocks(const uint8_t* in, int64_t n_bytes, int64_t b0, int64_t b1, int lb,
                             uint64_t* bases, uint64_t* nmask, int64_t sbase = 0);
 
+// Symbol codes (0..4, Sequence.symbols) instead of ASCII: code & 3 the base,
+// 4 OTHER; blocks [b0, b1) -> slot blk_slot(b, lb) - sbase as above, codes
+// past n encode as base 0.  Returns false when a code above 4 was seen.
+bool pack_codes_blocks(const uint8_t* codes, int64_t n, int64_t b0, int64_t b1, int lb, uint64_t* bases,
+                       uint64_t* nmask, int64_t sbase = 0);
+
 // Streaming-path form, whole tiles [t0, t1) (tile = 32 << lb blocks): each
 // tile is packed in a thread-local buffer, its bases streamed (non-temporal
 // stores) to `bases` in slot order; a tile holding OTHER appends its OTHER

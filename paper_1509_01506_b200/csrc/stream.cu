@@ -352,6 +352,15 @@ int ks_pack_host_ascii(const uint8_t* bytes, int64_t n_bytes, int32_t lb, uint64
     return KS_OK;
 }
 
+int ks_pack_host_codes(const uint8_t* codes, int64_t n, int32_t lb, uint64_t* bases, uint64_t* nmask) {
+    if (n < 0 || (n > 0 && (!codes || !bases || !nmask)) || lb < 0 || lb > 12) return fail(KS_E_INVALID, "bad argument");
+    const int64_t tb = int64_t(32) << lb;
+    const int64_t used = (n + 63) / 64 + tb - 1 - ((n + 63) / 64 + tb - 1) % tb;
+    if (!pack_codes_blocks(codes, n, 0, used, lb, bases, nmask))
+        return fail(KS_E_INVALID, "symbol code out of range (expected 0..4)");
+    return KS_OK;
+}
+
 int ks_pack_host_wire(const uint8_t* bytes, int64_t n_bytes, int32_t fasta, uint64_t* bases, uint64_t* special,
                       int64_t* kept) {
     if (n_bytes < 0 || (n_bytes > 0 && (!bytes || !bases || !special)) || !kept)

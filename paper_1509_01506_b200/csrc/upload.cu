@@ -4,6 +4,7 @@
 // lane-tiled bases + OTHER / soft-mask bitmaps, from codes, host ASCII or
 // device bytes through the encode kernels), plus their download helpers.
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -102,6 +103,66 @@ void seq_destroy(ks_seq* s) {
 }  // namespace ks
 
 using namespace ks;
+
+namespace ks {
+// Codes (1 B/symbol, often pageable numpy memory) packed on the host by the
+// worker pool into the tile-slot layout (0.375 B/symbol) in the pinned
+// staging ring, pieces of whole tiles copied on the copy stream while the
+// next piece is packed: a pageable 1 B/symbol copy runs at a fraction of the
+// link, the packed wire at the link rate.
+int upload_codes_host(ks_ctx* ctx, const uint8_t* codes, int64_t n, ks_seq* s) {
+    const int64_t tb = int64_t(32) << s->lb;   // blocks per tile
+    const int64_t nb = (n + 63) / 64;
+    const int64_t ntiles = (nb + tb - 1) / tb;
+    const int64_t tiles_per_piece = std::max<int64_t>(1, (int64_t(64) << 20) / 64 / tb);
+    const int64_t piece_slots = tiles_per_piece * tb;
+    const size_t stage = up(size_t(piece_slots) * 24);
+    if (!ctx->copy_stream) {
+        KS_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        for (auto& e : ctx->sev) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (auto& e : ctx->hev) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    if (ctx->hstage_bytes < 3 * stage) {
+        KS_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+        if (ctx->hstage) KS_CUDA(cudaFreeHost(ctx->hstage));
+        ctx->hstage = nullptr;
+        ctx->hstage_bytes = 0;
+        KS_CUDA(cudaMallocHost(&ctx->hstage, 3 * stage));
+        ctx->hstage_bytes = 3 * stage;
+    }
+    if (!ctx->pool) ctx->pool = new HostPool(host_pack_threads());
+    // the sequence's zeroing memset (seq_alloc, compute stream) precedes the copies
+    KS_CUDA(cudaEventRecord(ctx->sev[2], ctx->stream));
+    KS_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->sev[2], 0));
+    std::atomic<int> bad{0};
+    const int64_t npieces = (ntiles + tiles_per_piece - 1) / tiles_per_piece;
+    for (int64_t p = 0; p < npieces; ++p) {
+        const int st = int(p % 3);
+        uint64_t* hb = reinterpret_cast<uint64_t*>(static_cast<char*>(ctx->hstage) + st * stage);
+        uint64_t* hn = hb + 2 * piece_slots;
+        if (p >= 3) KS_CUDA(cudaEventSynchronize(ctx->hev[st]));   // staging slot free again
+        const int64_t t0 = p * tiles_per_piece, t1 = std::min(ntiles, t0 + tiles_per_piece);
+        const int64_t sbase = t0 * tb;
+        constexpr int64_t kTilesPerTask = 4;
+        ctx->pool->run((t1 - t0 + kTilesPerTask - 1) / kTilesPerTask, [&](int64_t k) {
+            const int64_t a0 = t0 + k * kTilesPerTask, a1 = std::min(t1, a0 + kTilesPerTask);
+            if (!pack_codes_blocks(codes, n, a0 * tb, a1 * tb, s->lb, hb, hn, sbase)) bad.store(1);
+        });
+        const size_t ns = size_t(t1 - t0) * size_t(tb);
+        KS_CUDA(cudaMemcpyAsync(s->d_bases + 2 * sbase, hb, ns * 16, cudaMemcpyHostToDevice, ctx->copy_stream));
+        KS_CUDA(cudaMemcpyAsync(s->d_nmask + sbase, hn, ns * 8, cudaMemcpyHostToDevice, ctx->copy_stream));
+        KS_CUDA(cudaEventRecord(ctx->hev[st], ctx->copy_stream));
+    }
+    // later work on the compute stream sees the sequence
+    KS_CUDA(cudaEventRecord(ctx->sev[2], ctx->copy_stream));
+    KS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->sev[2], 0));
+    KS_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+    if (bad.load()) return fail(KS_E_INVALID, "symbol code out of range (expected 0..4)");
+    s->n = n;
+    return KS_OK;
+}
+
+}  // namespace ks
 
 extern "C" {
 
@@ -257,6 +318,15 @@ int ks_seq_upload_codes(ks_ctx* ctx, const uint8_t* codes, int64_t n, ks_seq** o
     ks_seq* s = nullptr;
     int rc = seq_alloc(ctx, n, &s);
     if (rc) return rc;
+    if (n >= (int64_t(8) << 20) && !env_flag("KS_DEVICE_PACK_CODES")) {   // host-packed wire, pipelined
+        rc = upload_codes_host(ctx, codes, n, s);
+        if (rc) {
+            seq_destroy(s);
+            return rc;
+        }
+        *out = s;
+        return KS_OK;
+    }
     Arena ar;
     rc = ensure_scratch(ctx, size_t(n) + 1024, &ar);
     if (rc) {

@@ -1122,3 +1122,28 @@ def test_back_to_back_dynamic_and_deferred_wait(monkeypatch):
     assert int(flag.item()) == v
     for buf, want in outs:
         assert buf.cpu().numpy()[: want.size].tolist() == want.tolist()
+
+
+def test_upload_codes_host_packed(monkeypatch):
+    """ks_seq_upload_codes of >= 8 Mi symbols packs on the host (worker pool,
+    pinned staging ring, pieces copied while the next is packed): the
+    sequence equals the device-packed one (counts, locate rows, ranges) and a
+    code above 4 is rejected."""
+    w = workloads.make(4, 20_000_003)
+    codes = ks.encode_bytes(w.ascii.tobytes())
+    want, want_rows = O.ref_run(w.dfa, codes, 16, 10, True)[:2]
+    c2 = _native.DeviceContext(0)
+    dh = c2.dfa(w.dfa)
+    sh = c2.upload_codes(codes)
+    monkeypatch.setenv("KS_DEVICE_PACK_CODES", "1")
+    sd = c2.upload_codes(codes)
+    monkeypatch.delenv("KS_DEVICE_PACK_CODES")
+    for h in (sh, sd):
+        got, rows = c2.locate(dh, h)
+        assert got.tolist() == want.tolist() and np.array_equal(rows, want_rows)
+    b, e = 1_234_567, 17_654_321
+    assert c2.scan_range(dh, sh, b, e, 5)[0].tolist() == c2.scan_range(dh, sd, b, e, 5)[0].tolist()
+    bad = codes.copy()
+    bad[9_999_999] = 7
+    with pytest.raises(ValueError, match="out of range"):
+        c2.upload_codes(bad)

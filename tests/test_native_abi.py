@@ -176,3 +176,35 @@ def test_host_wire_packer(k, fasta):
     assert int(out[-1]) == want.size
     nb = special.size
     assert _wire_decode(out[:2 * nb], out[2 * nb:3 * nb], len(data)).tolist() == want.tolist()
+
+
+@pytest.mark.parametrize("n,lb", [(0, 0), (1, 0), (63, 1), (64, 2), (200_003, 3), (70_001, 4)])
+@pytest.mark.parametrize("scalar", [False, True])
+def test_host_codes_packer_matches_ascii_packer(n, lb, scalar):
+    """ks_pack_host_codes (the packed codes upload's host side; AVX-512 and
+    scalar paths) gives the ASCII packer's tile-slot output for the same
+    sequence spelled ACGTN, padding included; a code above 4 is rejected."""
+    rng = np.random.default_rng(n + 17 * lb)
+    codes = rng.choice(np.array([0, 1, 2, 3, 4], dtype=np.uint8), size=n, p=[0.24, 0.24, 0.24, 0.24, 0.04])
+    ascii_ = np.frombuffer(b"ACGTN", dtype=np.uint8)[codes].tobytes()
+    want_b, want_m, _ = _native.pack_host_ascii(ascii_, lb)
+    if scalar:
+        code = ("import sys, numpy as np; from paper_1509_01506_b200 import _native;"
+                f"b, m = _native.pack_host_codes(np.load(sys.argv[1]), {lb});"
+                "np.save(sys.argv[2], np.concatenate([b, m]))")
+        import tempfile
+        with tempfile.TemporaryDirectory() as d:
+            np.save(Path(d, "in.npy"), codes)
+            env = dict(__import__("os").environ, KS_HOST_SCALAR="1")
+            subprocess.run([sys.executable, "-c", code, str(Path(d, "in.npy")), str(Path(d, "out.npy"))],
+                           check=True, env=env, cwd=REPO)
+            out = np.load(Path(d, "out.npy"))
+        got_b, got_m = out[:want_b.size], out[want_b.size:]
+    else:
+        got_b, got_m = _native.pack_host_codes(codes, lb)
+    assert np.array_equal(got_b, want_b) and np.array_equal(got_m, want_m)
+    if n:
+        bad = codes.copy()
+        bad[n // 2] = 5
+        with pytest.raises(ValueError, match="out of range"):
+            _native.pack_host_codes(bad, lb)
