@@ -85,11 +85,22 @@ bool host_is_device_visible(const void* p) {
 namespace {
 
 // ------------------------------------------------------------ tiny kernels
+// Rows [0, *n_dev) into pinned host staging; with res_src, block 0 also
+// copies the results block (counts | err | exit, res_words words) and the
+// row / log totals to pinned memory, so one synchronisation returns all.
 __global__ void copy_rows_kernel(const longlong2* __restrict__ src, const int64_t* __restrict__ n_dev,
-                                 longlong2* __restrict__ dst) {
+                                 longlong2* __restrict__ dst, const unsigned int* res_src, uint32_t res_words,
+                                 unsigned int* res_dst, const unsigned long long* log_n, int64_t* tot_dst) {
     const int64_t n = *n_dev;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
         dst[i] = src[i];
+    if (res_src && blockIdx.x == 0) {
+        for (uint32_t i = threadIdx.x; i < res_words; i += blockDim.x) res_dst[i] = __ldcg(&res_src[i]);
+        if (threadIdx.x == 0) {
+            tot_dst[0] = n;
+            tot_dst[1] = int64_t(__ldcg(log_n));
+        }
+    }
 }
 
 template <class T>   // T: uint16_t tables, uint32_t for wide automata
@@ -428,7 +439,7 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
     const bool use_log = locate && plan.fast && nch > 0 && dfa->scan.hit_rate * double(end - begin) < 0.5 * double(cap);
     unsigned long long* log_n = nullptr;
     if (use_log) {
-        const size_t bytes = size_t(cap) * sizeof(LogEntry) + 64;
+        const size_t bytes = size_t(cap) * sizeof(LogEntry) + 64 + 4096 * 4;   // entries | total | per-CTA counts
         if (ctx->log_bytes < bytes) {
             KS_CUDA(cudaStreamSynchronize(ctx->stream));
             if (ctx->log_buf) KS_CUDA(cudaFree(ctx->log_buf));
@@ -441,6 +452,7 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
         KS_CUDA(cudaMemsetAsync(log_n, 0, 8, ctx->stream));
         a.log = static_cast<LogEntry*>(ctx->log_buf);
         a.log_n = log_n;
+        a.log_cta_n = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(log_n) + 64);
         a.log_cap = cap;
     }
     // plain counts on the fast kernel: its last CTA finalizes (one launch per call)
@@ -502,23 +514,32 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
         if (staged) {
             rc = exclusive_scan_rows(ctx, chunk_rows, nch, row_off, row_off + nch, rows_tmp, &launches);
             if (rc) return rc;
-            rc = launch_log_scatter(ctx, a.log, a.log_cap, log_n, row_off, dfa->d_acc_out_off, dfa->d_acc_out_ids,
-                                    static_cast<int64_t*>(ctx->rdev), &launches);
+            rc = launch_log_scatter(ctx, a.log, a.log_cta_n, ctx->log_segs, ctx->log_part, log_n, a.log_cap, row_off,
+                                    dfa->d_acc_out_off, dfa->d_acc_out_ids, static_cast<int64_t*>(ctx->rdev),
+                                    &launches);
             if (rc) return rc;
-            // rows [0, total) -> pinned host memory, coalesced (the total is read on the device)
-            copy_rows_kernel<<<std::max(1, std::min(ctx->num_sms * 4, int((a.log_cap + 255) / 256))), 256, 0,
-                               ctx->stream>>>(static_cast<const longlong2*>(ctx->rdev), row_off + nch,
-                                              static_cast<longlong2*>(ctx->rstage));
-            KS_CUDA(cudaGetLastError());
-            ++launches;
-            trace.mark("rows (staged)");
             rc = ensure_pinned(ctx, size_t(std::max(h.ne, 1)) * 8 + 64 + 16);
             if (rc) return rc;
             char* pin = static_cast<char*>(ctx->pinned);
             int64_t* tot = reinterpret_cast<int64_t*>(pin + size_t(std::max(h.ne, 1)) * 8 + 32);
-            KS_CUDA(cudaMemcpyAsync(pin, counts, res_bytes, cudaMemcpyDeviceToHost, ctx->stream));
-            KS_CUDA(cudaMemcpyAsync(tot, row_off + nch, 8, cudaMemcpyDeviceToHost, ctx->stream));
-            KS_CUDA(cudaMemcpyAsync(tot + 1, log_n, 8, cudaMemcpyDeviceToHost, ctx->stream));
+            // rows [0, total) -> pinned host memory, coalesced (the total is read
+            // on the device); the same kernel writes counts | err | exit, the
+            // row total and the log total there (no copy operations to wait on)
+            const bool dev_visible = host_is_device_visible(pin);
+            copy_rows_kernel<<<std::max(1, std::min(ctx->num_sms * 4, int((a.log_cap + 255) / 256))), 256, 0,
+                               ctx->stream>>>(static_cast<const longlong2*>(ctx->rdev), row_off + nch,
+                                              static_cast<longlong2*>(ctx->rstage),
+                                              dev_visible ? reinterpret_cast<const unsigned int*>(counts) : nullptr,
+                                              uint32_t(res_bytes / 4), reinterpret_cast<unsigned int*>(pin), log_n,
+                                              tot);
+            KS_CUDA(cudaGetLastError());
+            ++launches;
+            trace.mark("rows (staged)");
+            if (!dev_visible) {
+                KS_CUDA(cudaMemcpyAsync(pin, counts, res_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+                KS_CUDA(cudaMemcpyAsync(tot, row_off + nch, 8, cudaMemcpyDeviceToHost, ctx->stream));
+                KS_CUDA(cudaMemcpyAsync(tot + 1, log_n, 8, cudaMemcpyDeviceToHost, ctx->stream));
+            }
             KS_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
             KS_CUDA(cudaStreamSynchronize(ctx->stream));
             trace.mark("sync");
@@ -560,8 +581,8 @@ int scan_impl(ks_ctx* ctx, const ks_dfa* dfa, const ks_seq* seq, int64_t begin, 
         trace.mark("sync totals");
         if (total_rows > 0 && use_log && logged <= (unsigned long long)a.log_cap) {
             KS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_rows), size_t(total_rows) * 16, ctx->stream));
-            rc = launch_log_scatter(ctx, a.log, int64_t(logged), nullptr, row_off, dfa->d_acc_out_off,
-                                    dfa->d_acc_out_ids, d_rows, &launches);
+            rc = launch_log_scatter(ctx, a.log, a.log_cta_n, ctx->log_segs, ctx->log_part, log_n, a.log_cap, row_off,
+                                    dfa->d_acc_out_off, dfa->d_acc_out_ids, d_rows, &launches);
             if (rc) {
                 cudaFreeAsync(d_rows, ctx->stream);
                 return rc;

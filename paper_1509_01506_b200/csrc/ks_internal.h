@@ -193,6 +193,8 @@ struct ks_ctx {
     unsigned int* wctr = nullptr;   // task counter of the wide count kernel
     unsigned int* tctr = nullptr;   // dynamic-item counters of the fast count kernel (32 x 128 B)
     size_t log_bytes = 0;
+    int32_t log_segs = 0;           // segments (scan CTAs) of the last logged scan
+    int64_t log_part = 0;           // entries per segment
     // ks_count_async: one event pair per call until ks_async_wait
     std::vector<cudaEvent_t> aev;
     int n_async = 0;            // per-call event pairs in use (KS_ASYNC_EVENTS=1)

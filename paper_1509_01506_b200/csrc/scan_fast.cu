@@ -154,9 +154,9 @@ struct Ctx {
     uint32_t ring_thr;  // drain when a lane holds this many ring bytes (depth - chk_steps(K) entries)
     uint32_t t1_cols;   // 4 or 5
     uint32_t reset;     // OTHER target when t1_cols == 4
-    LogEntry* log;
-    unsigned long long* log_n;
-    int64_t log_cap;
+    LogEntry* log;       // this CTA's segment of the visit log
+    uint32_t log_slot;   // shared address of the CTA's visit counter
+    uint32_t log_part;   // entries per segment
 };
 
 template <int MODE>
@@ -183,8 +183,11 @@ __device__ __forceinline__ void record(const Ctx& c, Lane<MODE>& L, int64_t pos,
         red_shared_add(c.hist + 4u * s, 1u);
         const uint32_t local = L.nrows;
         L.nrows += __ldg(&c.outcnt[s]);
-        const unsigned long long i = atomicAdd(c.log_n, 1ull);
-        if (i < (unsigned long long)c.log_cap) {
+        // a slot in this CTA's segment (a shared-memory counter: one global
+        // counter serialised every visit of the grid)
+        uint32_t i;
+        asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(i) : "r"(c.log_slot) : "memory");
+        if (i < c.log_part) {
             LogEntry e;
             e.pos1 = c.row_base + pos + 1;
             e.chunk = L.ch;
@@ -444,8 +447,12 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     c.t1_cols = opaque(uint32_t(a.t1_cols));
     c.reset = uint32_t(a.reset_state);
     c.log = a.log;
-    c.log_n = a.log_n;
-    c.log_cap = a.log_cap;
+    __shared__ unsigned int s_logn;
+    c.log = a.log ? a.log + size_t(blockIdx.x) * uint32_t(a.log_part) : nullptr;
+    c.log_slot = smem_addr(&s_logn);
+    c.log_part = uint32_t(a.log_part);
+    if (MODE == kModeLog && threadIdx.x == 0) s_logn = 0u;
+    __syncthreads();
     const uint32_t idle = 0;  // state of lanes without work (their hits are masked)
     const uint32_t ring_stride = kRingStride;
     const uint32_t rp0 = smem_addr(p_ring) + 4u * threadIdx.x;
@@ -702,6 +709,14 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
             if (s_hist[i]) atomicAdd(&a.visits[i], (unsigned long long)s_hist[i]);
     }
     __syncthreads();
+    if constexpr (MODE == kModeLog) {
+        if (threadIdx.x == 0) {   // the segment's length; an overflowing segment poisons the total
+            const unsigned int nlog = s_logn;
+            a.log_cta_n[blockIdx.x] = nlog;
+            atomicAdd(a.log_n, nlog <= uint32_t(a.log_part) ? (unsigned long long)nlog
+                                                             : (unsigned long long)a.log_cap + 1ull);
+        }
+    }
     kt_mark(a.ktime, 6, true);
     kt_mark(a.ktime, 7, false);
     if (a.ktime == 2 && threadIdx.x == 0 && blockIdx.x < 1024) {
@@ -769,15 +784,17 @@ FastFn pick_mode(int mode, bool lean) {
     return nullptr;
 }
 
-__global__ void log_scatter_kernel(const LogEntry* __restrict__ log, int64_t n, const unsigned long long* n_dev,
-                                   const int64_t* __restrict__ row_off, const int32_t* __restrict__ off,
-                                   const int32_t* __restrict__ ids, int64_t* __restrict__ rows) {
-    if (n_dev) {   // entries logged on the device; none when the log overflowed (n = capacity)
-        const unsigned long long v = *n_dev;
-        n = v <= (unsigned long long)n ? int64_t(v) : 0;
-    }
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const LogEntry e = log[i];
+// One block per log segment (one per scan CTA): entry i < seg_n[b] of
+// segment b; nothing when the log overflowed (*n_dev > cap).
+__global__ void log_scatter_kernel(const LogEntry* __restrict__ log, int64_t part, const unsigned int* seg_n,
+                                   const unsigned long long* n_dev, int64_t cap, const int64_t* __restrict__ row_off,
+                                   const int32_t* __restrict__ off, const int32_t* __restrict__ ids,
+                                   int64_t* __restrict__ rows) {
+    if (*n_dev > (unsigned long long)cap) return;
+    const int64_t n = seg_n[blockIdx.x];
+    const LogEntry* seg = log + int64_t(blockIdx.x) * part;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const LogEntry e = seg[i];
         const int64_t base = row_off[e.chunk] + e.local;
         const int k0 = off[e.state], k1 = off[e.state + 1];
         for (int k = k0; k < k1; ++k) {
@@ -838,13 +855,12 @@ int fast_warps_per_cta(int64_t tiles, int num_sms) {
     return warps;
 }
 
-int launch_log_scatter(ks_ctx* ctx, const LogEntry* log, int64_t n, const unsigned long long* n_dev,
-                       const int64_t* row_off, const int32_t* acc_out_off, const int32_t* acc_out_ids, int64_t* rows,
-                       int* launches) {
-    if (n <= 0) return KS_OK;
-    const int threads = 256;
-    const int blocks = int(max64(1, min64((n + threads - 1) / threads, int64_t(ctx->num_sms) * 8)));
-    log_scatter_kernel<<<blocks, threads, 0, ctx->stream>>>(log, n, n_dev, row_off, acc_out_off, acc_out_ids, rows);
+int launch_log_scatter(ks_ctx* ctx, const LogEntry* log, const unsigned int* seg_n, int32_t segs, int64_t part,
+                       const unsigned long long* n_dev, int64_t cap, const int64_t* row_off, const int32_t* acc_out_off,
+                       const int32_t* acc_out_ids, int64_t* rows, int* launches) {
+    if (segs <= 0) return KS_OK;
+    log_scatter_kernel<<<segs, 256, 0, ctx->stream>>>(log, part, seg_n, n_dev, cap, row_off, acc_out_off, acc_out_ids,
+                                                      rows);
     if (launches) ++*launches;
     KS_CUDA(cudaGetLastError());
     return KS_OK;
@@ -924,6 +940,11 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
     }
     const int64_t need = (tiles + warps - 1) / warps;
     const int blocks = int(max64(1, min64(need, int64_t(ctx->num_sms))));
+    if (mode == kModeLog) {   // the visit log: one segment per CTA
+        a.log_part = a.log_cap / blocks;
+        ctx->log_segs = blocks;
+        ctx->log_part = a.log_part;
+    }
     if constexpr (KS_PDL) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(unsigned(blocks));

@@ -96,9 +96,11 @@ struct ScanArgs {
     // that holds OTHER (the table resets to the identity there) exits with
     // map_dirty[element since its last OTHER]
     const uint16_t* map_dirty = nullptr;
-    LogEntry* log = nullptr;                // kModeLog
-    unsigned long long* log_n = nullptr;    // kModeLog: visits appended (may exceed log_cap)
+    LogEntry* log = nullptr;                // kModeLog: log_cap entries, one segment of log_part per CTA
+    unsigned long long* log_n = nullptr;    // kModeLog: total logged (> log_cap when a segment overflowed)
+    unsigned int* log_cta_n = nullptr;      // kModeLog: entries of each CTA's segment
     int64_t log_cap = 0;
+    int64_t log_part = 0;                   // set by launch_scan_fast
     unsigned int* work_ctr = nullptr;       // wide count kernel: task counter (zeroed per launch)
     int32_t run_blocks = 0;                 // wide count kernel: blocks per run
     // fast kernel, count mode: dynamic work items (dyn_items: the caller's
@@ -194,9 +196,9 @@ int fast_threads();
 // rows of the logged visits: rows[row_off[chunk] + local + k] = (pos1, id_k)
 // Rows of the visit log at their chunk offsets.  With n_dev the count is read
 // on the device (n is then the log capacity; an overflowed log writes nothing).
-int launch_log_scatter(ks_ctx* ctx, const LogEntry* log, int64_t n, const unsigned long long* n_dev,
-                       const int64_t* row_off, const int32_t* acc_out_off, const int32_t* acc_out_ids, int64_t* rows,
-                       int* launches);
+int launch_log_scatter(ks_ctx* ctx, const LogEntry* log, const unsigned int* seg_n, int32_t segs, int64_t part,
+                       const unsigned long long* n_dev, int64_t cap, const int64_t* row_off, const int32_t* acc_out_off,
+                       const int32_t* acc_out_ids, int64_t* rows, int* launches);
 
 // Prefix scans (csrc/prefix_scan.cu).
 int exclusive_scan_rows(ks_ctx* ctx, const uint32_t* in, int64_t n, int64_t* out_excl,
