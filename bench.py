@@ -415,6 +415,17 @@ def measure_config(ctx, stream, local: int, config: int, steps: int, warmup: int
         par["rows"] = int(rows.shape[0])
         if rows.shape[0]:
             par["max_offset"] = int(rows[-1, 0])
+        # positions extraction (the config's "count and extract positions"):
+        # synchronous ks_locate, rows landed in host memory, median wall time
+        lts = []
+        for _ in range(7):
+            torch.cuda.synchronize()
+            l0 = time.perf_counter()
+            ctx.locate(dh, sh)
+            lts.append(time.perf_counter() - l0)
+        lt = statistics.median(lts[2:])
+        res["locate"] = {"value": n / lt / 1e9, "unit": UNIT, "ms_per_call": lt * 1e3, "rows": int(rows.shape[0]),
+                         "path": "ks_locate: counts + sorted (offset, id) rows in host memory, wall clock"}
     res["parity"] = par
     log(f"C{config}: {res['value']:.0f} GB/s, kernel {kms:.4f} ms, parity {par} "
         f"({time.perf_counter() - t0:.1f}s)")
