@@ -11,6 +11,15 @@ if str(REPO) not in sys.path:
     sys.path.insert(0, str(REPO))
 
 import paper_1509_01506_b200 as ks  # noqa: E402
+from paper_1509_01506_b200 import _native  # noqa: E402
+
+# a fresh checkout: build the C-ABI library (nvcc cross-compiles for sm_100a
+# without a GPU) and the oracle before any test loads them
+if not _native.LIB_PATH.exists():
+    import subprocess
+
+    subprocess.run(["make", "-C", str(REPO / "paper_1509_01506_b200" / "csrc"), "-j8"], check=True,
+                   stdout=subprocess.DEVNULL)
 
 TOY_PATTERNS = "acg\ncat\ncta\ntta"
 
