@@ -197,6 +197,23 @@ int dispatch(ks_ctx* ctx, const ks_dfa* dfa, const DevTable& T, const ScanPlan& 
         // bookkeeping, re-run the few that hit (KS_LEAN=0/1 overrides)
         a.lean = T.hit_rate * 64.0 * 32.0 < 0.05 ? 1 : 0;
         if (const char* e = std::getenv("KS_LEAN"); e && *e) a.lean = std::atoi(e) != 0;
+        // a fused K = 2 count takes the visit-class table when it has one
+        // and its histogram fits beside the tables (KS_NO_CLS=1: the ring)
+        if (mode == kModeCount && T.fast_k == 2 && !a.lean && a.fin_counts && &T == &dfa->scan && T.cls_rows > 0 &&
+            dfa->d_cls_visits && !env_flag("KS_NO_CLS") &&
+            fast_fixed_bytes(int32_t(T.cls_t1_bytes / 2), T.cls_nhist) + 256 <= ctx->smem_optin) {
+            a.cls = 1;
+            a.tk = T.cls_tk;
+            a.t1 = T.cls_t1;
+            a.t1_pad = int32_t(T.cls_t1_bytes / 2);
+            a.visits = dfa->d_cls_visits;
+            a.acc_out_off = T.cls_out_off;
+            a.acc_out_ids = T.cls_out_ids;
+            a.n_hist = T.cls_nhist;
+            a.cls_prim = T.cls_prim;
+            a.cls_used = T.cls_used;
+            a.n_used = T.cls_nused;
+        }
         return launch_scan_fast(ctx, a, mode, T.fast_k, launches);
     }
     return launch_scan(ctx, a, mode, T.stride, dfa->tables_in_smem, launches);

@@ -129,6 +129,111 @@ void build_stride_table(CompiledTable* t, size_t budget) {
     }
 }
 
+// Visit-class form of a K = 2 fast table (CompiledTable::cls_*).  A 2-base
+// step from s over (b1, b2) passes I = t1[s][b1] and ends in F = t1[I][b2].
+// When I accepts, the entry's row/sub names the pair (out(I), F): the row
+// carries F's transitions, (row, sub) the histogram slot whose multiset is
+// out(I) + out(F).  Each state holds three such pairs in subs 1-3 of its own
+// row (sub 0: I does not accept, the slot of out(F) alone); further pairs get
+// copies of the row.  One histogram add per accepting K-step, no re-walk of
+// the intermediate state.  Returns false (no class form) when the rows do
+// not fit 12-bit ids.
+bool build_class_table(CompiledTable* t, const std::vector<int32_t>& acc_off, const std::vector<int32_t>& acc_ids) {
+    t->cls_rows = t->cls_nhist = 0;
+    t->cls_tk.clear();
+    t->cls_t1.clear();
+    t->cls_prim.clear();
+    t->cls_out_off.clear();
+    t->cls_out_ids.clear();
+    t->cls_used.clear();
+    if (t->fast_k != 2 || t->t1z.empty()) return false;
+    const int nq = t->nq, A = t->n_accept;
+    auto key = [&](int s) { return std::vector<int32_t>(acc_ids.begin() + acc_off[s], acc_ids.begin() + acc_off[s + 1]); };
+    // accepting-intermediate multisets entering each state (sorted, distinct)
+    std::vector<std::vector<std::vector<int32_t>>> pairs(nq);
+    for (int s = 0; s < nq; ++s)
+        for (int b1 = 0; b1 < 4; ++b1) {
+            const int I = t->t1[size_t(s) * 5 + b1];
+            if (I >= A) continue;
+            for (int b2 = 0; b2 < 4; ++b2) pairs[t->t1[size_t(I) * 5 + b2]].push_back(key(I));
+        }
+    struct Slot { int row, sub; };
+    std::vector<std::unordered_map<std::vector<int32_t>, Slot, VecHash>> where(nq);
+    std::vector<uint16_t> prim(nq + 1);
+    std::iota(prim.begin(), prim.end(), uint16_t(0));
+    int next_row = nq + 1;   // row nq is the padding row
+    for (int F = 0; F < nq; ++F) {
+        auto& v = pairs[F];
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+        for (size_t k = 0; k < v.size(); ++k) {
+            Slot sl;
+            if (k < 3) {
+                sl = {F, int(k) + 1};
+            } else {
+                if ((k - 3) % 4 == 0) {
+                    prim.push_back(uint16_t(F));
+                    ++next_row;
+                }
+                sl = {next_row - 1, int((k - 3) % 4)};
+            }
+            where[F][v[k]] = sl;
+        }
+    }
+    const int rows = next_row;
+    if (rows > 4096) return false;
+    t->cls_tk.assign(size_t(1) << 16, uint16_t(nq << 1));
+    for (int r = 0; r < rows; ++r) {
+        if (r == nq) continue;
+        const int s = prim[r];
+        for (int w = 0; w < 16; ++w) {
+            const int I = t->t1[size_t(s) * 5 + (w & 3)];
+            const int F = t->t1[size_t(I) * 5 + (w >> 2)];
+            uint32_t v;
+            if (I < A) {
+                const Slot sl = where[F].at(key(I));
+                v = uint32_t(sl.row << 1) | uint32_t(sl.sub << 13) | 0x8000u;
+            } else {
+                v = uint32_t(F << 1) | (F < A ? 0x8000u : 0u);
+            }
+            t->cls_tk[(size_t(w) << 12) + r] = uint16_t(v);
+        }
+    }
+    const int cols = t->t1z_cols;
+    t->cls_t1.assign(size_t(rows) * cols, 0);
+    for (int r = 0; r < rows; ++r)
+        for (int c = 0; c < cols; ++c) t->cls_t1[size_t(r) * cols + c] = t->t1z[size_t(std::min<int>(prim[r], nq)) * cols + c];
+    // slot multisets: (sub << 12) | row
+    std::vector<std::vector<int32_t>> ms(size_t(4) << 12);
+    int nhist = 0;
+    for (int F = 0; F < A; ++F) {
+        ms[F] = key(F);
+        nhist = std::max(nhist, F + 1);
+    }
+    for (int F = 0; F < nq; ++F)
+        for (const auto& kv : where[F]) {
+            const int idx = (kv.second.sub << 12) | kv.second.row;
+            auto m = kv.first;
+            if (F < A) {
+                const auto o = key(F);
+                m.insert(m.end(), o.begin(), o.end());
+            }
+            ms[idx] = std::move(m);
+            nhist = std::max(nhist, idx + 1);
+        }
+    t->cls_out_off.assign(1, 0);
+    t->cls_used.clear();
+    for (int i = 0; i < nhist; ++i) {
+        t->cls_out_ids.insert(t->cls_out_ids.end(), ms[i].begin(), ms[i].end());
+        t->cls_out_off.push_back(int32_t(t->cls_out_ids.size()));
+        if (!ms[i].empty()) t->cls_used.push_back(i);
+    }
+    t->cls_prim = prim;
+    t->cls_rows = rows;
+    t->cls_nhist = nhist;
+    return true;
+}
+
 // Smallest D with |delta(Q, w)| == 1 for all |w| == D, or -1.
 template <class T>
 int synchronisation_depth(const std::vector<T>& t1, int nq) {
@@ -383,6 +488,8 @@ int compile_dfa(const int32_t* trans, int nq, const int32_t* out_off, const int3
     const size_t hist_bytes = size_t(h->n_accept) * 4;
     const size_t budget = smem_budget > hist_bytes + 4096 ? smem_budget - hist_bytes - 4096 : 0;
     build_stride_table(&t, budget);
+    if (!(std::getenv("KS_NO_CLS") && *std::getenv("KS_NO_CLS") == '1'))
+        build_class_table(&t, h->acc_out_off, h->acc_out_ids);
 
     h->sync_depth = synchronisation_depth(t.t1, nq);
     bool want_lookback = h->sync_depth >= 0 && force_strategy != KS_STRATEGY_MAPSCAN &&

@@ -58,6 +58,21 @@ struct CompiledTable {
     // cold (read the 32-bit 1-base table from L2)
     std::vector<uint16_t> ht;
     int hot_lo = 0, hot_n = 0;
+    // visit-class form of the K = 2 fast table (count mode; scan_fast.cu CLS):
+    // a row is a state plus, for the K-steps whose intermediate state
+    // accepts, the output multiset of that intermediate state.  Entry =
+    // (row << 1) | (sub << 13) | (hit << 15); the step's visits are counted
+    // once, in histogram slot (sub << 12) | row, whose output multiset is
+    // out(intermediate) + out(final).  Rows [0, nq) are the states, row nq
+    // the padding row, rows > nq copies of a state for its 4th, 5th, ...
+    // accepting intermediate multiset.
+    std::vector<uint16_t> cls_tk;        // 65536 entries, column-major like tkc
+    std::vector<uint16_t> cls_t1;        // (cls_rows + 1) x t1z_cols: 1-base table over rows
+    std::vector<uint16_t> cls_prim;      // cls_rows: the state of each row
+    std::vector<int32_t> cls_out_off;    // cls_nhist + 1: CSR of each slot's output multiset
+    std::vector<int32_t> cls_out_ids;
+    std::vector<int32_t> cls_used;       // the slots with a non-empty multiset (the only ones ever counted)
+    int cls_rows = 0, cls_nhist = 0;     // 0 = no class form
 };
 
 struct HostDfa {
@@ -109,6 +124,15 @@ struct DevTable {
     double hit_rate = 0;
     const uint16_t* ht = nullptr;   // wide automata: hot table (CompiledTable::ht)
     int hot_lo = 0, hot_n = 0;
+    const uint16_t* cls_tk = nullptr;   // visit-class form (CompiledTable::cls_*)
+    const uint16_t* cls_t1 = nullptr;
+    const uint16_t* cls_prim = nullptr;
+    const int32_t* cls_out_off = nullptr;
+    const int32_t* cls_out_ids = nullptr;
+    const int32_t* cls_used = nullptr;
+    int cls_nused = 0;
+    size_t cls_t1_bytes = 0;
+    int cls_rows = 0, cls_nhist = 0;
 };
 
 // Packed sequence layout ("lane-tiled").  The sequence is cut into units of
@@ -223,6 +247,9 @@ struct ks_dfa {
     // done | exit, the layout of scan_impl's result block); zero between
     // calls: the kernel's last CTA cleans it, so a count needs no memset
     void* d_cnt = nullptr;
+    // visit-class counters of the fused K = 2 count (cls_nhist), kept zero
+    // between calls like d_cnt
+    unsigned long long* d_cls_visits = nullptr;
     bool tables_in_smem = true;
 };
 

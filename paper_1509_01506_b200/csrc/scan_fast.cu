@@ -154,6 +154,7 @@ struct Ctx {
     uint32_t ring_thr;  // drain when a lane holds this many ring bytes (depth - chk_steps(K) entries)
     uint32_t t1_cols;   // 4 or 5
     uint32_t reset;     // OTHER target when t1_cols == 4
+    uint32_t one;       // ScanArgs::one
     LogEntry* log;       // this CTA's segment of the visit log
     uint32_t log_slot;   // shared address of the CTA's visit counter
     uint32_t log_part;   // entries per segment
@@ -375,12 +376,92 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
 }
 
 
+// ---- visit-class count (K = 2, CompiledTable::cls_*) ----------------------
+// An accepting K-step's entry is itself the record: (row << 1) | (sub << 13)
+// | 0x8000 names the histogram slot (sub << 12) | row that stands for both
+// visits of the step.  Records are pushed into 16-bit slots of KS_CLS_REGS
+// registers per lane (two PRMTs, predicated), not stored to shared memory;
+// every KS_CLS_CHK steps the warp votes whether some lane could overflow
+// before the next vote, and only then adds every lane's slots into the
+// shared-memory histogram (one predicated red per slot).  The data pipe
+// then carries the table gathers, the block loads and one red per
+// accepting step -- no ring stores, ring loads or intermediate re-walks.
+#ifndef KS_CLS_REGS
+#define KS_CLS_REGS 3
+#endif
+#ifndef KS_CLS_CHK
+#define KS_CLS_CHK 4
+#endif
+constexpr int kClsRegs = KS_CLS_REGS;
+constexpr int kClsChk = KS_CLS_CHK;
+static_assert(kClsChk >= 1 && kClsChk < 2 * kClsRegs, "class buffer: vote interval too long");
+// the slot whose occupancy triggers a flush: (2 regs - chk) entries already held
+constexpr int kClsTrig = 2 * kClsRegs - kClsChk;
+
+template <uint32_t SEL>
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "n"(SEL));
+    return d;
+}
+struct ClsBuf {
+    uint32_t r[kClsRegs];
+};
+// Push entry e (16 bits) into slot 0, moving every slot up by one (the
+// registers are one little-endian 16-bit shift register): byte permutes for
+// the upper registers (ALU pipe), a multiply-add for the lowest one (FMA
+// pipe: the scan's bit-selects, hit tests and votes fill the ALU pipe).
+__device__ __forceinline__ void cls_push(ClsBuf& b, uint32_t e) {
+#pragma unroll
+    for (int i = kClsRegs - 1; i > 0; --i) b.r[i] = prmt<0x5432>(b.r[i - 1], b.r[i]);
+    asm("mad.lo.u32 %0, %1, 65536, %2;" : "=r"(b.r[0]) : "r"(b.r[0]), "r"(e));
+}
+// Add every slot into the histogram (slot value v: (v << 1) & 0xFFFC is
+// its byte offset, bit 15 says it is occupied); predicated adds, no branches.
+__device__ __forceinline__ void red_slot(uint32_t hist, uint32_t occupied, uint32_t off, uint32_t one) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q red.shared.add.u32 [%1], %2;\n\t}"
+                 :: "r"(occupied), "r"(hist + off), "r"(one) : "memory");
+}
+// (one: a kernel-parameter 1, so the adds stay plain predicated adds
+// instead of branch-wrapped aggregated increments)
+__device__ __forceinline__ void cls_flush(uint32_t hist, ClsBuf& b, uint32_t one) {
+#pragma unroll
+    for (int i = 0; i < kClsRegs; ++i) {
+        const uint32_t x = b.r[i];
+        red_slot(hist, x & 0x8000u, (x << 1) & 0xFFFCu, one);
+        red_slot(hist, x & 0x80000000u, (x >> 15) & 0xFFFCu, one);
+        b.r[i] = 0u;
+    }
+}
+// One full, OTHER-free 64-base block on the class table; live lanes (lm =
+// 0x8000) push their accepting steps.
+__device__ __forceinline__ uint32_t fast_block_cls(const Ctx& c, uint32_t s, uint32_t lm, const uint4& xb,
+                                                   ClsBuf& b) {
+    constexpr int LC = 13;
+    constexpr uint32_t FM = 0xFu << LC;
+    uint32_t e = s << 1;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const uint32_t a = bitsel<FM>(field<2>(xb, j), e);
+        e = lds16(c.tk + a);
+        if (e & lm) cls_push(b, e);
+        if ((j % kClsChk) == kClsChk - 1) {
+            // occupied slots are non-zero (bit 15), empty ones zero
+            const uint32_t t = b.r[kClsTrig >> 1] & ((kClsTrig & 1) ? 0xFFFF0000u : 0xFFFFu);
+            if (__any_sync(0xffffffffu, t != 0u)) cls_flush(c.hist, b, c.one);
+        }
+    }
+    return (e >> 1) & 0xFFFu;
+}
+
 extern __shared__ __align__(128) unsigned char f_smem[];
 
-template <int K, int MODE, bool LEAN = false>
+template <int K, int MODE, bool LEAN = false, bool CLS = false>
 __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
-    constexpr bool RING = MODE == kModeCount || MODE == kModeRows;
-    constexpr bool HIST = RING || MODE == kModeLog;
+    static_assert(!CLS || (K == 2 && MODE == kModeCount && !LEAN), "class table: K = 2 count only");
+    constexpr bool RING = (MODE == kModeCount || MODE == kModeRows) && !CLS;
+    constexpr bool HIST = RING || MODE == kModeLog || CLS;
+    const int n_hist = CLS ? a.n_hist : a.n_accept;   // histogram slots
     constexpr int TK_BYTES = 1 << 17;
     // layout: table | t1 | ring (count/rows) | hist (count/rows/log)
     unsigned char* p_t1 = f_smem + TK_BYTES;
@@ -409,7 +490,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
             bulk_copy_g2s(smem_addr(p_t1) + o, reinterpret_cast<const char*>(a.t1) + o, min(kPart, t1_bytes - o), mbar);
     }
     if constexpr (HIST)
-        for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x) s_hist[i] = 0u;
+        for (int i = threadIdx.x; i < n_hist; i += blockDim.x) s_hist[i] = 0u;
     // Launched with programmatic stream serialisation: let the next kernel of
     // the stream start as our CTAs retire, and wait for the previous one only
     // before touching memory it may still use -- nothing above reads memory a
@@ -446,6 +527,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     c.ring_thr = uint32_t(a.ring_depth - chk_steps(K)) * kRingStride;
     c.t1_cols = opaque(uint32_t(a.t1_cols));
     c.reset = uint32_t(a.reset_state);
+    c.one = a.one;
     c.log = a.log;
     __shared__ unsigned int s_logn;
     c.log = a.log ? a.log + size_t(blockIdx.x) * uint32_t(a.log_part) : nullptr;
@@ -457,6 +539,9 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     const uint32_t ring_stride = kRingStride;
     const uint32_t rp0 = smem_addr(p_ring) + 4u * threadIdx.x;
     uint32_t rp = rp0;
+    ClsBuf cbuf;
+#pragma unroll
+    for (int i = 0; i < kClsRegs; ++i) cbuf.r[i] = 0u;
 
     const uint4* bases4 = reinterpret_cast<const uint4*>(a.seq.bases);
     const uint64_t* nmask = a.seq.nmask;
@@ -630,6 +715,8 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                         s2 = fast_block<K, MODE>(c, L, live ? s : idle, live ? 0x8000u : 0u, wb, p0, am, rp0, rp,
                                                  ring_stride);
                     }
+                } else if constexpr (CLS) {
+                    s2 = fast_block_cls(c, live ? s : idle, live ? 0x8000u : 0u, wb, cbuf);
                 } else {
                     s2 = fast_block<K, MODE>(c, L, live ? s : idle, live ? 0x8000u : 0u, wb, p0, am, rp0, rp,
                                              ring_stride);
@@ -676,7 +763,13 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                 asm volatile("griddepcontrol.wait;" ::: "memory");
                 waited = true;
             }
-            if (a.chunk_exit && ce == cend) a.chunk_exit[ch] = uint16_t(s);
+            if (a.chunk_exit && ce == cend) {
+                uint32_t sx = s;
+                if constexpr (CLS) {
+                    if (sx > uint32_t(a.nq)) sx = __ldg(&a.cls_prim[sx]);   // a row copy -> its state
+                }
+                a.chunk_exit[ch] = uint16_t(sx);
+            }
             if constexpr (MODE == kModeRows || MODE == kModeLog) a.chunk_rows[ch] = L.nrows;
             if constexpr (MODE == kModeEmit) {
                 if (L.cur != a.chunk_row_off[ch + 1]) atomicExch(a.error, 1);
@@ -698,14 +791,16 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
 
     kt_mark(a.ktime, 4, true, true);
     kt_mark(a.ktime, 5, false, true);
-    if constexpr (MODE == kModeCount) {   // the ring's leftovers
+    if constexpr (CLS) {
+        cls_flush(c.hist, cbuf, c.one);   // the class buffer's leftovers
+    } else if constexpr (MODE == kModeCount) {   // the ring's leftovers
         Lane<MODE> L;
         drain<K, MODE>(c, L, am, rp0, rp, ring_stride);
     }
     if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
     if constexpr (HIST) {
         __syncthreads();
-        for (int i = threadIdx.x; i < a.n_accept; i += blockDim.x)
+        for (int i = threadIdx.x; i < n_hist; i += blockDim.x)
             if (s_hist[i]) atomicAdd(&a.visits[i], (unsigned long long)s_hist[i]);
     }
     __syncthreads();
@@ -736,11 +831,17 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                 __threadfence();
                 if (threadIdx.x == 0 && a.fin_exit_src) *a.fin_exit_dst = __ldcg(a.fin_exit_src);
                 // counts accumulate in the (drained) ring's shared memory when they fit
-                const bool in_smem = size_t(a.n_expr) * 8 <= size_t(a.ring_depth) * 4 * blockDim.x;
-                unsigned long long* acc = in_smem ? reinterpret_cast<unsigned long long*>(p_ring) : a.fin_counts;
+                // (class tables: in the flushed histogram)
+                const bool in_smem = CLS ? size_t(a.n_expr) * 8 <= size_t(n_hist) * 4
+                                         : size_t(a.n_expr) * 8 <= size_t(a.ring_depth) * 4 * blockDim.x;
+                unsigned long long* acc = in_smem ? reinterpret_cast<unsigned long long*>(CLS ? (unsigned char*)s_hist : p_ring)
+                                                  : a.fin_counts;
                 for (int e = threadIdx.x; e < a.n_expr; e += blockDim.x) acc[e] = 0ull;
                 __syncthreads();
-                for (int st = threadIdx.x; st < a.n_accept; st += blockDim.x) {
+                // (class tables: only the slots that can be counted, a compact list)
+                const int n_fin = CLS ? a.n_used : n_hist;
+                for (int k = threadIdx.x; k < n_fin; k += blockDim.x) {
+                    const int st = CLS ? __ldg(&a.cls_used[k]) : k;
                     const unsigned long long v = __ldcg(&a.visits[st]);
                     if (!v) continue;
                     a.visits[st] = 0ull;   // clean for the next call
@@ -773,7 +874,12 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
 using FastFn = void (*)(const ScanArgs);
 
 template <int K>
-FastFn pick_mode(int mode, bool lean) {
+FastFn pick_mode(int mode, bool lean, bool cls) {
+    if constexpr (K == 2) {
+        if (cls) return mode == kModeCount && !lean ? scan_fast_kernel<2, kModeCount, false, true> : nullptr;
+    } else {
+        if (cls) return nullptr;
+    }
     switch (mode) {
         case kModeCount: return lean ? scan_fast_kernel<K, kModeCount, true> : scan_fast_kernel<K, kModeCount, false>;
         case kModeRows: return lean ? scan_fast_kernel<K, kModeRows, true> : scan_fast_kernel<K, kModeRows, false>;
@@ -806,11 +912,11 @@ __global__ void log_scatter_kernel(const LogEntry* __restrict__ log, int64_t par
     }
 }
 
-FastFn pick(int mode, int k, bool lean) {
+FastFn pick(int mode, int k, bool lean, bool cls) {
     switch (k) {
-        case 2: return pick_mode<2>(mode, lean);
-        case 3: return pick_mode<3>(mode, lean);
-        case 4: return pick_mode<4>(mode, lean);
+        case 2: return pick_mode<2>(mode, lean, cls);
+        case 3: return pick_mode<3>(mode, lean, cls);
+        case 4: return pick_mode<4>(mode, lean, cls);
     }
     return nullptr;
 }
@@ -868,12 +974,14 @@ int launch_log_scatter(ks_ctx* ctx, const LogEntry* log, const unsigned int* seg
 
 int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
     if (a.end <= a.begin || a.nchunks <= 0) return KS_OK;
-    const bool ring = mode == kModeCount || mode == kModeRows;
-    const bool hist = ring || mode == kModeLog;
+    const bool cls = a.cls != 0;
+    const bool ring = (mode == kModeCount || mode == kModeRows) && !cls;
+    const bool hist = ring || mode == kModeLog || cls;
     a.hist_smem = hist ? 1 : 0;
-    FastFn fn = pick(mode, k, a.lean != 0);
+    FastFn fn = pick(mode, k, a.lean != 0, cls);
     if (!fn) return fail(KS_E_INVALID, "fast scan: bad mode/stride");
-    size_t smem = fast_fixed_bytes(a.t1_pad, hist ? a.n_accept : 0);
+    size_t smem = fast_fixed_bytes(a.t1_pad, cls ? a.n_hist : hist ? a.n_accept : 0);
+    if (cls) a.ring_depth = 0;
     if (ring) {
         a.ring_depth = ring_depth_for(smem, ctx->smem_optin, kFastThreads);
         if (const char* env = std::getenv("KS_RING_DEPTH"))   // tuning knob

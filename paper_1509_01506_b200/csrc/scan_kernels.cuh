@@ -111,6 +111,14 @@ struct ScanArgs {
     int32_t split_tiles = 0, split_parts = 1;
     int64_t static_items = 0;               // items below this go round-robin
     int32_t early_wait = 0;                 // fast kernel: wait for the preceding kernel up front (KS_EARLY_WAIT=1)
+    // fast K = 2 count with the visit-class table (CompiledTable::cls_*): tk/t1
+    // are the class forms, visits / acc_out_* the n_hist class slots
+    int32_t cls = 0;
+    int32_t n_hist = 0;
+    const uint16_t* cls_prim = nullptr;     // row -> state (chunk exits)
+    const int32_t* cls_used = nullptr;      // the slots the finalize reads (n_used of them)
+    int32_t n_used = 0;
+    uint32_t one = 1;                       // a 1 the compiler cannot fold (multiply-add / add operands)
     int32_t ktime = 0;                      // fast kernel: per-phase timestamps (KS_KTIME=1, diagnostic)
 };
 
@@ -188,6 +196,7 @@ void chunk_geometry(int64_t begin, int64_t end, int64_t threads, int64_t* origin
 
 // Fast shared-memory kernel for tables with a fast form (csrc/scan_fast.cu).
 int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches);
+size_t fast_fixed_bytes(int32_t t1_pad, int32_t hist_words);
 size_t fast_smem_bytes(int mode, int32_t t1_pad, int32_t hist_words, int threads);
 // Warps per CTA of the fast scan for `tiles` tiles of 32 units: 32, or fewer
 // when that makes the tiles fill whole rounds over all SMs.

@@ -42,6 +42,18 @@ int upload_table(const CompiledTable& t, DevTable* d, char* blob, size_t* off, b
         d->tkc = reinterpret_cast<const uint16_t*>(place(t.tkc.data(), t.tkc.size() * 2));
         d->t1z = reinterpret_cast<const uint16_t*>(place(t.t1z.data(), t.t1z.size() * 2));
     }
+    d->cls_rows = t.cls_rows;
+    d->cls_nhist = t.cls_nhist;
+    d->cls_t1_bytes = align16(t.cls_t1.size() * 2);
+    if (t.cls_rows) {
+        d->cls_tk = reinterpret_cast<const uint16_t*>(place(t.cls_tk.data(), t.cls_tk.size() * 2));
+        d->cls_t1 = reinterpret_cast<const uint16_t*>(place(t.cls_t1.data(), t.cls_t1.size() * 2));
+        d->cls_prim = reinterpret_cast<const uint16_t*>(place(t.cls_prim.data(), t.cls_prim.size() * 2));
+        d->cls_out_off = reinterpret_cast<const int32_t*>(place(t.cls_out_off.data(), t.cls_out_off.size() * 4));
+        d->cls_out_ids = reinterpret_cast<const int32_t*>(place(t.cls_out_ids.data(), t.cls_out_ids.size() * 4));
+        d->cls_used = reinterpret_cast<const int32_t*>(place(t.cls_used.data(), t.cls_used.size() * 4));
+        d->cls_nused = int(t.cls_used.size());
+    }
     return KS_OK;
 }
 
@@ -240,6 +252,12 @@ int ks_dfa_upload_ex(ks_ctx* ctx, const int32_t* transitions, int32_t n_states, 
     rebase(d->scan.ht);
     rebase(d->scan.tkc);
     rebase(d->scan.t1z);
+    rebase(d->scan.cls_tk);
+    rebase(d->scan.cls_t1);
+    rebase(d->scan.cls_prim);
+    rebase(d->scan.cls_out_off);
+    rebase(d->scan.cls_out_ids);
+    rebase(d->scan.cls_used);
     rebase(d->d_acc_out_off);
     rebase(d->d_acc_out_ids);
     rebase(d->d_acc_outcnt);
@@ -265,9 +283,23 @@ int ks_dfa_upload_ex(ks_ctx* ctx, const int32_t* transitions, int32_t n_states, 
         cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
         cudaGetLastError();
         if (d->d_cnt) cudaFree(d->d_cnt);
+    if (d->d_cls_visits) cudaFree(d->d_cls_visits);
         cudaFree(d->d_blob);
         delete d;
         return fail(KS_E_CUDA, "cudaMalloc(dfa result block)");
+    }
+    if (d->scan.cls_rows) {
+        const size_t vb = size_t(d->scan.cls_nhist) * 8;
+        if (cudaMalloc(&d->d_cls_visits, vb) != cudaSuccess ||
+            cudaMemsetAsync(d->d_cls_visits, 0, vb, ctx->stream) != cudaSuccess ||
+            cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+            cudaGetLastError();
+            if (d->d_cls_visits) cudaFree(d->d_cls_visits);
+            cudaFree(d->d_cnt);
+            cudaFree(d->d_blob);
+            delete d;
+            return fail(KS_E_CUDA, "cudaMalloc(dfa class counters)");
+        }
     }
     const size_t smem_scan = d->scan.tk_bytes + d->scan.t1_bytes;
     const size_t smem_mono = h.strategy == KS_STRATEGY_MAPSCAN ? d->mono.tk_bytes + d->mono.t1_bytes : 0;
@@ -307,6 +339,7 @@ int ks_dfa_free(ks_dfa* d) {
     DeviceGuard guard(d->ctx->device);
     if (d->d_blob) cudaFree(d->d_blob);
     if (d->d_cnt) cudaFree(d->d_cnt);
+    if (d->d_cls_visits) cudaFree(d->d_cls_visits);
     delete d;
     return KS_OK;
 }

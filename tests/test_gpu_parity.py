@@ -1147,3 +1147,54 @@ def test_upload_codes_host_packed(monkeypatch):
     bad[9_999_999] = 7
     with pytest.raises(ValueError, match="out of range"):
         c2.upload_codes(bad)
+
+
+# ---------------------------------------------------------------- visit-class table (K = 2 fused count)
+
+def _k2_dfa(rng):
+    """A 1025..4095-state automaton (K = 2 fast table) with many short
+    literals, so many accepting states enter the same state: rows copied
+    for a 4th, 5th, ... intermediate multiset."""
+    while True:
+        lits = set()
+        for _ in range(int(rng.integers(150, 420))):
+            n = int(rng.choice([1, 2, 3, 4, 6, 8, 10, 12], p=[.02, .06, .1, .12, .2, .2, .15, .15]))
+            lits.add("".join("acgt"[x] for x in rng.integers(0, 4, n)))
+        lits = sorted(lits)
+        rng.shuffle(lits)
+        # 1-3 literals per expression: output multisets with repeated ids
+        lines, i = [], 0
+        while i < len(lits):
+            k = int(rng.integers(1, 4))
+            lines.append("|".join(lits[i:i + k]))
+            i += k
+        dfa = dfa_of("\n".join(lines))
+        if 1100 <= dfa.state_count <= 4000:
+            return dfa
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_class_table_counts_vs_oracle(monkeypatch, seed):
+    """The fused K = 2 count on the visit-class table (scan_fast CLS kernel)
+    equals the oracle and the ring kernel (KS_NO_CLS=1) on automata with
+    row copies, across N runs, OTHER symbols, tiny and block-ragged inputs."""
+    rng = np.random.default_rng(1000 + seed)
+    dfa = _k2_dfa(rng)
+    c = _native.DeviceContext(0)
+    dh = c.dfa(dfa)
+    assert dh.info["stride"] == 2, dh.info
+    for n in (0, 1, 2, 63, 64, 65, 4097, 200_003, 3_000_017):
+        codes = rng.integers(0, 4, n).astype(np.uint8)
+        codes[rng.random(n) < 0.002] = 4
+        if n > 5000:
+            codes[1000:1377] = 4          # an N run across block borders
+            codes[4000:4064] = 4          # exactly one block
+        sh = c.upload_codes(codes)
+        want = O.ref_sequential_count(dfa, codes)[0]
+        got = c.count(dh, sh)
+        assert got.tolist() == want.tolist(), (seed, n)
+        monkeypatch.setenv("KS_NO_CLS", "1")
+        assert c.count(dh, sh).tolist() == want.tolist(), (seed, n)
+        monkeypatch.delenv("KS_NO_CLS")
+        # back to back on the persistent class counters (kept zero by the kernel)
+        assert c.count(dh, sh).tolist() == want.tolist(), (seed, n)
