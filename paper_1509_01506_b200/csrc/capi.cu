@@ -135,6 +135,7 @@ SeqView view_of(const ks_seq* s) {
     SeqView v;
     v.bases = s->d_bases;
     v.nmask = s->d_nmask;
+    v.rowmask = s->sealed ? s->d_rowmask : nullptr;
     v.n = s->n;
     v.lb = s->lb;
     return v;
@@ -201,7 +202,7 @@ int dispatch(ks_ctx* ctx, const ks_dfa* dfa, const DevTable& T, const ScanPlan& 
         // and its histogram fits beside the tables (KS_NO_CLS=1: the ring)
         if (mode == kModeCount && T.fast_k == 2 && !a.lean && a.fin_counts && &T == &dfa->scan && T.cls_rows > 0 &&
             dfa->d_cls_visits && !env_flag("KS_NO_CLS") &&
-            fast_fixed_bytes(int32_t(T.cls_t1_bytes / 2), T.cls_nhist) + 256 <= ctx->smem_optin) {
+            fast_fixed_bytes(int32_t(T.cls_t1_bytes / 2), T.cls_nhist) + 256 + 1024 <= ctx->smem_optin) {   // + the class kernel's window shift
             a.cls = 1;
             a.tk = T.cls_tk;
             a.t1 = T.cls_t1;

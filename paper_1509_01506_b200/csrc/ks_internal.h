@@ -146,6 +146,10 @@ struct SeqView {
     const uint64_t* nmask = nullptr;
     int64_t n = 0;
     int32_t lb = 4;   // log2(blocks per unit)
+    // per tile: bit k = some block of row k (the 32 lanes' k-th blocks) holds
+    // OTHER; null when not computed (streamed pieces).  The fast scan skips
+    // the OTHER-bitmap loads of clear rows.
+    const uint64_t* rowmask = nullptr;
 };
 
 // Block slot of global block g (= position >> 6).
@@ -262,6 +266,10 @@ struct ks_seq {
     void* d_blob = nullptr;
     int64_t n_blocks = 0;   // block slots allocated (whole tiles + one padding tile)
     int32_t lb = 4;         // log2(blocks per unit), see SeqView
+    // SeqView::rowmask, one word per tile; filled by seq_seal() once an
+    // upload has finished (resident sequences are immutable from then on)
+    uint64_t* d_rowmask = nullptr;
+    bool sealed = false;
 };
 
 // Held for the duration of every public call that uses a context.

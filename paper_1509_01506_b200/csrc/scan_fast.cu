@@ -155,6 +155,7 @@ struct Ctx {
     uint32_t t1_cols;   // 4 or 5
     uint32_t reset;     // OTHER target when t1_cols == 4
     uint32_t one;       // ScanArgs::one
+    uint32_t hist2;     // class count: hist - 0x10000 (cls_flush)
     LogEntry* log;       // this CTA's segment of the visit log
     uint32_t log_slot;   // shared address of the CTA's visit counter
     uint32_t log_part;   // entries per segment
@@ -379,77 +380,102 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
 // ---- visit-class count (K = 2, CompiledTable::cls_*) ----------------------
 // An accepting K-step's entry is itself the record: (row << 1) | (sub << 13)
 // | 0x8000 names the histogram slot (sub << 12) | row that stands for both
-// visits of the step.  Records are pushed into 16-bit slots of KS_CLS_REGS
-// registers per lane (two PRMTs, predicated), not stored to shared memory;
-// every KS_CLS_CHK steps the warp votes whether some lane could overflow
-// before the next vote, and only then adds every lane's slots into the
-// shared-memory histogram (one predicated red per slot).  The data pipe
-// then carries the table gathers, the block loads and one red per
-// accepting step -- no ring stores, ring loads or intermediate re-walks.
+// visits of the step.  The entries of two consecutive K-steps make one
+// 32-bit pair (e0 | e1 << 16, one multiply-add); a pair in which either step
+// accepts (one LOP3 test per two steps) is pushed into a queue of
+// KS_CLS_REGS registers per lane by predicated register moves -- nothing is
+// stored to shared memory and the ALU pipe, which the scan's shifts,
+// bit-selects and tests fill, sees one instruction per two steps (the
+// 16-bit shift register of the first version cost three per step).  Every
+// two pairs the warp votes whether some lane could overflow before the next
+// vote, and only then adds every lane's pairs into the shared-memory
+// histogram: per queue slot one red for the lanes that hold a pair (its
+// first accepting half), and, behind one warp vote per flush, a second one
+// for pairs whose both halves accept.  The data pipe then carries the table
+// gathers, the block loads and one red per accepting step -- no ring
+// stores, ring loads or intermediate re-walks.  Idle lanes ride along in
+// the padding row (state nq), whose entries never accept.
 #ifndef KS_CLS_REGS
-#define KS_CLS_REGS 3
-#endif
-#ifndef KS_CLS_CHK
-#define KS_CLS_CHK 4
+#define KS_CLS_REGS 4
 #endif
 constexpr int kClsRegs = KS_CLS_REGS;
-constexpr int kClsChk = KS_CLS_CHK;
-static_assert(kClsChk >= 1 && kClsChk < 2 * kClsRegs, "class buffer: vote interval too long");
-// the slot whose occupancy triggers a flush: (2 regs - chk) entries already held
-constexpr int kClsTrig = 2 * kClsRegs - kClsChk;
+static_assert(kClsRegs >= 3, "class queue: two pushes between votes need a spare slot");
 
-template <uint32_t SEL>
-__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b) {
-    uint32_t d;
-    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "n"(SEL));
-    return d;
-}
 struct ClsBuf {
     uint32_t r[kClsRegs];
 };
-// Push entry e (16 bits) into slot 0, moving every slot up by one (the
-// registers are one little-endian 16-bit shift register): byte permutes for
-// the upper registers (ALU pipe), a multiply-add for the lowest one (FMA
-// pipe: the scan's bit-selects, hit tests and votes fill the ALU pipe).
-__device__ __forceinline__ void cls_push(ClsBuf& b, uint32_t e) {
+// The class kernel keeps its K-stride table at this absolute shared address
+// (the dynamic window is shifted to it): the table base is then an
+// instruction immediate, not a uniform register the compiler re-derives
+// after every divergent flush.
+constexpr uint32_t kClsTkAbs = 0x800;
+constexpr size_t kClsSmemPad = 1024;   // room for the shift (launch_scan_fast)
+__device__ __forceinline__ uint32_t lds16_tk(uint32_t off) {
+    unsigned short v;
+    asm("ld.shared.u16 %0, [%1+2048];" : "=h"(v) : "r"(off));
+    return v;
+}
+static_assert(kClsTkAbs == 2048, "lds16_tk's immediate");
+// d = s when t != 0, as a predicated multiply-add by the kernel-parameter 1:
+// the move runs on the FMA pipe (a plain conditional move compiles to SEL,
+// on the ALU pipe the scan saturates).
+__device__ __forceinline__ void move_if(uint32_t& d, uint32_t s, uint32_t t, uint32_t one) {
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p mad.lo.u32 %0, %1, %3, 0;\n\t}"
+        : "+r"(d) : "r"(s), "r"(t), "r"(one));
+}
+// Push `pair` when t != 0 (the newest pair in r[0]).
+__device__ __forceinline__ void cls_push_if(ClsBuf& b, uint32_t pair, uint32_t t, uint32_t one) {
 #pragma unroll
-    for (int i = kClsRegs - 1; i > 0; --i) b.r[i] = prmt<0x5432>(b.r[i - 1], b.r[i]);
-    asm("mad.lo.u32 %0, %1, 65536, %2;" : "=r"(b.r[0]) : "r"(b.r[0]), "r"(e));
+    for (int i = kClsRegs - 1; i > 0; --i) move_if(b.r[i], b.r[i - 1], t, one);
+    move_if(b.r[0], pair, t, one);
 }
-// Add every slot into the histogram (slot value v: (v << 1) & 0xFFFC is
-// its byte offset, bit 15 says it is occupied); predicated adds, no branches.
-__device__ __forceinline__ void red_slot(uint32_t hist, uint32_t occupied, uint32_t off, uint32_t one) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q red.shared.add.u32 [%1], %2;\n\t}"
-                 :: "r"(occupied), "r"(hist + off), "r"(one) : "memory");
+__device__ __forceinline__ void red_at(uint32_t addr, uint32_t one) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(one) : "memory");
 }
-// (one: a kernel-parameter 1, so the adds stay plain predicated adds
-// instead of branch-wrapped aggregated increments)
-__device__ __forceinline__ void cls_flush(uint32_t hist, ClsBuf& b, uint32_t one) {
+// hist2: the histogram's shared address - 0x10000 (an accepting entry e has
+// bit 15, its slot's byte offset is 2 * (e & 0x7FFF)); one: a
+// kernel-parameter 1 (an immediate would become an aggregated increment).
+__device__ __forceinline__ void cls_flush(uint32_t hist2, ClsBuf& b, uint32_t one) {
 #pragma unroll
     for (int i = 0; i < kClsRegs; ++i) {
         const uint32_t x = b.r[i];
-        red_slot(hist, x & 0x8000u, (x << 1) & 0xFFFCu, one);
-        red_slot(hist, x & 0x80000000u, (x >> 15) & 0xFFFCu, one);
+        if (x) {
+            // the first accepting half: low when it accepts, else high
+            const bool lo = (x & 0x8000u) != 0u;
+            const uint32_t t = lo ? x << 1 : x >> 15;
+            red_at(hist2 + (t & 0x1FFFCu), one);
+            if (lo && int32_t(x) < 0) red_at(hist2 + ((x >> 15) & 0x1FFFCu), one);   // both accept
+        }
         b.r[i] = 0u;
     }
 }
-// One full, OTHER-free 64-base block on the class table; live lanes (lm =
-// 0x8000) push their accepting steps.
-__device__ __forceinline__ uint32_t fast_block_cls(const Ctx& c, uint32_t s, uint32_t lm, const uint4& xb,
-                                                   ClsBuf& b) {
+// One full, OTHER-free 64-base block on the class table: a loop over the
+// block's four words (8 steps each; rolled, so the kernel's hot code stays
+// small), two votes per word.  The 2 bases of a step reach bits [13, 17) by
+// left shifts only (multiplies on the FMA pipe): the upper half of a word is
+// shifted down once (y) instead of one funnel shift per step.
+__device__ __forceinline__ uint32_t fast_block_cls(const Ctx& c, uint32_t s, const uint4& xb, ClsBuf& b) {
     constexpr int LC = 13;
     constexpr uint32_t FM = 0xFu << LC;
+    uint32_t w0 = xb.x, w1 = xb.y, w2 = xb.z, w3 = xb.w;
     uint32_t e = s << 1;
+#pragma unroll 1
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t x = w0, y = w0 >> 16;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-        const uint32_t a = bitsel<FM>(field<2>(xb, j), e);
-        e = lds16(c.tk + a);
-        if (e & lm) cls_push(b, e);
-        if ((j % kClsChk) == kClsChk - 1) {
-            // occupied slots are non-zero (bit 15), empty ones zero
-            const uint32_t t = b.r[kClsTrig >> 1] & ((kClsTrig & 1) ? 0xFFFF0000u : 0xFFFFu);
-            if (__any_sync(0xffffffffu, t != 0u)) cls_flush(c.hist, b, c.one);
+        for (int j = 0; j < 8; j += 2) {
+            const uint32_t f0 = j < 4 ? x << (13 - 4 * j) : y << (29 - 4 * j);
+            const uint32_t f1 = j + 1 < 4 ? x << (13 - 4 * (j + 1)) : y << (29 - 4 * (j + 1));
+            const uint32_t e0 = lds16_tk(bitsel<FM>(f0, e));
+            e = lds16_tk(bitsel<FM>(f1, e0));
+            uint32_t pair;
+            asm("mad.lo.u32 %0, %1, 65536, %2;" : "=r"(pair) : "r"(e), "r"(e0));
+            cls_push_if(b, pair, pair & 0x80008000u, c.one);
+            if ((j & 2) && __any_sync(0xffffffffu, b.r[kClsRegs - 2] != 0u)) cls_flush(c.hist2, b, c.one);
         }
+        w0 = w1;
+        w1 = w2;
+        w2 = w3;
     }
     return (e >> 1) & 0xFFFu;
 }
@@ -464,7 +490,11 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     const int n_hist = CLS ? a.n_hist : a.n_accept;   // histogram slots
     constexpr int TK_BYTES = 1 << 17;
     // layout: table | t1 | ring (count/rows) | hist (count/rows/log)
-    unsigned char* p_t1 = f_smem + TK_BYTES;
+    unsigned char* const smem0 = CLS ? f_smem + (kClsTkAbs - smem_addr(f_smem)) : f_smem;
+    if constexpr (CLS) {
+        if (smem_addr(f_smem) > kClsTkAbs) __trap();   // static shared memory outgrew the fixed table address
+    }
+    unsigned char* p_t1 = smem0 + TK_BYTES;
     unsigned char* p_ring = p_t1 + size_t(a.t1_pad) * 2;
     unsigned int* s_hist = reinterpret_cast<unsigned int*>(
         p_ring + (RING ? size_t(a.ring_depth) * 4 * kFastThreads : 0));
@@ -485,7 +515,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                      ::"r"(mbar), "r"(uint32_t(TK_BYTES) + t1_bytes) : "memory");
         constexpr uint32_t kPart = 32768;   // bytes per bulk copy
         for (uint32_t o = 0; o < uint32_t(TK_BYTES); o += kPart)
-            bulk_copy_g2s(smem_addr(f_smem) + o, reinterpret_cast<const char*>(a.tk) + o, kPart, mbar);
+            bulk_copy_g2s(smem_addr(smem0) + o, reinterpret_cast<const char*>(a.tk) + o, kPart, mbar);
         for (uint32_t o = 0; o < t1_bytes; o += kPart)
             bulk_copy_g2s(smem_addr(p_t1) + o, reinterpret_cast<const char*>(a.t1) + o, min(kPart, t1_bytes - o), mbar);
     }
@@ -515,7 +545,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     kt_mark(a.ktime, 3, false);
 
     Ctx c;
-    c.tk = smem_addr(f_smem);
+    c.tk = smem_addr(smem0);
     c.t1 = opaque(smem_addr(p_t1));
     c.hist = opaque(smem_addr(s_hist));
     c.outcnt = a.acc_outcnt;
@@ -528,6 +558,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     c.t1_cols = opaque(uint32_t(a.t1_cols));
     c.reset = uint32_t(a.reset_state);
     c.one = a.one;
+    c.hist2 = c.hist - 0x10000u;
     c.log = a.log;
     __shared__ unsigned int s_logn;
     c.log = a.log ? a.log + size_t(blockIdx.x) * uint32_t(a.log_part) : nullptr;
@@ -535,7 +566,9 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     c.log_part = uint32_t(a.log_part);
     if (MODE == kModeLog && threadIdx.x == 0) s_logn = 0u;
     __syncthreads();
-    const uint32_t idle = 0;  // state of lanes without work (their hits are masked)
+    // state of lanes without work: 0 with their hits masked; the class table's
+    // padding row, which never accepts
+    const uint32_t idle = CLS ? uint32_t(a.nq) : 0u;
     const uint32_t ring_stride = kRingStride;
     const uint32_t rp0 = smem_addr(p_ring) + 4u * threadIdx.x;
     uint32_t rp = rp0;
@@ -665,7 +698,31 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
         const uint4* pb = bases4 + ubase + (int64_t(k0) << 5);
         const uint64_t* pm = nmask + ubase + (int64_t(k0) << 5);
         uint4 wb = __ldg(pb);
-        uint64_t wm = __ldg(pm);
+        // rows of the tile without OTHER (SeqView::rowmask) skip the bitmap loads
+        const uint64_t tmask = a.seq.rowmask ? __ldg(a.seq.rowmask + t) : ~0ull;
+        uint64_t wm = ((tmask >> (k0 & 63)) & 1ull) ? __ldg(pm) : 0ull;
+        // The common item of the class count: whole, aligned block ranges in
+        // every lane and no OTHER in any of its rows (SeqView::rowmask) -- a
+        // loop of block load + scan, none of the per-lane range and bitmap
+        // tests, no votes.  Everything else takes the general loop below.
+        bool plain = false;
+        if constexpr (CLS) {
+            const uint64_t rows = nmax >= 64 ? ~0ull : ((1ull << nmax) - 1ull) << (k0 & 63);
+            const int k0u = __shfl_sync(am, k0, 0);
+            const bool mine = active & ((cb & 63) == 0) & ((ce & 63) == 0) & (nblk == nmax) & (k0 == k0u) &
+                              ((tmask & rows) == 0ull);
+            plain = __all_sync(am, mine) && a.seq.rowmask != nullptr;
+            if (plain) {
+#pragma unroll 1
+                for (int i = 0; i < nmax; ++i) {
+                    pb += 32;
+                    const uint4 nb = __ldg(pb);   // the slot exists: arrays are padded by a whole tile
+                    s = fast_block_cls(c, s, wb, cbuf);
+                    wb = nb;
+                }
+            }
+        }
+        if (!plain)
         for (int i = 0; i < nmax; ++i) {
             const bool has = i < nblk;
             const int k = k0 + (has ? i : 0);
@@ -675,7 +732,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                 pm += 32;
             }
             const uint4 nb = __ldg(pb);
-            const uint64_t nm = __ldg(pm);
+            const uint64_t nm = ((tmask >> ((k + (has ? 1 : 0)) & 63)) & 1ull) ? __ldg(pm) : 0ull;
             const int64_t p0 = (gfirst + k) << 6;
             const uint64_t w0 = (uint64_t(wb.y) << 32) | wb.x;
             const uint64_t w1 = (uint64_t(wb.w) << 32) | wb.z;
@@ -716,7 +773,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                                                  ring_stride);
                     }
                 } else if constexpr (CLS) {
-                    s2 = fast_block_cls(c, live ? s : idle, live ? 0x8000u : 0u, wb, cbuf);
+                    s2 = fast_block_cls(c, live ? s : idle, wb, cbuf);
                 } else {
                     s2 = fast_block<K, MODE>(c, L, live ? s : idle, live ? 0x8000u : 0u, wb, p0, am, rp0, rp,
                                              ring_stride);
@@ -792,7 +849,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     kt_mark(a.ktime, 4, true, true);
     kt_mark(a.ktime, 5, false, true);
     if constexpr (CLS) {
-        cls_flush(c.hist, cbuf, c.one);   // the class buffer's leftovers
+        cls_flush(c.hist2, cbuf, c.one);   // the class queue's leftovers
     } else if constexpr (MODE == kModeCount) {   // the ring's leftovers
         Lane<MODE> L;
         drain<K, MODE>(c, L, am, rp0, rp, ring_stride);
@@ -981,7 +1038,10 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
     FastFn fn = pick(mode, k, a.lean != 0, cls);
     if (!fn) return fail(KS_E_INVALID, "fast scan: bad mode/stride");
     size_t smem = fast_fixed_bytes(a.t1_pad, cls ? a.n_hist : hist ? a.n_accept : 0);
-    if (cls) a.ring_depth = 0;
+    if (cls) {
+        a.ring_depth = 0;
+        smem += kClsSmemPad;   // the window shift to kClsTkAbs
+    }
     if (ring) {
         a.ring_depth = ring_depth_for(smem, ctx->smem_optin, kFastThreads);
         if (const char* env = std::getenv("KS_RING_DEPTH"))   // tuning knob

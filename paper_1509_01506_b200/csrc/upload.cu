@@ -86,7 +86,8 @@ int seq_alloc(ks_ctx* ctx, int64_t n_capacity, ks_seq** out) {
     const int64_t tile_blocks = int64_t(32) << s->lb;
     const int64_t blocks = (n_capacity + 63) / 64;
     s->n_blocks = ((blocks + tile_blocks - 1) / tile_blocks + 1) * tile_blocks;
-    const size_t bytes = size_t(s->n_blocks) * 32;
+    const size_t rm_bytes = size_t(s->n_blocks / tile_blocks) * 8;
+    const size_t bytes = size_t(s->n_blocks) * 32 + rm_bytes;
     cudaError_t e = cudaMalloc(&s->d_blob, bytes);
     if (e != cudaSuccess) {
         delete s;
@@ -96,6 +97,7 @@ int seq_alloc(ks_ctx* ctx, int64_t n_capacity, ks_seq** out) {
     s->d_bases = reinterpret_cast<uint64_t*>(p);
     s->d_nmask = reinterpret_cast<uint64_t*>(p + size_t(s->n_blocks) * 16);
     s->d_soft = reinterpret_cast<uint64_t*>(p + size_t(s->n_blocks) * 24);
+    s->d_rowmask = reinterpret_cast<uint64_t*>(p + size_t(s->n_blocks) * 32);
     e = cudaMemsetAsync(s->d_blob, 0, bytes, ctx->stream);
     if (e != cudaSuccess) {
         cudaFree(s->d_blob);
@@ -103,6 +105,31 @@ int seq_alloc(ks_ctx* ctx, int64_t n_capacity, ks_seq** out) {
         return cuda_fail(e, "cudaMemset(sequence)");
     }
     *out = s;
+    return KS_OK;
+}
+
+// Row flags of a finished upload (SeqView::rowmask): one warp per tile ORs
+// the 32 lanes' OTHER bitmaps of every block row.
+__global__ void seq_rowmask_kernel(const uint64_t* __restrict__ nmask, int64_t n_tiles, int lb,
+                                   uint64_t* __restrict__ rowmask) {
+    const int64_t t = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (t >= n_tiles) return;
+    const int lane = threadIdx.x & 31;
+    const uint64_t* p = nmask + (t << (5 + lb)) + lane;
+    uint64_t m = 0;
+    for (int k = 0; k < (1 << lb); ++k)
+        if (__any_sync(0xffffffffu, __ldg(p + 32 * k) != 0ull)) m |= 1ull << k;
+    if (lane == 0) rowmask[t] = m;
+}
+
+int seq_seal(ks_ctx* ctx, ks_seq* s) {
+    if (!s->d_rowmask) return KS_OK;
+    const int64_t n_tiles = s->n_blocks >> (5 + s->lb);
+    const int threads = 256;
+    const int64_t blocks = (n_tiles * 32 + threads - 1) / threads;
+    seq_rowmask_kernel<<<unsigned(blocks), threads, 0, ctx->stream>>>(s->d_nmask, n_tiles, s->lb, s->d_rowmask);
+    KS_CUDA(cudaGetLastError());
+    s->sealed = true;
     return KS_OK;
 }
 
@@ -357,6 +384,10 @@ int ks_seq_upload_codes(ks_ctx* ctx, const uint8_t* codes, int64_t n, ks_seq** o
             seq_destroy(s);
             return rc;
         }
+        if ((rc = seq_seal(ctx, s)) != KS_OK) {
+            seq_destroy(s);
+            return rc;
+        }
         *out = s;
         return KS_OK;
     }
@@ -383,6 +414,7 @@ int ks_seq_upload_codes(ks_ctx* ctx, const uint8_t* codes, int64_t n, ks_seq** o
         if (e != cudaSuccess) rc = cuda_fail(e, "pack codes");
     }
     if (rc == KS_OK && bad) rc = fail(KS_E_INVALID, "symbol code out of range (expected 0..4)");
+    if (rc == KS_OK) rc = seq_seal(ctx, s);
     if (rc) {
         seq_destroy(s);
         return rc;
@@ -406,6 +438,7 @@ static int encode_common(ks_ctx* ctx, const uint8_t* d_bytes, int64_t n_bytes, i
     int launches = 0;
     rc = encode_ascii_device(ctx, d_bytes, n_bytes, fasta != 0, s, ar.take(encode_scratch_bytes(n_bytes)),
                              &launches);
+    if (rc == KS_OK) rc = seq_seal(ctx, s);
     if (rc) {
         seq_destroy(s);
         return rc;
