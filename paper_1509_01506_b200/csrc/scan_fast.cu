@@ -396,7 +396,13 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
 // stores, ring loads or intermediate re-walks.  Idle lanes ride along in
 // the padding row (state nq), whose entries never accept.
 #ifndef KS_CLS_REGS
-#define KS_CLS_REGS 4
+#define KS_CLS_REGS 5
+#endif
+#ifndef KS_CLS_UNROLL   // experiment: the block's word loop unrolled
+#define KS_CLS_UNROLL 1
+#endif
+#ifndef KS_CLS_DIRECT   // experiment: no queue, one histogram add per accepting pair
+#define KS_CLS_DIRECT 0
 #endif
 constexpr int kClsRegs = KS_CLS_REGS;
 static_assert(kClsRegs >= 3, "class queue: two pushes between votes need a spare slot");
@@ -424,10 +430,29 @@ __device__ __forceinline__ void move_if(uint32_t& d, uint32_t s, uint32_t t, uin
         : "+r"(d) : "r"(s), "r"(t), "r"(one));
 }
 // Push `pair` when t != 0 (the newest pair in r[0]).
+#ifndef KS_CLS_PUSH   // experiment: 1 = mask selects (LOP3, ALU pipe), 2 = upper half LOP3 / lower half FMA
+#define KS_CLS_PUSH 0
+#endif
+__device__ __forceinline__ uint32_t sel_mask(uint32_t a, uint32_t b, uint32_t m) {   // (a & m) | (b & ~m)
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(d) : "r"(a), "r"(b), "r"(m));
+    return d;
+}
 __device__ __forceinline__ void cls_push_if(ClsBuf& b, uint32_t pair, uint32_t t, uint32_t one) {
+#if KS_CLS_PUSH == 0
 #pragma unroll
     for (int i = kClsRegs - 1; i > 0; --i) move_if(b.r[i], b.r[i - 1], t, one);
     move_if(b.r[0], pair, t, one);
+#else
+    const uint32_t m = t ? ~0u : 0u;
+#pragma unroll
+    for (int i = kClsRegs - 1; i > 0; --i) {
+        if (KS_CLS_PUSH == 1 || i >= kClsRegs / 2) b.r[i] = sel_mask(b.r[i - 1], b.r[i], m);
+        else move_if(b.r[i], b.r[i - 1], t, one);
+    }
+    if (KS_CLS_PUSH == 1) b.r[0] = sel_mask(pair, b.r[0], m);
+    else move_if(b.r[0], pair, t, one);
+#endif
 }
 __device__ __forceinline__ void red_at(uint32_t addr, uint32_t one) {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(one) : "memory");
@@ -435,17 +460,37 @@ __device__ __forceinline__ void red_at(uint32_t addr, uint32_t one) {
 // hist2: the histogram's shared address - 0x10000 (an accepting entry e has
 // bit 15, its slot's byte offset is 2 * (e & 0x7FFF)); one: a
 // kernel-parameter 1 (an immediate would become an aggregated increment).
+// One queue slot into the histogram: the first accepting half of the pair
+// (low when it accepts, else high), then the high half when both accept.
+__device__ __forceinline__ void cls_flush_slot(uint32_t hist2, uint32_t x, uint32_t one) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p, lo, both;\n\t"
+        ".reg .u32 t, h;\n\t"
+        "and.b32 t, %0, 0x80008000;\n\t"
+        "setp.eq.u32 p, t, 0;\n\t"
+        "@p bra DONE;\n\t"
+        "and.b32 t, %0, 0x8000;\n\t"
+        "setp.ne.u32 lo, t, 0;\n\t"
+        "shr.u32 h, %0, 15;\n\t"
+        "shl.b32 t, %0, 1;\n\t"
+        "selp.u32 t, t, h, lo;\n\t"
+        "and.b32 t, t, 0x1FFFC;\n\t"
+        "add.u32 t, t, %1;\n\t"
+        "red.shared.add.u32 [t], %2;\n\t"
+        "setp.lt.and.s32 both, %0, 0, lo;\n\t"
+        "@!both bra DONE;\n\t"
+        "and.b32 h, h, 0x1FFFC;\n\t"
+        "add.u32 h, h, %1;\n\t"
+        "red.shared.add.u32 [h], %2;\n\t"
+        "DONE:\n\t"
+        "}"
+        :: "r"(x), "r"(hist2), "r"(one) : "memory");
+}
 __device__ __forceinline__ void cls_flush(uint32_t hist2, ClsBuf& b, uint32_t one) {
 #pragma unroll
     for (int i = 0; i < kClsRegs; ++i) {
-        const uint32_t x = b.r[i];
-        if (x) {
-            // the first accepting half: low when it accepts, else high
-            const bool lo = (x & 0x8000u) != 0u;
-            const uint32_t t = lo ? x << 1 : x >> 15;
-            red_at(hist2 + (t & 0x1FFFCu), one);
-            if (lo && int32_t(x) < 0) red_at(hist2 + ((x >> 15) & 0x1FFFCu), one);   // both accept
-        }
+        cls_flush_slot(hist2, b.r[i], one);
         b.r[i] = 0u;
     }
 }
@@ -459,7 +504,12 @@ __device__ __forceinline__ uint32_t fast_block_cls(const Ctx& c, uint32_t s, con
     constexpr uint32_t FM = 0xFu << LC;
     uint32_t w0 = xb.x, w1 = xb.y, w2 = xb.z, w3 = xb.w;
     uint32_t e = s << 1;
+    const uint32_t one = opaque(c.one);   // in a register: no constant-bank load per red
+#if KS_CLS_UNROLL
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
     for (int q = 0; q < 4; ++q) {
         const uint32_t x = w0, y = w0 >> 16;
 #pragma unroll
@@ -470,8 +520,12 @@ __device__ __forceinline__ uint32_t fast_block_cls(const Ctx& c, uint32_t s, con
             e = lds16_tk(bitsel<FM>(f1, e0));
             uint32_t pair;
             asm("mad.lo.u32 %0, %1, 65536, %2;" : "=r"(pair) : "r"(e), "r"(e0));
-            cls_push_if(b, pair, pair & 0x80008000u, c.one);
-            if ((j & 2) && __any_sync(0xffffffffu, b.r[kClsRegs - 2] != 0u)) cls_flush(c.hist2, b, c.one);
+#if KS_CLS_DIRECT
+            cls_flush_slot(c.hist2, pair, one);   // no queue: every pair goes straight to the histogram
+#else
+            cls_push_if(b, pair, pair & 0x80008000u, one);
+            if ((j & 2) && __any_sync(0xffffffffu, b.r[kClsRegs - 2] != 0u)) cls_flush(c.hist2, b, one);
+#endif
         }
         w0 = w1;
         w1 = w2;
@@ -1099,7 +1153,9 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
         a.split_tiles = parts > 1 ? int32_t(std::min<int64_t>(tiles, nw)) : 0;
         // round-robin for all but the last two rounds of items
         const int64_t items = tiles - a.split_tiles + int64_t(a.split_tiles) * parts;
-        a.static_items = std::max<int64_t>(nw, (items / nw - 2) * nw);
+        int64_t dyn_rounds = 2;
+        if (const char* e = std::getenv("KS_DYN_ROUNDS"); e && *e) dyn_rounds = std::max(1, std::atoi(e));
+        a.static_items = std::max<int64_t>(nw, (items / nw - dyn_rounds) * nw);
     }
     if (const char* e = std::getenv("KS_KTIME"); e && (*e == '1' || *e == '2')) {
         unsigned long long h[10] = {~0ull, 0, ~0ull, 0, ~0ull, 0, ~0ull, 0, 0, 0};
