@@ -401,6 +401,9 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
 #ifndef KS_CLS_UNROLL   // experiment: the block's word loop unrolled
 #define KS_CLS_UNROLL 1
 #endif
+#ifndef KS_CLS_PF2
+#define KS_CLS_PF2 0
+#endif
 #ifndef KS_CLS_DIRECT   // experiment: no queue, one histogram add per accepting pair
 #define KS_CLS_DIRECT 0
 #endif
@@ -767,6 +770,17 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                               ((tmask & rows) == 0ull);
             plain = __all_sync(am, mine) && a.seq.rowmask != nullptr;
             if (plain) {
+#if KS_CLS_PF2   // experiment: block loads two blocks ahead
+                uint4 nb = __ldg(pb + 32);
+#pragma unroll 1
+                for (int i = 0; i < nmax; ++i) {
+                    pb += 32;
+                    const uint4 nb2 = __ldg(pb + 32);   // the slots exist: arrays are padded by a whole tile
+                    s = fast_block_cls(c, s, wb, cbuf);
+                    wb = nb;
+                    nb = nb2;
+                }
+#else
 #pragma unroll 1
                 for (int i = 0; i < nmax; ++i) {
                     pb += 32;
@@ -774,6 +788,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                     s = fast_block_cls(c, s, wb, cbuf);
                     wb = nb;
                 }
+#endif
             }
         }
         if (!plain)
