@@ -398,14 +398,8 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
 #ifndef KS_CLS_REGS
 #define KS_CLS_REGS 5
 #endif
-#ifndef KS_CLS_UNROLL   // experiment: the block's word loop unrolled
+#ifndef KS_CLS_UNROLL   // 0: the block's word loop rolled (measured 1.2% slower)
 #define KS_CLS_UNROLL 1
-#endif
-#ifndef KS_CLS_PF2
-#define KS_CLS_PF2 0
-#endif
-#ifndef KS_CLS_DIRECT   // experiment: no queue, one histogram add per accepting pair
-#define KS_CLS_DIRECT 0
 #endif
 constexpr int kClsRegs = KS_CLS_REGS;
 static_assert(kClsRegs >= 3, "class queue: two pushes between votes need a spare slot");
@@ -433,32 +427,10 @@ __device__ __forceinline__ void move_if(uint32_t& d, uint32_t s, uint32_t t, uin
         : "+r"(d) : "r"(s), "r"(t), "r"(one));
 }
 // Push `pair` when t != 0 (the newest pair in r[0]).
-#ifndef KS_CLS_PUSH   // experiment: 1 = mask selects (LOP3, ALU pipe), 2 = upper half LOP3 / lower half FMA
-#define KS_CLS_PUSH 0
-#endif
-__device__ __forceinline__ uint32_t sel_mask(uint32_t a, uint32_t b, uint32_t m) {   // (a & m) | (b & ~m)
-    uint32_t d;
-    asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(d) : "r"(a), "r"(b), "r"(m));
-    return d;
-}
 __device__ __forceinline__ void cls_push_if(ClsBuf& b, uint32_t pair, uint32_t t, uint32_t one) {
-#if KS_CLS_PUSH == 0
 #pragma unroll
     for (int i = kClsRegs - 1; i > 0; --i) move_if(b.r[i], b.r[i - 1], t, one);
     move_if(b.r[0], pair, t, one);
-#else
-    const uint32_t m = t ? ~0u : 0u;
-#pragma unroll
-    for (int i = kClsRegs - 1; i > 0; --i) {
-        if (KS_CLS_PUSH == 1 || i >= kClsRegs / 2) b.r[i] = sel_mask(b.r[i - 1], b.r[i], m);
-        else move_if(b.r[i], b.r[i - 1], t, one);
-    }
-    if (KS_CLS_PUSH == 1) b.r[0] = sel_mask(pair, b.r[0], m);
-    else move_if(b.r[0], pair, t, one);
-#endif
-}
-__device__ __forceinline__ void red_at(uint32_t addr, uint32_t one) {
-    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(one) : "memory");
 }
 // hist2: the histogram's shared address - 0x10000 (an accepting entry e has
 // bit 15, its slot's byte offset is 2 * (e & 0x7FFF)); one: a
@@ -523,12 +495,8 @@ __device__ __forceinline__ uint32_t fast_block_cls(const Ctx& c, uint32_t s, con
             e = lds16_tk(bitsel<FM>(f1, e0));
             uint32_t pair;
             asm("mad.lo.u32 %0, %1, 65536, %2;" : "=r"(pair) : "r"(e), "r"(e0));
-#if KS_CLS_DIRECT
-            cls_flush_slot(c.hist2, pair, one);   // no queue: every pair goes straight to the histogram
-#else
             cls_push_if(b, pair, pair & 0x80008000u, one);
             if ((j & 2) && __any_sync(0xffffffffu, b.r[kClsRegs - 2] != 0u)) cls_flush(c.hist2, b, one);
-#endif
         }
         w0 = w1;
         w1 = w2;
@@ -656,7 +624,8 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     const bool dyn = MODE == kModeCount && a.tile_ctr != nullptr;
     const int ntiles = int(t1 - t0 + 1);
     const int whole = dyn ? ntiles - a.split_tiles : ntiles;
-    const int n_items = dyn ? whole + a.split_tiles * a.split_parts : ntiles;
+    const int n_split1 = (a.split_tiles - a.split2_tiles) * a.split_parts;   // items of the coarser split
+    const int n_items = dyn ? whole + n_split1 + a.split2_tiles * a.split2_parts : ntiles;
     const int static_items = int(a.static_items);
     const int ublocks = int(a.chunk_len >> 6);
     const int wid = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
@@ -680,10 +649,13 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
             t = t0 + item;
         } else {
             const int j = item - whole;
-            t = t0 + whole + j / a.split_parts;
-            const int q = j % a.split_parts;
-            pl = q * ublocks / a.split_parts;
-            ph = (q + 1) * ublocks / a.split_parts;
+            const bool fine = j >= n_split1;
+            const int jj = fine ? j - n_split1 : j;
+            const int parts = fine ? a.split2_parts : a.split_parts;
+            t = t0 + whole + (fine ? a.split_tiles - a.split2_tiles : 0) + jj / parts;
+            const int q = jj % parts;
+            pl = q * ublocks / parts;
+            ph = (q + 1) * ublocks / parts;
         }
         const int64_t u = (t << 5) + lane;
         const int64_t ch = u - u0;
@@ -770,17 +742,6 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                               ((tmask & rows) == 0ull);
             plain = __all_sync(am, mine) && a.seq.rowmask != nullptr;
             if (plain) {
-#if KS_CLS_PF2   // experiment: block loads two blocks ahead
-                uint4 nb = __ldg(pb + 32);
-#pragma unroll 1
-                for (int i = 0; i < nmax; ++i) {
-                    pb += 32;
-                    const uint4 nb2 = __ldg(pb + 32);   // the slots exist: arrays are padded by a whole tile
-                    s = fast_block_cls(c, s, wb, cbuf);
-                    wb = nb;
-                    nb = nb2;
-                }
-#else
 #pragma unroll 1
                 for (int i = 0; i < nmax; ++i) {
                     pb += 32;
@@ -788,7 +749,6 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                     s = fast_block_cls(c, s, wb, cbuf);
                     wb = nb;
                 }
-#endif
             }
         }
         if (!plain)
@@ -1152,7 +1112,9 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
     const int64_t nw = int64_t(warps) * std::max<int64_t>(1, std::min<int64_t>((tiles + warps - 1) / warps,
                                                                                ctx->num_sms));
     a.tile_ctr = nullptr;
-    if (mode == kModeCount && a.fin_counts && a.dyn_items && tiles > 6 * nw &&
+    int64_t dyn_min_rounds = 6;
+    if (const char* e = std::getenv("KS_DYN_MIN_ROUNDS"); e && *e) dyn_min_rounds = std::max(1, std::atoi(e));
+    if (mode == kModeCount && a.fin_counts && a.dyn_items && tiles > dyn_min_rounds * nw &&
         !(std::getenv("KS_STATIC_TILES") && *std::getenv("KS_STATIC_TILES") == '1')) {
         if (!ctx->tctr) {   // zero once; every fused count's finalizing CTA leaves them zero
             KS_CUDA(cudaMalloc(&ctx->tctr, size_t(kTileCtrs) * 128));
@@ -1167,7 +1129,13 @@ int launch_scan_fast(ks_ctx* ctx, ScanArgs a, int mode, int k, int* launches) {
         a.split_parts = parts;
         a.split_tiles = parts > 1 ? int32_t(std::min<int64_t>(tiles, nw)) : 0;
         // round-robin for all but the last two rounds of items
-        const int64_t items = tiles - a.split_tiles + int64_t(a.split_tiles) * parts;
+        // (KS_SPLIT2_PARTS=n: the last half of the split tiles in n ranges; experiment)
+        int parts2 = parts;
+        if (const char* e = std::getenv("KS_SPLIT2_PARTS"); e && *e && parts > 1) parts2 = std::max(parts, std::min(ub, std::atoi(e)));
+        a.split2_parts = parts2;
+        a.split2_tiles = parts2 > parts ? a.split_tiles / 2 : 0;
+        const int64_t items = tiles - a.split_tiles + int64_t(a.split_tiles - a.split2_tiles) * parts +
+                              int64_t(a.split2_tiles) * parts2;
         int64_t dyn_rounds = 2;
         if (const char* e = std::getenv("KS_DYN_ROUNDS"); e && *e) dyn_rounds = std::max(1, std::atoi(e));
         a.static_items = std::max<int64_t>(nw, (items / nw - dyn_rounds) * nw);

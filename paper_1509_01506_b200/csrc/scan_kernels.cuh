@@ -109,6 +109,9 @@ struct ScanArgs {
     int32_t dyn_items = 0;
     unsigned int* tile_ctr = nullptr;
     int32_t split_tiles = 0, split_parts = 1;
+    // the last split2_tiles of the split tiles are cut finer still (split2_parts ranges):
+    // the items handed out last are the smallest
+    int32_t split2_tiles = 0, split2_parts = 1;
     int64_t static_items = 0;               // items below this go round-robin
     int32_t early_wait = 0;                 // fast kernel: wait for the preceding kernel up front (KS_EARLY_WAIT=1)
     // fast K = 2 count with the visit-class table (CompiledTable::cls_*): tk/t1

@@ -1173,6 +1173,48 @@ def _k2_dfa(rng):
             return dfa
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("tile_lb", [None, "2", "5"])
+def test_row_flags_and_plain_items(monkeypatch, tile_lb):
+    """Per-tile row flags (SeqView::rowmask, computed when an upload ends) and
+    the class count's plain-item loop: OTHER placed so that whole tiles are
+    clean, single rows of a tile are dirty (one N in one lane's block), whole
+    units and whole tiles are N, and the sequence ends inside a tile -- through
+    the device encode, the device-packed and the host-packed codes uploads,
+    every count equal to the oracle and to the ring kernel."""
+    if tile_lb is not None:
+        monkeypatch.setenv("KS_TILE_LB", tile_lb)
+    rng = np.random.default_rng(77)
+    dfa = _k2_dfa(rng)
+    c = _native.DeviceContext(0)
+    dh = c.dfa(dfa)
+    assert dh.info["stride"] == 2, dh.info
+    lb = int(tile_lb) if tile_lb is not None else 4
+    unit = 64 << lb
+    tile = 32 * unit
+    for n in (6 * tile + 12345, (9 << 20) + 77):      # the second takes the host-packed codes upload
+        codes = rng.integers(0, 4, n).astype(np.uint8)
+        codes[tile + 5 * unit + 64 * 1 + 7] = 4                    # one N: row 1 of tile 1 dirty, the rest clean
+        codes[2 * tile + 3 * unit: 2 * tile + 4 * unit] = 4          # a whole unit of N (all rows of tile 2)
+        codes[3 * tile: 4 * tile] = 4                                # a whole tile of N
+        codes[4 * tile + unit - 1] = 4                               # last base of a unit
+        codes[4 * tile + 2 * unit] = 4                               # first base of a unit
+        codes[n - 3:] = 4                                            # the ragged end
+        want = O.ref_sequential_count(dfa, codes)[0]
+        ascii_bytes = np.frombuffer(b"ACGTN", dtype=np.uint8)[codes].tobytes()
+        for sh in (c.upload_codes(codes), c.upload_ascii(ascii_bytes)):
+            assert c.count(dh, sh).tolist() == want.tolist(), (tile_lb, n)
+            monkeypatch.setenv("KS_NO_CLS", "1")
+            assert c.count(dh, sh).tolist() == want.tolist(), (tile_lb, n)
+            monkeypatch.delenv("KS_NO_CLS")
+            # ranges (per-chunk entry states, partial first and last blocks) on the same sequence
+            for (b, e) in ((0, n), (tile + 17, 5 * tile + 4001), (n - 5000, n)):
+                st = int(rng.integers(0, dfa.state_count))
+                got, last, _ = c.scan_range(dh, sh, b, e, st)
+                ref, ref_last = O.ref_sequential_count(dfa, codes, b, e, st)
+                assert got.tolist() == ref.tolist() and last == ref_last, (tile_lb, n, b, e)
+
+
 @pytest.mark.parametrize("seed", range(4))
 def test_class_table_counts_vs_oracle(monkeypatch, seed):
     """The fused K = 2 count on the visit-class table (scan_fast CLS kernel)
