@@ -398,6 +398,9 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
 #ifndef KS_CLS_REGS
 #define KS_CLS_REGS 5
 #endif
+#ifndef KS_PLAIN_ALL   // plain items for every count / map kernel (0: the class count only)
+#define KS_PLAIN_ALL 1
+#endif
 #ifndef KS_CLS_UNROLL   // 0: the block's word loop rolled (measured 1.2% slower)
 #define KS_CLS_UNROLL 1
 #endif
@@ -730,12 +733,12 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
         // rows of the tile without OTHER (SeqView::rowmask) skip the bitmap loads
         const uint64_t tmask = a.seq.rowmask ? __ldg(a.seq.rowmask + t) : ~0ull;
         uint64_t wm = ((tmask >> (k0 & 63)) & 1ull) ? __ldg(pm) : 0ull;
-        // The common item of the class count: whole, aligned block ranges in
-        // every lane and no OTHER in any of its rows (SeqView::rowmask) -- a
+        // The common item of a count or map pass: whole, aligned block ranges
+        // in every lane and no OTHER in any of its rows (SeqView::rowmask) -- a
         // loop of block load + scan, none of the per-lane range and bitmap
         // tests, no votes.  Everything else takes the general loop below.
         bool plain = false;
-        if constexpr (CLS) {
+        if constexpr (KS_PLAIN_ALL ? (MODE == kModeCount || MODE == kModeMap) : CLS) {
             const uint64_t rows = nmax >= 64 ? ~0ull : ((1ull << nmax) - 1ull) << (k0 & 63);
             const int k0u = __shfl_sync(am, k0, 0);
             const bool mine = active & ((cb & 63) == 0) & ((ce & 63) == 0) & (nblk == nmax) & (k0 == k0u) &
@@ -746,7 +749,19 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                 for (int i = 0; i < nmax; ++i) {
                     pb += 32;
                     const uint4 nb = __ldg(pb);   // the slot exists: arrays are padded by a whole tile
-                    s = fast_block_cls(c, s, wb, cbuf);
+                    if constexpr (CLS) {
+                        s = fast_block_cls(c, s, wb, cbuf);
+                    } else if constexpr (LEAN && MODE != kModeMap) {
+                        uint32_t hm;
+                        uint32_t s2 = fast_block_lean<K>(c, s, wb, hm);
+                        if (__any_sync(am, (hm & 0x8000u) != 0u))   // rare: re-run the block recording
+                            s2 = fast_block<K, MODE>(c, L, s, 0x8000u, wb, (gfirst + k0 + i) << 6, am, rp0, rp,
+                                                     ring_stride);
+                        s = s2;
+                    } else {
+                        s = fast_block<K, MODE>(c, L, s, 0x8000u, wb, (gfirst + k0 + i) << 6, am, rp0, rp,
+                                                ring_stride);
+                    }
                     wb = nb;
                 }
             }
