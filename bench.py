@@ -108,34 +108,55 @@ def host_codes(ascii_: np.ndarray) -> np.ndarray:
 
 class ClockSampler:
     """SM clocks and throttle reasons sampled during the timed region: NVML
-    polled from a thread every ~1 ms (nvidia-smi's 100 ms floor would miss a
-    timed region of a few ms).  Native calls release the GIL."""
+    polled from a thread every ~2 ms (nvidia-smi's 100 ms floor would miss a
+    timed region of a few ms; every query perturbs the GPU a little -- 20-step
+    regions measured 0.3-1.5% slower under a 1 ms poll, tools/exp_bench_gap.py).
+    Native calls release the GIL."""
 
     REASONS = {  # NVML clocks-event reason bits
         "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
         "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4,
     }
 
-    def __init__(self, gpu: int, period_s: float = 0.001):
+    def __init__(self, gpu: int, period_s: float = 0.002, first_delay_s: float = 0.0005):
         self.gpu = gpu
         self.period = period_s
+        self.first_delay = first_delay_s
         self.samples: list[tuple[int, int, int]] = []
         self._stop = None
         self._thread = None
+        self._h = None
+        self._nvml = None
 
-    def __enter__(self):
-        import threading
+    def prepare(self):
+        """NVML set-up (tens of ms), done before the synchronisation that
+        precedes the timed region: the GPU must not sit idle between that
+        synchronisation and the first timed launch."""
+        if self._h is not None:
+            return self
         try:
             import pynvml
             pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
-            self._max = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self._max = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._nvml = pynvml
         except Exception as exc:  # pragma: no cover - no NVML
             log(f"clock sampling unavailable: {exc}")
+        return self
+
+    def __enter__(self):
+        import threading
+        self.prepare()
+        if self._h is None:
             return self
+        pynvml, h = self._nvml, self._h
         self._stop = threading.Event()
 
         def poll():
+            # the first sample waits until the host has enqueued the timed
+            # steps: an NVML query contends with kernel launches in the driver
+            # and would leave the GPU idle at the start of the timed region
+            self._stop.wait(self.first_delay)
             while not self._stop.is_set():
                 try:
                     sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
@@ -160,7 +181,7 @@ class ClockSampler:
         reasons = sorted({name for _, _, rs in self.samples for name, bit in self.REASONS.items() if rs & bit})
         return {"sm_mhz": statistics.median(s for s, _, _ in self.samples),
                 "sm_max_mhz": max(m for _, m, _ in self.samples), "reasons": reasons,
-                "samples": len(self.samples), "source": "NVML, 1 ms poll during the timed steps"}
+                "samples": len(self.samples), "source": "NVML, 2 ms poll during the timed steps"}
 
 
 def oracle_counts(dfa, codes: np.ndarray, workers: int, locate: bool = False):
@@ -270,10 +291,19 @@ def time_steps(ctx, step, stream, steps: int, flush, local: int, sync_each=None,
     ev1 = torch.cuda.Event(enable_timing=True)
     step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(steps if flush is not None else 0)]
+    sampler = ClockSampler(local).prepare()
+    # warm the timing machinery: the first pair of timing events recorded in a
+    # process costs ~50 us on the stream (measured: the first 20-step region
+    # 0.2769 ms/step against 0.2743 for every later one, tools/exp_bench_gap.py)
+    _p0, _p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    _p0.record(stream)
+    _p1.record(stream)
+    _p1.synchronize()
+    _p0.elapsed_time(_p1)
     if sync_each is not None:
         sync_each()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
+    with sampler as clocks:
         ev0.record(stream)
         for i in range(steps):
             if flush is not None:
