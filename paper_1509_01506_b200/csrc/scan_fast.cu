@@ -28,6 +28,14 @@
 //     hit-rate estimate) scan blocks with no hit bookkeeping at all -- one OR
 //     of the entries per step -- and re-run a block only when a lane's OR
 //     shows the accept flag (C4: 0.61 -> 0.53 ms).
+//   * the fused count of a K = 2 automaton (C3) runs on the visit-class table
+//     instead of the ring (CLS instantiation, "visit-class count" below): an
+//     accepting step names one histogram slot, hits are queued in registers
+//     as 32-bit pairs and flushed by batched shared adds.
+//   * items whose 32 lanes scan whole blocks of rows without OTHER (per-tile
+//     row flags, SeqView::rowmask) take a plain `load block; scan block` loop
+//     in every count and map kernel; the general block loop handles range
+//     ends, N runs and sequences without flags (streamed pieces).
 // Count mode: the last CTA turns the visit histogram into counts and writes
 // them straight into pinned host memory; the kernel is launched with
 // programmatic stream serialisation (table staging before
