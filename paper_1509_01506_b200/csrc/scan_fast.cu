@@ -364,7 +364,12 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
             // chk_steps(K) steps): drains then run with full lanes, and ring entries
             // (table addresses) are position-free, so they may cross blocks
             constexpr int CHK = chk_steps(K);
-            if ((j % CHK) == CHK - 1 && __any_sync(am, rp - rp0 >= c.ring_thr)) {
+            // (also after the block's last step: K = 3 has 21 steps, and the
+            // 5 after the vote at step 15 plus the next block's first 8 would
+            // be 13 pushes between two votes -- with dense hits a lane at the
+            // threshold wrote past its ring, into the histogram)
+            if (((j % CHK) == CHK - 1 || (NL % CHK != 0 && j == NL - 1)) &&
+                __any_sync(am, rp - rp0 >= c.ring_thr)) {
                 L.nrows += drain_out<K, MODE>(c, rp0, (rp - rp0) / kRingStride);
                 rp = rp0;
             }

@@ -1174,6 +1174,31 @@ def _k2_dfa(rng):
 
 
 @pytest.mark.gpu
+def test_dense_hits_k3_ring_never_overflows():
+    """A 3-base-stride automaton with 2-mers among its literals accepts in
+    most steps: the hit ring's fill check must also run after the last of a
+    block's 21 steps (13 pushes could pass between two checks and a lane at
+    the threshold wrote past its ring into the histogram: wrong counts at
+    1000 bases, an illegal access at 100000 -- found by tools/stress_class.py,
+    seed 20261036)."""
+    rng = np.random.default_rng(5)
+    lits = ["ta", "ga", "cc", "act", "ggc"]
+    lits += ["".join("acgt"[x] for x in rng.integers(0, 4, int(rng.integers(8, 13)))) for _ in range(60)]
+    dfa = dfa_of("\n".join(lits))
+    c = _native.DeviceContext(0)
+    dh = c.dfa(dfa)
+    assert dh.info["stride"] == 3, dh.info
+    for n in (1000, 20_000, 100_000, 400_000, 3_000_001):
+        codes = rng.integers(0, 4, n).astype(np.uint8)
+        want = O.ref_sequential_count(dfa, codes)[0]
+        sh = c.upload_codes(codes)
+        for _ in range(2):
+            assert c.count(dh, sh).tolist() == want.tolist(), n
+        counts, rows = c.locate(dh, sh)
+        assert counts.tolist() == want.tolist() and rows.shape[0] == int(want.sum()), n
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("tile_lb", [None, "2", "5"])
 def test_row_flags_and_plain_items(monkeypatch, tile_lb):
     """Per-tile row flags (SeqView::rowmask, computed when an upload ends) and
