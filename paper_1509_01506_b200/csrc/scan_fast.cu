@@ -954,13 +954,30 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
                 __syncthreads();
                 // (class tables: only the slots that can be counted, a compact list)
                 const int n_fin = CLS ? a.n_used : n_hist;
-                for (int k = threadIdx.x; k < n_fin; k += blockDim.x) {
-                    const int st = CLS ? __ldg(&a.cls_used[k]) : k;
-                    const unsigned long long v = __ldcg(&a.visits[st]);
-                    if (!v) continue;
-                    a.visits[st] = 0ull;   // clean for the next call
-                    for (int k = __ldg(&a.acc_out_off[st]); k < __ldg(&a.acc_out_off[st + 1]); ++k)
-                        atomicAdd(&acc[__ldg(&a.acc_out_ids[k])], v);
+                // four slots per thread at a time, their loads issued together
+                // (the chain slot id -> visits -> CSR bounds -> ids is 4 dependent
+                // L2 round trips per slot)
+                constexpr int FB = 4;
+                for (int k0 = threadIdx.x; k0 < n_fin; k0 += FB * blockDim.x) {
+                    int st[FB], o0[FB], o1[FB];
+                    unsigned long long v[FB];
+#pragma unroll
+                    for (int j = 0; j < FB; ++j) {
+                        const int k = k0 + j * int(blockDim.x);
+                        st[j] = k < n_fin ? (CLS ? __ldg(&a.cls_used[k]) : k) : -1;
+                    }
+#pragma unroll
+                    for (int j = 0; j < FB; ++j) {
+                        v[j] = st[j] >= 0 ? __ldcg(&a.visits[st[j]]) : 0ull;
+                        o0[j] = st[j] >= 0 ? __ldg(&a.acc_out_off[st[j]]) : 0;
+                        o1[j] = st[j] >= 0 ? __ldg(&a.acc_out_off[st[j] + 1]) : 0;
+                    }
+#pragma unroll
+                    for (int j = 0; j < FB; ++j) {
+                        if (!v[j]) continue;
+                        a.visits[st[j]] = 0ull;   // clean for the next call
+                        for (int k = o0[j]; k < o1[j]; ++k) atomicAdd(&acc[__ldg(&a.acc_out_ids[k])], v[j]);
+                    }
                 }
                 if (!in_smem) __threadfence();
                 __syncthreads();
