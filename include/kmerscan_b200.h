@@ -106,6 +106,9 @@ KS_API int ks_dfa_info_get(const ks_dfa* dfa, ks_dfa_info* out);
 KS_API int ks_dfa_free(ks_dfa* dfa);
 
 /* ---- sequences ---------------------------------------------------------- */
+/* A sequence is immutable once its upload call returns; the upload ends by
+ * writing per-tile row flags (which block rows hold OTHER) that the scans of
+ * a resident sequence use to skip OTHER-bitmap loads and per-lane tests. */
 /* Symbol codes 0..4 (Sequence.symbols, ingest.py:20-32) -> packed device form. */
 KS_API int ks_seq_upload_codes(ks_ctx* ctx, const uint8_t* codes, int64_t n, ks_seq** out);
 /* Raw ASCII bytes -> device encode (alphabet.py:20-37 / ingest.py:67-69):
