@@ -417,7 +417,12 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
 #ifndef KS_CLS_UNROLL   // 0: the block's word loop rolled (measured 1.2% slower)
 #define KS_CLS_UNROLL 1
 #endif
+#ifndef KS_CLS_FLUSH   // newest slots flushed when a queue fills (KS_CLS_REGS: all)
+#define KS_CLS_FLUSH 2
+#endif
 constexpr int kClsRegs = KS_CLS_REGS;
+constexpr int kClsFlush = KS_CLS_FLUSH < KS_CLS_REGS ? KS_CLS_FLUSH : KS_CLS_REGS;
+static_assert(kClsFlush >= 2, "class queue: a flush must make room for the two pushes before the next vote");
 static_assert(kClsRegs >= 3, "class queue: two pushes between votes need a spare slot");
 
 struct ClsBuf {
@@ -478,12 +483,16 @@ __device__ __forceinline__ void cls_flush_slot(uint32_t hist2, uint32_t x, uint3
         "}"
         :: "r"(x), "r"(hist2), "r"(one) : "memory");
 }
+// Flush the NF newest slots of every lane and move the older ones down.  In
+// the scan NF = KS_CLS_FLUSH (2): the deep slots are held by a few lanes only
+// (24 / 13 / 5 / 1.4 lanes in slots 0..3 when a queue fills), so their adds
+// would run nearly empty; kept, they become slots 0 and 1 of a later flush.
+template <int NF>
 __device__ __forceinline__ void cls_flush(uint32_t hist2, ClsBuf& b, uint32_t one) {
 #pragma unroll
-    for (int i = 0; i < kClsRegs; ++i) {
-        cls_flush_slot(hist2, b.r[i], one);
-        b.r[i] = 0u;
-    }
+    for (int i = 0; i < NF; ++i) cls_flush_slot(hist2, b.r[i], one);
+#pragma unroll
+    for (int i = 0; i < kClsRegs; ++i) b.r[i] = i + NF < kClsRegs ? b.r[i + NF] : 0u;
 }
 // One full, OTHER-free 64-base block on the class table: a loop over the
 // block's four words (8 steps each; rolled, so the kernel's hot code stays
@@ -512,7 +521,7 @@ __device__ __forceinline__ uint32_t fast_block_cls(const Ctx& c, uint32_t s, con
             uint32_t pair;
             asm("mad.lo.u32 %0, %1, 65536, %2;" : "=r"(pair) : "r"(e), "r"(e0));
             cls_push_if(b, pair, pair & 0x80008000u, one);
-            if ((j & 2) && __any_sync(0xffffffffu, b.r[kClsRegs - 2] != 0u)) cls_flush(c.hist2, b, one);
+            if ((j & 2) && __any_sync(0xffffffffu, b.r[kClsRegs - 2] != 0u)) cls_flush<kClsFlush>(c.hist2, b, one);
         }
         w0 = w1;
         w1 = w2;
@@ -906,7 +915,7 @@ __global__ void __launch_bounds__(1024, 1) scan_fast_kernel(const ScanArgs a) {
     kt_mark(a.ktime, 4, true, true);
     kt_mark(a.ktime, 5, false, true);
     if constexpr (CLS) {
-        cls_flush(c.hist2, cbuf, c.one);   // the class queue's leftovers
+        cls_flush<kClsRegs>(c.hist2, cbuf, c.one);   // the class queue's leftovers
     } else if constexpr (MODE == kModeCount) {   // the ring's leftovers
         Lane<MODE> L;
         drain<K, MODE>(c, L, am, rp0, rp, ring_stride);
