@@ -409,7 +409,7 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
 // stores, ring loads or intermediate re-walks.  Idle lanes ride along in
 // the padding row (state nq), whose entries never accept.
 #ifndef KS_CLS_REGS
-#define KS_CLS_REGS 5
+#define KS_CLS_REGS 6
 #endif
 #ifndef KS_PLAIN_ALL   // plain items for every count / map kernel (0: the class count only)
 #define KS_PLAIN_ALL 1
