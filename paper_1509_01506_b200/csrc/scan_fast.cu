@@ -401,11 +401,12 @@ __device__ __forceinline__ uint32_t fast_block(const Ctx& c, Lane<MODE>& L, uint
 // bit-selects and tests fill, sees one instruction per two steps (the
 // 16-bit shift register of the first version cost three per step).  Every
 // two pairs the warp votes whether some lane could overflow before the next
-// vote, and only then adds every lane's pairs into the shared-memory
-// histogram: per queue slot one red for the lanes that hold a pair (its
-// first accepting half), and, behind one warp vote per flush, a second one
-// for pairs whose both halves accept.  The data pipe then carries the table
-// gathers, the block loads and one red per accepting step -- no ring
+// vote, and only then the lanes add their KS_CLS_FLUSH newest pairs into the
+// shared-memory histogram (cls_flush): per flushed slot one red for the
+// lanes that hold a pair there (its first accepting half) and a second one
+// for the few pairs whose both halves accept; older pairs stay queued.  The
+// data pipe then carries the table gathers, the block loads and about one
+// red wavefront per five accepting steps -- no ring
 // stores, ring loads or intermediate re-walks.  Idle lanes ride along in
 // the padding row (state nq), whose entries never accept.
 #ifndef KS_CLS_REGS
